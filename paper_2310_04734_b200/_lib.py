@@ -1,0 +1,88 @@
+"""ctypes binding of libvibro_b200.so (the C ABI declared in include/vibro_b200.h).
+
+The library is built in-tree by `paper_2310_04734_b200.build.build_library()`
+(nvcc, sm_100a).  There is no CPU fallback: if the library is missing or a
+call fails, a RuntimeError is raised (the reference CLI maps RuntimeError to
+exit code 3, vibrofem/cli.py:465-474).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import torch
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "libvibro_b200.so"
+
+_z = C.c_void_p  # vb_complex* (device)
+_SIGS = {
+    "vb_version": (C.c_char_p, []),
+    "vb_last_error": (C.c_char_p, []),
+    "vb_launch_count": (C.c_int64, []),
+    "vb_rom_sweep_path": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "vb_rom_sweep_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64]),
+    "vb_rom_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _z, _z, _z, C.c_int64,
+                               _z, _z, C.c_void_p, _z, C.c_void_p, C.c_void_p, C.c_size_t,
+                               C.c_void_p]),
+}
+
+_lib = None
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def load():
+    """Load (once) and return the ctypes handle; raises if the build is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"vibro_b200 native library not built: {LIB_PATH} missing "
+                           "(run __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().vb_last_error().decode()
+        raise RuntimeError(f"{what} failed (rc={rc}): {msg}")
+
+
+def ptr(t) -> C.c_void_p | None:
+    """Device pointer of a CUDA tensor (None for None)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise RuntimeError("vibro_b200: expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise RuntimeError("vibro_b200: expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def stream_handle(stream=None) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def launch_count() -> int:
+    return int(load().vb_launch_count())
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("vibro_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+    if os.environ.get("VB_ALLOW_NON_SM100") != "1":
+        major, minor = torch.cuda.get_device_capability()
+        if (major, minor) != (10, 0):
+            raise RuntimeError(f"vibro_b200 is built for sm_100a; found sm_{major}{minor}")

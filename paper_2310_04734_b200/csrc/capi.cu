@@ -1,0 +1,64 @@
+// extern "C" entry points of libvibro_b200.so (declared in include/vibro_b200.h).
+#include <atomic>
+#include <string>
+
+#include "../../include/vibro_b200.h"
+#include "common.cuh"
+#include "sweep.cuh"
+
+namespace vb {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int check_cuda(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return 0;
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return 2;
+}
+
+int check_launch(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return check_cuda(e, where);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return 0;
+}
+
+void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+}  // namespace vb
+
+using vb::z_t;
+
+extern "C" {
+
+const char* vb_version(void) { return "vibro_b200 0.1.0 sm_100a"; }
+
+const char* vb_last_error(void) { return vb::g_last_error.c_str(); }
+
+int64_t vb_launch_count(void) { return vb::g_launches.load(); }
+
+int vb_rom_sweep_path(int r, int nprim, int s, int n_out) { return vb::sweep_path(r, nprim, s, n_out); }
+
+size_t vb_rom_sweep_workspace_bytes(int r, int nprim, int s, int n_out, int64_t F) {
+  return vb::sweep_workspace_bytes(r, nprim, s, n_out, F);
+}
+
+int vb_rom_sweep(int r, int nprim, int s, int n_out, int64_t F, const vb_complex* prims,
+                 const vb_complex* alpha, const vb_complex* b, int64_t b_stride_f,
+                 const vb_complex* c_r, vb_complex* y, double* spl, vb_complex* x, int32_t* info,
+                 void* work, size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(r >= 1 && nprim >= 1 && nprim <= 64 && s >= 1 && n_out >= 0 && F >= 0,
+               "vb_rom_sweep: bad sizes");
+  VB_CHECK_ARG(prims && alpha && b, "vb_rom_sweep: null input");
+  VB_CHECK_ARG(n_out == 0 || c_r, "vb_rom_sweep: c_r is NULL with n_out > 0");
+  VB_CHECK_ARG(b_stride_f == 0 || b_stride_f >= (int64_t)r * s, "vb_rom_sweep: bad b_stride_f");
+  if (F == 0) return 0;
+  return vb::sweep_run(r, nprim, s, n_out, F, (const z_t*)prims, (const z_t*)alpha, (const z_t*)b,
+                       b_stride_f, (const z_t*)c_r, (z_t*)y, spl, (z_t*)x, info, work, work_bytes,
+                       (cudaStream_t)stream);
+}
+
+}  // extern "C"

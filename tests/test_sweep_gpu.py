@@ -1,0 +1,114 @@
+"""GPU parity of the batched reduced sweep (vb_rom_sweep) against the oracle
+(oracle.mor.affine_sweep = mor.py:73-102 + solvers.py:334-338 with
+numpy.linalg.solve).  Tolerances (north_star): relative transfer-function
+error <= 1e-8 (mor.py:194-208 metric) and |dSPL| <= 0.01 dB."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import mor as omor
+
+TF_TOL = 1e-8
+SPL_TOL = 0.01
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cuda, prims, alpha, b, c_r, want_x=False):
+    import torch
+    from paper_2310_04734_b200 import sweep
+    P = sweep.as_ctensor(prims, cuda)
+    A = sweep.as_ctensor(alpha, cuda)
+    B = sweep.as_ctensor(b, cuda)
+    Cr = sweep.as_ctensor(c_r, cuda)
+    out = sweep.rom_sweep_affine(P, A, B, Cr, want_x=want_x)
+    torch.cuda.synchronize()
+    return out
+
+
+def _check(y_gpu, spl_gpu, y_ref, spl_ref):
+    F = y_ref.shape[0]
+    worst = 0.0
+    for i in range(F):
+        _, e, _, _ = omor.relative_error(y_ref[i].ravel(), y_gpu[i].ravel())
+        worst = max(worst, e)
+    assert worst <= TF_TOL, worst
+    assert np.abs(spl_gpu - spl_ref).max() <= SPL_TOL
+    return worst
+
+
+@pytest.mark.parametrize("r,s,n_out,K", [(32, 1, 50, 3), (8, 3, 5, 2), (60, 4, 50, 3), (76, 1, 1, 4),
+                                          (96, 16, 50, 3), (1, 1, 1, 1)])
+def test_small_path_matches_oracle(cuda, r, s, n_out, K):
+    from paper_2310_04734_b200 import _lib
+    assert _lib.load().vb_rom_sweep_path(r, K, s, n_out) == 0
+    rng = np.random.default_rng(r * 100 + s)
+    F = 37
+    prims = rng.standard_normal((K, r, r)) + 1j * rng.standard_normal((K, r, r))
+    prims[0] += 4 * np.sqrt(r) * np.eye(r)
+    alpha = rng.standard_normal((F, K)) + 1j * rng.standard_normal((F, K))
+    alpha[:, 0] = 1.0
+    b = rng.standard_normal((r, s)) + 1j * rng.standard_normal((r, s))
+    c_r = rng.standard_normal((n_out, r)) + 1j * rng.standard_normal((n_out, r))
+    y_ref, spl_ref = omor.affine_sweep(prims, alpha, b, c_r)
+    out = _run(cuda, prims, alpha, b, c_r, want_x=True)
+    assert int(out.info.abs().sum()) == 0
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+    x_ref = np.stack([np.linalg.solve(np.tensordot(alpha[i], prims, 1), b) for i in range(F)])
+    assert np.abs(out.x.cpu().numpy() - x_ref).max() <= 1e-9 * np.abs(x_ref).max()
+
+
+def test_frequency_dependent_rhs(cuda):
+    rng = np.random.default_rng(3)
+    r, s, F, K = 20, 2, 11, 3
+    prims = rng.standard_normal((K, r, r)) + 1j * rng.standard_normal((K, r, r))
+    alpha = rng.standard_normal((F, K)) + 1j * rng.standard_normal((F, K))
+    b = rng.standard_normal((F, r, s)) + 1j * rng.standard_normal((F, r, s))
+    c_r = rng.standard_normal((7, r)) + 0j
+    y_ref, spl_ref = omor.affine_sweep(prims, alpha, b, c_r)
+    out = _run(cuda, prims, alpha, b, c_r)
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+
+
+def test_pivoting_required(cuda):
+    """Zero leading diagonal: fails without row interchanges (zgesv pivots)."""
+    r = 12
+    P = np.zeros((1, r, r), complex)
+    for i in range(r):
+        P[0, i, (i + 1) % r] = 1.0 + 0.5j * i
+    alpha = np.ones((2, 1), complex)
+    b = np.arange(1, r + 1, dtype=complex)[:, None]
+    c_r = np.eye(r, dtype=complex)
+    y_ref, spl_ref = omor.affine_sweep(P, alpha, b, c_r)
+    out = _run(cuda, P, alpha, b, c_r)
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+
+
+def test_singular_reports_info(cuda):
+    """numpy.linalg.solve raises LinAlgError on an exactly singular matrix (mor.py:94)."""
+    from paper_2310_04734_b200 import sweep
+    r = 6
+    P = np.zeros((1, r, r), complex)
+    P[0, :5, :5] = np.eye(5)
+    alpha = np.ones((3, 1), complex)
+    b = np.ones((r, 1), complex)
+    c_r = np.ones((1, r), complex)
+    with pytest.raises(np.linalg.LinAlgError):
+        np.linalg.solve(P[0], b)
+    out = _run(cuda, P, alpha, b, c_r)
+    assert out.info.cpu().tolist() == [6, 6, 6]
+    with pytest.raises(np.linalg.LinAlgError):
+        sweep.raise_if_singular(out.info)
+
+
+def test_cfg5_r256_sample(cuda):
+    from paper_2310_04734_b200 import workloads
+    w = workloads.cfg5(r=256, n_freq=100_000)
+    idx = np.linspace(0, 99_999, 24).astype(int)
+    f = w.freqs[idx]
+    alpha = w.alpha(f)
+    y_ref, spl_ref = omor.affine_sweep(w.prims, alpha, w.b, w.c_r)
+    out = _run(cuda, w.prims, alpha, w.b, w.c_r)
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
