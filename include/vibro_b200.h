@@ -74,6 +74,11 @@ int vb_rom_sweep(int r, int nprim, int s, int n_out, int64_t F, const vb_complex
  * resident (one CTA per frequency), 1 = blocked (global-memory batched LU). */
 int vb_rom_sweep_path(int r, int nprim, int s, int n_out);
 
+/* Testing hook: force the sweep algorithm (0 shared-memory, 1 blocked) for
+ * every later call in this process; -1 restores the automatic choice.  A
+ * forced shared-memory path still fails with rc=3 when it does not fit. */
+void vb_set_sweep_path_override(int path);
+
 /* Number of this library's kernel launches since load (process-wide counter,
  * incremented on every successful launch). */
 int64_t vb_launch_count(void);

@@ -23,6 +23,7 @@ _SIGS = {
     "vb_last_error": (C.c_char_p, []),
     "vb_launch_count": (C.c_int64, []),
     "vb_rom_sweep_path": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "vb_set_sweep_path_override": (None, [C.c_int]),
     "vb_rom_sweep_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64]),
     "vb_rom_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _z, _z, _z, C.c_int64,
                                _z, _z, C.c_void_p, _z, C.c_void_p, C.c_void_p, C.c_size_t,

@@ -42,6 +42,8 @@ int64_t vb_launch_count(void) { return vb::g_launches.load(); }
 
 int vb_rom_sweep_path(int r, int nprim, int s, int n_out) { return vb::sweep_path(r, nprim, s, n_out); }
 
+void vb_set_sweep_path_override(int path) { vb::sweep_set_override(path); }
+
 size_t vb_rom_sweep_workspace_bytes(int r, int nprim, int s, int n_out, int64_t F) {
   return vb::sweep_workspace_bytes(r, nprim, s, n_out, F);
 }

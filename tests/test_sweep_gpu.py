@@ -112,3 +112,47 @@ def test_cfg5_r256_sample(cuda):
     y_ref, spl_ref = omor.affine_sweep(w.prims, alpha, w.b, w.c_r)
     out = _run(cuda, w.prims, alpha, w.b, w.c_r)
     _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+
+
+@pytest.fixture
+def force_blocked(cuda):
+    from paper_2310_04734_b200 import _lib
+    _lib.load().vb_set_sweep_path_override(1)
+    yield
+    _lib.load().vb_set_sweep_path_override(-1)
+
+
+@pytest.mark.parametrize("r,s,n_out,K", [(1, 1, 1, 1), (5, 2, 3, 2), (33, 1, 50, 3), (64, 16, 50, 3),
+                                          (65, 3, 7, 3), (100, 1, 50, 3), (130, 16, 50, 4),
+                                          (200, 5, 20, 3)])
+def test_blocked_path_matches_oracle(cuda, force_blocked, r, s, n_out, K):
+    rng = np.random.default_rng(7 * r + s)
+    F = 19
+    prims = rng.standard_normal((K, r, r)) + 1j * rng.standard_normal((K, r, r))
+    alpha = rng.standard_normal((F, K)) + 1j * rng.standard_normal((F, K))
+    b = rng.standard_normal((r, s)) + 1j * rng.standard_normal((r, s))
+    c_r = rng.standard_normal((n_out, r)) + 1j * rng.standard_normal((n_out, r))
+    y_ref, spl_ref = omor.affine_sweep(prims, alpha, b, c_r)
+    out = _run(cuda, prims, alpha, b, c_r, want_x=True)
+    assert int(out.info.abs().sum()) == 0
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+    x_ref = np.stack([np.linalg.solve(np.tensordot(alpha[i], prims, 1), b) for i in range(F)])
+    rel = np.abs(out.x.cpu().numpy() - x_ref).max() / np.abs(x_ref).max()
+    assert rel <= 1e-9, rel
+
+
+def test_blocked_pivoting_and_singular(cuda, force_blocked):
+    r = 70
+    P = np.zeros((1, r, r), complex)
+    for i in range(r):
+        P[0, i, (i + 3) % r] = 1.0 + 0.5j * i
+    alpha = np.ones((2, 1), complex)
+    b = np.arange(1, r + 1, dtype=complex)[:, None]
+    c_r = np.eye(r, dtype=complex)
+    y_ref, spl_ref = omor.affine_sweep(P, alpha, b, c_r)
+    out = _run(cuda, P, alpha, b, c_r)
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+    P2 = np.zeros((1, r, r), complex)
+    P2[0, :r - 1, :r - 1] = np.eye(r - 1)
+    out = _run(cuda, P2, alpha, b, c_r)
+    assert out.info.cpu().tolist() == [r, r]
