@@ -79,6 +79,11 @@ int vb_rom_sweep_path(int r, int nprim, int s, int n_out);
  * forced shared-memory path still fails with rc=3 when it does not fit. */
 void vb_set_sweep_path_override(int path);
 
+/* Measured FP64 tensor-pipe (DMMA, mma.sync.m8n8k4.f64) throughput of this
+ * device in TFLOP/s, written to *tflops_host; synchronous (~10 ms).  Used as
+ * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */
+int vb_probe_fp64_peak(double* tflops_host, void* stream);
+
 /* Number of this library's kernel launches since load (process-wide counter,
  * incremented on every successful launch). */
 int64_t vb_launch_count(void);

@@ -24,6 +24,7 @@ _SIGS = {
     "vb_launch_count": (C.c_int64, []),
     "vb_rom_sweep_path": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "vb_set_sweep_path_override": (None, [C.c_int]),
+    "vb_probe_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.c_void_p]),
     "vb_rom_sweep_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64]),
     "vb_rom_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _z, _z, _z, C.c_int64,
                                _z, _z, C.c_void_p, _z, C.c_void_p, C.c_void_p, C.c_size_t,
@@ -87,3 +88,9 @@ def require_cuda():
         major, minor = torch.cuda.get_device_capability()
         if (major, minor) != (10, 0):
             raise RuntimeError(f"vibro_b200 is built for sm_100a; found sm_{major}{minor}")
+
+
+def probe_fp64_peak() -> float:
+    v = C.c_double(0.0)
+    check(load().vb_probe_fp64_peak(C.byref(v), stream_handle()), "vb_probe_fp64_peak")
+    return float(v.value)

@@ -44,6 +44,11 @@ int vb_rom_sweep_path(int r, int nprim, int s, int n_out) { return vb::sweep_pat
 
 void vb_set_sweep_path_override(int path) { vb::sweep_set_override(path); }
 
+int vb_probe_fp64_peak(double* tflops_host, void* stream) {
+  VB_CHECK_ARG(tflops_host != nullptr, "vb_probe_fp64_peak: null output");
+  return vb::probe_fp64_peak(tflops_host, (cudaStream_t)stream);
+}
+
 size_t vb_rom_sweep_workspace_bytes(int r, int nprim, int s, int n_out, int64_t F) {
   return vb::sweep_workspace_bytes(r, nprim, s, n_out, F);
 }

@@ -107,3 +107,61 @@ def raise_if_singular(info: torch.Tensor):
         i = int(bad[0])
         raise np.linalg.LinAlgError(f"Singular matrix (frequency index {i}, zero pivot "
                                     f"{int(info[i])})")
+
+
+class ReducedSweep:
+    """Affine reduced operator on the device and its batched frequency sweep.
+
+    A_r(f) = sum_k alpha_k(f) P_k with alpha from `kinds` (K -> 1, D -> i w,
+    M -> -w^2, mor.py:79-85) or an explicit `coeff_fn(freqs) -> (F, n_prim)`;
+    b_r (r, s) and c_r (n_out, r) as in ReducedModel.reduced_system / output.
+    Host numpy inputs are copied to the device once here (pinned staging).
+    """
+
+    def __init__(self, prims, b_r, c_r, kinds=None, coeff_fn=None, device=None, stream=None):
+        _lib.require_cuda()
+        self.device = torch.device(device or "cuda")
+        self.stream = stream
+        self.P = _to_dev(prims, self.device)
+        self.b = _to_dev(b_r if np.ndim(b_r) != 1 else np.asarray(b_r)[:, None], self.device)
+        self.c = _to_dev(np.atleast_2d(c_r) if not isinstance(c_r, torch.Tensor) else c_r, self.device)
+        if (kinds is None) == (coeff_fn is None):
+            raise ValueError("give exactly one of kinds / coeff_fn")
+        self.kinds = tuple(kinds) if kinds is not None else None
+        self.coeff_fn = coeff_fn
+
+    @property
+    def r(self):
+        return self.P.shape[1]
+
+    def alpha(self, freqs: torch.Tensor) -> torch.Tensor:
+        if self.coeff_fn is not None:
+            return _to_dev(self.coeff_fn(freqs), self.device)
+        return affine_coefficients(freqs, [(k, 1.0) for k in self.kinds])
+
+    def sweep_device(self, freqs: torch.Tensor, want_y=True, want_spl=True, want_x=False) -> SweepOut:
+        f = freqs.to(self.device, torch.float64)
+        return rom_sweep_affine(self.P, self.alpha(f), self.b, self.c, want_y=want_y,
+                                want_spl=want_spl, want_x=want_x, stream=self.stream)
+
+    def sweep(self, freqs, check_singular=True):
+        """Host in, host out: (y (F, n_out, s), spl (F, s)) numpy arrays."""
+        f = torch.as_tensor(np.asarray(freqs, dtype=np.float64)).pin_memory().to(self.device, non_blocking=True)
+        out = self.sweep_device(f)
+        y = torch.empty(out.y.shape, dtype=out.y.dtype, pin_memory=True)
+        spl = torch.empty(out.spl.shape, dtype=out.spl.dtype, pin_memory=True)
+        y.copy_(out.y, non_blocking=True)
+        spl.copy_(out.spl, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        if check_singular:
+            raise_if_singular(out.info)
+        return y.numpy(), spl.numpy()
+
+
+def _to_dev(a, device) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        if a.device.type == "cpu" and not a.is_pinned():
+            a = a.pin_memory()
+        return a.to(device=device, dtype=CDT, non_blocking=True).contiguous()
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128)).pin_memory()
+    return t.to(device, non_blocking=True)
