@@ -247,6 +247,21 @@ def kron_box(box, nx, ny, nz):
     return Kg.tocsr(), Mn.tocsr()
 
 
+def kron_pattern(nx, ny, nz):
+    """Structural hex27 box pattern as a Kronecker product of 1D element-block
+    patterns (independent of values): canonical CSR of ones."""
+    def p1(ne):
+        n = 2 * ne + 1
+        P = np.zeros((n, n))
+        for e in range(ne):
+            P[2 * e:2 * e + 3, 2 * e:2 * e + 3] = 1.0
+        return sp.csr_matrix(P)
+    K = sp.kron(sp.kron(p1(nz), p1(ny), format="csr"), p1(nx), format="csr")
+    K.sum_duplicates()
+    K.sort_indices()
+    return K
+
+
 def hex27_pattern_counts(nx, ny, nz):
     """n and structural nnz of a structured hex27 box (SURVEY §8 shared numbers)."""
     return (2 * nx + 1) * (2 * ny + 1) * (2 * nz + 1), (8 * nx + 1) * (8 * ny + 1) * (8 * nz + 1)
