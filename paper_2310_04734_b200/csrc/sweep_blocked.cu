@@ -87,87 +87,119 @@ __device__ __forceinline__ void warp_cmma(double (&cr)[FM][FN][2], double (&ci)[
 }
 
 // CTA-wide C[M x N] -= A[M x K] * B[K x N] on global (workspace) operands.
-// Tiles TM x TN over WM x WN warps; operands streamed through shared memory in
-// KC-deep chunks with a two-stage cp.async pipeline.
-template <int TM, int TN, int WM, int WN>
+// Tiles TM x TN over WM x WN warps.  One flat software pipeline runs over all
+// (tile, k-chunk) iterations: A/B chunks stream through a STAGES-deep
+// cp.async ring, and the C tile of the next output tile is prefetched into
+// shared memory while the current tile computes, so neither the operand nor
+// the C-tile latency is exposed at tile boundaries.  Accumulation starts from
+// zero; the epilogue writes C_old - A*B.
+template <int TM, int TN, int WM, int WN, int STAGES = 3>
 struct Gemm {
   static_assert(WM * WN == NT / 32, "warp grid");
   static constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
   static constexpr int LDA = KC + 4;  // == 4 (mod 8): conflict-free 128-bit fragment loads
   static constexpr int LDB = TN + 2;  // == 2 (mod 8)
-  static constexpr int A_EL = TM * LDA, B_EL = KC * LDB;
-  static constexpr size_t SMEM = 2 * (size_t)(A_EL + B_EL) * sizeof(z_t);
+  static constexpr int LDC = TN + 1;  // == 1 (mod 8): conflict-free epilogue reads
+  static constexpr int A_EL = TM * LDA, B_EL = KC * LDB, C_EL = TM * LDC;
+  static constexpr size_t SMEM = (size_t)(STAGES * (A_EL + B_EL) + C_EL) * sizeof(z_t);
 
   __device__ static void load_chunk(z_t* As, z_t* Bs, const z_t* A, int lda, const z_t* B, int ldb,
                                     int M, int N, int K, int m0, int n0, int k0) {
     const int tid = threadIdx.x;
-    for (int e = tid; e < TM * KC; e += NT) {
-      int i = e / KC, k = e - i * KC;
-      bool p = (m0 + i < M) && (k0 + k < K);
-      const z_t* src = p ? A + (size_t)(m0 + i) * lda + k0 + k : A;
-      cp_async16(As + i * LDA + k, src, p);
+#pragma unroll
+    for (int q = 0; q < (TM * KC + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      if ((TM * KC) % NT == 0 || e < TM * KC) {
+        const int i = e / KC, k = e % KC;
+        const bool p = (m0 + i < M) && (k0 + k < K);
+        cp_async16(As + i * LDA + k, p ? A + (size_t)(m0 + i) * lda + k0 + k : A, p);
+      }
     }
-    for (int e = tid; e < KC * TN; e += NT) {
-      int k = e / TN, j = e - k * TN;
-      bool p = (k0 + k < K) && (n0 + j < N);
-      const z_t* src = p ? B + (size_t)(k0 + k) * ldb + n0 + j : B;
-      cp_async16(Bs + k * LDB + j, src, p);
+#pragma unroll
+    for (int q = 0; q < (KC * TN + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      if ((KC * TN) % NT == 0 || e < KC * TN) {
+        const int k = e / TN, j = e % TN;
+        const bool p = (k0 + k < K) && (n0 + j < N);
+        cp_async16(Bs + k * LDB + j, p ? B + (size_t)(k0 + k) * ldb + n0 + j : B, p);
+      }
     }
-    cp_commit();
+  }
+
+  __device__ static void load_c(z_t* Cs, const z_t* C, int ldc, int M, int N, int m0, int n0) {
+    const int tid = threadIdx.x;
+#pragma unroll 4
+    for (int e = tid; e < TM * TN; e += NT) {
+      const int i = e / TN, j = e % TN;
+      const bool p = (m0 + i < M) && (n0 + j < N);
+      cp_async16(Cs + i * LDC + j, p ? C + (size_t)(m0 + i) * ldc + n0 + j : C, p);
+    }
   }
 
   __device__ static void run(z_t* C, int ldc, const z_t* A, int lda, const z_t* B, int ldb, int M,
                              int N, int K, z_t* smem) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     z_t* As = smem;
-    z_t* Bs = smem + 2 * A_EL;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    z_t* Bs = smem + STAGES * A_EL;
+    z_t* Cs = Bs + STAGES * B_EL;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp / WN, wn = warp % WN;
-    const int ntm = (M + TM - 1) / TM, ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
-    for (int t = 0; t < ntm * ntn; ++t) {
-      const int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
-      load_chunk(As, Bs, A, lda, B, ldb, M, N, K, m0, n0, 0);
-      double cr[FM][FN][2], ci[FM][FN][2];
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            int row = m0 + wm * FM * 8 + i * 8 + (lane >> 2);
-            int col = n0 + wn * FN * 8 + j * 8 + 2 * (lane & 3) + v;
-            z_t c = zmake(0.0, 0.0);
-            if (row < M && col < N) c = C[(size_t)row * ldc + col];
-            cr[i][j][v] = c.x;
-            ci[i][j][v] = c.y;
-          }
-      for (int kc = 0; kc < nk; ++kc) {
-        if (kc + 1 < nk) {
-          load_chunk(As + ((kc + 1) & 1) * A_EL, Bs + ((kc + 1) & 1) * B_EL, A, lda, B, ldb, M, N,
-                     K, m0, n0, (kc + 1) * KC);
-          cp_wait<1>();
-        } else {
-          cp_wait<0>();
-        }
-        __syncthreads();
-        const z_t* as = As + (kc & 1) * A_EL + (wm * FM * 8) * LDA;
-        const z_t* bs = Bs + (kc & 1) * B_EL + wn * FN * 8;
-        int k4 = min(KC, K - kc * KC);
-        k4 = (k4 + 3) >> 2;
-        warp_cmma<FM, FN, true>(cr, ci, as, LDA, bs, LDB, k4);
-        __syncthreads();
+    const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
+    const int T = ((M + TM - 1) / TM) * ntn * nk;
+    auto issue = [&](int j) {
+      if (j < T) {
+        const int t = j / nk, kc = j - t * nk;
+        load_chunk(As + (j % STAGES) * A_EL, Bs + (j % STAGES) * B_EL, A, lda, B, ldb, M, N, K,
+                   (t / ntn) * TM, (t % ntn) * TN, kc * KC);
       }
+    };
+    load_c(Cs, C, ldc, M, N, 0, 0);
 #pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            int row = m0 + wm * FM * 8 + i * 8 + (lane >> 2);
-            int col = n0 + wn * FN * 8 + j * 8 + 2 * (lane & 3) + v;
-            if (row < M && col < N) C[(size_t)row * ldc + col] = zmake(cr[i][j][v], ci[i][j][v]);
-          }
+    for (int j = 0; j < STAGES - 1; ++j) {
+      issue(j);
+      cp_commit();
     }
+    double cr[FM][FN][2], ci[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int it = 0; it < T; ++it) {
+      const int t = it / nk, kc = it - t * nk;
+      cp_wait<STAGES - 2>();
+      __syncthreads();
+      issue(it + STAGES - 1);
+      if (kc == 0 && it > 0) load_c(Cs, C, ldc, M, N, (t / ntn) * TM, (t % ntn) * TN);
+      cp_commit();
+      const int st = it % STAGES;
+      int k4 = min(KC, K - kc * KC);
+      k4 = (k4 + 3) >> 2;
+      warp_cmma<FM, FN, false>(cr, ci, As + st * A_EL + (wm * FM * 8) * LDA, LDA,
+                               Bs + st * B_EL + wn * FN * 8, LDB, k4);
+      if (kc == nk - 1) {
+        if (nk < STAGES) {  // the C-tile group may still be in flight
+          cp_wait<0>();
+          __syncthreads();
+        }
+        const int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int lr = wm * FM * 8 + i * 8 + (lane >> 2);
+              const int lc = wn * FN * 8 + j * 8 + 2 * (lane & 3) + v;
+              if (m0 + lr < M && n0 + lc < N) {
+                const z_t c = Cs[lr * LDC + lc];
+                C[(size_t)(m0 + lr) * ldc + n0 + lc] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+              }
+              cr[i][j][v] = 0.0;
+              ci[i][j][v] = 0.0;
+            }
+      }
+    }
+    cp_wait<0>();
   }
 };
 
@@ -408,6 +440,52 @@ __device__ void diag_backsolve(z_t* A, int ldw, int r, int s, int kb, int nb, z_
   __syncthreads();
 }
 
+// A = sum_k alpha_k P_k into the workspace.  Bandwidth-bound: each thread keeps
+// KP x 4 independent 16-byte loads in flight (prims are shared by all CTAs and
+// mostly L2-resident).
+template <int KP>
+__device__ __forceinline__ void form_quads(const Params& P, z_t* A, const z_t* alph) {
+  const int r = P.r, ldw = P.ldw;
+  const int64_t rr = (int64_t)r * r, nq = rr >> 2;
+  z_t a[KP];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) a[k] = alph[k];
+  for (int64_t q = threadIdx.x; q < nq; q += NT) {
+    z_t v[KP][4];
+#pragma unroll
+    for (int k = 0; k < KP; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[k][e] = __ldg(P.prims + k * rr + 4 * q + e);
+    const int64_t i = (4 * q) / r, j = 4 * q - i * r;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      z_t acc = zmul(a[0], v[0][e]);
+#pragma unroll
+      for (int k = 1; k < KP; ++k) acc = zfma(acc, a[k], v[k][e]);
+      A[i * ldw + j + e] = acc;
+    }
+  }
+}
+
+__device__ void form_matrix(const Params& P, z_t* A, const z_t* alph) {
+  const int r = P.r, ldw = P.ldw;
+  if ((r & 3) == 0 && P.nprim <= 4) {
+    switch (P.nprim) {
+      case 1: form_quads<1>(P, A, alph); return;
+      case 2: form_quads<2>(P, A, alph); return;
+      case 3: form_quads<3>(P, A, alph); return;
+      default: form_quads<4>(P, A, alph); return;
+    }
+  }
+  const int64_t rr = (int64_t)r * r;
+  for (int64_t idx = threadIdx.x; idx < rr; idx += NT) {
+    z_t acc = zmake(0.0, 0.0);
+    for (int k = 0; k < P.nprim; ++k) acc = zfma(acc, alph[k], __ldg(P.prims + k * rr + idx));
+    const int64_t i = idx / r, j = idx - i * r;
+    A[i * ldw + j] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
   extern __shared__ double2 smem[];
   __shared__ int piv[NB];
@@ -426,12 +504,7 @@ __global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
     if (tid == 0) s_info = 0;
     __syncthreads();
     // ---- form [A | B] ----
-    for (int64_t idx = tid; idx < rr; idx += NT) {
-      z_t acc = zmake(0.0, 0.0);
-      for (int k = 0; k < P.nprim; ++k) acc = zfma(acc, alph[k], __ldg(P.prims + k * rr + idx));
-      int64_t i = idx / r, j = idx - i * r;
-      A[i * ldw + j] = acc;
-    }
+    form_matrix(P, A, alph);
     const z_t* bf = P.b + f * P.b_stride_f;
     for (int idx = tid; idx < r * s; idx += NT) {
       int i = idx / s, c = idx - i * s;
