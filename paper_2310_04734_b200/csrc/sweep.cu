@@ -16,7 +16,7 @@ int sweep_path(int r, int nprim, int s, int n_out) {
 
 size_t sweep_workspace_bytes(int r, int nprim, int s, int n_out, int64_t F) {
   if (sweep_path(r, nprim, s, n_out) == 0) return 0;
-  return sweep_blocked_workspace_bytes(r, s, F);
+  return sweep_blocked_workspace_bytes(r, s, n_out, F);
 }
 
 int sweep_run(int r, int nprim, int s, int n_out, int64_t F, const z_t* prims, const z_t* alpha,

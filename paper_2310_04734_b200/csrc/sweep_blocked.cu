@@ -92,8 +92,8 @@ __device__ __forceinline__ void warp_cmma(double (&cr)[FM][FN][2], double (&ci)[
 // cp.async ring, and the C tile of the next output tile is prefetched into
 // shared memory while the current tile computes, so neither the operand nor
 // the C-tile latency is exposed at tile boundaries.  Accumulation starts from
-// zero; the epilogue writes C_old - A*B.
-template <int TM, int TN, int WM, int WN, int STAGES = 3>
+// zero; the epilogue writes C_old - A*B (SUB) or A*B (!SUB, C not read).
+template <int TM, int TN, int WM, int WN, int STAGES, bool SUB>
 struct Gemm {
   static_assert(WM * WN == NT / 32, "warp grid");
   static constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
@@ -101,7 +101,7 @@ struct Gemm {
   static constexpr int LDB = TN + 2;  // == 2 (mod 8)
   static constexpr int LDC = TN + 1;  // == 1 (mod 8): conflict-free epilogue reads
   static constexpr int A_EL = TM * LDA, B_EL = KC * LDB, C_EL = TM * LDC;
-  static constexpr size_t SMEM = (size_t)(STAGES * (A_EL + B_EL) + C_EL) * sizeof(z_t);
+  static constexpr size_t SMEM = (size_t)(STAGES * (A_EL + B_EL) + (SUB ? C_EL : 0)) * sizeof(z_t);
 
   __device__ static void load_chunk(z_t* As, z_t* Bs, const z_t* A, int lda, const z_t* B, int ldb,
                                     int M, int N, int K, int m0, int n0, int k0) {
@@ -153,7 +153,7 @@ struct Gemm {
                    (t / ntn) * TM, (t % ntn) * TN, kc * KC);
       }
     };
-    load_c(Cs, C, ldc, M, N, 0, 0);
+    if (SUB) load_c(Cs, C, ldc, M, N, 0, 0);
 #pragma unroll
     for (int j = 0; j < STAGES - 1; ++j) {
       issue(j);
@@ -169,7 +169,7 @@ struct Gemm {
       cp_wait<STAGES - 2>();
       __syncthreads();
       issue(it + STAGES - 1);
-      if (kc == 0 && it > 0) load_c(Cs, C, ldc, M, N, (t / ntn) * TM, (t % ntn) * TN);
+      if (SUB && kc == 0 && it > 0) load_c(Cs, C, ldc, M, N, (t / ntn) * TM, (t % ntn) * TN);
       cp_commit();
       const int st = it % STAGES;
       int k4 = min(KC, K - kc * KC);
@@ -177,7 +177,7 @@ struct Gemm {
       warp_cmma<FM, FN, false>(cr, ci, As + st * A_EL + (wm * FM * 8) * LDA, LDA,
                                Bs + st * B_EL + wn * FN * 8, LDB, k4);
       if (kc == nk - 1) {
-        if (nk < STAGES) {  // the C-tile group may still be in flight
+        if (SUB && nk < STAGES) {  // the C-tile group may still be in flight
           cp_wait<0>();
           __syncthreads();
         }
@@ -191,8 +191,12 @@ struct Gemm {
               const int lr = wm * FM * 8 + i * 8 + (lane >> 2);
               const int lc = wn * FN * 8 + j * 8 + 2 * (lane & 3) + v;
               if (m0 + lr < M && n0 + lc < N) {
-                const z_t c = Cs[lr * LDC + lc];
-                C[(size_t)(m0 + lr) * ldc + n0 + lc] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+                if (SUB) {
+                  const z_t c = Cs[lr * LDC + lc];
+                  C[(size_t)(m0 + lr) * ldc + n0 + lc] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+                } else {
+                  C[(size_t)(m0 + lr) * ldc + n0 + lc] = zmake(cr[i][j][v], ci[i][j][v]);
+                }
               }
               cr[i][j][v] = 0.0;
               ci[i][j][v] = 0.0;
@@ -203,13 +207,20 @@ struct Gemm {
   }
 };
 
-using GemmWide = Gemm<64, 64, 2, 4>;    // trailing updates
-using GemmNarrow = Gemm<128, 16, 8, 1>; // back-substitution updates (N = s <= 16)
 
-// Shared-memory layout of the TRSM stage: L11^-1 (NB x LDL) and a B strip.
-constexpr int LDL = NB + 4;
-constexpr int LDS_B = NB + 2;
+// Two CTAs per SM (<= 128 registers, <= ~110 KB shared memory each) so that one
+// frequency's latency-bound phases (panel, triangular inverses) overlap the
+// other's tensor-core GEMMs.
+using GemmWide = Gemm<64, 32, 4, 2, 2, true>;   // trailing / in-panel updates
+using GemmNarrow = Gemm<64, 16, 8, 1, 2, true>; // back-substitution updates (N = s <= 16)
+using GemmOut = Gemm<64, 16, 8, 1, 2, false>;   // y = C_R x
+
+constexpr int LDL = NB + 4;     // == 4 (mod 8): triangular inverse used as A operand
+constexpr int TRS_N = 32;       // U12 strip width
+constexpr int LDS_B = TRS_N + 2;
+constexpr int LDY = 16 + 2;
 constexpr size_t TRSM_SMEM = (size_t)(NB * LDL + NB * LDS_B) * sizeof(z_t);
+constexpr size_t BACK_SMEM = (size_t)(NB * LDL + NB * LDY) * sizeof(z_t);
 
 struct Params {
   int r, nprim, s, n_out;
@@ -224,8 +235,9 @@ struct Params {
   z_t* x;
   int* info;
   z_t* work;
-  int ldw;  // leading dimension of the augmented matrix
-  int w;    // inner panel width
+  int ldw;            // leading dimension of the augmented matrix
+  int w;              // inner panel width
+  size_t cta_stride;  // workspace elements per CTA
 };
 
 __device__ __forceinline__ void block_argmax(double& v, int& idx, double* rv, int* ri) {
@@ -240,25 +252,27 @@ __device__ __forceinline__ void block_argmax(double& v, int& idx, double* rv, in
   }
 }
 
-// Factor the inner panel rows [j0, r) x cols [j0, j0+wc) in shared memory.
+// Factor the inner panel rows [j0, r) x cols [j0, j0+wc) in shared memory
+// (unblocked zgetf2 order; the argmax for column jj+1 is fused into the
+// rank-1 update of column jj).
 __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* piv,
                             int* s_info, double* rv, int* ri, int* s_p, z_t* s_pv) {
   const int r = P.r, ldw = P.ldw, w = P.w;
   const int H = r - j0;
   const int tid = threadIdx.x;
   for (int e = tid; e < H * wc; e += NT) {
-    int i = e / wc, c = e - i * wc;
+    const int i = e / wc, c = e - i * wc;
     Ps[i * w + c] = A[(size_t)(j0 + i) * ldw + j0 + c];
   }
   __syncthreads();
+  double v = -1.0;
+  int pi = 0x7fffffff;
+  for (int i = tid; i < H; i += NT) {
+    const double a = zabs1(Ps[i * w]);
+    if (a > v) { v = a; pi = i; }
+  }
+  block_argmax(v, pi, rv, ri);
   for (int jj = 0; jj < wc; ++jj) {
-    double v = -1.0;
-    int pi = 0x7fffffff;
-    for (int i = jj + tid; i < H; i += NT) {
-      double a = zabs1(Ps[i * w + jj]);
-      if (a > v) { v = a; pi = i; }
-    }
-    block_argmax(v, pi, rv, ri);
     if (tid == 0) {
       if (v == 0.0) {
         if (*s_info == 0) *s_info = j0 + jj + 1;
@@ -271,36 +285,49 @@ __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t
     }
     __syncthreads();
     const int p = *s_p;
-    if (p < 0) continue;
-    const z_t pv = *s_pv;
-    const z_t pinv = zrecip(pv);
-    for (int i = jj + 1 + tid; i < H; i += NT) {
-      int src = (i == p) ? jj : i;
-      Ps[i * w + jj] = zmul(Ps[src * w + jj], pinv);
-    }
-    if (p != jj) {
-      // whole-row interchange within the inner panel (column jj is read through the swap above)
-      for (int c = tid; c < wc; c += NT) {
-        if (c == jj) continue;
-        z_t t = Ps[jj * w + c];
-        Ps[jj * w + c] = Ps[p * w + c];
-        Ps[p * w + c] = t;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) Ps[jj * w + jj] = pv;
     const int nc = wc - jj - 1;
-    if (nc > 0) {
-      for (int e = tid; e < (H - jj - 1) * nc; e += NT) {
-        int ii = e / nc;
-        int i = jj + 1 + ii, c = jj + 1 + (e - ii * nc);
-        Ps[i * w + c] = zfms(Ps[i * w + c], Ps[i * w + jj], Ps[jj * w + c]);
+    v = -1.0;
+    pi = 0x7fffffff;
+    if (p >= 0) {
+      const z_t pv = *s_pv;
+      const z_t pinv = zrecip(pv);
+      for (int i = jj + 1 + tid; i < H; i += NT) {
+        const int src = (i == p) ? jj : i;
+        Ps[i * w + jj] = zmul(Ps[src * w + jj], pinv);
+      }
+      if (p != jj) {
+        for (int c = tid; c < wc; c += NT) {
+          if (c == jj) continue;
+          const z_t t = Ps[jj * w + c];
+          Ps[jj * w + c] = Ps[p * w + c];
+          Ps[p * w + c] = t;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) Ps[jj * w + jj] = pv;
+      if (nc > 0) {
+        for (int e = tid; e < (H - jj - 1) * nc; e += NT) {
+          const int ii = e / nc, cc = e - ii * nc;
+          const int i = jj + 1 + ii, c = jj + 1 + cc;
+          const z_t nv = zfms(Ps[i * w + c], Ps[i * w + jj], Ps[jj * w + c]);
+          Ps[i * w + c] = nv;
+          if (cc == 0) {
+            const double a = zabs1(nv);
+            if (a > v || (a == v && i < pi)) { v = a; pi = i; }
+          }
+        }
+      }
+    } else if (nc > 0) {
+      for (int i = jj + 1 + tid; i < H; i += NT) {
+        const double a = zabs1(Ps[i * w + jj + 1]);
+        if (a > v) { v = a; pi = i; }
       }
     }
-    __syncthreads();
+    if (nc > 0) block_argmax(v, pi, rv, ri);
   }
+  __syncthreads();
   for (int e = tid; e < H * wc; e += NT) {
-    int i = e / wc, c = e - i * wc;
+    const int i = e / wc, c = e - i * wc;
     A[(size_t)(j0 + i) * ldw + j0 + c] = Ps[i * w + c];
   }
   __syncthreads();
@@ -311,9 +338,9 @@ __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t
 __device__ void apply_swaps(z_t* A, int ldw, const int* piv, int k0, int a, int b, int c0, int c1) {
   for (int c = c0 + threadIdx.x; c < c1; c += NT) {
     for (int i = a; i < b; ++i) {
-      int p = piv[i - k0];
+      const int p = piv[i - k0];
       if (p != i) {
-        z_t t = A[(size_t)i * ldw + c];
+        const z_t t = A[(size_t)i * ldw + c];
         A[(size_t)i * ldw + c] = A[(size_t)p * ldw + c];
         A[(size_t)p * ldw + c] = t;
       }
@@ -322,82 +349,169 @@ __device__ void apply_swaps(z_t* A, int ldw, const int* piv, int k0, int a, int 
 }
 
 // U = L^-1 U for the wc rows of an inner panel (unit lower L = Ps[0:wc, 0:wc]),
-// columns [c0, c1): one thread per column.
+// columns [c0, c1): one thread per column, forward substitution through L1
+// (each thread re-reads only values it wrote itself).
 __device__ void inner_trsm(z_t* A, int ldw, const z_t* Ps, int w, int j0, int wc, int c0, int c1) {
   for (int c = c0 + threadIdx.x; c < c1; c += NT) {
-    z_t xv[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < wc) xv[i] = A[(size_t)(j0 + i) * ldw + c];
-#pragma unroll
-    for (int i = 1; i < 16; ++i) {
-      if (i < wc) {
-        z_t acc = xv[i];
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (k < i) acc = zfms(acc, Ps[i * w + k], xv[k]);
-        xv[i] = acc;
-      }
+    z_t* col = A + (size_t)j0 * ldw + c;
+    for (int i = 1; i < wc; ++i) {
+      z_t acc = col[(size_t)i * ldw];
+      for (int k = 0; k < i; ++k) acc = zfms(acc, Ps[i * w + k], col[(size_t)k * ldw]);
+      col[(size_t)i * ldw] = acc;
     }
-#pragma unroll
-    for (int i = 1; i < 16; ++i)
-      if (i < wc) A[(size_t)(j0 + i) * ldw + c] = xv[i];
   }
 }
 
-// L11^-1 of the unit-lower nb x nb diagonal block at (k0, k0) into Li (NB x LDL,
-// zero padded), then U12 = L11^-1 A12 in place for columns [c0, c1).
+// In-place inverse of a 64 x 64 triangular matrix in shared memory by recursive
+// doubling: 8x8 diagonal blocks per warp, then three levels of
+// [A 0; C D]^-1 = [A^-1 0; -D^-1 C A^-1 D^-1]  (lower, unit diagonal) or
+// [A B; 0 D]^-1 = [A^-1 -A^-1 B D^-1; 0 D^-1]  (upper, general diagonal).
+// 13 barriers instead of one per row.
+template <bool LOWER>
+__device__ __noinline__ void tri_inv64(z_t* T, int ld) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const int o = warp * 8, j = lane;
+    z_t x[8];
+    if (lane < 8) {
+      if (LOWER) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = zmake(i == j ? 1.0 : 0.0, 0.0);
+#pragma unroll
+        for (int i = 1; i < 8; ++i) {
+          if (i > j) {
+            z_t acc = zmake(0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k >= j && k < i) acc = zfma(acc, T[(o + i) * ld + o + k], x[k]);
+            x[i] = zmake(-acc.x, -acc.y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = zmake(0.0, 0.0);
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          if (i <= j) {
+            z_t acc = zmake(i == j ? 1.0 : 0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k > i && k <= j) acc = zfms(acc, T[(o + i) * ld + o + k], x[k]);
+            x[i] = zmul(acc, zrecip(T[(o + i) * ld + o + i]));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane < 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (LOWER ? (i > j) : (i <= j)) T[(o + i) * ld + o + j] = x[i];
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int h = 8; h < 64; h *= 2) {
+    const int hh = h * h, nel = (64 / (2 * h)) * hh;  // = 32 h <= 1024
+    z_t tv[4];
+    // step 1: T = C A^-1 (lower) or T = B D^-1 (upper), into the off-diagonal block
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        z_t acc = zmake(0.0, 0.0);
+        if (LOWER) {
+          for (int k = j; k < h; ++k) acc = zfma(acc, T[(o + h + i) * ld + o + k], T[(o + k) * ld + o + j]);
+        } else {
+          for (int k = 0; k <= j; ++k)
+            acc = zfma(acc, T[(o + i) * ld + o + h + k], T[(o + h + k) * ld + o + h + j]);
+        }
+        tv[q] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        if (LOWER) T[(o + h + i) * ld + o + j] = tv[q];
+        else T[(o + i) * ld + o + h + j] = tv[q];
+      }
+    }
+    __syncthreads();
+    // step 2: X = -D^-1 T (lower) or X = -A^-1 T (upper)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        z_t acc = zmake(0.0, 0.0);
+        if (LOWER) {
+          for (int k = 0; k <= i; ++k)
+            acc = zfma(acc, T[(o + h + i) * ld + o + h + k], T[(o + h + k) * ld + o + j]);
+        } else {
+          for (int k = i; k < h; ++k) acc = zfma(acc, T[(o + i) * ld + o + k], T[(o + k) * ld + o + h + j]);
+        }
+        tv[q] = zmake(-acc.x, -acc.y);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        if (LOWER) T[(o + h + i) * ld + o + j] = tv[q];
+        else T[(o + i) * ld + o + h + j] = tv[q];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// U12 = L11^-1 A12 in place for columns [c0, c1), L11^-1 formed explicitly
+// (identity-padded to 64) and applied with DMMA in 64 x 32 strips.
 __device__ void panel_trsm(z_t* A, int ldw, int k0, int nb, int c0, int c1, z_t* smem) {
   z_t* Li = smem;             // NB x LDL
   z_t* Bs = smem + NB * LDL;  // NB x LDS_B
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // L (strictly lower part) staged in Bs, Li = I
   for (int e = tid; e < NB * NB; e += NT) {
-    int i = e / NB, j = e - i * NB;
-    Li[i * LDL + j] = zmake(i == j && i < nb ? 1.0 : 0.0, 0.0);
-    Bs[i * LDS_B + j] = (i < nb && j < i) ? A[(size_t)(k0 + i) * ldw + k0 + j] : zmake(0.0, 0.0);
+    const int i = e / NB, j = e - i * NB;
+    z_t v = zmake(i == j ? 1.0 : 0.0, 0.0);
+    if (i < nb && j < i) v = A[(size_t)(k0 + i) * ldw + k0 + j];
+    Li[i * LDL + j] = v;
   }
   __syncthreads();
-  // row i of L^-1: Li[i, j] = -sum_{k=j}^{i-1} L[i,k] Li[k,j], 4 threads per j
-  {
-    const int j = tid >> 2, q = tid & 3;
-    for (int i = 1; i < nb; ++i) {
-      z_t acc = zmake(0.0, 0.0);
-      if (j < i)
-        for (int k = j + q; k < i; k += 4) acc = zfma(acc, Bs[i * LDS_B + k], Li[k * LDL + j]);
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
-      if (q == 0 && j < i) Li[i * LDL + j] = zmake(-acc.x, -acc.y);
-      __syncthreads();
-    }
-  }
-  // U12 strips of NB columns: C(nb x NB) = Li(nb x nb) * B(nb x NB)
-  constexpr int FM = 4, FN = 2;  // warp grid 2 x 4 over the 64 x 64 strip
-  const int wm = warp / 4, wn = warp % 4;
+  tri_inv64<true>(Li, LDL);
+  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps over the 64 x 32 strip
   const int k4 = (nb + 3) >> 2;
-  for (int cs = c0; cs < c1; cs += NB) {
-    const int ncol = min(NB, c1 - cs);
-    for (int e = tid; e < NB * NB; e += NT) {
-      int i = e / NB, j = e - i * NB;
+  for (int cs = c0; cs < c1; cs += TRS_N) {
+    const int ncol = min(TRS_N, c1 - cs);
+    for (int e = tid; e < NB * TRS_N; e += NT) {
+      const int i = e / TRS_N, j = e - i * TRS_N;
       Bs[i * LDS_B + j] = (i < nb && j < ncol) ? A[(size_t)(k0 + i) * ldw + cs + j] : zmake(0.0, 0.0);
     }
     __syncthreads();
-    double cr[FM][FN][2], ci[FM][FN][2];
+    double cr[2][2][2], ci[2][2][2];
 #pragma unroll
-    for (int i = 0; i < FM; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < FN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-    warp_cmma<FM, FN, false>(cr, ci, Li + (wm * 32) * LDL, LDL, Bs + wn * 16, LDS_B, k4);
+      for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    warp_cmma<2, 2, false>(cr, ci, Li + (wm * 16) * LDL, LDL, Bs + wn * 16, LDS_B, k4);
 #pragma unroll
-    for (int i = 0; i < FM; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < FN; ++j)
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          int row = wm * 32 + i * 8 + (lane >> 2);
-          int col = wn * 16 + j * 8 + 2 * (lane & 3) + v;
+          const int row = wm * 16 + i * 8 + (lane >> 2);
+          const int col = wn * 16 + j * 8 + 2 * (lane & 3) + v;
           if (row < nb && col < ncol)
             A[(size_t)(k0 + row) * ldw + cs + col] = zmake(cr[i][j][v], ci[i][j][v]);
         }
@@ -405,44 +519,41 @@ __device__ void panel_trsm(z_t* A, int ldw, int k0, int nb, int c0, int c1, z_t*
   }
 }
 
-// Solve U[kb:kb+nb, kb:kb+nb] X = Y in place on columns [r, r+s).
+// X = U_kk^-1 Y on the diagonal block rows [kb, kb+nb) of the RHS columns.
 __device__ void diag_backsolve(z_t* A, int ldw, int r, int s, int kb, int nb, z_t* smem) {
-  z_t* Us = smem;                 // NB x (NB+1)
-  z_t* Ys = smem + NB * (NB + 1); // NB x s
-  const int tid = threadIdx.x;
-  for (int e = tid; e < nb * nb; e += NT) {
-    int i = e / nb, j = e - i * nb;
-    Us[i * (NB + 1) + j] = A[(size_t)(kb + i) * ldw + kb + j];
+  z_t* Us = smem;              // NB x LDL
+  z_t* Ys = smem + NB * LDL;   // NB x LDY
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < NB * NB; e += NT) {
+    const int i = e / NB, j = e - i * NB;
+    z_t v = zmake(i == j ? 1.0 : 0.0, 0.0);
+    if (i < nb && j < nb) v = (j >= i) ? A[(size_t)(kb + i) * ldw + kb + j] : zmake(0.0, 0.0);
+    Us[i * LDL + j] = v;
   }
-  for (int e = tid; e < nb * s; e += NT) {
-    int i = e / s, c = e - i * s;
-    Ys[i * s + c] = A[(size_t)(kb + i) * ldw + r + c];
-  }
-  __syncthreads();
-  if (tid < s) {
-    int k = nb - 1;
-    Ys[k * s + tid] = zmul(Ys[k * s + tid], zrecip(Us[k * (NB + 1) + k]));
+  for (int e = tid; e < NB * 16; e += NT) {
+    const int i = e >> 4, c = e & 15;
+    Ys[i * LDY + c] = (i < nb && c < s) ? A[(size_t)(kb + i) * ldw + r + c] : zmake(0.0, 0.0);
   }
   __syncthreads();
-  for (int k = nb - 1; k > 0; --k) {
-    for (int e = tid; e < k * s; e += NT) {
-      int i = e / s, c = e - i * s;
-      z_t v = zfms(Ys[i * s + c], Us[i * (NB + 1) + k], Ys[k * s + c]);
-      if (i == k - 1) v = zmul(v, zrecip(Us[i * (NB + 1) + i]));
-      Ys[i * s + c] = v;
+  tri_inv64<false>(Us, LDL);
+  double cr[1][2][2], ci[1][2][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) cr[0][j][0] = cr[0][j][1] = ci[0][j][0] = ci[0][j][1] = 0.0;
+  warp_cmma<1, 2, false>(cr, ci, Us + (warp * 8) * LDL, LDL, Ys, LDY, (nb + 3) >> 2);
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int row = warp * 8 + (lane >> 2);
+      const int col = j * 8 + 2 * (lane & 3) + v;
+      if (row < nb && col < s) A[(size_t)(kb + row) * ldw + r + col] = zmake(cr[0][j][v], ci[0][j][v]);
     }
-    __syncthreads();
-  }
-  for (int e = tid; e < nb * s; e += NT) {
-    int i = e / s, c = e - i * s;
-    A[(size_t)(kb + i) * ldw + r + c] = Ys[i * s + c];
-  }
   __syncthreads();
 }
 
 // A = sum_k alpha_k P_k into the workspace.  Bandwidth-bound: each thread keeps
-// KP x 4 independent 16-byte loads in flight (prims are shared by all CTAs and
-// mostly L2-resident).
+// KP x 4 independent 16-byte loads in flight (the primitives are shared by all
+// CTAs and pinned in L2 when they fit, see sweep_blocked_launch).
 template <int KP>
 __device__ __forceinline__ void form_quads(const Params& P, z_t* A, const z_t* alph) {
   const int r = P.r, ldw = P.ldw;
@@ -486,7 +597,7 @@ __device__ void form_matrix(const Params& P, z_t* A, const z_t* alph) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
+__global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(Params P) {
   extern __shared__ double2 smem[];
   __shared__ int piv[NB];
   __shared__ double rv[NT / 32];
@@ -496,8 +607,8 @@ __global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
   __shared__ z_t alph[64];
   const int r = P.r, s = P.s, ldw = P.ldw, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  z_t* A = P.work + (size_t)blockIdx.x * r * ldw;
-  const int64_t rr = (int64_t)r * r;
+  z_t* A = P.work + (size_t)blockIdx.x * P.cta_stride;
+  z_t* yscratch = A + (size_t)r * ldw;
 
   for (int64_t f = blockIdx.x; f < P.F; f += gridDim.x) {
     if (tid < P.nprim) alph[tid] = P.alpha[f * P.nprim + tid];
@@ -507,7 +618,7 @@ __global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
     form_matrix(P, A, alph);
     const z_t* bf = P.b + f * P.b_stride_f;
     for (int idx = tid; idx < r * s; idx += NT) {
-      int i = idx / s, c = idx - i * s;
+      const int i = idx / s, c = idx - i * s;
       A[(size_t)i * ldw + r + c] = __ldg(bf + idx);
     }
     __syncthreads();
@@ -535,7 +646,6 @@ __global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
       apply_swaps(A, ldw, piv, k0, k0, k0 + nb, c0, c1);
       __syncthreads();
       panel_trsm(A, ldw, k0, nb, c0, c1, smem);
-      __syncthreads();
       if (c0 < r) {
         GemmWide::run(A + (size_t)c0 * ldw + c0, ldw, A + (size_t)c0 * ldw + k0, ldw,
                       A + (size_t)k0 * ldw + c0, ldw, r - c0, c1 - c0, nb, smem);
@@ -554,32 +664,25 @@ __global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
       }
     }
 
-    // ---- outputs ----
+    // ---- outputs: x, y = C_R x (DMMA GEMM), SPL ----
     if (P.x) {
       z_t* xf = P.x + f * (int64_t)r * s;
       for (int idx = tid; idx < r * s; idx += NT) {
-        int i = idx / s, c = idx - i * s;
+        const int i = idx / s, c = idx - i * s;
         xf[idx] = A[(size_t)i * ldw + r + c];
       }
     }
     if (P.n_out > 0 && (P.y || P.spl)) {
-      double* p2 = (double*)smem;
-      for (int idx = tid; idx < P.n_out * s; idx += NT) {
-        int o = idx / s, c = idx - o * s;
-        const z_t* cr = P.c_r + (int64_t)o * r;
-        z_t acc = zmake(0.0, 0.0);
-        for (int i = 0; i < r; ++i) acc = zfma(acc, __ldg(cr + i), A[(size_t)i * ldw + r + c]);
-        if (P.y) P.y[(f * P.n_out + o) * s + c] = acc;
-        p2[idx] = zabs2(acc);
-      }
+      z_t* yt = P.y ? P.y + f * (int64_t)P.n_out * s : yscratch;
+      GemmOut::run(yt, s, P.c_r, r, A + r, ldw, P.n_out, s, r, smem);
       __syncthreads();
       if (P.spl) {
         for (int c = warp; c < s; c += NT / 32) {
           double acc = 0.0;
-          for (int o = lane; o < P.n_out; o += 32) acc += p2[o * s + c];
+          for (int o = lane; o < P.n_out; o += 32) acc += zabs2(yt[(size_t)o * s + c]);
           acc = warp_sum(acc);
           if (lane == 0) {
-            double prms = sqrt(acc / P.n_out / 2.0);
+            const double prms = sqrt(acc / P.n_out / 2.0);
             P.spl[f * s + c] = 20.0 * log10(fmax(prms, 1e-300) / 20e-6);
           }
         }
@@ -592,24 +695,26 @@ __global__ void __launch_bounds__(NT, 1) rom_sweep_blocked_kernel(Params P) {
 
 static int ldw_of(int r, int s) { return (r + s + 3) & ~3; }
 
-static size_t smem_bytes(int r, int s, int n_out, int w) {
+static size_t smem_bytes(int r, int w) {
   size_t m = GemmWide::SMEM;
   m = m > GemmNarrow::SMEM ? m : GemmNarrow::SMEM;
+  m = m > GemmOut::SMEM ? m : GemmOut::SMEM;
   m = m > TRSM_SMEM ? m : TRSM_SMEM;
-  size_t bs = (size_t)(NB * (NB + 1) + NB * s) * sizeof(z_t);
-  m = m > bs ? m : bs;
-  size_t ps = (size_t)r * w * sizeof(z_t);
-  m = m > ps ? m : ps;
-  size_t p2 = (size_t)n_out * s * sizeof(double);
-  m = m > p2 ? m : p2;
-  return m;
+  m = m > BACK_SMEM ? m : BACK_SMEM;
+  const size_t ps = (size_t)r * w * sizeof(z_t);
+  return m > ps ? m : ps;
 }
 
-static int pick_w(int r, int s, int n_out) {
-  const size_t limit = 200 * 1024;
+static const size_t kSmemPerCta = 110 * 1024;  // two CTAs per SM
+
+static int pick_w(int r) {
   for (int w = 16; w >= 1; w >>= 1)
-    if (smem_bytes(r, s, n_out, w) <= limit && (size_t)r * w * sizeof(z_t) <= limit) return w;
+    if (smem_bytes(r, w) <= kSmemPerCta) return w;
   return 0;
+}
+
+static size_t cta_stride(int r, int s, int n_out) {
+  return ((size_t)r * ldw_of(r, s) + (size_t)n_out * s + 7) & ~(size_t)7;
 }
 
 }  // namespace blk
@@ -618,16 +723,15 @@ static int blocked_grid(int64_t F) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  return (int)(F < nsm ? F : nsm);
+  const int64_t g = 2 * (int64_t)nsm;
+  return (int)(F < g ? F : g);
 }
 
-size_t sweep_blocked_workspace_bytes(int r, int s, int64_t F) {
-  return (size_t)blocked_grid(F) * r * blk::ldw_of(r, s) * sizeof(z_t);
+size_t sweep_blocked_workspace_bytes(int r, int s, int n_out, int64_t F) {
+  return (size_t)blocked_grid(F) * blk::cta_stride(r, s, n_out) * sizeof(z_t);
 }
 
-int sweep_blocked_supported(int r, int s, int n_out) {
-  return s <= 16 && blk::pick_w(r, s, n_out) > 0;
-}
+int sweep_blocked_supported(int r, int s, int n_out) { return s <= 16 && blk::pick_w(r) > 0; }
 
 int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_t* prims,
                          const z_t* alpha, const z_t* b, int64_t b_stride_f, const z_t* c_r, z_t* y,
@@ -635,19 +739,50 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
                          cudaStream_t stream) {
   VB_CHECK_ARG(s <= 16, "vb_rom_sweep (blocked): at most 16 RHS columns");
   VB_CHECK_ARG(nprim <= 64, "vb_rom_sweep (blocked): at most 64 primitives");
-  const int w = blk::pick_w(r, s, n_out);
+  const int w = blk::pick_w(r);
   VB_CHECK_ARG(w > 0, "vb_rom_sweep (blocked): reduced order too large for the inner panel");
-  const size_t need = sweep_blocked_workspace_bytes(r, s, F);
+  const size_t need = sweep_blocked_workspace_bytes(r, s, n_out, F);
   VB_CHECK_ARG(work != nullptr && work_bytes >= need, "vb_rom_sweep (blocked): workspace too small");
   blk::Params P;
   P.r = r; P.nprim = nprim; P.s = s; P.n_out = n_out; P.F = F;
   P.prims = prims; P.alpha = alpha; P.b = b; P.b_stride_f = b_stride_f; P.c_r = c_r;
   P.y = y; P.spl = spl; P.x = x; P.info = info;
   P.work = (z_t*)work; P.ldw = blk::ldw_of(r, s); P.w = w;
-  const size_t smem = blk::smem_bytes(r, s, n_out, w);
+  P.cta_stride = blk::cta_stride(r, s, n_out);
+  const size_t smem = blk::smem_bytes(r, w);
   VB_CUDA(cudaFuncSetAttribute(blk::rom_sweep_blocked_kernel,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  blk::rom_sweep_blocked_kernel<<<blocked_grid(F), blk::NT, smem, stream>>>(P);
+
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocked_grid(F));
+  cfg.blockDim = dim3(blk::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  // Pin the primitives (read by every CTA for every frequency) in L2 so the
+  // workspace streaming does not evict them.
+  cudaLaunchAttribute attr[1];
+  int dev = 0, max_persist = 0, max_window = 0;
+  VB_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  const size_t pbytes = (size_t)nprim * r * r * sizeof(z_t);
+  if (max_persist > 0 && max_window > 0) {
+    const size_t win = pbytes < (size_t)max_window ? pbytes : (size_t)max_window;
+    const size_t lim = win < (size_t)max_persist ? win : (size_t)max_persist;
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < lim) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = (void*)prims;
+    attr[0].val.accessPolicyWindow.num_bytes = win;
+    attr[0].val.accessPolicyWindow.hitRatio = (float)((double)lim / (double)win);
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaGetLastError();  // clear any error from the optional persistence queries
+  VB_CUDA(cudaLaunchKernelEx(&cfg, blk::rom_sweep_blocked_kernel, P));
   VB_LAUNCHED("rom_sweep_blocked_kernel");
   return 0;
 }
