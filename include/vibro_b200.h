@@ -79,6 +79,48 @@ int vb_rom_sweep_path(int r, int nprim, int s, int n_out);
  * forced shared-memory path still fails with rc=3 when it does not fit. */
 void vb_set_sweep_path_override(int path);
 
+/* ------------------------------------------------------------------------
+ * FE primitives
+ * ---------------------------------------------------------------------- */
+
+/*
+ * Canonical CSR pattern of an element triplet stream.  Replaces
+ * vibrofem/assembly.py:160-175 (rows = repeat(dofs, e), cols = tile(dofs, e)
+ * per element in index order; scipy coo_matrix.tocsr() + sum_duplicates()):
+ * indptr/indices are bit-identical to scipy's (sorted int32 column indices,
+ * explicit zeros kept because the pattern is structural).
+ *  conn        [n_elem][npe] int32 global dof ids
+ *  indptr      [n+1]  out
+ *  indices     [n_elem*npe*npe] out (first *nnz_host used)
+ *  gather_ptr  [n_elem*npe*npe + 1] out: slot s sums triplets
+ *              gather_idx[gather_ptr[s] .. gather_ptr[s+1]) in element order
+ *  gather_idx  [n_elem*npe*npe] out
+ *  nnz_host    out (HOST pointer); the call synchronises the stream.
+ */
+size_t vb_csr_pattern_workspace_bytes(int n, int n_elem, int npe);
+int vb_csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, int32_t* indptr,
+                                 int32_t* indices, int64_t* gather_ptr, int32_t* gather_idx,
+                                 int64_t* nnz_host, void* work, size_t work_bytes, void* stream);
+
+/* CSR values from triplet values: vals[s] = sum of triplet_vals over the
+ * slot's gather list, in element order (deterministic; assembly.py:172-173). */
+int vb_csr_gather(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx,
+                  const double* triplet_vals, double* vals, void* stream);
+
+/* Unscaled Helmholtz integrals of 27-node hexahedra (vibrofem/assembly.py:77-91
+ * generalised to 3D: J = dshape^T X, dN = dshape inv(J), 3x3x3 Gauss):
+ *  xyz [n_nodes][3], conn [n_elem][27] (local node a + 3b + 9c),
+ *  Ke, Me [n_elem][27][27] out (row-major; the triplet value order of
+ *  assembly.py:166-170).  *bad_elem_host = first element with detJ <= 0, or -1
+ *  (the reference raises ValueError); synchronises the stream. */
+int vb_hex27_helmholtz_elements(int n_elem, const double* xyz, const int32_t* conn, double* Ke,
+                                double* Me, int32_t* bad_elem_host, void* stream);
+
+/* Impedance-wall primitive: int_Gamma N N^T dGamma on 9-node faces
+ * (face_conn [n_faces][9], lexicographic), Fe [n_faces][9][9] out. */
+int vb_quad9_face_mass(int n_faces, const double* xyz, const int32_t* face_conn, double* Fe,
+                       void* stream);
+
 /* Measured FP64 tensor-pipe (DMMA, mma.sync.m8n8k4.f64) throughput of this
  * device in TFLOP/s, written to *tflops_host; synchronous (~10 ms).  Used as
  * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */

@@ -26,6 +26,15 @@ _SIGS = {
     "vb_set_sweep_path_override": (None, [C.c_int]),
     "vb_probe_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.c_void_p]),
     "vb_rom_sweep_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64]),
+    "vb_csr_pattern_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    "vb_csr_pattern_from_elements": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                               C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.POINTER(C.c_int64), C.c_void_p, C.c_size_t,
+                                               C.c_void_p]),
+    "vb_csr_gather": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vb_hex27_helmholtz_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.POINTER(C.c_int32), C.c_void_p]),
+    "vb_quad9_face_mass": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vb_rom_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _z, _z, _z, C.c_int64,
                                _z, _z, C.c_void_p, _z, C.c_void_p, C.c_void_p, C.c_size_t,
                                C.c_void_p]),

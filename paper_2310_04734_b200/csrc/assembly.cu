@@ -1,0 +1,378 @@
+// FE primitives on the GPU (SURVEY §8a rows A1–A3):
+//   shape.py:20-26, 56-65   quadratic Lagrange bases and Gauss rules (constant tables)
+//   assembly.py:77-91       Helmholtz element integrals Kgrad_e, Mnn_e (hex27 here)
+//   assembly.py:142-175     triplet stream (rows = repeat(dofs), cols = tile(dofs),
+//                           elements in index order) -> canonical CSR, duplicates
+//                           summed, explicit zeros kept.
+//
+// Pattern: a STABLE radix sort of the triplet keys row*n+col carrying the triplet
+// index, so duplicates of one (row, col) stay in element order; the unique keys
+// are the canonical pattern (sorted int32 column indices per row, bit-identical
+// to scipy's coo -> csr -> sum_duplicates), and the sorted triplet indices are a
+// gather map.  Values are then summed per CSR slot in element order by a
+// gather kernel: no atomics, run-to-run bit-identical.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "sweep.cuh"
+
+namespace vb {
+
+// ---------------------------------------------------------------- tables ---
+// 3-point Gauss-Legendre (shape.py:56-57 = numpy leggauss(3)), closed form.
+__constant__ double c_gx[3];
+__constant__ double c_gw[3];
+// hex27: N[g][i], dN/dxi[g][i][a]; local node i = a + 3b + 9c, Gauss point
+// g = gx + 3 gy + 9 gz (x fastest, shape.py:60-65 generalised).
+__constant__ double c_hexN[27 * 27];
+__constant__ double c_hexdN[27 * 27 * 3];
+__constant__ double c_hexW[27];
+// quad9 face (lexicographic a + 3b): N[g][i], dN/dxi[g][i][2], weights.
+__constant__ double c_qN[9 * 9];
+__constant__ double c_qdN[9 * 9 * 2];
+__constant__ double c_qW[9];
+
+static void lag1d(double x, double* v) {  // shape.py:20-22
+  v[0] = 0.5 * x * (x - 1.0);
+  v[1] = 1.0 - x * x;
+  v[2] = 0.5 * x * (x + 1.0);
+}
+static void dlag1d(double x, double* v) {  // shape.py:25-26
+  v[0] = x - 0.5;
+  v[1] = -2.0 * x;
+  v[2] = x + 0.5;
+}
+
+static int init_tables() {
+  static bool done = false;
+  if (done) return 0;
+  const double gx[3] = {-0.7745966692414834, 0.0, 0.7745966692414834};
+  const double gw[3] = {0.5555555555555556, 0.8888888888888888, 0.5555555555555556};
+  double hN[27 * 27], hdN[27 * 27 * 3], hW[27], qN[81], qdN[162], qW[9];
+  for (int g = 0; g < 27; ++g) {
+    const int g3[3] = {g % 3, (g / 3) % 3, g / 9};
+    double L[3][3], D[3][3];
+    for (int d = 0; d < 3; ++d) {
+      lag1d(gx[g3[d]], L[d]);
+      dlag1d(gx[g3[d]], D[d]);
+    }
+    hW[g] = gw[g3[0]] * gw[g3[1]] * gw[g3[2]];
+    for (int i = 0; i < 27; ++i) {
+      const int n3[3] = {i % 3, (i / 3) % 3, i / 9};
+      hN[g * 27 + i] = L[0][n3[0]] * L[1][n3[1]] * L[2][n3[2]];
+      for (int a = 0; a < 3; ++a) {
+        double v = 1.0;
+        for (int d = 0; d < 3; ++d) v *= (d == a ? D : L)[d][n3[d]];
+        hdN[(g * 27 + i) * 3 + a] = v;
+      }
+    }
+  }
+  for (int g = 0; g < 9; ++g) {
+    const int g2[2] = {g % 3, g / 3};
+    double L[2][3], D[2][3];
+    for (int d = 0; d < 2; ++d) {
+      lag1d(gx[g2[d]], L[d]);
+      dlag1d(gx[g2[d]], D[d]);
+    }
+    qW[g] = gw[g2[0]] * gw[g2[1]];
+    for (int i = 0; i < 9; ++i) {
+      const int n2[2] = {i % 3, i / 3};
+      qN[g * 9 + i] = L[0][n2[0]] * L[1][n2[1]];
+      qdN[(g * 9 + i) * 2 + 0] = D[0][n2[0]] * L[1][n2[1]];
+      qdN[(g * 9 + i) * 2 + 1] = L[0][n2[0]] * D[1][n2[1]];
+    }
+  }
+  VB_CUDA(cudaMemcpyToSymbol(c_gx, gx, sizeof(gx)));
+  VB_CUDA(cudaMemcpyToSymbol(c_gw, gw, sizeof(gw)));
+  VB_CUDA(cudaMemcpyToSymbol(c_hexN, hN, sizeof(hN)));
+  VB_CUDA(cudaMemcpyToSymbol(c_hexdN, hdN, sizeof(hdN)));
+  VB_CUDA(cudaMemcpyToSymbol(c_hexW, hW, sizeof(hW)));
+  VB_CUDA(cudaMemcpyToSymbol(c_qN, qN, sizeof(qN)));
+  VB_CUDA(cudaMemcpyToSymbol(c_qdN, qdN, sizeof(qdN)));
+  VB_CUDA(cudaMemcpyToSymbol(c_qW, qW, sizeof(qW)));
+  done = true;
+  return 0;
+}
+
+// ------------------------------------------------------- element kernels ---
+// One CTA per hex27 element.  Follows assembly.py:77-91 exactly:
+// J = dshape^T X, detJ <= 0 rejected, dN = dshape inv(J),
+// Kgrad += w detJ dN dN^T, Mnn += w detJ N N^T.
+constexpr int EL_NT = 128;
+
+__global__ void __launch_bounds__(EL_NT) hex27_helmholtz_kernel(int n_elem, const double* __restrict__ xyz,
+                                                                const int32_t* __restrict__ conn,
+                                                                double* __restrict__ Ke,
+                                                                double* __restrict__ Me,
+                                                                int* __restrict__ bad) {
+  __shared__ double X[27][3];
+  __shared__ double wdet[27];
+  __shared__ double dNx[27][27][3];  // [g][i][b]
+  const int tid = threadIdx.x;
+  for (int e = blockIdx.x; e < n_elem; e += gridDim.x) {
+    for (int q = tid; q < 81; q += EL_NT) X[q / 3][q % 3] = xyz[(size_t)conn[(size_t)e * 27 + q / 3] * 3 + q % 3];
+    __syncthreads();
+    if (tid < 27) {
+      const int g = tid;
+      double J[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+          double s = 0.0;
+          for (int i = 0; i < 27; ++i) s += c_hexdN[(g * 27 + i) * 3 + a] * X[i][b];
+          J[a][b] = s;
+        }
+      const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                         J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                         J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      if (!(det > 0.0)) atomicMin(bad, e);
+      const double id = 1.0 / det;
+      double iJ[3][3];
+      iJ[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
+      iJ[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+      iJ[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+      iJ[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
+      iJ[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+      iJ[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+      iJ[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
+      iJ[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+      iJ[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+      wdet[g] = c_hexW[g] * det;
+      for (int i = 0; i < 27; ++i)
+        for (int b = 0; b < 3; ++b) {
+          double s = 0.0;
+          for (int a = 0; a < 3; ++a) s += c_hexdN[(g * 27 + i) * 3 + a] * iJ[a][b];
+          dNx[g][i][b] = s;
+        }
+    }
+    __syncthreads();
+    for (int q = tid; q < 729; q += EL_NT) {
+      const int i = q / 27, j = q % 27;
+      double k = 0.0, m = 0.0;
+      for (int g = 0; g < 27; ++g) {
+        const double w = wdet[g];
+        k += w * (dNx[g][i][0] * dNx[g][j][0] + dNx[g][i][1] * dNx[g][j][1] + dNx[g][i][2] * dNx[g][j][2]);
+        m += w * (c_hexN[g * 27 + i] * c_hexN[g * 27 + j]);
+      }
+      Ke[(size_t)e * 729 + q] = k;
+      Me[(size_t)e * 729 + q] = m;
+    }
+    __syncthreads();
+  }
+}
+
+// One warp per 9-node face: int_Gamma N N^T dGamma with dA = |t_xi x t_eta|.
+__global__ void quad9_face_mass_kernel(int n_faces, const double* __restrict__ xyz,
+                                       const int32_t* __restrict__ fconn, double* __restrict__ Fe) {
+  const int lane = threadIdx.x & 31;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (f >= n_faces) return;
+  double dA = 0.0;
+  if (lane < 9) {
+    const int g = lane;
+    double t[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    for (int i = 0; i < 9; ++i) {
+      const int node = fconn[(size_t)f * 9 + i];
+      for (int b = 0; b < 3; ++b) {
+        const double x = xyz[(size_t)node * 3 + b];
+        t[0][b] += c_qdN[(g * 9 + i) * 2 + 0] * x;
+        t[1][b] += c_qdN[(g * 9 + i) * 2 + 1] * x;
+      }
+    }
+    const double cx = t[0][1] * t[1][2] - t[0][2] * t[1][1];
+    const double cy = t[0][2] * t[1][0] - t[0][0] * t[1][2];
+    const double cz = t[0][0] * t[1][1] - t[0][1] * t[1][0];
+    dA = c_qW[g] * sqrt(cx * cx + cy * cy + cz * cz);
+  }
+  double w9[9];
+#pragma unroll
+  for (int g = 0; g < 9; ++g) w9[g] = __shfl_sync(0xffffffffu, dA, g);
+  for (int q = lane; q < 81; q += 32) {
+    const int i = q / 9, j = q % 9;
+    double m = 0.0;
+#pragma unroll
+    for (int g = 0; g < 9; ++g) m += w9[g] * c_qN[g * 9 + i] * c_qN[g * 9 + j];
+    Fe[(size_t)f * 81 + q] = m;
+  }
+}
+
+// ------------------------------------------------------------ pattern ---
+__global__ void make_keys_kernel(int64_t T, int npe, int n, const int32_t* __restrict__ conn,
+                                 uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int64_t pe = (int64_t)npe * npe;
+  const int64_t e = t / pe;
+  const int a = (int)((t / npe) % npe), b = (int)(t % npe);
+  const uint64_t row = (uint64_t)conn[e * npe + a], col = (uint64_t)conn[e * npe + b];
+  keys[t] = row * (uint64_t)n + col;
+  vals[t] = (int32_t)t;
+}
+
+__global__ void head_flags_kernel(int64_t T, const uint64_t* __restrict__ keys, int32_t* __restrict__ head) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  head[t] = (t == 0 || keys[t] != keys[t - 1]) ? 1 : 0;
+}
+
+__global__ void emit_pattern_kernel(int64_t T, int n, const uint64_t* __restrict__ keys,
+                                    const int32_t* __restrict__ head, const int32_t* __restrict__ slot,
+                                    int32_t* __restrict__ indices, int64_t* __restrict__ gptr,
+                                    int32_t* __restrict__ row_count) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  if (head[t]) {
+    const int s = slot[t];
+    const uint64_t k = keys[t];
+    indices[s] = (int32_t)(k % (uint64_t)n);
+    gptr[s] = t;
+    atomicAdd(row_count + (int)(k / (uint64_t)n), 1);
+  }
+}
+
+__global__ void finish_gptr_kernel(int64_t T, const int32_t* nnz_dev, int64_t* gptr) {
+  gptr[*nnz_dev] = T;
+}
+
+__global__ void nnz_kernel(int64_t T, const int32_t* head, const int32_t* slot, int32_t* nnz) {
+  *nnz = slot[T - 1] + head[T - 1];
+}
+
+__global__ void csr_gather_kernel(int64_t nnz, const int64_t* __restrict__ gptr,
+                                  const int32_t* __restrict__ gidx, const double* __restrict__ tv,
+                                  double* __restrict__ vals) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nnz) return;
+  double acc = 0.0;
+  const int64_t b = gptr[s], e = gptr[s + 1];
+  for (int64_t t = b; t < e; ++t) acc += __ldg(tv + gidx[t]);
+  vals[s] = acc;
+}
+
+// ------------------------------------------------------------- host side ---
+struct PatternWs {
+  size_t keys_a, keys_b, vals_a, head, slot, cnt, nnz, cub;
+  size_t total;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int pattern_ws(int64_t T, int n, PatternWs* w) {
+  size_t cub_sort = 0, cub_scan = 0;
+  VB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, cub_sort, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                          (int32_t*)nullptr, (int32_t*)nullptr, (int64_t)T));
+  VB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_scan, (int32_t*)nullptr, (int32_t*)nullptr,
+                                        (int64_t)(T > n + 1 ? T : n + 1)));
+  size_t off = 0;
+  w->keys_a = off; off += align256(T * 8);
+  w->keys_b = off; off += align256(T * 8);
+  w->vals_a = off; off += align256(T * 4);
+  w->head = off; off += align256(T * 4);
+  w->slot = off; off += align256(T * 4);
+  w->cnt = off; off += align256((size_t)(n + 1) * 4);
+  w->nnz = off; off += 256;
+  w->cub = off; off += align256(cub_sort > cub_scan ? cub_sort : cub_scan);
+  w->total = off;
+  return 0;
+}
+
+size_t csr_pattern_workspace_bytes(int n, int64_t T) {
+  PatternWs w;
+  if (pattern_ws(T, n, &w)) return 0;
+  return w.total;
+}
+
+static int end_bit_for(uint64_t maxkey) {
+  int b = 1;
+  while (b < 64 && (maxkey >> b)) ++b;
+  return b;
+}
+
+int csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, int32_t* indptr,
+                              int32_t* indices, int64_t* gptr, int32_t* gidx, int64_t* nnz_host,
+                              void* work, size_t work_bytes, cudaStream_t stream) {
+  const int64_t T = (int64_t)n_elem * npe * npe;
+  VB_CHECK_ARG(T > 0 && T < ((int64_t)1 << 31), "vb_csr_pattern_from_elements: triplet count out of range");
+  PatternWs w;
+  if (int rc = pattern_ws(T, n, &w)) return rc;
+  VB_CHECK_ARG(work && work_bytes >= w.total, "vb_csr_pattern_from_elements: workspace too small");
+  char* base = (char*)work;
+  uint64_t* ka = (uint64_t*)(base + w.keys_a);
+  uint64_t* kb = (uint64_t*)(base + w.keys_b);
+  int32_t* va = (int32_t*)(base + w.vals_a);
+  int32_t* head = (int32_t*)(base + w.head);
+  int32_t* slot = (int32_t*)(base + w.slot);
+  int32_t* cnt = (int32_t*)(base + w.cnt);
+  int32_t* nnz_dev = (int32_t*)(base + w.nnz);
+  void* cubtmp = base + w.cub;
+  size_t cubbytes = work_bytes - w.cub;
+  const int nt = 256;
+  const unsigned nb = (unsigned)((T + nt - 1) / nt);
+  make_keys_kernel<<<nb, nt, 0, stream>>>(T, npe, n, conn, ka, va);
+  VB_LAUNCHED("make_keys_kernel");
+  const int eb = end_bit_for((uint64_t)n * (uint64_t)n);
+  VB_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, cubbytes, ka, kb, va, gidx, T, 0, eb, stream));
+  count_launches(1);
+  head_flags_kernel<<<nb, nt, 0, stream>>>(T, kb, head);
+  VB_LAUNCHED("head_flags_kernel");
+  VB_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, cubbytes, head, slot, T, stream));
+  count_launches(1);
+  VB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 4, stream));
+  emit_pattern_kernel<<<nb, nt, 0, stream>>>(T, n, kb, head, slot, indices, gptr, cnt);
+  VB_LAUNCHED("emit_pattern_kernel");
+  VB_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, cubbytes, cnt, indptr, n + 1, stream));
+  count_launches(1);
+  nnz_kernel<<<1, 1, 0, stream>>>(T, head, slot, nnz_dev);
+  VB_LAUNCHED("nnz_kernel");
+  finish_gptr_kernel<<<1, 1, 0, stream>>>(T, nnz_dev, gptr);
+  VB_LAUNCHED("finish_gptr_kernel");
+  int32_t nnz = 0;
+  VB_CUDA(cudaMemcpyAsync(&nnz, nnz_dev, 4, cudaMemcpyDeviceToHost, stream));
+  VB_CUDA(cudaStreamSynchronize(stream));
+  *nnz_host = nnz;
+  return 0;
+}
+
+int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv, double* vals,
+               cudaStream_t stream) {
+  if (nnz <= 0) return 0;
+  const int nt = 256;
+  csr_gather_kernel<<<(unsigned)((nnz + nt - 1) / nt), nt, 0, stream>>>(nnz, gptr, gidx, tv, vals);
+  VB_LAUNCHED("csr_gather_kernel");
+  return 0;
+}
+
+int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* Ke, double* Me,
+                    int32_t* bad_elem_host, cudaStream_t stream) {
+  if (int rc = init_tables()) return rc;
+  int* bad = nullptr;
+  VB_CUDA(cudaMallocAsync(&bad, sizeof(int), stream));
+  const int big = 0x7fffffff;
+  VB_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, stream));
+  int dev = 0, nsm = 148;
+  VB_CUDA(cudaGetDevice(&dev));
+  VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = n_elem < nsm * 16 ? n_elem : nsm * 16;
+  if (grid > 0) {
+    hex27_helmholtz_kernel<<<grid, EL_NT, 0, stream>>>(n_elem, xyz, conn, Ke, Me, bad);
+    VB_LAUNCHED("hex27_helmholtz_kernel");
+  }
+  int hb = big;
+  VB_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  VB_CUDA(cudaFreeAsync(bad, stream));
+  VB_CUDA(cudaStreamSynchronize(stream));
+  *bad_elem_host = hb == big ? -1 : hb;
+  return 0;
+}
+
+int quad9_face_mass(int n_faces, const double* xyz, const int32_t* fconn, double* Fe,
+                    cudaStream_t stream) {
+  if (int rc = init_tables()) return rc;
+  if (n_faces <= 0) return 0;
+  const int nt = 128;
+  const unsigned grid = (unsigned)(((int64_t)n_faces * 32 + nt - 1) / nt);
+  quad9_face_mass_kernel<<<grid, nt, 0, stream>>>(n_faces, xyz, fconn, Fe);
+  VB_LAUNCHED("quad9_face_mass_kernel");
+  return 0;
+}
+
+}  // namespace vb

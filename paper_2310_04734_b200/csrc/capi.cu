@@ -68,4 +68,37 @@ int vb_rom_sweep(int r, int nprim, int s, int n_out, int64_t F, const vb_complex
                        (cudaStream_t)stream);
 }
 
+size_t vb_csr_pattern_workspace_bytes(int n, int n_elem, int npe) {
+  return vb::csr_pattern_workspace_bytes(n, (int64_t)n_elem * npe * npe);
+}
+
+int vb_csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, int32_t* indptr,
+                                 int32_t* indices, int64_t* gather_ptr, int32_t* gather_idx,
+                                 int64_t* nnz_host, void* work, size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(n > 0 && n_elem > 0 && npe > 0, "vb_csr_pattern_from_elements: bad sizes");
+  VB_CHECK_ARG(conn && indptr && indices && gather_ptr && gather_idx && nnz_host,
+               "vb_csr_pattern_from_elements: null pointer");
+  return vb::csr_pattern_from_elements(n, n_elem, npe, conn, indptr, indices, gather_ptr, gather_idx,
+                                       nnz_host, work, work_bytes, (cudaStream_t)stream);
+}
+
+int vb_csr_gather(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx,
+                  const double* triplet_vals, double* vals, void* stream) {
+  VB_CHECK_ARG(nnz >= 0, "vb_csr_gather: bad nnz");
+  return vb::csr_gather(nnz, gather_ptr, gather_idx, triplet_vals, vals, (cudaStream_t)stream);
+}
+
+int vb_hex27_helmholtz_elements(int n_elem, const double* xyz, const int32_t* conn, double* Ke,
+                                double* Me, int32_t* bad_elem_host, void* stream) {
+  VB_CHECK_ARG(n_elem >= 0 && xyz && conn && Ke && Me && bad_elem_host,
+               "vb_hex27_helmholtz_elements: bad arguments");
+  return vb::hex27_helmholtz(n_elem, xyz, conn, Ke, Me, bad_elem_host, (cudaStream_t)stream);
+}
+
+int vb_quad9_face_mass(int n_faces, const double* xyz, const int32_t* face_conn, double* Fe,
+                       void* stream) {
+  VB_CHECK_ARG(n_faces >= 0 && xyz && face_conn && Fe, "vb_quad9_face_mass: bad arguments");
+  return vb::quad9_face_mass(n_faces, xyz, face_conn, Fe, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -25,4 +25,17 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
                          double* spl, z_t* x, int* info, void* work, size_t work_bytes,
                          cudaStream_t stream);
 
+
+// assembly.cu
+size_t csr_pattern_workspace_bytes(int n, int64_t T);
+int csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, int32_t* indptr,
+                              int32_t* indices, int64_t* gptr, int32_t* gidx, int64_t* nnz_host,
+                              void* work, size_t work_bytes, cudaStream_t stream);
+int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv, double* vals,
+               cudaStream_t stream);
+int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* Ke, double* Me,
+                    int32_t* bad_elem_host, cudaStream_t stream);
+int quad9_face_mass(int n_faces, const double* xyz, const int32_t* fconn, double* Fe,
+                    cudaStream_t stream);
+
 }  // namespace vb
