@@ -121,6 +121,42 @@ int vb_hex27_helmholtz_elements(int n_elem, const double* xyz, const int32_t* co
 int vb_quad9_face_mass(int n_faces, const double* xyz, const int32_t* face_conn, double* Fe,
                        void* stream);
 
+/* ------------------------------------------------------------------------
+ * Offline-phase linear algebra
+ * ---------------------------------------------------------------------- */
+
+/* Y = alpha * A X + beta * Y with A a real CSR (float64 values, int32 indices)
+ * and X (n_cols x k), Y (n_rows x k) complex row-major.  Replaces scipy
+ * csr_matvecs in `K @ V`, `M @ v` (vibrofem/mor.py:81-85, 117, 162-179). */
+int vb_csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
+                const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha,
+                vb_complex beta, void* stream);
+
+/* D += alpha * A: scatter a scaled real CSR primitive into a dense complex
+ * matrix (row-major, ldd) — assembles K - w^2 M + i w D at an expansion point
+ * (vibrofem/mor.py:41-46) for the dense full-order LU. */
+int vb_csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
+                      vb_complex alpha, vb_complex* D, int64_t ldd, void* stream);
+
+/* Complex GEMM on the FP64 tensor cores (DMMA).  Replaces numpy/BLAS zgemm in
+ * vibrofem/mor.py:81-89, 102, 105, 117-118, 129-131.
+ *  transa = 'N': C (m x n) = alpha A B + beta C,    A m x k, B k x n
+ *  transa = 'C': C (m x n) = alpha A^H B + beta C,  A k x m, B k x n
+ *                (split-K over k with a fixed-order reduction: deterministic)
+ * All row-major with the given leading dimensions. */
+size_t vb_zgemm_workspace_bytes(char transa, int m, int n, int k);
+int vb_zgemm(char transa, int m, int n, int k, vb_complex alpha, const vb_complex* A, int64_t lda,
+             const vb_complex* B, int64_t ldb, vb_complex beta, vb_complex* C, int64_t ldc, void* work,
+             size_t work_bytes, void* stream);
+
+/* norms[j] = ||W[:, j]||_2 for an n x m complex row-major W (deterministic). */
+size_t vb_column_norms_workspace_bytes(int n, int m);
+int vb_column_norms(int n, int m, const vb_complex* W, int64_t ldw, double* norms, void* work,
+                    size_t work_bytes, void* stream);
+
+/* W[:, j] *= scale[j] (scale: device float64[m]). */
+int vb_scale_columns(int n, int m, vb_complex* W, int64_t ldw, const double* scale, void* stream);
+
 /* Measured FP64 tensor-pipe (DMMA, mma.sync.m8n8k4.f64) throughput of this
  * device in TFLOP/s, written to *tflops_host; synchronous (~10 ms).  Used as
  * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */

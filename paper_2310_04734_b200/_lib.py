@@ -18,6 +18,15 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libvibro_b200.so"
 
 _z = C.c_void_p  # vb_complex* (device)
+
+
+class VbComplex(C.Structure):
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
+
+
+def zc(v) -> VbComplex:
+    v = complex(v)
+    return VbComplex(v.real, v.imag)
 _SIGS = {
     "vb_version": (C.c_char_p, []),
     "vb_last_error": (C.c_char_p, []),
@@ -35,6 +44,17 @@ _SIGS = {
     "vb_hex27_helmholtz_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.POINTER(C.c_int32), C.c_void_p]),
     "vb_quad9_face_mass": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vb_csr_spmm": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _z, C.c_int64, _z,
+                              C.c_int64, VbComplex, VbComplex, C.c_void_p]),
+    "vb_csr_axpy_dense": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, VbComplex, _z, C.c_int64,
+                                    C.c_void_p]),
+    "vb_zgemm_workspace_bytes": (C.c_size_t, [C.c_char, C.c_int, C.c_int, C.c_int]),
+    "vb_zgemm": (C.c_int, [C.c_char, C.c_int, C.c_int, C.c_int, VbComplex, _z, C.c_int64, _z, C.c_int64,
+                           VbComplex, _z, C.c_int64, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vb_column_norms_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "vb_column_norms": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t,
+                                  C.c_void_p]),
+    "vb_scale_columns": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p]),
     "vb_rom_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _z, _z, _z, C.c_int64,
                                _z, _z, C.c_void_p, _z, C.c_void_p, C.c_void_p, C.c_size_t,
                                C.c_void_p]),

@@ -101,4 +101,44 @@ int vb_quad9_face_mass(int n_faces, const double* xyz, const int32_t* face_conn,
   return vb::quad9_face_mass(n_faces, xyz, face_conn, Fe, (cudaStream_t)stream);
 }
 
+static inline z_t zc(vb_complex a) { return vb::zmake(a.re, a.im); }
+
+int vb_csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
+                const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha,
+                vb_complex beta, void* stream) {
+  VB_CHECK_ARG(n_rows >= 0 && k >= 0, "vb_csr_spmm: bad sizes");
+  return vb::csr_spmm(n_rows, indptr, indices, vals, k, (const z_t*)X, ldx, (z_t*)Y, ldy, zc(alpha),
+                      zc(beta), (cudaStream_t)stream);
+}
+
+int vb_csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
+                      vb_complex alpha, vb_complex* D, int64_t ldd, void* stream) {
+  VB_CHECK_ARG(n_rows >= 0 && D, "vb_csr_axpy_dense: bad arguments");
+  return vb::csr_axpy_dense(n_rows, indptr, indices, vals, zc(alpha), (z_t*)D, ldd, (cudaStream_t)stream);
+}
+
+size_t vb_zgemm_workspace_bytes(char transa, int m, int n, int k) {
+  return vb::zgemm_workspace_bytes(transa, m, n, k);
+}
+
+int vb_zgemm(char transa, int m, int n, int k, vb_complex alpha, const vb_complex* A, int64_t lda,
+             const vb_complex* B, int64_t ldb, vb_complex beta, vb_complex* C, int64_t ldc, void* work,
+             size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(m >= 0 && n >= 0 && k >= 0, "vb_zgemm: bad sizes");
+  return vb::zgemm(transa, m, n, k, zc(alpha), (const z_t*)A, lda, (const z_t*)B, ldb, zc(beta),
+                   (z_t*)C, ldc, work, work_bytes, (cudaStream_t)stream);
+}
+
+size_t vb_column_norms_workspace_bytes(int n, int m) { return vb::column_norms_workspace_bytes(n, m); }
+
+int vb_column_norms(int n, int m, const vb_complex* W, int64_t ldw, double* norms, void* work,
+                    size_t work_bytes, void* stream) {
+  return vb::column_norms(n, m, (const z_t*)W, ldw, norms, work, work_bytes, (cudaStream_t)stream);
+}
+
+int vb_scale_columns(int n, int m, vb_complex* W, int64_t ldw, const double* scale, void* stream) {
+  VB_CHECK_ARG(n >= 0 && m >= 0, "vb_scale_columns: bad sizes");
+  return vb::scale_columns(n, m, (z_t*)W, ldw, scale, (cudaStream_t)stream);
+}
+
 }  // extern "C"

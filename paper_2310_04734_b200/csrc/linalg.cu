@@ -1,0 +1,317 @@
+// Dense/sparse building blocks of the offline MOR phase (SURVEY §8a A7–A9):
+//   CSR SpMM (real CSR x complex dense)        mor.py:81-85,117 (scipy csr_matvecs)
+//   complex GEMM, op(A) in {N, C} on DMMA      mor.py:81-89,102,105 (BLAS zgemm)
+//   deterministic column norms                 mor.py:127,132,157,184,188 (numpy norm)
+//   dense scatter of scaled CSR primitives     mor.py:41-46 (operator at an expansion point)
+#include "common.cuh"
+#include "mma.cuh"
+#include "sweep.cuh"
+
+namespace vb {
+
+// ------------------------------------------------------------------ SpMM ---
+// Y = alpha * A X + beta * Y, A real CSR (n_rows x *), X/Y complex row-major.
+// k > 1: one warp per row, lanes over the k columns (coalesced X rows), the
+// row's (value, index) pairs fetched 32 at a time and broadcast by shuffle.
+__global__ void spmm_kernel(int n_rows, const int32_t* __restrict__ indptr,
+                            const int32_t* __restrict__ indices, const double* __restrict__ vals,
+                            int k, const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y,
+                            int64_t ldy, z_t alpha, z_t beta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+  for (int64_t row = warp; row < n_rows; row += nwarps) {
+    const int b = indptr[row], e = indptr[row + 1];
+    for (int c0 = 0; c0 < k; c0 += 32) {
+      const int c = c0 + lane;
+      z_t acc = zmake(0.0, 0.0);
+      for (int j0 = b; j0 < e; j0 += 32) {
+        double v = 0.0;
+        int col = 0;
+        if (j0 + lane < e) {
+          v = vals[j0 + lane];
+          col = indices[j0 + lane];
+        }
+        const int cnt = min(32, e - j0);
+        for (int q = 0; q < cnt; ++q) {
+          const double a = __shfl_sync(0xffffffffu, v, q);
+          const int cc = __shfl_sync(0xffffffffu, col, q);
+          if (c < k) {
+            const z_t x = X[(int64_t)cc * ldx + c];
+            acc.x += a * x.x;
+            acc.y += a * x.y;
+          }
+        }
+      }
+      if (c < k) {
+        z_t out = zmul(alpha, acc);
+        if (!beta0) out = zfma(out, beta, Y[row * ldy + c]);
+        Y[row * ldy + c] = out;
+      }
+    }
+  }
+}
+
+// k == 1 (SpMV): lanes split the row's nonzeros, warp reduction in a fixed order.
+__global__ void spmv_kernel(int n_rows, const int32_t* __restrict__ indptr,
+                            const int32_t* __restrict__ indices, const double* __restrict__ vals,
+                            const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y, int64_t ldy,
+                            z_t alpha, z_t beta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+  for (int64_t row = warp; row < n_rows; row += nwarps) {
+    const int b = indptr[row], e = indptr[row + 1];
+    double re = 0.0, im = 0.0;
+    for (int j = b + lane; j < e; j += 32) {
+      const double a = vals[j];
+      const z_t x = X[(int64_t)indices[j] * ldx];
+      re += a * x.x;
+      im += a * x.y;
+    }
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) {
+      z_t out = zmul(alpha, zmake(re, im));
+      if (!beta0) out = zfma(out, beta, Y[row * ldy]);
+      Y[row * ldy] = out;
+    }
+  }
+}
+
+int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
+             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
+  if (n_rows <= 0 || k <= 0) return 0;
+  const int nt = 256;
+  const int64_t warps = n_rows;
+  unsigned grid = (unsigned)((warps * 32 + nt - 1) / nt);
+  if (grid > 148u * 64u) grid = 148u * 64u;
+  if (k == 1)
+    spmv_kernel<<<grid, nt, 0, st>>>(n_rows, indptr, indices, vals, X, ldx, Y, ldy, alpha, beta);
+  else
+    spmm_kernel<<<grid, nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
+  VB_LAUNCHED("spmm_kernel");
+  return 0;
+}
+
+// D += alpha * A (real CSR scattered into a dense complex matrix): the operator
+// K - w^2 M + i w D at an expansion point (mor.py:41-46) for the dense FOM LU.
+__global__ void csr_axpy_dense_kernel(int n_rows, const int32_t* __restrict__ indptr,
+                                      const int32_t* __restrict__ indices,
+                                      const double* __restrict__ vals, z_t alpha, z_t* __restrict__ D,
+                                      int64_t ldd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = warp; row < n_rows; row += nwarps) {
+    const int b = indptr[row], e = indptr[row + 1];
+    for (int j = b + lane; j < e; j += 32) {
+      const double a = vals[j];
+      z_t* d = D + row * ldd + indices[j];
+      *d = zmake(d->x + alpha.x * a, d->y + alpha.y * a);
+    }
+  }
+}
+
+int csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
+                   z_t alpha, z_t* D, int64_t ldd, cudaStream_t st) {
+  if (n_rows <= 0) return 0;
+  const int nt = 256;
+  unsigned grid = (unsigned)(((int64_t)n_rows * 32 + nt - 1) / nt);
+  if (grid > 148u * 64u) grid = 148u * 64u;
+  csr_axpy_dense_kernel<<<grid, nt, 0, st>>>(n_rows, indptr, indices, vals, alpha, D, ldd);
+  VB_LAUNCHED("csr_axpy_dense_kernel");
+  return 0;
+}
+
+// ------------------------------------------------------------------ GEMM ---
+using blk::NT;
+using blk::KC;
+
+// C = alpha A B + beta C, A (m x k), B (k x n): DMMA tiles over the grid.
+using GemmNN = blk::Gemm<64, 32, 4, 2, 3, blk::EPI_AXPBY>;
+
+__global__ void __launch_bounds__(NT) zgemm_nn_kernel(int m, int n, int k, z_t alpha, const z_t* A,
+                                                      int64_t lda, const z_t* B, int64_t ldb,
+                                                      z_t beta, z_t* C, int64_t ldc) {
+  extern __shared__ double2 smem[];
+  GemmNN::run(C, (int)ldc, A, (int)lda, B, (int)ldb, m, n, k, smem, alpha, beta, blockIdx.x,
+              gridDim.x);
+}
+
+// Split-K C_part[s] = A_s^H B_s over k-chunks s (A: k x m, B: k x n, row-major),
+// A^H staged transposed+conjugated in shared memory; one (tile, chunk) per CTA.
+constexpr int CN_TM = 64, CN_TN = 32, CN_KCH = 512;
+constexpr int CN_LDA = KC + 4, CN_LDB = CN_TN + 2;
+
+__global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int k, const z_t* __restrict__ A,
+                                                              int64_t lda, const z_t* __restrict__ B,
+                                                              int64_t ldb, z_t* __restrict__ part) {
+  __shared__ z_t As[CN_TM * CN_LDA];
+  __shared__ z_t Bs[KC * CN_LDB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps, 16 x 16 each
+  const int ntn = (n + CN_TN - 1) / CN_TN, ntm = (m + CN_TM - 1) / CN_TM;
+  const int tile = blockIdx.x % (ntm * ntn), split = blockIdx.x / (ntm * ntn);
+  const int m0 = (tile / ntn) * CN_TM, n0 = (tile % ntn) * CN_TN;
+  const int kb = split * CN_KCH, ke = min(k, kb + CN_KCH);
+  double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  for (int k0 = kb; k0 < ke; k0 += KC) {
+    for (int e = tid; e < KC * CN_TM; e += NT) {
+      const int kk = e / CN_TM, i = e - kk * CN_TM;
+      z_t v = zmake(0.0, 0.0);
+      if (k0 + kk < ke && m0 + i < m) v = A[(int64_t)(k0 + kk) * lda + m0 + i];
+      As[i * CN_LDA + kk] = zmake(v.x, -v.y);
+    }
+    for (int e = tid; e < KC * CN_TN; e += NT) {
+      const int kk = e / CN_TN, j = e - kk * CN_TN;
+      z_t v = zmake(0.0, 0.0);
+      if (k0 + kk < ke && n0 + j < n) v = B[(int64_t)(k0 + kk) * ldb + n0 + j];
+      Bs[kk * CN_LDB + j] = v;
+    }
+    __syncthreads();
+    blk::warp_cmma<2, 2, false>(cr, ci, As + (wm * 16) * CN_LDA, CN_LDA, Bs + wn * 16, CN_LDB, KC / 4);
+    __syncthreads();
+  }
+  z_t* P = part + (int64_t)split * m * n;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int row = m0 + wm * 16 + i * 8 + (lane >> 2);
+        const int col = n0 + wn * 16 + j * 8 + 2 * (lane & 3) + v;
+        if (row < m && col < n) P[(int64_t)row * n + col] = zmake(cr[i][j][v], ci[i][j][v]);
+      }
+}
+
+__global__ void zgemm_cn_reduce_kernel(int m, int n, int nsplit, const z_t* __restrict__ part, z_t alpha,
+                                       z_t beta, z_t* __restrict__ C, int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)m * n) return;
+  z_t acc = zmake(0.0, 0.0);
+  for (int s = 0; s < nsplit; ++s) acc = zadd(acc, part[(int64_t)s * m * n + e]);  // fixed order
+  const int64_t i = e / n, j = e - i * n;
+  z_t out = zmul(alpha, acc);
+  if (beta.x != 0.0 || beta.y != 0.0) out = zfma(out, beta, C[i * ldc + j]);
+  C[i * ldc + j] = out;
+}
+
+size_t zgemm_workspace_bytes(char transa, int m, int n, int k) {
+  if (transa == 'N' || transa == 'n') return 0;
+  const int64_t nsplit = (k + CN_KCH - 1) / CN_KCH;
+  return (size_t)nsplit * m * n * sizeof(z_t);
+}
+
+int zgemm(char transa, int m, int n, int k, z_t alpha, const z_t* A, int64_t lda, const z_t* B,
+          int64_t ldb, z_t beta, z_t* C, int64_t ldc, void* work, size_t work_bytes,
+          cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  if (transa == 'N' || transa == 'n') {
+    if (k <= 0) {
+      set_error("vb_zgemm: k must be positive");
+      return 1;
+    }
+    const int ntiles = ((m + 63) / 64) * ((n + 31) / 32);
+    int dev = 0, nsm = 148;
+    VB_CUDA(cudaGetDevice(&dev));
+    VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = ntiles < 2 * nsm ? ntiles : 2 * nsm;
+    VB_CUDA(cudaFuncSetAttribute(zgemm_nn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GemmNN::SMEM));
+    zgemm_nn_kernel<<<grid, NT, GemmNN::SMEM, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    VB_LAUNCHED("zgemm_nn_kernel");
+    return 0;
+  }
+  if (transa != 'C' && transa != 'c') {
+    set_error("vb_zgemm: transa must be 'N' or 'C'");
+    return 1;
+  }
+  const int nsplit = (k + CN_KCH - 1) / CN_KCH;
+  VB_CHECK_ARG(k > 0, "vb_zgemm: k must be positive");
+  VB_CHECK_ARG(work && work_bytes >= zgemm_workspace_bytes(transa, m, n, k), "vb_zgemm: workspace too small");
+  const int ntiles = ((m + CN_TM - 1) / CN_TM) * ((n + CN_TN - 1) / CN_TN);
+  zgemm_cn_partial_kernel<<<(unsigned)(ntiles * nsplit), NT, 0, st>>>(m, n, k, A, lda, B, ldb, (z_t*)work);
+  VB_LAUNCHED("zgemm_cn_partial_kernel");
+  const int64_t mn = (int64_t)m * n;
+  zgemm_cn_reduce_kernel<<<(unsigned)((mn + 255) / 256), 256, 0, st>>>(m, n, nsplit, (const z_t*)work,
+                                                                         alpha, beta, C, ldc);
+  VB_LAUNCHED("zgemm_cn_reduce_kernel");
+  return 0;
+}
+
+// --------------------------------------------------------- column norms ---
+// norms[j] = ||W[:, j]||_2, deterministic: fixed row blocks, fixed-order reduce.
+constexpr int NRM_ROWS = 2048;
+
+__global__ void colnorm_partial_kernel(int n, int m, const z_t* __restrict__ W, int64_t ldw,
+                                       double* __restrict__ part) {
+  // block = (row block, column); threads stride the rows of the block
+  const int nb = (n + NRM_ROWS - 1) / NRM_ROWS;
+  const int rb = blockIdx.x % nb, j = blockIdx.x / nb;
+  const int r0 = rb * NRM_ROWS, r1 = min(n, r0 + NRM_ROWS);
+  double s = 0.0;
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) s += zabs2(W[(int64_t)i * ldw + j]);
+  __shared__ double red[32];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    s = warp_sum(s);
+    if (threadIdx.x == 0) part[(int64_t)j * nb + rb] = s;
+  }
+}
+
+__global__ void colnorm_final_kernel(int m, int nb, const double* __restrict__ part, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)j * nb + b];
+  out[j] = sqrt(s);
+}
+
+size_t column_norms_workspace_bytes(int n, int m) {
+  const int nb = (n + NRM_ROWS - 1) / NRM_ROWS;
+  return (size_t)nb * m * sizeof(double);
+}
+
+int column_norms(int n, int m, const z_t* W, int64_t ldw, double* out, void* work, size_t wb,
+                 cudaStream_t st) {
+  if (m <= 0) return 0;
+  VB_CHECK_ARG(n > 0, "vb_column_norms: n must be positive");
+  VB_CHECK_ARG(work && wb >= column_norms_workspace_bytes(n, m), "vb_column_norms: workspace too small");
+  const int nb = (n + NRM_ROWS - 1) / NRM_ROWS;
+  colnorm_partial_kernel<<<(unsigned)(nb * m), 256, 0, st>>>(n, m, W, ldw, (double*)work);
+  VB_LAUNCHED("colnorm_partial_kernel");
+  colnorm_final_kernel<<<(m + 127) / 128, 128, 0, st>>>(m, nb, (const double*)work, out);
+  VB_LAUNCHED("colnorm_final_kernel");
+  return 0;
+}
+
+// W[:, j] *= scale[j] for the m columns.
+__global__ void scale_columns_kernel(int n, int m, z_t* W, int64_t ldw, const double* scale) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * m) return;
+  const int64_t i = e / m, j = e - i * m;
+  const double s = scale[j];
+  z_t* p = W + i * ldw + j;
+  *p = zmake(p->x * s, p->y * s);
+}
+
+int scale_columns(int n, int m, z_t* W, int64_t ldw, const double* scale, cudaStream_t st) {
+  const int64_t tot = (int64_t)n * m;
+  if (tot <= 0) return 0;
+  scale_columns_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, m, W, ldw, scale);
+  VB_LAUNCHED("scale_columns_kernel");
+  return 0;
+}
+
+}  // namespace vb

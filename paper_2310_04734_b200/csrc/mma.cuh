@@ -1,0 +1,323 @@
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) complex-MMA building blocks and
+// cp.async helpers shared by the sweep, GEMM and LU kernels.
+#pragma once
+#include "common.cuh"
+
+namespace vb {
+namespace blk {
+
+constexpr int NT = 256;  // threads per CTA (8 warps)
+constexpr int NB = 64;   // outer panel width
+constexpr int KC = 16;   // complex k-chunk per shared-memory stage
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Warp-level complex MMA on shared-memory operands, 8x8 fragments:
+// acc (FM x FN fragments of the warp tile) += sign * A(rows) * B(cols) over
+// `k4` steps of 4.  A: row-major [m][k] with leading dim lda (complex),
+// B: row-major [k][n] with leading dim ldb.  Fragment layouts of
+// mma.m8n8k4.row.col.f64: A[lane/4][lane%4], B[k=lane%4][n=lane/4],
+// C[lane/4][2*(lane%4)+v].
+template <int FM, int FN, bool NEG>
+__device__ __forceinline__ void warp_cmma(double (&cr)[FM][FN][2], double (&ci)[FM][FN][2],
+                                          const z_t* as, int lda, const z_t* bs, int ldb,
+                                          int k4) {
+  const int lane = threadIdx.x & 31;
+  const int ar = lane >> 2, ak = lane & 3;
+#pragma unroll 2
+  for (int kk = 0; kk < k4; ++kk) {
+    z_t a[FM], b[FN];
+#pragma unroll
+    for (int i = 0; i < FM; ++i) a[i] = as[(i * 8 + ar) * lda + kk * 4 + ak];
+#pragma unroll
+    for (int j = 0; j < FN; ++j) b[j] = bs[(kk * 4 + ak) * ldb + j * 8 + ar];
+#pragma unroll
+    for (int j = 0; j < FN; ++j) {
+      // C -= A B :  Cr += ar(-br) + ai(bi) ; Ci += ar(-bi) + ai(-br)
+      // C += A B :  Cr += ar(br) + ai(-bi) ; Ci += ar(bi) + ai(br)
+      const double br = NEG ? -b[j].x : b[j].x;
+      const double bi = NEG ? -b[j].y : b[j].y;
+      const double nbi = -bi;
+#pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        dmma(cr[i][j][0], cr[i][j][1], a[i].x, br);
+        dmma(cr[i][j][0], cr[i][j][1], a[i].y, nbi);
+        dmma(ci[i][j][0], ci[i][j][1], a[i].x, bi);
+        dmma(ci[i][j][0], ci[i][j][1], a[i].y, br);
+      }
+    }
+  }
+}
+
+
+// CTA-wide C[M x N] -= A[M x K] * B[K x N] on global (workspace) operands.
+// Tiles TM x TN over WM x WN warps.  One flat software pipeline runs over all
+// (tile, k-chunk) iterations: A/B chunks stream through a STAGES-deep
+// cp.async ring, and the C tile of the next output tile is prefetched into
+// shared memory while the current tile computes, so neither the operand nor
+// the C-tile latency is exposed at tile boundaries.  Accumulation starts from
+// zero; the epilogue writes C_old - A*B (SUB) or A*B (!SUB, C not read).
+// Epilogue modes: EPI_SUB  C = C_old - A*B   (LU updates)
+//                 EPI_SET  C = A*B           (C not read)
+//                 EPI_AXPBY C = alpha*A*B + beta*C_old
+enum { EPI_SUB = 0, EPI_SET = 1, EPI_AXPBY = 2 };
+
+template <int TM, int TN, int WM, int WN, int STAGES, int EPI>
+struct Gemm {
+  static constexpr bool SUB = EPI != EPI_SET;  // reads C_old
+  static_assert(WM * WN == NT / 32, "warp grid");
+  static constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
+  static constexpr int LDA = KC + 4;  // == 4 (mod 8): conflict-free 128-bit fragment loads
+  static constexpr int LDB = TN + 2;  // == 2 (mod 8)
+  static constexpr int LDC = TN + 1;  // == 1 (mod 8): conflict-free epilogue reads
+  static constexpr int A_EL = TM * LDA, B_EL = KC * LDB, C_EL = TM * LDC;
+  static constexpr size_t SMEM = (size_t)(STAGES * (A_EL + B_EL) + (SUB ? C_EL : 0)) * sizeof(z_t);
+
+  __device__ static void load_chunk(z_t* As, z_t* Bs, const z_t* A, int lda, const z_t* B, int ldb,
+                                    int M, int N, int K, int m0, int n0, int k0) {
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < (TM * KC + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      if ((TM * KC) % NT == 0 || e < TM * KC) {
+        const int i = e / KC, k = e % KC;
+        const bool p = (m0 + i < M) && (k0 + k < K);
+        cp_async16(As + i * LDA + k, p ? A + (size_t)(m0 + i) * lda + k0 + k : A, p);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < (KC * TN + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      if ((KC * TN) % NT == 0 || e < KC * TN) {
+        const int k = e / TN, j = e % TN;
+        const bool p = (k0 + k < K) && (n0 + j < N);
+        cp_async16(Bs + k * LDB + j, p ? B + (size_t)(k0 + k) * ldb + n0 + j : B, p);
+      }
+    }
+  }
+
+  __device__ static void load_c(z_t* Cs, const z_t* C, int ldc, int M, int N, int m0, int n0) {
+    const int tid = threadIdx.x;
+#pragma unroll 4
+    for (int e = tid; e < TM * TN; e += NT) {
+      const int i = e / TN, j = e % TN;
+      const bool p = (m0 + i < M) && (n0 + j < N);
+      cp_async16(Cs + i * LDC + j, p ? C + (size_t)(m0 + i) * ldc + n0 + j : C, p);
+    }
+  }
+
+  // Tiles t = t_first, t_first + t_step, ... of the (M/TM) x (N/TN) grid (row-major);
+  // the default covers all tiles with one CTA.
+  __device__ static void run(z_t* C, int ldc, const z_t* A, int lda, const z_t* B, int ldb, int M,
+                             int N, int K, z_t* smem, z_t alpha = zmake(1.0, 0.0),
+                             z_t beta = zmake(0.0, 0.0), int t_first = 0, int t_step = 1) {
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    z_t* As = smem;
+    z_t* Bs = smem + STAGES * A_EL;
+    z_t* Cs = Bs + STAGES * B_EL;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
+    const int ntiles = ((M + TM - 1) / TM) * ntn;
+    if (t_first >= ntiles) return;
+    const int my_tiles = (ntiles - t_first + t_step - 1) / t_step;
+    const int T = my_tiles * nk;
+    auto issue = [&](int j) {
+      if (j < T) {
+        const int t = t_first + (j / nk) * t_step, kc = j - (j / nk) * nk;
+        load_chunk(As + (j % STAGES) * A_EL, Bs + (j % STAGES) * B_EL, A, lda, B, ldb, M, N, K,
+                   (t / ntn) * TM, (t % ntn) * TN, kc * KC);
+      }
+    };
+    if (SUB) load_c(Cs, C, ldc, M, N, (t_first / ntn) * TM, (t_first % ntn) * TN);
+#pragma unroll
+    for (int j = 0; j < STAGES - 1; ++j) {
+      issue(j);
+      cp_commit();
+    }
+    double cr[FM][FN][2], ci[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int it = 0; it < T; ++it) {
+      const int t = t_first + (it / nk) * t_step, kc = it - (it / nk) * nk;
+      cp_wait<STAGES - 2>();
+      __syncthreads();
+      issue(it + STAGES - 1);
+      if (SUB && kc == 0 && it > 0) load_c(Cs, C, ldc, M, N, (t / ntn) * TM, (t % ntn) * TN);
+      cp_commit();
+      const int st = it % STAGES;
+      int k4 = min(KC, K - kc * KC);
+      k4 = (k4 + 3) >> 2;
+      warp_cmma<FM, FN, false>(cr, ci, As + st * A_EL + (wm * FM * 8) * LDA, LDA,
+                               Bs + st * B_EL + wn * FN * 8, LDB, k4);
+      if (kc == nk - 1) {
+        if (SUB && nk < STAGES) {  // the C-tile group may still be in flight
+          cp_wait<0>();
+          __syncthreads();
+        }
+        const int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int lr = wm * FM * 8 + i * 8 + (lane >> 2);
+              const int lc = wn * FN * 8 + j * 8 + 2 * (lane & 3) + v;
+              if (m0 + lr < M && n0 + lc < N) {
+                const z_t acc = zmake(cr[i][j][v], ci[i][j][v]);
+                z_t out;
+                if (EPI == EPI_SUB) {
+                  const z_t c = Cs[lr * LDC + lc];
+                  out = zmake(c.x - acc.x, c.y - acc.y);
+                } else if (EPI == EPI_SET) {
+                  out = zmul(alpha, acc);
+                } else if (beta.x == 0.0 && beta.y == 0.0) {
+                  out = zmul(alpha, acc);  // C_old never contributes (may be uninitialised)
+                } else {
+                  out = zfma(zmul(alpha, acc), beta, Cs[lr * LDC + lc]);
+                }
+                C[(size_t)(m0 + lr) * ldc + n0 + lc] = out;
+              }
+              cr[i][j][v] = 0.0;
+              ci[i][j][v] = 0.0;
+            }
+      }
+    }
+    cp_wait<0>();
+  }
+};
+
+
+// In-place inverse of a 64 x 64 triangular matrix in shared memory by recursive
+// doubling: 8x8 diagonal blocks per warp, then three levels of
+// [A 0; C D]^-1 = [A^-1 0; -D^-1 C A^-1 D^-1]  (lower, unit diagonal) or
+// [A B; 0 D]^-1 = [A^-1 -A^-1 B D^-1; 0 D^-1]  (upper, general diagonal).
+// 13 barriers instead of one per row.
+template <bool LOWER>
+__device__ __noinline__ void tri_inv64(z_t* T, int ld) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const int o = warp * 8, j = lane;
+    z_t x[8];
+    if (lane < 8) {
+      if (LOWER) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = zmake(i == j ? 1.0 : 0.0, 0.0);
+#pragma unroll
+        for (int i = 1; i < 8; ++i) {
+          if (i > j) {
+            z_t acc = zmake(0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k >= j && k < i) acc = zfma(acc, T[(o + i) * ld + o + k], x[k]);
+            x[i] = zmake(-acc.x, -acc.y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = zmake(0.0, 0.0);
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          if (i <= j) {
+            z_t acc = zmake(i == j ? 1.0 : 0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k > i && k <= j) acc = zfms(acc, T[(o + i) * ld + o + k], x[k]);
+            x[i] = zmul(acc, zrecip(T[(o + i) * ld + o + i]));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane < 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (LOWER ? (i > j) : (i <= j)) T[(o + i) * ld + o + j] = x[i];
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int h = 8; h < 64; h *= 2) {
+    const int hh = h * h, nel = (64 / (2 * h)) * hh;  // = 32 h <= 1024
+    z_t tv[4];
+    // step 1: T = C A^-1 (lower) or T = B D^-1 (upper), into the off-diagonal block
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        z_t acc = zmake(0.0, 0.0);
+        if (LOWER) {
+          for (int k = j; k < h; ++k) acc = zfma(acc, T[(o + h + i) * ld + o + k], T[(o + k) * ld + o + j]);
+        } else {
+          for (int k = 0; k <= j; ++k)
+            acc = zfma(acc, T[(o + i) * ld + o + h + k], T[(o + h + k) * ld + o + h + j]);
+        }
+        tv[q] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        if (LOWER) T[(o + h + i) * ld + o + j] = tv[q];
+        else T[(o + i) * ld + o + h + j] = tv[q];
+      }
+    }
+    __syncthreads();
+    // step 2: X = -D^-1 T (lower) or X = -A^-1 T (upper)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        z_t acc = zmake(0.0, 0.0);
+        if (LOWER) {
+          for (int k = 0; k <= i; ++k)
+            acc = zfma(acc, T[(o + h + i) * ld + o + h + k], T[(o + h + k) * ld + o + j]);
+        } else {
+          for (int k = i; k < h; ++k) acc = zfma(acc, T[(o + i) * ld + o + k], T[(o + k) * ld + o + h + j]);
+        }
+        tv[q] = zmake(-acc.x, -acc.y);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * NT;
+      if (e < nel) {
+        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
+        const int o = pn * 2 * h;
+        if (LOWER) T[(o + h + i) * ld + o + j] = tv[q];
+        else T[(o + i) * ld + o + h + j] = tv[q];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace blk
+}  // namespace vb

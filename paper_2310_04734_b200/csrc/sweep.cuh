@@ -38,4 +38,18 @@ int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* 
 int quad9_face_mass(int n_faces, const double* xyz, const int32_t* fconn, double* Fe,
                     cudaStream_t stream);
 
+
+// linalg.cu
+int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
+             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st);
+int csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
+                   z_t alpha, z_t* D, int64_t ldd, cudaStream_t st);
+size_t zgemm_workspace_bytes(char transa, int m, int n, int k);
+int zgemm(char transa, int m, int n, int k, z_t alpha, const z_t* A, int64_t lda, const z_t* B,
+          int64_t ldb, z_t beta, z_t* C, int64_t ldc, void* work, size_t work_bytes, cudaStream_t st);
+size_t column_norms_workspace_bytes(int n, int m);
+int column_norms(int n, int m, const z_t* W, int64_t ldw, double* out, void* work, size_t wb,
+                 cudaStream_t st);
+int scale_columns(int n, int m, z_t* W, int64_t ldw, const double* scale, cudaStream_t st);
+
 }  // namespace vb

@@ -1,0 +1,103 @@
+"""Thin torch-facing wrappers of the C-ABI linear-algebra entry points
+(vb_csr_spmm, vb_csr_axpy_dense, vb_zgemm, vb_column_norms, vb_scale_columns).
+All tensors are CUDA, complex128 row-major (2-D views with a row stride)."""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .assembly import DeviceCSR
+
+CDT = torch.complex128
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.dim() == 1:
+        return 1
+    if t.stride(1) != 1:
+        raise ValueError("row-major tensor with unit column stride expected")
+    return t.stride(0)
+
+
+def _cols(t: torch.Tensor) -> int:
+    return 1 if t.dim() == 1 else t.shape[1]
+
+
+def spmm(A: DeviceCSR, X: torch.Tensor, alpha=1.0, beta=0.0, Y: torch.Tensor | None = None):
+    """Y = alpha A X + beta Y (A real CSR, X/Y complex)."""
+    lib = _lib.load()
+    k = _cols(X)
+    if Y is None:
+        Y = torch.empty((A.n, k) if X.dim() == 2 else (A.n,), dtype=CDT, device=X.device)
+        beta = 0.0
+    ldx = _ld(X) if X.dim() == 2 else 1
+    ldy = _ld(Y) if Y.dim() == 2 else 1
+    _lib.check(lib.vb_csr_spmm(A.n, _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(A.data), k,
+                               C_ptr(X), ldx, C_ptr(Y), ldy, _lib.zc(alpha), _lib.zc(beta),
+                               _lib.stream_handle()), "vb_csr_spmm")
+    return Y
+
+
+def C_ptr(t: torch.Tensor):
+    import ctypes
+    if not t.is_cuda:
+        raise RuntimeError("vibro_b200: expected a CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def axpy_dense(A: DeviceCSR, alpha, D: torch.Tensor):
+    lib = _lib.load()
+    _lib.check(lib.vb_csr_axpy_dense(A.n, _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(A.data),
+                                     _lib.zc(alpha), C_ptr(D), _ld(D), _lib.stream_handle()),
+               "vb_csr_axpy_dense")
+    return D
+
+
+def zgemm(transa: str, A: torch.Tensor, B: torch.Tensor, alpha=1.0, beta=0.0,
+          C: torch.Tensor | None = None, m: int | None = None, n: int | None = None,
+          k: int | None = None) -> torch.Tensor:
+    """transa 'N': C = alpha A B + beta C;  'C': C = alpha A^H B + beta C."""
+    lib = _lib.load()
+    A2 = A if A.dim() == 2 else A.view(-1, 1)
+    B2 = B if B.dim() == 2 else B.view(-1, 1)
+    if transa == "N":
+        m = A2.shape[0] if m is None else m
+        k = A2.shape[1] if k is None else k
+    else:
+        k = A2.shape[0] if k is None else k
+        m = A2.shape[1] if m is None else m
+    n = B2.shape[1] if n is None else n
+    if C is None:
+        C = torch.empty((m, n), dtype=CDT, device=A.device)
+        beta = 0.0
+    C2 = C if C.dim() == 2 else C.view(-1, 1)
+    wb = lib.vb_zgemm_workspace_bytes(transa.encode(), m, n, k)
+    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=A.device)
+    _lib.check(lib.vb_zgemm(transa.encode(), m, n, k, _lib.zc(alpha), C_ptr(A2), _ld(A2), C_ptr(B2),
+                            _ld(B2), _lib.zc(beta), C_ptr(C2), _ld(C2), C_ptr(work), wb,
+                            _lib.stream_handle()), "vb_zgemm")
+    return C
+
+
+def column_norms(W: torch.Tensor, m: int | None = None) -> torch.Tensor:
+    lib = _lib.load()
+    W2 = W if W.dim() == 2 else W.view(-1, 1)
+    n = W2.shape[0]
+    m = W2.shape[1] if m is None else m
+    out = torch.empty(m, dtype=torch.float64, device=W.device)
+    wb = lib.vb_column_norms_workspace_bytes(n, m)
+    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=W.device)
+    _lib.check(lib.vb_column_norms(n, m, C_ptr(W2), _ld(W2), C_ptr(out), C_ptr(work), wb,
+                                   _lib.stream_handle()), "vb_column_norms")
+    return out
+
+
+def scale_columns(W: torch.Tensor, scale: torch.Tensor, m: int | None = None):
+    lib = _lib.load()
+    W2 = W if W.dim() == 2 else W.view(-1, 1)
+    m = W2.shape[1] if m is None else m
+    _lib.check(lib.vb_scale_columns(W2.shape[0], m, C_ptr(W2), _ld(W2),
+                                    C_ptr(scale.to(torch.float64).contiguous()), _lib.stream_handle()),
+               "vb_scale_columns")
+    return W

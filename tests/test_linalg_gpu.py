@@ -1,0 +1,87 @@
+"""GPU SpMM / dense scatter / DMMA ZGEMM / column norms vs numpy/scipy."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev_csr(A, cuda):
+    import torch
+    from paper_2310_04734_b200.assembly import DeviceCSR
+    A = sp.csr_matrix(A)
+    return DeviceCSR(A.shape[0], torch.as_tensor(A.indptr.astype(np.int32), device=cuda),
+                     torch.as_tensor(A.indices.astype(np.int32), device=cuda),
+                     torch.as_tensor(A.data, device=cuda))
+
+
+def _c(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+@pytest.mark.parametrize("k", [1, 3, 32, 45])
+def test_spmm(cuda, k):
+    import torch
+    from paper_2310_04734_b200 import linalg
+    rng = np.random.default_rng(k)
+    A = sp.random(300, 300, density=0.05, random_state=k, format="csr")
+    X = _c(rng, 300, k)
+    Y0 = _c(rng, 300, k)
+    alpha, beta = 0.5 - 2j, 1.5 + 0.25j
+    Xd = torch.as_tensor(X, device=cuda)
+    Yd = torch.as_tensor(Y0, device=cuda)
+    linalg.spmm(_dev_csr(A, cuda), Xd if k > 1 else Xd[:, 0], alpha, beta, Yd if k > 1 else Yd[:, 0].contiguous())
+    if k > 1:
+        np.testing.assert_allclose(Yd.cpu().numpy(), alpha * (A @ X) + beta * Y0, rtol=1e-13, atol=1e-12)
+    out = linalg.spmm(_dev_csr(A, cuda), Xd)
+    np.testing.assert_allclose(out.cpu().numpy(), A @ X, rtol=1e-13, atol=1e-12)
+
+
+def test_axpy_dense(cuda):
+    import torch
+    from paper_2310_04734_b200 import linalg
+    rng = np.random.default_rng(1)
+    A = sp.random(50, 50, density=0.2, random_state=1, format="csr")
+    D0 = _c(rng, 50, 50)
+    Dd = torch.as_tensor(D0, device=cuda)
+    linalg.axpy_dense(_dev_csr(A, cuda), 2 - 1j, Dd)
+    np.testing.assert_allclose(Dd.cpu().numpy(), D0 + (2 - 1j) * A.toarray(), rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("m,n,k", [(32, 32, 4641), (76, 76, 8102), (5, 1, 1000), (400, 40, 3000), (1, 7, 13)])
+def test_zgemm_conj(cuda, m, n, k):
+    import torch
+    from paper_2310_04734_b200 import linalg
+    rng = np.random.default_rng(m + n + k)
+    A, B, C0 = _c(rng, k, m), _c(rng, k, n), _c(rng, m, n)
+    Cd = torch.as_tensor(C0, device=cuda)
+    linalg.zgemm("C", torch.as_tensor(A, device=cuda), torch.as_tensor(B, device=cuda), 2.0, 0.5j, Cd)
+    ref = 2.0 * A.conj().T @ B + 0.5j * C0
+    np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-12, atol=1e-10 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("m,n,k", [(4641, 8, 32), (100, 33, 70), (1, 1, 1), (257, 16, 513)])
+def test_zgemm_nn(cuda, m, n, k):
+    import torch
+    from paper_2310_04734_b200 import linalg
+    rng = np.random.default_rng(m * n + k)
+    A, B, C0 = _c(rng, m, k), _c(rng, k, n), _c(rng, m, n)
+    Cd = torch.as_tensor(C0, device=cuda)
+    linalg.zgemm("N", torch.as_tensor(A, device=cuda), torch.as_tensor(B, device=cuda), -1.0, 1.0, Cd)
+    ref = C0 - A @ B
+    np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-12, atol=1e-11 * np.abs(ref).max())
+    out = linalg.zgemm("N", torch.as_tensor(A, device=cuda), torch.as_tensor(B, device=cuda))
+    np.testing.assert_allclose(out.cpu().numpy(), A @ B, rtol=1e-12, atol=1e-11 * np.abs(ref).max())
+
+
+def test_column_norms_and_scale(cuda):
+    import torch
+    from paper_2310_04734_b200 import linalg
+    rng = np.random.default_rng(3)
+    W = _c(rng, 5000, 7)
+    Wd = torch.as_tensor(W, device=cuda)
+    nr = linalg.column_norms(Wd).cpu().numpy()
+    np.testing.assert_allclose(nr, np.linalg.norm(W, axis=0), rtol=1e-14)
+    linalg.scale_columns(Wd, torch.as_tensor(1 / nr, device=cuda))
+    np.testing.assert_allclose(np.linalg.norm(Wd.cpu().numpy(), axis=0), 1.0, rtol=1e-14)
