@@ -149,6 +149,29 @@ int vb_zgemm(char transa, int m, int n, int k, vb_complex alpha, const vb_comple
              const vb_complex* B, int64_t ldb, vb_complex beta, vb_complex* C, int64_t ldc, void* work,
              size_t work_bytes, void* stream);
 
+/*
+ * Dense complex LU with partial pivoting of ONE n x n matrix (row-major, lda),
+ * in place, on the whole GPU (persistent cooperative kernel).  The full-order
+ * solver at expansion / certification frequencies: replaces scipy
+ * splu(csc(A(f))) in vibrofem/mor.py:48-49, 153-156 (and the residual
+ * contract of solvers.py:62-78) for n up to ~25k.  Pivoting follows LAPACK
+ * zgetf2 (izamax: max |Re|+|Im|, lowest row on ties).
+ *  ipiv [n] out (0-based row interchanged with row j at step j)
+ *  info [1] out (device): 0, or k+1 for the first exactly-zero pivot
+ *  aux  out: diagonal-block inverses + permutation used by vb_zgetrs
+ *  (vb_zgetrf_aux_bytes(n)); keep it with the factors.
+ */
+size_t vb_zgetrf_workspace_bytes(int n);
+size_t vb_zgetrf_aux_bytes(int n);
+int vb_zgetrf(int n, vb_complex* A, int64_t lda, int32_t* ipiv, int32_t* info, void* aux,
+              size_t aux_bytes, void* work, size_t work_bytes, void* stream);
+
+/* X = A^-1 B from vb_zgetrf factors (1 <= nrhs <= 16; B may alias X).
+ * Replaces SuperLU `lu.solve` (vibrofem/mor.py:49, 156, 166, 175). */
+size_t vb_zgetrs_workspace_bytes(int n, int nrhs);
+int vb_zgetrs(int n, int nrhs, const vb_complex* LU, int64_t lda, const void* aux, const vb_complex* B,
+              int64_t ldb, vb_complex* X, int64_t ldx, void* work, size_t work_bytes, void* stream);
+
 /* norms[j] = ||W[:, j]||_2 for an n x m complex row-major W (deterministic). */
 size_t vb_column_norms_workspace_bytes(int n, int m);
 int vb_column_norms(int n, int m, const vb_complex* W, int64_t ldw, double* norms, void* work,

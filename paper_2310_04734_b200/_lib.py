@@ -55,6 +55,13 @@ _SIGS = {
     "vb_column_norms": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t,
                                   C.c_void_p]),
     "vb_scale_columns": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vb_zgetrf_workspace_bytes": (C.c_size_t, [C.c_int]),
+    "vb_zgetrf_aux_bytes": (C.c_size_t, [C.c_int]),
+    "vb_zgetrf": (C.c_int, [C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                            C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vb_zgetrs_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "vb_zgetrs": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, _z, C.c_int64, _z, C.c_int64,
+                            C.c_void_p, C.c_size_t, C.c_void_p]),
     "vb_rom_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _z, _z, _z, C.c_int64,
                                _z, _z, C.c_void_p, _z, C.c_void_p, C.c_void_p, C.c_size_t,
                                C.c_void_p]),

@@ -141,4 +141,22 @@ int vb_scale_columns(int n, int m, vb_complex* W, int64_t ldw, const double* sca
   return vb::scale_columns(n, m, (z_t*)W, ldw, scale, (cudaStream_t)stream);
 }
 
+size_t vb_zgetrf_workspace_bytes(int n) { return vb::zgetrf_workspace_bytes(n); }
+size_t vb_zgetrf_aux_bytes(int n) { return vb::zgetrf_aux_bytes(n); }
+
+int vb_zgetrf(int n, vb_complex* A, int64_t lda, int32_t* ipiv, int32_t* info, void* aux,
+              size_t aux_bytes, void* work, size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(A && ipiv && info, "vb_zgetrf: null pointer");
+  return vb::zgetrf(n, (z_t*)A, lda, ipiv, info, aux, aux_bytes, work, work_bytes, (cudaStream_t)stream);
+}
+
+size_t vb_zgetrs_workspace_bytes(int n, int nrhs) { return (size_t)n * nrhs * sizeof(vb_complex); }
+
+int vb_zgetrs(int n, int nrhs, const vb_complex* LU, int64_t lda, const void* aux, const vb_complex* B,
+              int64_t ldb, vb_complex* X, int64_t ldx, void* work, size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(LU && aux && B && X, "vb_zgetrs: null pointer");
+  return vb::zgetrs(n, nrhs, (const z_t*)LU, lda, aux, (const z_t*)B, ldb, (z_t*)X, ldx, work, work_bytes,
+                    (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -1,0 +1,489 @@
+// Dense complex LU of ONE large matrix across the whole GPU: the full-order
+// solver at the rational expansion points and certification frequencies
+// (SURVEY §8a A6).  Replaces scipy `splu(...).solve` in vibrofem/mor.py:48-49,
+// 153-156 and solvers.py:62-78 for n up to ~25k (cfg1 n = 4,641).
+//
+// A persistent cooperative kernel (one CTA per SM, grid-wide barriers):
+//   panel   : right-looking column steps over the NB = 64 panel; every CTA owns a
+//             contiguous row range.  Per column: local izamax over own rows,
+//             candidate rows + row j published to double-buffered scratch, ONE
+//             grid barrier, then every CTA picks the same pivot (max |Re|+|Im|,
+//             lowest row on ties), swaps/eliminates only its own rows.
+//   swaps   : the panel's interchanges applied to all other columns (LAPACK laswp
+//             on the whole row, so L stays consistent with P).
+//   TRSM    : U12 = L11^-1 A12, L11^-1 by recursive doubling, DMMA strips.
+//   GEMM    : A22 -= L21 U12, DMMA tiles distributed over all CTAs.
+// The diagonal-block inverses L_kk^-1, U_kk^-1 and the final row permutation are
+// kept for the blocked triangular solves of vb_zgetrs.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "mma.cuh"
+#include "sweep.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace vb {
+namespace lu {
+
+using blk::KC;
+using blk::NB;
+using blk::NT;
+
+using GemmLU = blk::Gemm<64, 64, 2, 4, 3, blk::EPI_SUB>;
+constexpr int LDL = NB + 4;
+constexpr int TRS_N = 32;
+constexpr int LDS_B = TRS_N + 2;
+constexpr size_t TRSM_SMEM = (size_t)(NB * LDL + NB * LDS_B) * sizeof(z_t);
+constexpr size_t LU_SMEM = GemmLU::SMEM > TRSM_SMEM ? GemmLU::SMEM : TRSM_SMEM;
+
+struct LuParams {
+  int n;
+  z_t* A;
+  int64_t lda;
+  int* ipiv;      // [n]   row interchanged with row j at step j
+  int* perm;      // [n]   final permutation: row i of P A is row perm[i] of A
+  int* info;      // [1]
+  double* pval;   // [2][grid]
+  int* pidx;      // [2][grid]
+  z_t* prow;      // [2][grid][NB]
+  z_t* rowj;      // [2][NB]
+  z_t* Linv;      // [nblk][NB][NB]
+  z_t* Uinv;      // [nblk][NB][NB]
+};
+
+__device__ __forceinline__ void row_range(int n, int& lo, int& hi) {
+  const int rpc = (n + gridDim.x - 1) / gridDim.x;
+  lo = blockIdx.x * rpc;
+  hi = min(n, lo + rpc);
+}
+
+// Block inverse of the 64x64 diagonal block at (k0, k0) into smem T (LDL),
+// identity-padded beyond nb; LOWER uses the strictly lower part + unit diagonal.
+template <bool LOWER>
+__device__ void load_diag_block(const z_t* A, int64_t lda, int k0, int nb, z_t* T) {
+  for (int e = threadIdx.x; e < NB * NB; e += NT) {
+    const int i = e / NB, j = e - i * NB;
+    z_t v = zmake(i == j ? 1.0 : 0.0, 0.0);
+    if (i < nb && j < nb) {
+      if (LOWER) {
+        if (j < i) v = __ldcg(A + (int64_t)(k0 + i) * lda + k0 + j);
+      } else {
+        v = (j >= i) ? __ldcg(A + (int64_t)(k0 + i) * lda + k0 + j) : zmake(0.0, 0.0);
+      }
+    }
+    T[i * LDL + j] = v;
+  }
+  __syncthreads();
+  blk::tri_inv64<LOWER>(T, LDL);
+}
+
+__global__ void __launch_bounds__(NT, 1) zgetrf_kernel(LuParams P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double2 smem[];
+  __shared__ z_t s_prow[NB];
+  __shared__ z_t s_rowj[NB];
+  __shared__ double rv[NT / 32];
+  __shared__ int ri[NT / 32];
+  __shared__ int s_piv, s_idx;
+  __shared__ double s_val;
+  const int n = P.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int64_t lda = P.lda;
+  z_t* A = P.A;
+  int lo, hi;
+  row_range(n, lo, hi);
+  if (c == 0 && tid == 0) *P.info = 0;
+
+  for (int k0 = 0; k0 < n; k0 += NB) {
+    const int nb = min(NB, n - k0), kend = k0 + nb;
+    // ------------------------------------------------------------ panel
+    for (int j = k0; j < kend; ++j) {
+      const int buf = j & 1;
+      double v = -1.0;
+      int pi = 0x7fffffff;
+      for (int i = max(lo, j) + tid; i < hi; i += NT) {
+        const double a = zabs1(A[(int64_t)i * lda + j]);
+        if (a > v) { v = a; pi = i; }
+      }
+      warp_argmax(v, pi);
+      if (lane == 0) { rv[warp] = v; ri[warp] = pi; }
+      __syncthreads();
+      if (warp == 0) {
+        v = lane < NT / 32 ? rv[lane] : -1.0;
+        pi = lane < NT / 32 ? ri[lane] : 0x7fffffff;
+        warp_argmax(v, pi);
+        if (lane == 0) { s_val = v; s_idx = pi; }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        P.pval[buf * G + c] = s_val;
+        P.pidx[buf * G + c] = s_idx;
+      }
+      if (s_val >= 0.0)
+        for (int t = tid; t < nb; t += NT)
+          P.prow[((int64_t)buf * G + c) * NB + t] = A[(int64_t)s_idx * lda + k0 + t];
+      if (j >= lo && j < hi)
+        for (int t = tid; t < nb; t += NT) P.rowj[buf * NB + t] = A[(int64_t)j * lda + k0 + t];
+      grid.sync();
+      // every CTA resolves the same pivot from the published partials
+      if (warp == 0) {
+        double bv = -1.0;
+        int bi = 0x7fffffff, bc = 0;
+        for (int q = lane; q < G; q += 32) {
+          const double pv = __ldcg(P.pval + buf * G + q);
+          const int px = __ldcg(P.pidx + buf * G + q);
+          if (pv > bv || (pv == bv && px < bi)) { bv = pv; bi = px; bc = q; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; bc = oc; }
+        }
+        if (lane == 0) {
+          s_val = bv;
+          s_piv = bv > 0.0 ? bi : -1;
+          s_idx = bc;
+        }
+      }
+      __syncthreads();
+      const int p = s_piv;
+      if (p < 0) {  // exactly singular column (LAPACK: INFO = j+1, no interchange)
+        if (c == 0 && tid == 0) {
+          if (*P.info == 0) *P.info = j + 1;
+          P.ipiv[j] = j;
+        }
+        __syncthreads();
+        continue;
+      }
+      for (int t = tid; t < nb; t += NT) {
+        s_prow[t] = __ldcg(P.prow + ((int64_t)buf * G + s_idx) * NB + t);
+        s_rowj[t] = __ldcg(P.rowj + buf * NB + t);
+      }
+      if (c == 0 && tid == 0) P.ipiv[j] = p;
+      __syncthreads();
+      const int jj = j - k0;
+      const z_t pinv = zrecip(s_prow[jj]);
+      if (p != j) {
+        if (j >= lo && j < hi)
+          for (int t = tid; t < nb; t += NT) A[(int64_t)j * lda + k0 + t] = s_prow[t];
+      }
+      // eliminate own rows i > j; row p (if swapped) now holds the old row j
+      const int r0 = max(lo, j + 1);
+      const int nrows = hi - r0, ncols = nb - jj - 1;
+      if (nrows > 0) {
+        // multipliers first (column j), then the rank-1 update of the panel
+        for (int i = r0 + tid; i < hi; i += NT) {
+          const z_t aij = (i == p) ? s_rowj[jj] : A[(int64_t)i * lda + j];
+          A[(int64_t)i * lda + j] = zmul(aij, pinv);
+        }
+        if (p != j && p >= r0 && p < hi)
+          for (int t = tid; t < nb; t += NT)
+            if (t != jj) A[(int64_t)p * lda + k0 + t] = s_rowj[t];
+        __syncthreads();
+        if (ncols > 0)
+          for (int e = tid; e < nrows * ncols; e += NT) {
+            const int ii = e / ncols, t = jj + 1 + (e - ii * ncols);
+            const int64_t off = (int64_t)(r0 + ii) * lda;
+            A[off + k0 + t] = zfms(A[off + k0 + t], A[off + j], s_prow[t]);
+          }
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    // ------------------------------------------------------------ swaps
+    {
+      const int64_t ncol = (int64_t)n - nb;
+      for (int64_t q = (int64_t)c * NT + tid; q < ncol; q += (int64_t)G * NT) {
+        const int col = q < k0 ? (int)q : (int)(q + nb);
+        for (int j = k0; j < kend; ++j) {
+          const int p = __ldcg(P.ipiv + j);
+          if (p != j) {
+            const z_t t = A[(int64_t)j * lda + col];
+            A[(int64_t)j * lda + col] = A[(int64_t)p * lda + col];
+            A[(int64_t)p * lda + col] = t;
+          }
+        }
+      }
+    }
+    grid.sync();
+    // ------------------------------------------------------------ TRSM
+    {
+      z_t* Li = smem;
+      z_t* Bs = smem + NB * LDL;
+      const int nblk = k0 / NB;
+      const int nstrips = (n - kend + TRS_N - 1) / TRS_N;
+      if (nstrips > c || c == 0) {
+        load_diag_block<true>(A, lda, k0, nb, Li);
+        if (c == 0)
+          for (int e = tid; e < NB * NB; e += NT) P.Linv[(int64_t)nblk * NB * NB + e] = Li[(e / NB) * LDL + e % NB];
+        const int wm = warp >> 1, wn = warp & 1;
+        for (int st = c; st < nstrips; st += G) {
+          const int cs = kend + st * TRS_N, ncol = min(TRS_N, n - cs);
+          for (int e = tid; e < NB * TRS_N; e += NT) {
+            const int i = e / TRS_N, jx = e - i * TRS_N;
+            Bs[i * LDS_B + jx] = (i < nb && jx < ncol) ? A[(int64_t)(k0 + i) * lda + cs + jx] : zmake(0.0, 0.0);
+          }
+          __syncthreads();
+          double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+          blk::warp_cmma<2, 2, false>(cr, ci, Li + (wm * 16) * LDL, LDL, Bs + wn * 16, LDS_B, (nb + 3) >> 2);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+              for (int vv = 0; vv < 2; ++vv) {
+                const int row = wm * 16 + a * 8 + (lane >> 2);
+                const int col = wn * 16 + b * 8 + 2 * (lane & 3) + vv;
+                if (row < nb && col < ncol) A[(int64_t)(k0 + row) * lda + cs + col] = zmake(cr[a][b][vv], ci[a][b][vv]);
+              }
+          __syncthreads();
+        }
+      }
+      // U_kk^-1 for the triangular solves (U11 is final after the panel)
+      if (c == (G > 1 ? 1 : 0)) {
+        __syncthreads();
+        load_diag_block<false>(A, lda, k0, nb, Li);
+        for (int e = tid; e < NB * NB; e += NT) P.Uinv[(int64_t)nblk * NB * NB + e] = Li[(e / NB) * LDL + e % NB];
+      }
+    }
+    grid.sync();
+    // ------------------------------------------------------------ GEMM
+    if (kend < n) {
+      GemmLU::run(A + (int64_t)kend * lda + kend, (int)lda, A + (int64_t)kend * lda + k0, (int)lda,
+                  A + (int64_t)k0 * lda + kend, (int)lda, n - kend, n - kend, nb, smem,
+                  zmake(1.0, 0.0), zmake(0.0, 0.0), c, G);
+    }
+    grid.sync();
+  }
+  // final permutation from the interchange sequence (LAPACK ipiv semantics)
+  if (c == 0) {
+    for (int i = tid; i < n; i += NT) P.perm[i] = i;
+    __syncthreads();
+    if (tid == 0)
+      for (int j = 0; j < n; ++j) {
+        const int p = P.ipiv[j];
+        if (p != j) {
+          const int t = P.perm[j];
+          P.perm[j] = P.perm[p];
+          P.perm[p] = t;
+        }
+      }
+  }
+}
+
+// ---------------------------------------------------------------- solve ---
+struct SolveParams {
+  int n, nrhs;
+  const z_t* LU;
+  int64_t lda;
+  const int* perm;
+  const z_t* Linv;
+  const z_t* Uinv;
+  const z_t* B;   // input RHS (may alias X)
+  int64_t ldb;
+  z_t* X;         // output / work, n x nrhs
+  int64_t ldx;
+  z_t* tmp;       // n x nrhs scratch for the permuted RHS when B aliases X
+};
+
+constexpr int MAXRHS = 16;
+
+__global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double2 smem_s[];
+  z_t* Ti = smem_s;                 // NB x (NB+1)
+  z_t* yb = smem_s + NB * (NB + 1);  // NB x MAXRHS
+  const int n = S.n, s = S.nrhs, tid = threadIdx.x;
+  const int G = gridDim.x, c = blockIdx.x;
+  int lo, hi;
+  row_range(n, lo, hi);
+  // X = P B
+  for (int64_t e = (int64_t)c * NT + tid; e < (int64_t)n * s; e += (int64_t)G * NT) {
+    const int i = (int)(e / s), q = (int)(e - (int64_t)i * s);
+    S.tmp[(int64_t)i * s + q] = S.B[(int64_t)S.perm[i] * S.ldb + q];
+  }
+  grid.sync();
+  for (int64_t e = (int64_t)c * NT + tid; e < (int64_t)n * s; e += (int64_t)G * NT) {
+    const int i = (int)(e / s), q = (int)(e - (int64_t)i * s);
+    S.X[(int64_t)i * S.ldx + q] = __ldcg(S.tmp + (int64_t)i * s + q);
+  }
+  grid.sync();
+  const int nblk = (n + NB - 1) / NB;
+  // forward: L y = P b, right-looking by diagonal blocks
+  for (int kb = 0; kb < nblk; ++kb) {
+    const int k0 = kb * NB, nb = min(NB, n - k0), kend = k0 + nb;
+    for (int e = tid; e < NB * NB; e += NT) Ti[(e / NB) * (NB + 1) + e % NB] = __ldcg(S.Linv + (int64_t)kb * NB * NB + e);
+    for (int e = tid; e < nb * s; e += NT) yb[e] = __ldcg(S.X + (int64_t)(k0 + e / s) * S.ldx + e % s);
+    __syncthreads();
+    // y_kb = Linv * b_kb (every CTA redundantly; the owner writes it back)
+    z_t yv[(NB * MAXRHS + NT - 1) / NT];
+#pragma unroll
+    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      yv[q] = zmake(0.0, 0.0);
+      if (e < nb * s) {
+        const int i = e / s, r = e - i * s;
+        z_t acc = zmake(0.0, 0.0);
+        for (int k = 0; k <= i; ++k) acc = zfma(acc, Ti[i * (NB + 1) + k], yb[k * s + r]);
+        yv[q] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      if (e < nb * s) {
+        yb[e] = yv[q];
+        const int i = k0 + e / s;
+        if (i >= lo && i < hi) S.X[(int64_t)i * S.ldx + e % s] = yv[q];
+      }
+    }
+    __syncthreads();
+    // own rows below the block: b_i -= L[i, k0:kend] y_kb
+    for (int64_t e = tid; e < (int64_t)max(0, hi - max(lo, kend)) * s; e += NT) {
+      const int i = max(lo, kend) + (int)(e / s), r = (int)(e % s);
+      z_t acc = S.X[(int64_t)i * S.ldx + r];
+      const z_t* Lrow = S.LU + (int64_t)i * S.lda + k0;
+      for (int k = 0; k < nb; ++k) acc = zfms(acc, Lrow[k], yb[k * s + r]);
+      S.X[(int64_t)i * S.ldx + r] = acc;
+    }
+    grid.sync();
+  }
+  // backward: U x = y
+  for (int kb = nblk - 1; kb >= 0; --kb) {
+    const int k0 = kb * NB, nb = min(NB, n - k0);
+    for (int e = tid; e < NB * NB; e += NT) Ti[(e / NB) * (NB + 1) + e % NB] = __ldcg(S.Uinv + (int64_t)kb * NB * NB + e);
+    for (int e = tid; e < nb * s; e += NT) yb[e] = __ldcg(S.X + (int64_t)(k0 + e / s) * S.ldx + e % s);
+    __syncthreads();
+    z_t yv[(NB * MAXRHS + NT - 1) / NT];
+#pragma unroll
+    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      yv[q] = zmake(0.0, 0.0);
+      if (e < nb * s) {
+        const int i = e / s, r = e - i * s;
+        z_t acc = zmake(0.0, 0.0);
+        for (int k = i; k < nb; ++k) acc = zfma(acc, Ti[i * (NB + 1) + k], yb[k * s + r]);
+        yv[q] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+      const int e = tid + q * NT;
+      if (e < nb * s) {
+        yb[e] = yv[q];
+        const int i = k0 + e / s;
+        if (i >= lo && i < hi) S.X[(int64_t)i * S.ldx + e % s] = yv[q];
+      }
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < (int64_t)max(0, min(hi, k0) - lo) * s; e += NT) {
+      const int i = lo + (int)(e / s), r = (int)(e % s);
+      z_t acc = S.X[(int64_t)i * S.ldx + r];
+      const z_t* Urow = S.LU + (int64_t)i * S.lda + k0;
+      for (int k = 0; k < nb; ++k) acc = zfms(acc, Urow[k], yb[k * s + r]);
+      S.X[(int64_t)i * S.ldx + r] = acc;
+    }
+    grid.sync();
+  }
+}
+
+constexpr size_t SOLVE_SMEM = (size_t)(NB * (NB + 1) + NB * MAXRHS) * sizeof(z_t);
+
+static int coop_grid(const void* kern, size_t smem, int* grid) {
+  int dev = 0, nsm = 0, per = 0, coop = 0;
+  VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  VB_CUDA(cudaGetDevice(&dev));
+  VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  VB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) {
+    set_error("device does not support cooperative launches");
+    return 2;
+  }
+  VB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, smem));
+  if (per < 1) {
+    set_error("zgetrf/zgetrs kernel does not fit on an SM");
+    return 2;
+  }
+  *grid = nsm;  // one CTA per SM
+  return 0;
+}
+
+}  // namespace lu
+
+size_t zgetrf_workspace_bytes(int n) {
+  int grid = 148;
+  lu::coop_grid((const void*)lu::zgetrf_kernel, lu::LU_SMEM, &grid);
+  const int nblk = (n + lu::NB - 1) / lu::NB;
+  size_t b = 0;
+  b += 2 * (size_t)grid * sizeof(double);
+  b += 2 * (size_t)grid * sizeof(int);
+  b += 2 * (size_t)grid * lu::NB * sizeof(z_t);
+  b += 2 * (size_t)lu::NB * sizeof(z_t);
+  b += 2 * (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
+  return b + 1024;
+}
+
+// Factor data kept for the solves: Linv/Uinv of the diagonal blocks and the
+// permutation live in `factor_aux` (layout below), so a factorisation is
+// (A overwritten by L\U, ipiv, aux).
+size_t zgetrf_aux_bytes(int n) {
+  const int nblk = (n + lu::NB - 1) / lu::NB;
+  return 2 * (size_t)nblk * lu::NB * lu::NB * sizeof(z_t) + (size_t)n * sizeof(int) + 256;
+}
+
+int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size_t aux_bytes, void* work,
+           size_t work_bytes, cudaStream_t st) {
+  VB_CHECK_ARG(n > 0 && lda >= n, "vb_zgetrf: bad sizes");
+  VB_CHECK_ARG(aux && aux_bytes >= zgetrf_aux_bytes(n), "vb_zgetrf: aux too small");
+  int grid = 0;
+  if (int rc = lu::coop_grid((const void*)lu::zgetrf_kernel, lu::LU_SMEM, &grid)) return rc;
+  const int nblk = (n + lu::NB - 1) / lu::NB;
+  VB_CHECK_ARG(work && work_bytes >= zgetrf_workspace_bytes(n), "vb_zgetrf: workspace too small");
+  lu::LuParams P;
+  P.n = n; P.A = A; P.lda = lda; P.ipiv = ipiv; P.info = info_dev;
+  char* w = (char*)work;
+  P.pval = (double*)w; w += 2 * (size_t)grid * sizeof(double);
+  P.pidx = (int*)w; w += 2 * (size_t)grid * sizeof(int);
+  w = (char*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  P.prow = (z_t*)w; w += 2 * (size_t)grid * lu::NB * sizeof(z_t);
+  P.rowj = (z_t*)w; w += 2 * (size_t)lu::NB * sizeof(z_t);
+  char* x = (char*)aux;
+  P.Linv = (z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
+  P.Uinv = (z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
+  P.perm = (int*)x;
+  void* args[] = {&P};
+  VB_CUDA(cudaLaunchCooperativeKernel((const void*)lu::zgetrf_kernel, grid, lu::NT, args, lu::LU_SMEM, st));
+  VB_LAUNCHED("zgetrf_kernel");
+  return 0;
+}
+
+int zgetrs(int n, int nrhs, const z_t* LU, int64_t lda, const void* aux, const z_t* B, int64_t ldb,
+           z_t* X, int64_t ldx, void* work, size_t work_bytes, cudaStream_t st) {
+  VB_CHECK_ARG(n > 0 && nrhs >= 1 && nrhs <= lu::MAXRHS, "vb_zgetrs: 1 <= nrhs <= 16");
+  VB_CHECK_ARG(work && work_bytes >= (size_t)n * nrhs * sizeof(z_t), "vb_zgetrs: workspace too small");
+  int grid = 0;
+  if (int rc = lu::coop_grid((const void*)lu::zgetrs_kernel, lu::SOLVE_SMEM, &grid)) return rc;
+  const int nblk = (n + lu::NB - 1) / lu::NB;
+  lu::SolveParams S;
+  S.n = n; S.nrhs = nrhs; S.LU = LU; S.lda = lda;
+  const char* x = (const char*)aux;
+  S.Linv = (const z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
+  S.Uinv = (const z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
+  S.perm = (const int*)x;
+  S.B = B; S.ldb = ldb; S.X = X; S.ldx = ldx; S.tmp = (z_t*)work;
+  void* args[] = {&S};
+  VB_CUDA(cudaLaunchCooperativeKernel((const void*)lu::zgetrs_kernel, grid, lu::NT, args, lu::SOLVE_SMEM, st));
+  VB_LAUNCHED("zgetrs_kernel");
+  return 0;
+}
+
+}  // namespace vb

@@ -52,4 +52,13 @@ int column_norms(int n, int m, const z_t* W, int64_t ldw, double* out, void* wor
                  cudaStream_t st);
 int scale_columns(int n, int m, z_t* W, int64_t ldw, const double* scale, cudaStream_t st);
 
+
+// lu.cu
+size_t zgetrf_workspace_bytes(int n);
+size_t zgetrf_aux_bytes(int n);
+int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size_t aux_bytes, void* work,
+           size_t work_bytes, cudaStream_t st);
+int zgetrs(int n, int nrhs, const z_t* LU, int64_t lda, const void* aux, const z_t* B, int64_t ldb,
+           z_t* X, int64_t ldx, void* work, size_t work_bytes, cudaStream_t st);
+
 }  // namespace vb
