@@ -73,3 +73,52 @@ def cfg5(r: int = 1024, n_freq: int = CFG5_NFREQ, s: int = CFG5_RHS, n_out: int 
     freqs = np.linspace(f_lo, f_hi, n_freq)
     return ReducedWorkload(name=f"cfg5_r{r}", prims=np.stack([K, D, M]), kinds=("K", "D", "M"),
                            b=B, c_r=C, freqs=freqs, seed=seed)
+
+
+# ---------------------------------------------------------------- cfg1 -----
+CFG1_BOX = (0.0, 0.0, 0.0, 2.0, 1.6, 1.2)
+CFG1_NE = (10, 8, 6)
+AIR_RHO, AIR_C = 1.21, 343.0
+CFG1_Z = AIR_RHO * AIR_C * (5 + 1j)
+CFG1_POINTS = (42.5, 87.5, 132.5, 177.5)   # quartile midpoints of [20, 200]
+CFG1_MOMENTS = 8
+CFG1_NREC = 50
+
+
+def cfg1_layout(seed: int = 1, box=CFG1_BOX, ne=CFG1_NE, n_rec: int = CFG1_NREC):
+    """Host-side layout of cfg1: mesh, seeded source node and receivers.
+
+    Source: one seeded interior node; receivers: n_rec distinct seeded interior
+    nodes excluding the source."""
+    from .assembly import hex27_box, interior_nodes
+    xyz, conn = hex27_box(box, *ne)
+    inner = interior_nodes(xyz, box)
+    rng = np.random.default_rng(seed)
+    src = int(rng.choice(inner))
+    rec = np.sort(rng.choice(np.setdiff1d(inner, [src]), n_rec, replace=False)).astype(np.int64)
+    return xyz, conn, src, rec
+
+
+def cfg1_model(seed: int = 1, box=CFG1_BOX, ne=CFG1_NE, n_rec: int = CFG1_NREC, device=None):
+    """cfg1 (BASELINE configs[0]): rigid air box 2.0 x 1.6 x 1.2 m, 10 x 8 x 6
+    hex27 Helmholtz elements (n = 4641), floor impedance Z = rho c (5 + 1i),
+    unit point source, 50 receivers.  All primitives assembled on the GPU;
+    returns (FullOrderModel with an affine operator, layout dict)."""
+    import torch
+    from . import assembly
+    from .mor import AffineOperator, AffineTerm, FullOrderModel
+    xyz, conn, src, rec = cfg1_layout(seed, box, ne, n_rec)
+    Kg, Mn = assembly.assemble_helmholtz(xyz, conn, device)
+    F = assembly.assemble_face_mass(xyz, assembly.hex27_box_face(ne, "z0", conn), device)
+    n = xyz.shape[0]
+    b = torch.zeros(n, dtype=torch.complex128, device=Kg.data.device)
+    b[src] = 1.0
+    C = np.zeros((len(rec), n))
+    C[np.arange(len(rec)), rec] = 1.0
+    aff = AffineOperator(K=[AffineTerm(Kg, 1.0 / AIR_RHO)],
+                         M=[AffineTerm(Mn, 1.0 / (AIR_RHO * AIR_C * AIR_C))],
+                         D=[AffineTerm(F, 1.0 / CFG1_Z)], load=b)
+    fom = FullOrderModel(c_out=C, n=n, affine=aff)
+    return fom, {"xyz": xyz, "conn": conn, "src": src, "rec": rec, "Kg": Kg, "Mn": Mn, "F": F,
+                 "freqs": np.arange(20.0, 200.5, 1.0), "points": CFG1_POINTS,
+                 "moments": CFG1_MOMENTS}
