@@ -88,36 +88,52 @@ struct Gemm {
   static constexpr int A_EL = TM * LDA, B_EL = KC * LDB, C_EL = TM * LDC;
   static constexpr size_t SMEM = (size_t)(STAGES * (A_EL + B_EL) + (SUB ? C_EL : 0)) * sizeof(z_t);
 
-  __device__ static void load_chunk(z_t* As, z_t* Bs, const z_t* A, int lda, const z_t* B, int ldb,
-                                    int M, int N, int K, int m0, int n0, int k0) {
-    const int tid = threadIdx.x;
+  static_assert(NT % KC == 0 && NT % TN == 0, "loader mapping");
+  static_assert((TM * KC) % NT == 0 && (KC * TN) % NT == 0 && (TM * TN) % NT == 0, "loader mapping");
+  static constexpr int A_PER = TM * KC / NT, A_RS = NT / KC;  // rows a thread loads / row stride
+  static constexpr int B_PER = KC * TN / NT, B_RS = NT / TN;
+  static constexpr int C_PER = TM * TN / NT, C_RS = NT / TN;
+
+  __device__ static __forceinline__ void cp16(unsigned s, const void* g, bool p) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(p ? 16 : 0));
+  }
+
+  // Per-thread loader state: the element a thread copies has a fixed column
+  // (k for A, j for B/C) and rows i0 + q * RS, so only bases move per chunk.
+  struct Loader {
+    unsigned as0, bs0, cs0;  // shared addresses of this thread's first element
+    int a_i0, a_k, b_k0, b_j;
+  };
+
+  __device__ static __forceinline__ void load_chunk(const Loader& L, int stage, const z_t* A, int lda,
+                                                    const z_t* B, int ldb, int M, int N, int K, int m0,
+                                                    int n0, int k0) {
+    const bool kva = k0 + L.a_k < K;
+    const z_t* Ab = A + (size_t)(m0 + L.a_i0) * lda + k0 + L.a_k;
+    const unsigned as = L.as0 + (unsigned)(stage * A_EL * sizeof(z_t));
 #pragma unroll
-    for (int q = 0; q < (TM * KC + NT - 1) / NT; ++q) {
-      const int e = tid + q * NT;
-      if ((TM * KC) % NT == 0 || e < TM * KC) {
-        const int i = e / KC, k = e % KC;
-        const bool p = (m0 + i < M) && (k0 + k < K);
-        cp_async16(As + i * LDA + k, p ? A + (size_t)(m0 + i) * lda + k0 + k : A, p);
-      }
+    for (int q = 0; q < A_PER; ++q) {
+      const bool p = kva && (m0 + L.a_i0 + q * A_RS < M);
+      cp16(as + (unsigned)(q * A_RS * LDA * sizeof(z_t)), p ? (const void*)(Ab + (size_t)q * A_RS * lda) : (const void*)A, p);
     }
+    const bool jv = n0 + L.b_j < N;
+    const z_t* Bb = B + (size_t)(k0 + L.b_k0) * ldb + n0 + L.b_j;
+    const unsigned bs = L.bs0 + (unsigned)(stage * B_EL * sizeof(z_t));
 #pragma unroll
-    for (int q = 0; q < (KC * TN + NT - 1) / NT; ++q) {
-      const int e = tid + q * NT;
-      if ((KC * TN) % NT == 0 || e < KC * TN) {
-        const int k = e / TN, j = e % TN;
-        const bool p = (k0 + k < K) && (n0 + j < N);
-        cp_async16(Bs + k * LDB + j, p ? B + (size_t)(k0 + k) * ldb + n0 + j : B, p);
-      }
+    for (int q = 0; q < B_PER; ++q) {
+      const bool p = jv && (k0 + L.b_k0 + q * B_RS < K);
+      cp16(bs + (unsigned)(q * B_RS * LDB * sizeof(z_t)), p ? (const void*)(Bb + (size_t)q * B_RS * ldb) : (const void*)B, p);
     }
   }
 
-  __device__ static void load_c(z_t* Cs, const z_t* C, int ldc, int M, int N, int m0, int n0) {
-    const int tid = threadIdx.x;
-#pragma unroll 4
-    for (int e = tid; e < TM * TN; e += NT) {
-      const int i = e / TN, j = e % TN;
-      const bool p = (m0 + i < M) && (n0 + j < N);
-      cp_async16(Cs + i * LDC + j, p ? C + (size_t)(m0 + i) * ldc + n0 + j : C, p);
+  __device__ static __forceinline__ void load_c(const Loader& L, const z_t* C, int ldc, int M, int N,
+                                                int m0, int n0) {
+    const bool jv = n0 + L.b_j < N;
+    const z_t* Cb = C + (size_t)(m0 + L.b_k0) * ldc + n0 + L.b_j;
+#pragma unroll
+    for (int q = 0; q < C_PER; ++q) {
+      const bool p = jv && (m0 + L.b_k0 + q * C_RS < M);
+      cp16(L.cs0 + (unsigned)(q * C_RS * LDC * sizeof(z_t)), p ? (const void*)(Cb + (size_t)q * C_RS * ldc) : (const void*)C, p);
     }
   }
 
@@ -130,24 +146,36 @@ struct Gemm {
     z_t* As = smem;
     z_t* Bs = smem + STAGES * A_EL;
     z_t* Cs = Bs + STAGES * B_EL;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
     const int ntiles = ((M + TM - 1) / TM) * ntn;
     if (t_first >= ntiles) return;
     const int my_tiles = (ntiles - t_first + t_step - 1) / t_step;
     const int T = my_tiles * nk;
-    auto issue = [&](int j) {
-      if (j < T) {
-        const int t = t_first + (j / nk) * t_step, kc = j - (j / nk) * nk;
-        load_chunk(As + (j % STAGES) * A_EL, Bs + (j % STAGES) * B_EL, A, lda, B, ldb, M, N, K,
-                   (t / ntn) * TM, (t % ntn) * TN, kc * KC);
+    Loader L;
+    L.a_i0 = tid / KC;
+    L.a_k = tid % KC;
+    L.b_k0 = tid / TN;
+    L.b_j = tid % TN;
+    L.as0 = (unsigned)__cvta_generic_to_shared(As + L.a_i0 * LDA + L.a_k);
+    L.bs0 = (unsigned)__cvta_generic_to_shared(Bs + L.b_k0 * LDB + L.b_j);
+    L.cs0 = (unsigned)__cvta_generic_to_shared(Cs + L.b_k0 * LDC + L.b_j);
+    // producer cursor (iteration p -> tile pt, chunk pk) advanced without divisions
+    int pt = t_first, pk = 0, pm0 = (pt / ntn) * TM, pn0 = (pt % ntn) * TN;
+    auto issue_next = [&](int p) {
+      if (p < T) load_chunk(L, p % STAGES, A, lda, B, ldb, M, N, K, pm0, pn0, pk * KC);
+      if (++pk == nk) {
+        pk = 0;
+        pt += t_step;
+        pm0 = (pt / ntn) * TM;
+        pn0 = (pt % ntn) * TN;
       }
     };
-    if (SUB) load_c(Cs, C, ldc, M, N, (t_first / ntn) * TM, (t_first % ntn) * TN);
+    if (SUB) load_c(L, C, ldc, M, N, pm0, pn0);
 #pragma unroll
     for (int j = 0; j < STAGES - 1; ++j) {
-      issue(j);
+      issue_next(j);
       cp_commit();
     }
     double cr[FM][FN][2], ci[FM][FN][2];
@@ -155,24 +183,26 @@ struct Gemm {
     for (int i = 0; i < FM; ++i)
 #pragma unroll
       for (int j = 0; j < FN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    int t = t_first, kc = 0;
+    int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
+    const z_t* as_w = As + (wm * FM * 8) * LDA;
+    const z_t* bs_w = Bs + wn * FN * 8;
     for (int it = 0; it < T; ++it) {
-      const int t = t_first + (it / nk) * t_step, kc = it - (it / nk) * nk;
       cp_wait<STAGES - 2>();
       __syncthreads();
-      issue(it + STAGES - 1);
-      if (SUB && kc == 0 && it > 0) load_c(Cs, C, ldc, M, N, (t / ntn) * TM, (t % ntn) * TN);
+      issue_next(it + STAGES - 1);
+      if (SUB && kc == 0 && it > 0) load_c(L, C, ldc, M, N, m0, n0);
       cp_commit();
       const int st = it % STAGES;
       int k4 = min(KC, K - kc * KC);
       k4 = (k4 + 3) >> 2;
-      warp_cmma<FM, FN, false>(cr, ci, As + st * A_EL + (wm * FM * 8) * LDA, LDA,
-                               Bs + st * B_EL + wn * FN * 8, LDB, k4);
+      warp_cmma<FM, FN, false>(cr, ci, as_w + st * A_EL, LDA, bs_w + st * B_EL, LDB, k4);
       if (kc == nk - 1) {
         if (SUB && nk < STAGES) {  // the C-tile group may still be in flight
           cp_wait<0>();
           __syncthreads();
         }
-        const int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
+        const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -187,9 +217,7 @@ struct Gemm {
                 if (EPI == EPI_SUB) {
                   const z_t c = Cs[lr * LDC + lc];
                   out = zmake(c.x - acc.x, c.y - acc.y);
-                } else if (EPI == EPI_SET) {
-                  out = zmul(alpha, acc);
-                } else if (beta.x == 0.0 && beta.y == 0.0) {
+                } else if (EPI == EPI_SET || beta0) {
                   out = zmul(alpha, acc);  // C_old never contributes (may be uninitialised)
                 } else {
                   out = zfma(zmul(alpha, acc), beta, Cs[lr * LDC + lc]);
@@ -199,6 +227,12 @@ struct Gemm {
               cr[i][j][v] = 0.0;
               ci[i][j][v] = 0.0;
             }
+        kc = 0;
+        t += t_step;
+        m0 = (t / ntn) * TM;
+        n0 = (t % ntn) * TN;
+      } else {
+        ++kc;
       }
     }
     cp_wait<0>();

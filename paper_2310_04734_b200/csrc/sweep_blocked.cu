@@ -170,15 +170,21 @@ __device__ void apply_swaps(z_t* A, int ldw, const int* piv, int k0, int a, int 
   }
 }
 
-// U = L^-1 U for the wc rows of an inner panel (unit lower L = Ps[0:wc, 0:wc]),
-// columns [c0, c1): one thread per column, forward substitution through L1
-// (each thread re-reads only values it wrote itself).
-__device__ void inner_trsm(z_t* A, int ldw, const z_t* Ps, int w, int j0, int wc, int c0, int c1) {
+// U = L^-1 U for rows [cl, cl+n1) (unit lower L = A[cl:cl+n1, cl:cl+n1], n1 <= 32)
+// on columns [c0, c1): L staged in shared memory, one thread per column.
+__device__ void trsm_small(z_t* A, int ldw, int cl, int n1, int c0, int c1, z_t* smem) {
+  constexpr int LD = 33;
+  z_t* Ls = smem;
+  for (int e = threadIdx.x; e < n1 * n1; e += NT) {
+    const int i = e / n1, k = e - i * n1;
+    Ls[i * LD + k] = A[(size_t)(cl + i) * ldw + cl + k];
+  }
+  __syncthreads();
   for (int c = c0 + threadIdx.x; c < c1; c += NT) {
-    z_t* col = A + (size_t)j0 * ldw + c;
-    for (int i = 1; i < wc; ++i) {
+    z_t* col = A + (size_t)cl * ldw + c;
+    for (int i = 1; i < n1; ++i) {
       z_t acc = col[(size_t)i * ldw];
-      for (int k = 0; k < i; ++k) acc = zfms(acc, Ps[i * w + k], col[(size_t)k * ldw]);
+      for (int k = 0; k < i; ++k) acc = zfms(acc, Ls[i * LD + k], col[(size_t)k * ldw]);
       col[(size_t)i * ldw] = acc;
     }
   }
@@ -335,19 +341,28 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(Params P) {
     // ---- blocked right-looking LU on [A | B] ----
     for (int k0 = 0; k0 < r; k0 += NB) {
       const int nb = min(NB, r - k0);
-      for (int j0 = k0; j0 < k0 + nb; j0 += P.w) {
+      // Recursive (zgetrf2-order) panel: leaves of w columns are factored in
+      // shared memory; after leaf l the right sibling of the largest completed
+      // left subtree (size 2^k leaves, k = trailing ones of l) is updated with
+      // one TRSM + one GEMM of depth 2^k w.  In-panel traffic ~ r NB log2(NB/w)
+      // instead of r NB^2 / w for rank-w updates after every leaf.
+      const int nleaves = (nb + P.w - 1) / P.w;
+      for (int l = 0; l < nleaves; ++l) {
+        const int j0 = k0 + l * P.w;
         const int wc = min(P.w, k0 + nb - j0);
         inner_panel(P, A, k0, j0, wc, smem, piv, &s_info, rv, ri, &s_p, &s_pv);
-        // fold the inner panel into the rest of the outer panel
         apply_swaps(A, ldw, piv, k0, j0, j0 + wc, k0, j0);
         apply_swaps(A, ldw, piv, k0, j0, j0 + wc, j0 + wc, k0 + nb);
         __syncthreads();
-        if (j0 + wc < k0 + nb) {
-          inner_trsm(A, ldw, smem, P.w, j0, wc, j0 + wc, k0 + nb);
+        if (l + 1 < nleaves) {
+          const int kk = __ffs(~l) - 1;           // trailing ones of l
+          const int n1 = (1 << kk) * P.w;         // left subtree width
+          const int cl = j0 + wc - n1;            // left subtree start column
+          const int rc0 = j0 + wc, rc1 = min(rc0 + n1, k0 + nb);
+          trsm_small(A, ldw, cl, n1, rc0, rc1, smem);
           __syncthreads();
-          GemmWide::run(A + (size_t)(j0 + wc) * ldw + j0 + wc, ldw, A + (size_t)(j0 + wc) * ldw + j0,
-                        ldw, A + (size_t)j0 * ldw + j0 + wc, ldw, r - j0 - wc, k0 + nb - j0 - wc, wc,
-                        smem);
+          GemmWide::run(A + (size_t)rc0 * ldw + rc0, ldw, A + (size_t)rc0 * ldw + cl, ldw,
+                        A + (size_t)cl * ldw + rc0, ldw, r - rc0, rc1 - rc0, n1, smem);
           __syncthreads();
         }
       }
