@@ -287,9 +287,9 @@ def run_ours(args):
     achieved = fl * B / (kern_avg_ms * 1e-3) / 1e12
     traffic = None
     tfile = ROOT / "profiles" / f"traffic_cfg5_r{r}.json"
-    if tfile.exists():
+    if tfile.exists():  # ncu --set full capture of the same kernel (profiles/), per launch
         try:
-            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+            traffic = json.loads(tfile.read_text())["dram_bytes_per_freq"] * B
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -297,7 +297,8 @@ def run_ours(args):
                 "kernel": "rom_sweep_blocked_kernel" if path == 1 else "rom_sweep_small_kernel",
                 "peak_source": "FP64 DMMA (mma.sync.m8n8k4.f64) throughput measured live by "
                                "vb_probe_fp64_peak on this GPU (MEASURED_PEAKS.json has no FP64)",
-                "flops_per_freq": fl, "freqs_per_launch": B}
+                "flops_per_freq": fl, "freqs_per_launch": B,
+                "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu)"}
 
     cpu = None
     if ws == 1 and not args.no_cpu:

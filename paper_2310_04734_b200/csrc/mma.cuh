@@ -77,7 +77,7 @@ __device__ __forceinline__ void warp_cmma(double (&cr)[FM][FN][2], double (&ci)[
 //                 EPI_AXPBY C = alpha*A*B + beta*C_old
 enum { EPI_SUB = 0, EPI_SET = 1, EPI_AXPBY = 2 };
 
-template <int TM, int TN, int WM, int WN, int STAGES, int EPI>
+template <int TM, int TN, int WM, int WN, int STAGES, int EPI, int KC = 16>
 struct Gemm {
   static constexpr bool SUB = EPI != EPI_SET;  // reads C_old
   static_assert(WM * WN == NT / 32, "warp grid");

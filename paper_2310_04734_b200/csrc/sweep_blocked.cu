@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "mma.cuh"
 #include "sweep.cuh"
+#include "tma.cuh"
 
 namespace vb {
 namespace blk {
@@ -44,7 +45,10 @@ constexpr int LDY = 16 + 2;
 constexpr size_t TRSM_SMEM = (size_t)(NB * LDL + NB * LDS_B) * sizeof(z_t);
 constexpr size_t BACK_SMEM = (size_t)(NB * LDL + NB * LDY) * sizeof(z_t);
 
-struct Params {
+using GemmT = tma::GemmTma<3>;
+
+struct __align__(64) Params {
+  tma::Maps maps;  // TMA descriptors over all CTAs' workspaces (must stay first: 64-B aligned)
   int r, nprim, s, n_out;
   int64_t F;
   const z_t* prims;
@@ -312,8 +316,11 @@ __device__ void form_matrix(const Params& P, z_t* A, const z_t* alph) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(Params P) {
-  extern __shared__ double2 smem[];
+__global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_constant__ Params P) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  // 1024-byte aligned base (128B-swizzled TMA boxes)
+  double2* smem = (double2*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ GemmT::Bars bars;
   __shared__ int piv[NB];
   __shared__ double rv[NT / 32];
   __shared__ int ri[NT / 32];
@@ -335,6 +342,13 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(Params P) {
     for (int idx = tid; idx < r * s; idx += NT) {
       const int i = idx / s, c = idx - i * s;
       A[(size_t)i * ldw + r + c] = __ldg(bf + idx);
+    }
+    if (ldw > r + s) {  // padding columns are read (never used) by TMA boxes: keep them finite
+      const int pw = ldw - r - s;
+      for (int idx = tid; idx < r * pw; idx += NT) {
+        const int i = idx / pw, c = idx - i * pw;
+        A[(size_t)i * ldw + r + s + c] = zmake(0.0, 0.0);
+      }
     }
     __syncthreads();
 
@@ -361,8 +375,8 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(Params P) {
           const int rc0 = j0 + wc, rc1 = min(rc0 + n1, k0 + nb);
           trsm_small(A, ldw, cl, n1, rc0, rc1, smem);
           __syncthreads();
-          GemmWide::run(A + (size_t)rc0 * ldw + rc0, ldw, A + (size_t)rc0 * ldw + cl, ldw,
-                        A + (size_t)cl * ldw + rc0, ldw, r - rc0, rc1 - rc0, n1, smem);
+          GemmT::run(&P.maps, A, ldw, rc0, cl, cl, rc0, r - rc0, rc1 - rc0, n1, (char*)smem, &bars,
+                     blockIdx.x);
           __syncthreads();
         }
       }
@@ -371,8 +385,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(Params P) {
       __syncthreads();
       panel_trsm(A, ldw, k0, nb, c0, c1, smem);
       if (c0 < r) {
-        GemmWide::run(A + (size_t)c0 * ldw + c0, ldw, A + (size_t)c0 * ldw + k0, ldw,
-                      A + (size_t)k0 * ldw + c0, ldw, r - c0, c1 - c0, nb, smem);
+        GemmT::run(&P.maps, A, ldw, c0, k0, k0, c0, r - c0, c1 - c0, nb, (char*)smem, &bars, blockIdx.x);
         __syncthreads();
       }
     }
@@ -420,16 +433,16 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(Params P) {
 static int ldw_of(int r, int s) { return (r + s + 3) & ~3; }
 
 static size_t smem_bytes(int r, int w) {
-  size_t m = GemmWide::SMEM;
+  size_t m = GemmT::SMEM;
   m = m > GemmNarrow::SMEM ? m : GemmNarrow::SMEM;
   m = m > GemmOut::SMEM ? m : GemmOut::SMEM;
   m = m > TRSM_SMEM ? m : TRSM_SMEM;
   m = m > BACK_SMEM ? m : BACK_SMEM;
   const size_t ps = (size_t)r * w * sizeof(z_t);
-  return m > ps ? m : ps;
+  return (m > ps ? m : ps) + 1024;  // + alignment slack for the 1024-B aligned base
 }
 
-static const size_t kSmemPerCta = 110 * 1024;  // two CTAs per SM
+static const size_t kSmemPerCta = 111 * 1024;  // two CTAs per SM
 
 static int pick_w(int r) {
   for (int w = 16; w >= 1; w >>= 1)
@@ -455,6 +468,31 @@ size_t sweep_blocked_workspace_bytes(int r, int s, int n_out, int64_t F) {
   return (size_t)blocked_grid(F) * blk::cta_stride(r, s, n_out) * sizeof(z_t);
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static int encode_map(CUtensorMap* map, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                      const cuuint32_t* box, const cuuint32_t* es) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    VB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return 2;
+    }
+  }
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return 2;
+  }
+  return 0;
+}
+
 int sweep_blocked_supported(int r, int s, int n_out) { return s <= 16 && blk::pick_w(r) > 0; }
 
 int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_t* prims,
@@ -473,6 +511,14 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
   P.y = y; P.spl = spl; P.x = x; P.info = info;
   P.work = (z_t*)work; P.ldw = blk::ldw_of(r, s); P.w = w;
   P.cta_stride = blk::cta_stride(r, s, n_out);
+  {
+    const int grid = blocked_grid(F);
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * P.ldw, (cuuint64_t)r, (cuuint64_t)grid};
+    const cuuint64_t strides[2] = {(cuuint64_t)P.ldw * 16, (cuuint64_t)P.cta_stride * 16};
+    const cuuint32_t box64[3] = {16, 64, 1}, box16[3] = {16, 16, 1}, es[3] = {1, 1, 1};
+    if (int rc = encode_map(&P.maps.a64, work, dims, strides, box64, es)) return rc;
+    if (int rc = encode_map(&P.maps.b16, work, dims, strides, box16, es)) return rc;
+  }
   const size_t smem = blk::smem_bytes(r, w);
   VB_CUDA(cudaFuncSetAttribute(blk::rom_sweep_blocked_kernel,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

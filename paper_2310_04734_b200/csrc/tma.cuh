@@ -1,0 +1,250 @@
+// TMA (cp.async.bulk.tensor) + mbarrier staged complex GEMM for the blocked
+// reduced-sweep kernel: C -= A * B where A, B and C are sub-blocks of the
+// CTA's own workspace matrix [A_r | B] (one 3-D tensor map over all CTAs'
+// workspaces: doubles x rows x CTA).
+//
+//  * One elected thread issues 128B-swizzled TMA boxes (8 complex x rows) into
+//    a STAGES-deep shared-memory ring; completion is signalled through
+//    full[] mbarriers (expect_tx), release through empty[] mbarriers (one
+//    arrival per warp).  No block-wide barrier in the k-loop.
+//  * The next C tile is fetched by TMA while the current tile computes.
+//  * Fragment reads undo the swizzle; MMA rows/columns are permuted
+//    (perm = 0,4,1,5,2,6,3,7) so that the 128-bit DMMA fragment loads of a
+//    quarter-warp hit 8 distinct 16-byte bank groups.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "mma.cuh"
+
+namespace vb {
+namespace tma {
+
+using blk::NT;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_inval(uint64_t* b) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+// 3-D tiled TMA load: coords (x = double index, y = row, z = CTA)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int perm8(int x) { return (x >> 1) | ((x & 1) << 2); }
+
+// byte offset of complex element (row, chunk) inside a 128B-swizzled box
+__device__ __forceinline__ unsigned swz(int row, int chunk) {
+  return (unsigned)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+struct Maps {
+  CUtensorMap a64;  // box: 16 doubles x 64 rows x 1 CTA
+  CUtensorMap b16;  // box: 16 doubles x 16 rows x 1 CTA
+};
+
+// C[M x N] -= A[M x K] B[K x N]; operand origins are (row, col) coordinates in
+// the CTA's workspace matrix.  TM = 64, TN = 32, KC = 16, 8 warps as 4 x 2.
+template <int STAGES>
+struct GemmTma {
+  static constexpr int TM = 64, TN = 32, KC = 16;
+  static constexpr unsigned A_BYTES = TM * KC * 16;   // 2 boxes of 64 rows x 8 complex
+  static constexpr unsigned B_BYTES = KC * TN * 16;   // 4 boxes of 16 rows x 8 complex
+  static constexpr unsigned C_BYTES = TM * TN * 16;   // 4 boxes of 64 rows x 8 complex
+  static constexpr size_t SMEM = (size_t)STAGES * (A_BYTES + B_BYTES) + C_BYTES;
+
+  struct Bars {
+    uint64_t full[STAGES], empty[STAGES], cfull, cempty;
+  };
+
+  // issue the A and B boxes of chunk (m0, n0, k0) into stage st
+  __device__ static __forceinline__ void issue_chunk(const Maps* mp, char* As, char* Bs, uint64_t* bar, int cta,
+                                                     int ar0, int ac0, int br0, int bc0, int m0, int n0, int k0) {
+    mbar_expect_tx(bar, A_BYTES + B_BYTES);
+    tma_load_3d(As, &mp->a64, 2 * (ac0 + k0), ar0 + m0, cta, bar);
+    tma_load_3d(As + 8192, &mp->a64, 2 * (ac0 + k0 + 8), ar0 + m0, cta, bar);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) tma_load_3d(Bs + b * 2048, &mp->b16, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
+  }
+  __device__ static __forceinline__ void issue_c(const Maps* mp, char* Cs, uint64_t* bar, int cta, int cr0, int cc0,
+                                                 int m0, int n0) {
+    mbar_expect_tx(bar, C_BYTES);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) tma_load_3d(Cs + b * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0, cta, bar);
+  }
+
+  // ar0/ac0: A origin; br0/bc0: B origin; cr0/cc0: C origin (= (ar0, bc0)); ldw
+  // for the generic-store epilogue.  smem must be 1024-byte aligned.
+  __device__ static void run(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int M, int N,
+                             int K, char* smem, Bars* bars, int cta) {
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
+    const int ntiles = ((M + TM - 1) / TM) * ntn;
+    const int T = ntiles * nk;
+    char* As = smem;
+    char* Bs = smem + STAGES * A_BYTES;
+    char* Cs = Bs + STAGES * B_BYTES;
+    const int cr0 = ar0, cc0 = bc0;
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&bars->full[s], 1);
+        mbar_init(&bars->empty[s], NT / 32);
+      }
+      mbar_init(&bars->cfull, 1);
+      mbar_init(&bars->cempty, NT / 32);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    // producer cursor (thread 0 only)
+    int pt = 0, pk = 0;
+    if (tid == 0) {
+      fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
+      issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, 0, 0);
+      for (int j = 0; j < STAGES - 1 && j < T; ++j) {
+        issue_chunk(mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], cta, ar0, ac0, br0, bc0,
+                    (pt / ntn) * TM, (pt % ntn) * TN, pk * KC);
+        if (++pk == nk) { pk = 0; ++pt; }
+      }
+    }
+    unsigned full_ph = 0, empty_ph = 0, c_ph = 0, cempty_ph = 0;
+    double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    const int ar = lane >> 2, ak = lane & 3;
+    const int prow = perm8(ar);
+    int t = 0, kc = 0;
+    for (int it = 0; it < T; ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&bars->full[st], (full_ph >> st) & 1);
+      full_ph ^= 1u << st;
+      const char* as = As + st * A_BYTES;
+      const char* bs = Bs + st * B_BYTES;
+      const int kvalid = min(KC, K - kc * KC);
+      const int k4n = (kvalid + 3) >> 2;
+      for (int kk = 0; kk < k4n; ++kk) {
+        const int kcol = kk * 4 + ak;
+        const bool kin = kcol < kvalid;
+        z_t a[2], b[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = wm * 16 + i * 8 + prow;
+          a[i] = *(const z_t*)(as + (kcol >> 3) * 8192 + swz(row, kcol & 7));
+          if (!kin) a[i] = zmake(0.0, 0.0);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          b[j] = *(const z_t*)(bs + (wn * 2 + j) * 2048 + swz(kcol, prow));
+          if (!kin) b[j] = zmake(0.0, 0.0);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const double br = b[j].x, bi = b[j].y, nbi = -bi;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            blk::dmma(cr[i][j][0], cr[i][j][1], a[i].x, br);
+            blk::dmma(cr[i][j][0], cr[i][j][1], a[i].y, nbi);
+            blk::dmma(ci[i][j][0], ci[i][j][1], a[i].x, bi);
+            blk::dmma(ci[i][j][0], ci[i][j][1], a[i].y, br);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->empty[st]);
+      // refill the stage consumed in the previous iteration
+      if (tid == 0 && it + STAGES - 1 < T) {
+        const int s2 = (it + STAGES - 1) % STAGES;
+        if (it >= 1) {
+          mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
+          empty_ph ^= 1u << s2;
+        }
+        issue_chunk(mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], cta, ar0, ac0, br0, bc0,
+                    (pt / ntn) * TM, (pt % ntn) * TN, pk * KC);
+        if (++pk == nk) { pk = 0; ++pt; }
+      }
+      if (kc == nk - 1) {
+        const int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
+        mbar_wait(&bars->cfull, c_ph);
+        c_ph ^= 1;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int row = wm * 16 + i * 8 + prow;
+              const int cfrag = 2 * ak + v;  // fragment column 0..7
+              const int col = wn * 16 + j * 8 + perm8(cfrag);
+              if (m0 + row < M && n0 + col < N) {
+                const z_t c = *(const z_t*)(Cs + (col >> 3) * 8192 + swz(row, col & 7));
+                Cg[(size_t)(cr0 + m0 + row) * ldw + cc0 + n0 + col] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+              }
+              cr[i][j][v] = 0.0;
+              ci[i][j][v] = 0.0;
+            }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->cempty);
+        if (tid == 0 && t + 1 < ntiles) {
+          mbar_wait(&bars->cempty, cempty_ph);
+          cempty_ph ^= 1;
+          fence_proxy_async_global();
+          issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, ((t + 1) / ntn) * TM, ((t + 1) % ntn) * TN);
+        }
+        kc = 0;
+        ++t;
+      } else {
+        ++kc;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_inval(&bars->full[s]);
+        mbar_inval(&bars->empty[s]);
+      }
+      mbar_inval(&bars->cfull);
+      mbar_inval(&bars->cempty);
+    }
+  }
+};
+
+}  // namespace tma
+}  // namespace vb
