@@ -172,6 +172,22 @@ size_t vb_zgetrs_workspace_bytes(int n, int nrhs);
 int vb_zgetrs(int n, int nrhs, const vb_complex* LU, int64_t lda, const void* aux, const vb_complex* B,
               int64_t ldb, vb_complex* X, int64_t ldx, void* work, size_t work_bytes, void* stream);
 
+/*
+ * Fast-diagonalisation full-order solver on structured hex27 boxes (cfg3,
+ * n = 376k, where scipy splu — vibrofem/mor.py:48-49, 153-156 — is
+ * impractical).  The box operator is a Kronecker sum; the host computes the
+ * per-direction generalised eigenpairs, the device applies
+ *   x = V (Lz (+) Ly (+) Lx + sigma)^-1 V^T b,  V = Vz (x) Vy (x) Vx.
+ * Arrays are (n2, n1, n0) nodes x nrhs, RHS fastest (node id k n1 n0 + j n0 + i).
+ *  vb_axis_apply: Y = S applied along axis (0 = x, 1 = y, 2 = z); S is
+ *                 n_axis x n_axis row-major; X and Y must not alias.
+ *  vb_fdm_diag:   X /= (lz[k] + ly[j] + lx[i] + sigma).
+ */
+int vb_axis_apply(int n2, int n1, int n0, int nrhs, int axis, const vb_complex* S, const vb_complex* X,
+                  vb_complex* Y, void* stream);
+int vb_fdm_diag(int n2, int n1, int n0, int nrhs, const vb_complex* lz, const vb_complex* ly,
+                const vb_complex* lx, vb_complex sigma, vb_complex* X, void* stream);
+
 /* norms[j] = ||W[:, j]||_2 for an n x m complex row-major W (deterministic). */
 size_t vb_column_norms_workspace_bytes(int n, int m);
 int vb_column_norms(int n, int m, const vb_complex* W, int64_t ldw, double* norms, void* work,

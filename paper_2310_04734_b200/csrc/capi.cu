@@ -159,4 +159,16 @@ int vb_zgetrs(int n, int nrhs, const vb_complex* LU, int64_t lda, const void* au
                     (cudaStream_t)stream);
 }
 
+int vb_axis_apply(int n2, int n1, int n0, int nrhs, int axis, const vb_complex* S, const vb_complex* X,
+                  vb_complex* Y, void* stream) {
+  return vb::axis_apply(n2, n1, n0, nrhs, axis, (const z_t*)S, (const z_t*)X, (z_t*)Y, (cudaStream_t)stream);
+}
+
+int vb_fdm_diag(int n2, int n1, int n0, int nrhs, const vb_complex* lz, const vb_complex* ly,
+                const vb_complex* lx, vb_complex sigma, vb_complex* X, void* stream) {
+  VB_CHECK_ARG(n0 > 0 && n1 > 0 && n2 > 0 && nrhs > 0 && lz && ly && lx && X, "vb_fdm_diag: bad arguments");
+  return vb::fdm_diag(n2, n1, n0, nrhs, (const z_t*)lz, (const z_t*)ly, (const z_t*)lx, zc(sigma), (z_t*)X,
+                      (cudaStream_t)stream);
+}
+
 }  // extern "C"

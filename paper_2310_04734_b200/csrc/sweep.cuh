@@ -61,4 +61,10 @@ int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size
 int zgetrs(int n, int nrhs, const z_t* LU, int64_t lda, const void* aux, const z_t* B, int64_t ldb,
            z_t* X, int64_t ldx, void* work, size_t work_bytes, cudaStream_t st);
 
+
+// fdm.cu
+int axis_apply(int n2, int n1, int n0, int nrhs, int axis, const z_t* S, const z_t* X, z_t* Y, cudaStream_t st);
+int fdm_diag(int n2, int n1, int n0, int nrhs, const z_t* lz, const z_t* ly, const z_t* lx, z_t sigma, z_t* X,
+             cudaStream_t st);
+
 }  // namespace vb

@@ -36,6 +36,7 @@ from .solvers import DenseLU
 from .sweep import rom_sweep_affine
 
 ORTH_DROP_TOL = 1e-10  # mor.py:22
+DENSE_MAX_N = 25_000   # dense GPU LU up to ~10 GB of complex128 factors
 CDT = torch.complex128
 
 
@@ -101,6 +102,8 @@ class FullOrderModel:
     n: int = 0
     damping: object = None
     affine: AffineOperator | None = None
+    fdm: object = None            # fdm.BoxFDM for structured boxes (cfg3-size solves)
+    prefer_fdm: bool = False
 
     def __post_init__(self):
         if self.affine is not None:
@@ -152,7 +155,14 @@ class FullOrderModel:
         b = torch.as_tensor(np.asarray(self.load(f))).to(device=dev, dtype=CDT)
         return b.view(-1, 1) if b.dim() == 1 else b.contiguous()
 
-    def factor(self, f: float) -> DenseLU:
+    def factor(self, f: float):
+        """GPU factorisation of A(f): dense LU (n <= DENSE_MAX_N) or the
+        fast-diagonalisation solver of a structured box (any n)."""
+        if self.fdm is not None and (self.prefer_fdm or self.n > DENSE_MAX_N):
+            return self.fdm.factor(f, self)
+        if self.n > DENSE_MAX_N:
+            raise RuntimeError(f"n = {self.n} exceeds the dense GPU LU limit ({DENSE_MAX_N}); "
+                               "attach a BoxFDM solver (FullOrderModel.fdm)")
         return DenseLU(self.operator_dense(f))
 
     def solve(self, f: float) -> np.ndarray:
@@ -402,6 +412,23 @@ def _cgs2_against(Q: torch.Tensor | None, w: torch.Tensor) -> torch.Tensor:
     return w
 
 
+REORTH_RATIO = 1e-4  # kept columns this close to dependence get a third (DGKS) pass
+
+
+def _polish(bases, w: torch.Tensor, nw: float, ref: float):
+    """Extra orthogonalisation pass for a KEPT column whose two-pass residual is
+    tiny relative to its raw norm (Kahan/DGKS: "twice is enough" needs the
+    residual not to be near the rounding level); the drop decision itself is
+    the reference's and is taken before this pass."""
+    if nw >= REORTH_RATIO * ref:
+        return w, nw
+    for Q in bases:
+        if Q is not None and Q.shape[1]:
+            g = linalg.zgemm("C", Q, w)
+            linalg.zgemm("N", Q, g, -1.0, 1.0, w)
+    return w, float(linalg.column_norms(w).item())
+
+
 def _orthonormalise(V, block):
     """Append the columns of `block` to V, twice-orthogonalised; columns that
     become negligible after projection are dropped (mor.py:122-135):
@@ -418,18 +445,39 @@ def _orthonormalise(V, block):
         Vd = _as_dev(V, dev) if V.size else None
     refs = linalg.column_norms(B).cpu().numpy()
     W = B.clone()
+
+    def against_V(X):
+        for _ in range(2):
+            G = linalg.zgemm("C", Vd, X)
+            linalg.zgemm("N", Vd, G, -1.0, 1.0, X)
+
+    # pass 1: project on V (two CGS sweeps = the reference's two MGS passes),
+    # then Gram-Schmidt inside the block with the reference drop rule
     if Vd is not None:
-        for _ in range(2):                                 # block CGS2 against V
-            G = linalg.zgemm("C", Vd, W)
-            linalg.zgemm("N", Vd, G, -1.0, 1.0, W)
+        against_V(W)
     cols = []
     for j in range(W.shape[1]):
         w = W[:, j:j + 1].contiguous()
-        if cols:                                           # CGS2 against the accepted block columns
+        if cols:
             w = _cgs2_against(torch.cat(cols, 1).contiguous(), w)
         nw = float(linalg.column_norms(w).item())
         if refs[j] > 0 and nw > ORTH_DROP_TOL * refs[j]:
+            w, nw = _polish((torch.cat(cols, 1).contiguous() if cols else None,), w, nw, refs[j])
             cols.append(w / nw)
+    # pass 2 (block CGS2, Barlow-Smoktunowicz): re-project the kept, now
+    # orthonormal columns on V and re-orthonormalise inside the block.  Strong
+    # cancellation inside the block in pass 1 amplifies the rounding-level V
+    # components of a column; this pass removes them at block cost.
+    if Vd is not None and cols:
+        Q1 = torch.cat(cols, 1).contiguous()
+        against_V(Q1)
+        cols2 = []
+        for j in range(Q1.shape[1]):
+            w = Q1[:, j:j + 1].contiguous()
+            if cols2:
+                w = _cgs2_against(torch.cat(cols2, 1).contiguous(), w)
+            cols2.append(w / float(linalg.column_norms(w).item()))
+        cols = cols2
     newV = torch.cat([Vd] + [c for c in cols], dim=1) if Vd is not None else (
         torch.cat(cols, dim=1) if cols else torch.zeros((n, 0), dtype=CDT, device=dev))
     newV = newV.contiguous()
@@ -476,13 +524,64 @@ def krylov_block_dev(fom: FullOrderModel, f_j: float, m: int, second_order: bool
         w = lu.solve(rhs)
         w.neg_()
         ref = float(linalg.column_norms(w).item())
-        w = _cgs2_against(torch.cat(cols, 1).contiguous(), w)
+        Qb = torch.cat(cols, 1).contiguous()
+        w = _cgs2_against(Qb, w)
         nw = float(linalg.column_norms(w).item())
         if ref == 0 or nw <= ORTH_DROP_TOL * ref:
             breakdown = True
             break
+        w, nw = _polish((Qb,), w, nw, ref)
         cols.append(w / nw)
     return torch.cat(cols, 1).contiguous(), breakdown
+
+
+def krylov_blocks_mimo_dev(fom: FullOrderModel, f_j: float, m: int, second_order: bool = False, lu=None):
+    """Multi-input moments (cfg3's 8-source block RHS).  The reference is
+    single-input; MIMO is emulated as one single-input Krylov
+    block per load column (mor.py:138-191 per column) sharing ONE factorisation
+    and batching the solves of all columns; returns [(Q_j, breakdown_j)]."""
+    if m < 1:
+        raise ValueError("moment count must be >= 1")
+    dev = _device()
+    lu = lu or fom.factor(f_j)
+    Bm = fom.load_dev(f_j, dev)
+    s = Bm.shape[1]
+    Vb = lu.solve(Bm)                                        # all columns at once
+    nv = linalg.column_norms(Vb).cpu().numpy()
+    if np.any(nv == 0):
+        raise ValueError("zero load at expansion point")
+    cols = [[Vb[:, j:j + 1] / nv[j]] for j in range(s)]
+    alive = [True] * s
+    use2 = second_order and fom.damping is not None
+    w0 = 2.0 * math.pi * f_j
+    prev = [torch.zeros_like(c[0]) for c in cols]
+    for _ in range(1, m):
+        act = [j for j in range(s) if alive[j]]
+        if not act:
+            break
+        cur = torch.cat([cols[j][-1] for j in act], 1).contiguous()
+        if use2:
+            P = torch.cat([prev[j] for j in act], 1).contiguous()
+            rhs = fom.apply("D", f_j, cur)
+            fom.apply("M", f_j, cur, scale=2j * w0, out=rhs, beta=1.0)
+            fom.apply("M", f_j, P, out=rhs, beta=1.0)
+            for j in act:
+                prev[j] = cols[j][-1]
+        else:
+            rhs = fom.apply("M", f_j, cur)
+        W = lu.solve(rhs)
+        W.neg_()
+        refs = linalg.column_norms(W).cpu().numpy()
+        for q, j in enumerate(act):
+            Qb = torch.cat(cols[j], 1).contiguous()
+            w = _cgs2_against(Qb, W[:, q:q + 1].contiguous())
+            nw = float(linalg.column_norms(w).item())
+            if refs[q] == 0 or nw <= ORTH_DROP_TOL * refs[q]:
+                alive[j] = False
+                continue
+            w, nw = _polish((Qb,), w, nw, refs[q])
+            cols[j].append(w / nw)
+    return [(torch.cat(c, 1).contiguous(), not alive[j]) for j, c in enumerate(cols)]
 
 
 # ------------------------------------------------------ certification ----

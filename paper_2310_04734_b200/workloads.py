@@ -122,3 +122,47 @@ def cfg1_model(seed: int = 1, box=CFG1_BOX, ne=CFG1_NE, n_rec: int = CFG1_NREC, 
     return fom, {"xyz": xyz, "conn": conn, "src": src, "rec": rec, "Kg": Kg, "Mn": Mn, "F": F,
                  "freqs": np.arange(20.0, 200.5, 1.0), "points": CFG1_POINTS,
                  "moments": CFG1_MOMENTS}
+
+
+# ---------------------------------------------------------------- cfg3 -----
+CFG3_BOX = (0.0, 0.0, 0.0, 6.0, 3.0, 2.5)
+CFG3_NE = (60, 30, 25)
+CFG3_WALLS = ("x0", "y1", "z1")                 # three absorbing walls (recorded choice)
+CFG3_POINTS = (48.0, 104.0, 160.0, 216.0, 272.0)  # quintile midpoints of [20, 300]
+CFG3_MOMENTS = 10                               # 5 x 10 x 8 sources -> r <= 400
+CFG3_NSRC = 8
+
+
+def cfg3_model(seed: int = 3, box=CFG3_BOX, ne=CFG3_NE, n_src: int = CFG3_NSRC, n_rec: int = CFG1_NREC,
+               device=None):
+    """cfg3 (BASELINE configs[2]): 6 x 3 x 2.5 m air box, 60 x 30 x 25 hex27
+    (n = 376,431, nnz = 23,300,121), three absorbing walls with seeded
+    Z_w = rho c U[2, 10] (real, one value per wall — keeps the FDM solver
+    exact), 8 seeded interior point sources (block RHS), 50 receivers,
+    20:0.25:300 Hz.  Returns (FullOrderModel with affine operator + BoxFDM, layout)."""
+    import torch
+    from . import assembly
+    from .fdm import BoxFDM
+    from .mor import AffineOperator, AffineTerm, FullOrderModel
+    rng = np.random.default_rng(seed)
+    xyz, conn = assembly.hex27_box(box, *ne)
+    inner = assembly.interior_nodes(xyz, box)
+    src = np.sort(rng.choice(inner, n_src, replace=False)).astype(np.int64)
+    rec = np.sort(rng.choice(np.setdiff1d(inner, src), n_rec, replace=False)).astype(np.int64)
+    Zs = {w: AIR_RHO * AIR_C * float(rng.uniform(2.0, 10.0)) for w in CFG3_WALLS}
+    Kg, Mn = assembly.assemble_helmholtz(xyz, conn, device)
+    n = xyz.shape[0]
+    D_terms = []
+    for w, Z in Zs.items():
+        F = assembly.assemble_face_mass(xyz, assembly.hex27_box_face(ne, w, conn), device)
+        D_terms.append(AffineTerm(F, 1.0 / Z))
+    b = torch.zeros((n, n_src), dtype=torch.complex128, device=Kg.data.device)
+    b[torch.as_tensor(src, device=b.device), torch.arange(n_src, device=b.device)] = 1.0
+    C = np.zeros((n_rec, n))
+    C[np.arange(n_rec), rec] = 1.0
+    aff = AffineOperator(K=[AffineTerm(Kg, 1.0 / AIR_RHO)],
+                         M=[AffineTerm(Mn, 1.0 / (AIR_RHO * AIR_C * AIR_C))], D=D_terms, load=b)
+    fom = FullOrderModel(c_out=C, n=n, affine=aff, fdm=BoxFDM(box, ne, AIR_RHO, AIR_C, Zs))
+    return fom, {"xyz": xyz, "conn": conn, "src": src, "rec": rec, "walls": Zs, "Kg": Kg, "Mn": Mn,
+                 "freqs": np.arange(20.0, 300.0 + 1e-9, 0.25), "points": CFG3_POINTS,
+                 "moments": CFG3_MOMENTS}

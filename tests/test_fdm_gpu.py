@@ -1,0 +1,114 @@
+"""Fast-diagonalisation full-order solver (cfg3-size FOM) and the cfg3 MOR
+chain: residual <= 1e-10 against the assembled CSR operator (the direct_solve
+contract of solvers.py:62-78), agreement with the dense GPU LU on a small box,
+MIMO Krylov, r = 400 projection and batched sweep vs the oracle."""
+
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import mor as omor
+
+pytestmark = pytest.mark.gpu
+
+
+def _small_box(cuda):
+    import torch
+    from paper_2310_04734_b200 import assembly, mor
+    from paper_2310_04734_b200.fdm import BoxFDM
+    box, ne = (0.0, 0.0, 0.0, 1.0, 0.8, 0.6), (5, 4, 3)
+    rho, c = 1.21, 343.0
+    walls = {"x0": rho * c * 3.0, "y1": rho * c * 7.5, "z1": rho * c * (4 + 1j)}
+    xyz, conn = assembly.hex27_box(box, *ne)
+    Kg, Mn = assembly.assemble_helmholtz(xyz, conn)
+    D = [mor.AffineTerm(assembly.assemble_face_mass(xyz, assembly.hex27_box_face(ne, w, conn)), 1 / Z)
+         for w, Z in walls.items()]
+    n = Kg.n
+    b = torch.zeros((n, 2), dtype=torch.complex128, device=cuda)
+    b[100, 0] = 1.0
+    b[377, 1] = 1.0
+    aff = mor.AffineOperator(K=[mor.AffineTerm(Kg, 1 / rho)], M=[mor.AffineTerm(Mn, 1 / (rho * c * c))], D=D, load=b)
+    fom = mor.FullOrderModel(c_out=np.eye(n)[:5], n=n, affine=aff, fdm=BoxFDM(box, ne, rho, c, walls))
+    return fom, b
+
+
+def test_fdm_matches_dense_lu(cuda):
+    import torch
+    from paper_2310_04734_b200.solvers import DenseLU
+    fom, b = _small_box(cuda)
+    b0 = b.clone()
+    for f in (60.0, 333.0):
+        fd = fom.fdm.factor(f, fom)
+        x1 = fd.solve(b).cpu().numpy()
+        assert torch.equal(b, b0), "solve must not modify its right-hand side"
+        assert fd.last_residual <= 1e-10
+        x2 = DenseLU(fom.operator_dense(f)).solve(b).cpu().numpy()
+        np.testing.assert_allclose(x1, x2, rtol=0, atol=1e-9 * np.abs(x2).max())
+        A = fom.operator(f)
+        bh = b.cpu().numpy()
+        res = np.linalg.norm(A @ x1 - bh) / np.linalg.norm(bh)
+        assert res <= 1e-10, res
+
+
+def test_fdm_cfg3_scale_residual(cuda):
+    """n = 376,431: GPU FDM + refinement reaches ||Ax - b|| / ||b|| <= 1e-10,
+    checked independently on the host with the assembled CSR primitives."""
+    from paper_2310_04734_b200 import workloads
+    fom, lay = workloads.cfg3_model()
+    assert fom.n == 376_431 and lay["Kg"].nnz == 23_300_121
+    f = 104.0
+    fd = fom.factor(f)
+    X = fd.solve(fom.load_dev(f))
+    assert fd.last_residual <= 1e-10
+    x = X[:, 3].cpu().numpy()
+    w = 2 * math.pi * f
+    K = lay["Kg"].to_scipy() / workloads.AIR_RHO
+    M = lay["Mn"].to_scipy() / (workloads.AIR_RHO * workloads.AIR_C ** 2)
+    Ax = K @ x - w * w * (M @ x)
+    for t in fom.affine.D:
+        Ax = Ax + 1j * w * t.at(f) * (t.P.to_scipy() @ x)
+    bvec = np.zeros(fom.n, complex)
+    bvec[lay["src"][3]] = 1.0
+    assert np.linalg.norm(Ax - bvec) / np.linalg.norm(bvec) <= 1e-10
+
+
+def test_cfg3_mor_chain(cuda):
+    """MIMO Krylov (5 points x 10 moments x 8 sources) -> CGS2 union -> r <= 400
+    projection -> batched sweep; GPU sweep == oracle zgesv sweep on the same
+    reduced operator (TF <= 1e-8), ROM vs FDM full-order solves at sampled
+    frequencies."""
+    import torch
+    from paper_2310_04734_b200 import mor, workloads
+    fom, lay = workloads.cfg3_model()
+    V = None
+    for f0 in lay["points"]:
+        for Q, _ in mor.krylov_blocks_mimo_dev(fom, f0, lay["moments"], second_order=True):
+            V = mor._orthonormalise(V, Q)
+    r = V.shape[1]
+    assert 300 <= r <= 400
+    G = V[:, :64].conj().T @ V[:, :64]
+    assert torch.abs(G - torch.eye(64, dtype=G.dtype, device=G.device)).max().item() <= 1e-10
+    rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 300.0))
+    grid = list(lay["freqs"][::40])
+    y, spl, _, info = rom.sweep(grid)
+    assert int(info.abs().sum()) == 0
+    P, kinds, br = rom._projected()
+    alpha = rom._alpha(np.array(grid), kinds)
+    yo, splo = omor.affine_sweep(P.cpu().numpy(), alpha[::7], br.cpu().numpy(), rom._cR.cpu().numpy())
+    yg = y.cpu().numpy()[::7]
+    for i in range(len(yo)):
+        _, e, _, _ = omor.relative_error(yo[i].ravel(), yg[i].ravel())
+        assert e <= 1e-8
+    np.testing.assert_allclose(spl.cpu().numpy()[::7], splo, atol=0.01)
+    # ROM approximation vs the full-order model at sampled frequencies
+    C = np.atleast_2d(fom.c_out)
+    worst = 0.0
+    for i in (3, 10, 17):
+        f = grid[i]
+        X = fom.factor(f).solve(fom.load_dev(f)).cpu().numpy()
+        yf = C @ X
+        _, e, _, _ = omor.relative_error(yf.ravel(), yg[0].ravel() if False else y.cpu().numpy()[i].ravel())
+        worst = max(worst, e)
+    assert worst <= 5e-2, worst
