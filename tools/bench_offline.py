@@ -1,0 +1,79 @@
+"""Timed offline-phase kernels at cfg3 size (n = 376,431, nnz = 23.3M): assembly,
+SpMM (k = 400), split-K projection GEMM, FDM solve; CUDA events, warm runs.
+Prints one JSON object with achieved bandwidth / flops vs the algorithmic counts."""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np
+import torch
+
+from paper_2310_04734_b200 import _lib, assembly, linalg, workloads
+
+
+def timed(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best
+
+
+def main():
+    dev = torch.device("cuda")
+    peak_hbm = json.load(open(Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"))["hbm_gbs"] \
+        if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6650.0
+    box, ne = workloads.CFG3_BOX, workloads.CFG3_NE
+    xyz, conn = assembly.hex27_box(box, *ne)
+    n = xyz.shape[0]
+    xyz_d = torch.as_tensor(xyz, device=dev)
+    conn_d = torch.as_tensor(conn, device=dev)
+    out = {"n": n}
+    pat = [None]
+    out["pattern_ms"] = timed(lambda: pat.__setitem__(0, assembly.pattern_from_elements(n, conn_d)), 2)
+    P = pat[0]
+    nnz = P.nnz
+    out["nnz"] = nnz
+    KM = [None]
+    out["element_ms"] = timed(lambda: KM.__setitem__(0, assembly.hex27_helmholtz(xyz_d, conn_d)))
+    Ke, Me = KM[0]
+    out["gather_ms"] = timed(lambda: (P.gather(Ke), P.gather(Me)))
+    Kg = P.gather(Ke)
+    alg_asm = nnz * (8 * 2 + 4) + (n + 1) * 4 + xyz.nbytes + conn.nbytes
+    t_val = out["element_ms"] + out["gather_ms"]
+    out["assembly_values_GBps"] = alg_asm / (t_val * 1e-3) / 1e9
+    out["assembly_values_frac_hbm"] = out["assembly_values_GBps"] / peak_hbm
+    for k in (32, 400):
+        X = torch.randn(n, k, dtype=torch.complex128, device=dev)
+        t = timed(lambda: linalg.spmm(Kg, X))
+        alg = nnz * 12 + 2 * n * k * 16
+        out[f"spmm_k{k}_ms"] = t
+        out[f"spmm_k{k}_GBps"] = alg / (t * 1e-3) / 1e9
+        out[f"spmm_k{k}_frac_hbm"] = out[f"spmm_k{k}_GBps"] / peak_hbm
+    V = torch.randn(n, 400, dtype=torch.complex128, device=dev)
+    W = torch.randn(n, 400, dtype=torch.complex128, device=dev)
+    t = timed(lambda: linalg.zgemm("C", V, W))
+    out["proj_zgemm_ms"] = t
+    out["proj_zgemm_TFLOPs"] = 8 * n * 400 * 400 / (t * 1e-3) / 1e12
+    out["peak_fp64_TFLOPs"] = _lib.probe_fp64_peak()
+    out["proj_zgemm_frac"] = out["proj_zgemm_TFLOPs"] / out["peak_fp64_TFLOPs"]
+    fom, lay = workloads.cfg3_model()
+    fd = fom.factor(104.0)
+    B = fom.load_dev(104.0)
+    out["fdm_solve_8rhs_ms"] = timed(lambda: fd.solve(B), 2)
+    out["fdm_refinements"] = fd.iterations
+    out["fdm_residual"] = fd.last_residual
+    out["peak_hbm_GBps"] = peak_hbm
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
