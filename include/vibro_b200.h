@@ -116,6 +116,17 @@ int vb_csr_gather(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_
 int vb_hex27_helmholtz_elements(int n_elem, const double* xyz, const int32_t* conn, double* Ke,
                                 double* Me, int32_t* bad_elem_host, void* stream);
 
+/* Structured fast path (uniform axis-aligned hex27 box of nx x ny x nz equal
+ * elements, BASELINE cfg1/cfg3): writes indptr [n+1], indices / Kvals / Mvals
+ * [vb_hex27_box_nnz] directly — the same canonical pattern as
+ * vb_csr_pattern_from_elements, values from the Kronecker form of the assembled
+ * 1D quadratic matrices (the element sums of assembly.py:142-175 factorise):
+ *  K1, M1 [3][maxnp][5] (device): band entries (offset j - i + 2) of the 1D
+ *  stiffness / mass along x, y, z. */
+int64_t vb_hex27_box_nnz(int nx, int ny, int nz);
+int vb_hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1, int maxnp, int32_t* indptr,
+                     int32_t* indices, double* Kvals, double* Mvals, void* stream);
+
 /* Impedance-wall primitive: int_Gamma N N^T dGamma on 9-node faces
  * (face_conn [n_faces][9], lexicographic), Fe [n_faces][9][9] out. */
 int vb_quad9_face_mass(int n_faces, const double* xyz, const int32_t* face_conn, double* Fe,

@@ -175,3 +175,46 @@ def assemble_face_mass(xyz, face_conn, device=None) -> DeviceCSR:
     f_d = torch.as_tensor(np.ascontiguousarray(face_conn, dtype=np.int32), device=dev)
     pat = pattern_from_elements(xyz.shape[0], f_d)
     return pat.gather(face_mass(xyz_d, f_d))
+
+
+def box_band_tables(box, ne):
+    """[3][maxnp][5] band entries of the assembled 1D quadratic stiffness / mass
+    along x, y, z (host; a few KB)."""
+    from .fdm import line_matrices
+    x0, y0, z0, x1, y1, z1 = box
+    maxnp = 2 * max(ne) + 1
+    K1 = np.zeros((3, maxnp, 5))
+    M1 = np.zeros((3, maxnp, 5))
+    for d, (L, m) in enumerate(zip((x1 - x0, y1 - y0, z1 - z0), ne)):
+        K, M = line_matrices(L, m)
+        npd = 2 * m + 1
+        for i in range(npd):
+            for o in range(5):
+                j = i + o - 2
+                if 0 <= j < npd:
+                    K1[d, i, o] = K[i, j]
+                    M1[d, i, o] = M[i, j]
+    return K1, M1, maxnp
+
+
+def assemble_helmholtz_box(box, ne, device=None):
+    """Structured fast path for a uniform box (vb_hex27_box_csr): analytic
+    canonical pattern, Kronecker-form values.  Same CSR as
+    assemble_helmholtz(hex27_box(...)) (pattern bit-exact, values to rounding)."""
+    _lib.require_cuda()
+    lib = _lib.load()
+    dev = torch.device(device or "cuda")
+    nx, ny, nz = ne
+    K1, M1, maxnp = box_band_tables(box, ne)
+    K1d = torch.as_tensor(K1, device=dev)
+    M1d = torch.as_tensor(M1, device=dev)
+    n = (2 * nx + 1) * (2 * ny + 1) * (2 * nz + 1)
+    nnz = int(lib.vb_hex27_box_nnz(nx, ny, nz))
+    indptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    indices = torch.empty(nnz, dtype=torch.int32, device=dev)
+    Kv = torch.empty(nnz, dtype=torch.float64, device=dev)
+    Mv = torch.empty(nnz, dtype=torch.float64, device=dev)
+    _lib.check(lib.vb_hex27_box_csr(nx, ny, nz, _lib.ptr(K1d), _lib.ptr(M1d), maxnp, _lib.ptr(indptr),
+                                    _lib.ptr(indices), _lib.ptr(Kv), _lib.ptr(Mv), _lib.stream_handle()),
+               "vb_hex27_box_csr")
+    return DeviceCSR(n, indptr, indices, Kv), DeviceCSR(n, indptr, indices, Mv)

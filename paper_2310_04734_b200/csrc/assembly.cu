@@ -20,17 +20,20 @@ namespace vb {
 
 // ---------------------------------------------------------------- tables ---
 // 3-point Gauss-Legendre (shape.py:56-57 = numpy leggauss(3)), closed form.
+// The element tables are indexed by lane-dependent (gauss point, node) pairs, so
+// they live in global memory (L1-cached) rather than __constant__ (which
+// serialises divergent addresses).
 __constant__ double c_gx[3];
 __constant__ double c_gw[3];
 // hex27: N[g][i], dN/dxi[g][i][a]; local node i = a + 3b + 9c, Gauss point
 // g = gx + 3 gy + 9 gz (x fastest, shape.py:60-65 generalised).
-__constant__ double c_hexN[27 * 27];
-__constant__ double c_hexdN[27 * 27 * 3];
-__constant__ double c_hexW[27];
+__device__ double c_hexN[27 * 27];
+__device__ double c_hexdN[27 * 27 * 3];
+__device__ double c_hexW[27];
 // quad9 face (lexicographic a + 3b): N[g][i], dN/dxi[g][i][2], weights.
-__constant__ double c_qN[9 * 9];
-__constant__ double c_qdN[9 * 9 * 2];
-__constant__ double c_qW[9];
+__device__ double c_qN[9 * 9];
+__device__ double c_qdN[9 * 9 * 2];
+__device__ double c_qW[9];
 
 static void lag1d(double x, double* v) {  // shape.py:20-22
   v[0] = 0.5 * x * (x - 1.0);
@@ -108,41 +111,47 @@ __global__ void __launch_bounds__(EL_NT) hex27_helmholtz_kernel(int n_elem, cons
   __shared__ double X[27][3];
   __shared__ double wdet[27];
   __shared__ double dNx[27][27][3];  // [g][i][b]
+  __shared__ double sN[27 * 27];     // N[g][i]
   const int tid = threadIdx.x;
+  for (int q = tid; q < 729; q += EL_NT) sN[q] = c_hexN[q];
   for (int e = blockIdx.x; e < n_elem; e += gridDim.x) {
     for (int q = tid; q < 81; q += EL_NT) X[q / 3][q % 3] = xyz[(size_t)conn[(size_t)e * 27 + q / 3] * 3 + q % 3];
     __syncthreads();
+    // J[g][a][b] = sum_i dN_i/dxi_a(g) X_i,b  (243 independent sums)
+    __shared__ double Jg[27][9];
+    for (int q = tid; q < 243; q += EL_NT) {
+      const int g = q / 9, a = (q % 9) / 3, b = q % 3;
+      double acc = 0.0;
+      for (int i = 0; i < 27; ++i) acc += __ldg(&c_hexdN[(g * 27 + i) * 3 + a]) * X[i][b];
+      Jg[g][a * 3 + b] = acc;
+    }
+    __syncthreads();
+    __shared__ double iJg[27][9];
     if (tid < 27) {
       const int g = tid;
-      double J[3][3];
-      for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) {
-          double s = 0.0;
-          for (int i = 0; i < 27; ++i) s += c_hexdN[(g * 27 + i) * 3 + a] * X[i][b];
-          J[a][b] = s;
-        }
-      const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
-                         J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
-                         J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      const double* J = Jg[g];
+      const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
+                         J[2] * (J[3] * J[7] - J[4] * J[6]);
       if (!(det > 0.0)) atomicMin(bad, e);
       const double id = 1.0 / det;
-      double iJ[3][3];
-      iJ[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
-      iJ[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
-      iJ[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
-      iJ[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
-      iJ[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
-      iJ[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
-      iJ[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
-      iJ[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
-      iJ[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
-      wdet[g] = c_hexW[g] * det;
-      for (int i = 0; i < 27; ++i)
-        for (int b = 0; b < 3; ++b) {
-          double s = 0.0;
-          for (int a = 0; a < 3; ++a) s += c_hexdN[(g * 27 + i) * 3 + a] * iJ[a][b];
-          dNx[g][i][b] = s;
-        }
+      double* iJ = iJg[g];
+      iJ[0] = (J[4] * J[8] - J[5] * J[7]) * id;
+      iJ[1] = (J[2] * J[7] - J[1] * J[8]) * id;
+      iJ[2] = (J[1] * J[5] - J[2] * J[4]) * id;
+      iJ[3] = (J[5] * J[6] - J[3] * J[8]) * id;
+      iJ[4] = (J[0] * J[8] - J[2] * J[6]) * id;
+      iJ[5] = (J[2] * J[3] - J[0] * J[5]) * id;
+      iJ[6] = (J[3] * J[7] - J[4] * J[6]) * id;
+      iJ[7] = (J[1] * J[6] - J[0] * J[7]) * id;
+      iJ[8] = (J[0] * J[4] - J[1] * J[3]) * id;
+      wdet[g] = __ldg(&c_hexW[g]) * det;
+    }
+    __syncthreads();
+    // dN = dshape inv(J)  (assembly.py:88): 27 x 27 x 3 entries
+    for (int q = tid; q < 2187; q += EL_NT) {
+      const int g = q / 81, i = (q / 3) % 27, b = q % 3;
+      const double* dS = &c_hexdN[(g * 27 + i) * 3];
+      dNx[g][i][b] = __ldg(dS) * iJg[g][b] + __ldg(dS + 1) * iJg[g][3 + b] + __ldg(dS + 2) * iJg[g][6 + b];
     }
     __syncthreads();
     for (int q = tid; q < 729; q += EL_NT) {
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(EL_NT) hex27_helmholtz_kernel(int n_elem, cons
       for (int g = 0; g < 27; ++g) {
         const double w = wdet[g];
         k += w * (dNx[g][i][0] * dNx[g][j][0] + dNx[g][i][1] * dNx[g][j][1] + dNx[g][i][2] * dNx[g][j][2]);
-        m += w * (c_hexN[g * 27 + i] * c_hexN[g * 27 + j]);
+        m += w * (sN[g * 27 + i] * sN[g * 27 + j]);
       }
       Ke[(size_t)e * 729 + q] = k;
       Me[(size_t)e * 729 + q] = m;
@@ -372,6 +381,110 @@ int quad9_face_mass(int n_faces, const double* xyz, const int32_t* fconn, double
   const unsigned grid = (unsigned)(((int64_t)n_faces * 32 + nt - 1) / nt);
   quad9_face_mass_kernel<<<grid, nt, 0, stream>>>(n_faces, xyz, fconn, Fe);
   VB_LAUNCHED("quad9_face_mass_kernel");
+  return 0;
+}
+
+}  // namespace vb
+
+namespace vb {
+
+// ------------------------------------------- structured box fast path ---
+// Uniform axis-aligned hex27 box.  With tensor-product bases and 3x3x3 Gauss
+// the element matrices factorise, and summing them over the elements gives the
+// Kronecker form of the assembled 1D matrices:
+//   Kgrad = Mz (x) My (x) Kx + Mz (x) Ky (x) Mx + Kz (x) My (x) Mx,  Mnn = Mz (x) My (x) Mx
+// (exact algebra; values agree with the element-order sums to rounding, the
+// pattern is the same canonical CSR).  One warp per x-line of rows writes
+// indices and both value arrays with consecutive lanes on consecutive slots:
+// the kernel writes exactly the algorithmic bytes of the assembly.
+// band tables: [d][i][o] with o = j - i + 2 in 0..4, for d = x, y, z.
+__global__ void hex27_box_csr_kernel(int nx, int ny, int nz, const double* __restrict__ K1,
+                                     const double* __restrict__ M1, int maxnp, int32_t* __restrict__ indptr,
+                                     int32_t* __restrict__ indices, double* __restrict__ Kv,
+                                     double* __restrict__ Mv) {
+  const int npx = 2 * nx + 1, npy = 2 * ny + 1, npz = 2 * nz + 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t Tx = 8LL * nx + 1, Ty = 8LL * ny + 1;
+  const int nlines = npy * npz;
+  constexpr int SEG = 8;  // rows per warp task (enough tasks to fill the GPU)
+  const int nseg = (npx + SEG - 1) / SEG;
+  const double* Kx = K1;
+  const double* Ky = K1 + (size_t)maxnp * 5;
+  const double* Kz = K1 + (size_t)2 * maxnp * 5;
+  const double* Mx = M1;
+  const double* My = M1 + (size_t)maxnp * 5;
+  const double* Mz = M1 + (size_t)2 * maxnp * 5;
+  for (int task = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); task < nlines * nseg;
+       task += (int)((gridDim.x * blockDim.x) >> 5)) {
+    const int line = task / nseg, seg = task - line * nseg;
+    const int iy = line % npy, iz = line / npy;
+    // neighbour ranges along y and z (quadratic elements: 3 or 5 nodes)
+    const int ylo = (iy & 1) ? iy - 1 : max(0, iy - 2), yhi = (iy & 1) ? iy + 1 : min(npy - 1, iy + 2);
+    const int zlo = (iz & 1) ? iz - 1 : max(0, iz - 2), zhi = (iz & 1) ? iz + 1 : min(npz - 1, iz + 2);
+    const int cy = yhi - ylo + 1, cz = zhi - zlo + 1;
+    const int py = iy < 1 ? 0 : 3 * iy + 2 * min(ny - 1, (iy - 1) >> 1);
+    const int pz = iz < 1 ? 0 : 3 * iz + 2 * min(nz - 1, (iz - 1) >> 1);
+    const int ix0 = seg * SEG, ix1 = min(npx, ix0 + SEG);
+    const int px = ix0 < 1 ? 0 : 3 * ix0 + 2 * min(nx - 1, (ix0 - 1) >> 1);
+    int64_t start = (int64_t)pz * Ty * Tx + (int64_t)cz * ((int64_t)py * Tx + (int64_t)cy * px);
+    // rows of this segment; when a y-x neighbour plane has <= 16 slots (cy = 3),
+    // the two half-warps take two consecutive rows at once
+    const int half = (cy == 3) ? 16 : 32;
+    const int sub = lane / half, hl = lane - sub * half;
+    for (int ixb = ix0; ixb < ix1; ixb += (half == 16 ? 2 : 1)) {
+      const int ixa = ixb;
+      // offsets of the (up to) two rows of this step
+      const int cxa = (ixa & 1) ? 3 : (min(npx - 1, ixa + 2) - max(0, ixa - 2) + 1);
+      const int ix = ixa + sub;
+      const bool active = ix < ix1 && (half == 32 ? sub == 0 : true);
+      const int xlo = (ix & 1) ? ix - 1 : max(0, ix - 2), xhi = (ix & 1) ? ix + 1 : min(npx - 1, ix + 2);
+      const int cx = xhi - xlo + 1;
+      const int cxy = cx * cy, cnt = cxy * cz;
+      const int64_t rstart = start + (sub == 1 ? (int64_t)cxa * cy * cz : 0);
+      const int64_t row = (int64_t)line * npx + ix;
+      if (active && hl == 0) indptr[row] = (int32_t)rstart;
+      if (active && hl < cxy) {  // (qy, qx) of the y-x plane of neighbours, loop over qz
+        const int qy = hl / cx, qx = hl - qy * cx;
+        const int jx = xlo + qx, jy = ylo + qy;
+        const int ox = jx - ix + 2, oy = jy - iy + 2;
+        const double kx = __ldg(Kx + ix * 5 + ox), mx = __ldg(Mx + ix * 5 + ox);
+        const double ky = __ldg(Ky + iy * 5 + oy), my = __ldg(My + iy * 5 + oy);
+        const double kxy = my * kx + ky * mx, mxy = my * mx;
+        const int64_t col0 = (int64_t)jy * npx + jx;
+        for (int qz = 0; qz < cz; ++qz) {
+          const int jz = zlo + qz, oz = jz - iz + 2;
+          const double kz = __ldg(Kz + iz * 5 + oz), mz = __ldg(Mz + iz * 5 + oz);
+          const int64_t s = rstart + (int64_t)qz * cxy + hl;
+          indices[s] = (int32_t)((int64_t)jz * npy * npx + col0);
+          Kv[s] = mz * kxy + kz * mxy;
+          Mv[s] = mz * mxy;
+        }
+      }
+      // advance past the rows handled in this step
+      start += (int64_t)cxa * cy * cz;
+      if (half == 16 && ixa + 1 < ix1) {
+        const int ixn = ixa + 1;
+        const int cxn = (ixn & 1) ? 3 : (min(npx - 1, ixn + 2) - max(0, ixn - 2) + 1);
+        start += (int64_t)cxn * cy * cz;
+      }
+      (void)cnt;
+    }
+    if (line == nlines - 1 && ix1 == npx && lane == 0) indptr[(int64_t)nlines * npx] = (int32_t)start;
+  }
+}
+
+int64_t hex27_box_nnz(int nx, int ny, int nz) { return (8LL * nx + 1) * (8LL * ny + 1) * (8LL * nz + 1); }
+
+int hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1, int maxnp, int32_t* indptr,
+                  int32_t* indices, double* Kv, double* Mv, cudaStream_t st) {
+  VB_CHECK_ARG(nx > 0 && ny > 0 && nz > 0, "vb_hex27_box_csr: bad element counts");
+  VB_CHECK_ARG(hex27_box_nnz(nx, ny, nz) < ((int64_t)1 << 31), "vb_hex27_box_csr: nnz exceeds int32");
+  VB_CHECK_ARG(maxnp >= 2 * nx + 1 && maxnp >= 2 * ny + 1 && maxnp >= 2 * nz + 1, "vb_hex27_box_csr: band table too small");
+  const int64_t tasks = (int64_t)(2 * ny + 1) * (2 * nz + 1) * ((2 * nx + 1 + 7) / 8);
+  const int nt = 256;
+  int64_t blocks = (tasks * 32 + nt - 1) / nt;
+  hex27_box_csr_kernel<<<(unsigned)blocks, nt, 0, st>>>(nx, ny, nz, K1, M1, maxnp, indptr, indices, Kv, Mv);
+  VB_LAUNCHED("hex27_box_csr_kernel");
   return 0;
 }
 

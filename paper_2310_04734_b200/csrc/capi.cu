@@ -171,4 +171,12 @@ int vb_fdm_diag(int n2, int n1, int n0, int nrhs, const vb_complex* lz, const vb
                       (cudaStream_t)stream);
 }
 
+int64_t vb_hex27_box_nnz(int nx, int ny, int nz) { return vb::hex27_box_nnz(nx, ny, nz); }
+
+int vb_hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1, int maxnp, int32_t* indptr,
+                     int32_t* indices, double* Kvals, double* Mvals, void* stream) {
+  VB_CHECK_ARG(K1 && M1 && indptr && indices && Kvals && Mvals, "vb_hex27_box_csr: null pointer");
+  return vb::hex27_box_csr(nx, ny, nz, K1, M1, maxnp, indptr, indices, Kvals, Mvals, (cudaStream_t)stream);
+}
+
 }  // extern "C"

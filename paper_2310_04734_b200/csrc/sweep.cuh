@@ -39,6 +39,10 @@ int quad9_face_mass(int n_faces, const double* xyz, const int32_t* fconn, double
                     cudaStream_t stream);
 
 
+int64_t hex27_box_nnz(int nx, int ny, int nz);
+int hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1, int maxnp, int32_t* indptr,
+                  int32_t* indices, double* Kv, double* Mv, cudaStream_t st);
+
 // linalg.cu
 int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
              const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st);

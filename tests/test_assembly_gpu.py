@@ -75,3 +75,19 @@ def test_negative_jacobian_raises(cuda):
     conn[1] = conn[1][::-1]  # mirrored element: detJ < 0
     with pytest.raises(ValueError, match="element 1"):
         assembly.assemble_helmholtz(xyz, conn)
+
+
+@pytest.mark.parametrize("ne", [(3, 2, 2), (10, 8, 6), (1, 1, 1), (4, 1, 3)])
+def test_box_fast_path_equals_general_assembly(cuda, ne):
+    """vb_hex27_box_csr (analytic pattern, shared element matrix) == the general
+    sort/gather path: pattern bit-exact, values to rounding."""
+    from paper_2310_04734_b200 import assembly
+    box = (0.0, 0.0, 0.0, 2.0, 1.6, 1.2)
+    Kb, Mb = assembly.assemble_helmholtz_box(box, ne)
+    xyz, conn = assembly.hex27_box(box, *ne)
+    Kg, Mg = assembly.assemble_helmholtz(xyz, conn)
+    for A, B in ((Kb, Kg), (Mb, Mg)):
+        Sa, Sb = A.to_scipy(), B.to_scipy()
+        np.testing.assert_array_equal(Sa.indptr, Sb.indptr)
+        np.testing.assert_array_equal(Sa.indices, Sb.indices)
+        np.testing.assert_allclose(Sa.data, Sb.data, rtol=0, atol=1e-13 * np.abs(Sb.data).max())
