@@ -157,6 +157,25 @@ def gold_reduced_dense():
                         r=w.r, s=w.b.shape[1], n_out=w.c_r.shape[0], seed=w.seed, n_freq=2000)
 
 
+def gold_artifacts():
+    """Reference rom.npz (cli.save_roms) and frf_mor.csv (cli.write_csv) bytes."""
+    from vibrofem import cli as rcli
+    fom, K, M, b, c = frozen_fom()
+    Q, _ = rmor.krylov_block(fom, 35.0, 4)
+    roms = [rmor.ReducedModel(fom=fom, V=Q, window=(10.0, 50.0), expansion_points=[35.0],
+                              error_log=[(10.0, 1e-3), (50.0, 2e-3)], converged=True),
+            rmor.ReducedModel(fom=fom, V=Q[:, :2], window=(50.0, 100.0), expansion_points=[35.0],
+                              error_log=[(50.0, 5e-2)], stalled=True)]
+    rcli.save_roms(HERE / "rom_ref.npz", roms)
+    grid = [10.0, 30.0, 50.0, 75.0, 100.0]
+    sw = rmor.rom_sweep(roms, grid)
+    rows = [[f, y.real, y.imag, 20.0 * np.log10(max(abs(y), 1e-300) / 20e-6), w]
+            for f, y, w in zip(sw.freqs, sw.frf, sw.window_index)]
+    rcli.write_csv(HERE / "frf_ref.csv", ["f_hz", "re_p", "im_p", "abs_db", "window"], rows)
+    np.savez_compressed(HERE / "frf_ref_values.npz", freqs=np.array(grid), frf=np.array(sw.frf),
+                        window_index=np.array(sw.window_index))
+
+
 def gold_spl():
     vals = {"ones": mean_spl(np.ones(64, complex)), "zeros": mean_spl(np.zeros(5, complex))}
     rng = np.random.default_rng(4)
@@ -171,5 +190,6 @@ if __name__ == "__main__":
     gold_box_mor()
     gold_reduced_dense()
     gold_spl()
+    gold_artifacts()
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size)

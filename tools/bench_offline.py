@@ -27,7 +27,7 @@ def timed(fn, reps=3):
     return best
 
 
-def main():
+def measure():
     dev = torch.device("cuda")
     peak_hbm = json.load(open(Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"))["hbm_gbs"] \
         if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6650.0
@@ -89,7 +89,11 @@ def main():
     out["fdm_refinements"] = fd.iterations
     out["fdm_residual"] = fd.last_residual
     out["peak_hbm_GBps"] = peak_hbm
-    print(json.dumps(out))
+    return out
+
+
+def main():
+    print(json.dumps(measure()))
 
 
 if __name__ == "__main__":
