@@ -175,7 +175,9 @@ __device__ void apply_swaps(z_t* A, int ldw, const int* piv, int k0, int a, int 
 }
 
 // U = L^-1 U for rows [cl, cl+n1) (unit lower L = A[cl:cl+n1, cl:cl+n1], n1 <= 32)
-// on columns [c0, c1): L staged in shared memory, one thread per column.
+// on columns [c0, c1): L staged in shared memory; for long chains (n1 >= 16) one
+// WARP per column with the column's rows on the lanes (forward substitution by
+// shuffles), else one thread per column.
 __device__ void trsm_small(z_t* A, int ldw, int cl, int n1, int c0, int c1, z_t* smem) {
   constexpr int LD = 33;
   z_t* Ls = smem;
@@ -184,13 +186,26 @@ __device__ void trsm_small(z_t* A, int ldw, int cl, int n1, int c0, int c1, z_t*
     Ls[i * LD + k] = A[(size_t)(cl + i) * ldw + cl + k];
   }
   __syncthreads();
-  for (int c = c0 + threadIdx.x; c < c1; c += NT) {
-    z_t* col = A + (size_t)cl * ldw + c;
-    for (int i = 1; i < n1; ++i) {
-      z_t acc = col[(size_t)i * ldw];
-      for (int k = 0; k < i; ++k) acc = zfms(acc, Ls[i * LD + k], col[(size_t)k * ldw]);
-      col[(size_t)i * ldw] = acc;
+  if (n1 < 16) {  // short chains: one thread per column (coalesced across the warp)
+    for (int c = c0 + threadIdx.x; c < c1; c += NT) {
+      z_t* col = A + (size_t)cl * ldw + c;
+      for (int i = 1; i < n1; ++i) {
+        z_t acc = col[(size_t)i * ldw];
+        for (int k = 0; k < i; ++k) acc = zfms(acc, Ls[i * LD + k], col[(size_t)k * ldw]);
+        col[(size_t)i * ldw] = acc;
+      }
     }
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = c0 + warp; c < c1; c += NT / 32) {
+    z_t x = zmake(0.0, 0.0);
+    if (lane < n1) x = A[(size_t)(cl + lane) * ldw + c];
+    for (int k = 0; k + 1 < n1; ++k) {
+      const double xr = __shfl_sync(0xffffffffu, x.x, k), xi = __shfl_sync(0xffffffffu, x.y, k);
+      if (lane > k && lane < n1) x = zfms(x, Ls[lane * LD + k], zmake(xr, xi));
+    }
+    if (lane >= 1 && lane < n1) A[(size_t)(cl + lane) * ldw + c] = x;
   }
 }
 
