@@ -102,6 +102,25 @@ int vb_csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn
                                  int32_t* indices, int64_t* gather_ptr, int32_t* gather_idx,
                                  int64_t* nnz_host, void* work, size_t work_bytes, void* stream);
 
+/* Rectangular / constrained generalisation: triplet t = e*nr*nc + a*nc + b has
+ * row row_dofs[e][a] and column col_dofs[e][b] (n_rows x n_cols matrix); a
+ * negative DoF (eliminated, e.g. clamped) drops the triplet.  Same outputs and
+ * gather semantics as vb_csr_pattern_from_elements (gather lists index the
+ * full triplet stream, so dropped triplets are simply never referenced). */
+size_t vb_csr_pattern_blocks_workspace_bytes(int n_rows, int n_cols, int n_elem, int nr, int nc);
+int vb_csr_pattern_from_blocks(int n_rows, int n_cols, int n_elem, int nr, int nc, const int32_t* row_dofs,
+                               const int32_t* col_dofs, int32_t* indptr, int32_t* indices, int64_t* gather_ptr,
+                               int32_t* gather_idx, int64_t* nnz_host, void* work, size_t work_bytes, void* stream);
+
+/* 9-node Reissner-Mindlin + membrane plate element matrices (cfg2 plate; no
+ * reference counterpart — restated with the conventions of
+ * vibrofem/assembly.py:31-67): node DoFs (u, v, w, bx, by), local nodes a + 3b,
+ * xyz [n_nodes][3] (plate in the x-y plane), conn [n_elem][9],
+ * Ke, Me [n_elem][45][45] out (undamped; the loss factor is applied as a
+ * complex scalar (1 + i eta(f)) on the assembled stiffness). */
+int vb_rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, double E, double nu, double rho,
+                         double t, double* Ke, double* Me, int32_t* bad_elem_host, void* stream);
+
 /* CSR values from triplet values: vals[s] = sum of triplet_vals over the
  * slot's gather list, in element order (deterministic; assembly.py:172-173). */
 int vb_csr_gather(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx,

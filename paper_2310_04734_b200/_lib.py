@@ -40,6 +40,12 @@ _SIGS = {
                                                C.c_void_p, C.c_void_p, C.c_void_p,
                                                C.POINTER(C.c_int64), C.c_void_p, C.c_size_t,
                                                C.c_void_p]),
+    "vb_csr_pattern_blocks_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "vb_csr_pattern_from_blocks": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.POINTER(C.c_int64), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vb_rm_plate_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p]),
     "vb_csr_gather": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vb_hex27_helmholtz_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.POINTER(C.c_int32), C.c_void_p]),

@@ -34,6 +34,10 @@ __device__ double c_hexW[27];
 __device__ double c_qN[9 * 9];
 __device__ double c_qdN[9 * 9 * 2];
 __device__ double c_qW[9];
+// quad9 at the 2x2 (reduced) rule, for the Reissner-Mindlin shear term
+__device__ double c_rN[4 * 9];
+__device__ double c_rdN[4 * 9 * 2];
+__device__ double c_rW[4];
 
 static void lag1d(double x, double* v) {  // shape.py:20-22
   v[0] = 0.5 * x * (x - 1.0);
@@ -85,6 +89,25 @@ static int init_tables() {
       qdN[(g * 9 + i) * 2 + 1] = L[0][n2[0]] * D[1][n2[1]];
     }
   }
+  double rN[36], rdN[72], rW[4];
+  const double g2[2] = {-0.5773502691896258, 0.5773502691896258};
+  for (int g = 0; g < 4; ++g) {
+    double L[2][3], D[2][3];
+    lag1d(g2[g % 2], L[0]);
+    dlag1d(g2[g % 2], D[0]);
+    lag1d(g2[g / 2], L[1]);
+    dlag1d(g2[g / 2], D[1]);
+    rW[g] = 1.0;
+    for (int i = 0; i < 9; ++i) {
+      const int n2[2] = {i % 3, i / 3};
+      rN[g * 9 + i] = L[0][n2[0]] * L[1][n2[1]];
+      rdN[(g * 9 + i) * 2 + 0] = D[0][n2[0]] * L[1][n2[1]];
+      rdN[(g * 9 + i) * 2 + 1] = L[0][n2[0]] * D[1][n2[1]];
+    }
+  }
+  VB_CUDA(cudaMemcpyToSymbol(c_rN, rN, sizeof(rN)));
+  VB_CUDA(cudaMemcpyToSymbol(c_rdN, rdN, sizeof(rdN)));
+  VB_CUDA(cudaMemcpyToSymbol(c_rW, rW, sizeof(rW)));
   VB_CUDA(cudaMemcpyToSymbol(c_gx, gx, sizeof(gx)));
   VB_CUDA(cudaMemcpyToSymbol(c_gw, gw, sizeof(gw)));
   VB_CUDA(cudaMemcpyToSymbol(c_hexN, hN, sizeof(hN)));
@@ -204,42 +227,159 @@ __global__ void quad9_face_mass_kernel(int n_faces, const double* __restrict__ x
   }
 }
 
-// ------------------------------------------------------------ pattern ---
-__global__ void make_keys_kernel(int64_t T, int npe, int n, const int32_t* __restrict__ conn,
-                                 uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  const int64_t pe = (int64_t)npe * npe;
-  const int64_t e = t / pe;
-  const int a = (int)((t / npe) % npe), b = (int)(t % npe);
-  const uint64_t row = (uint64_t)conn[e * npe + a], col = (uint64_t)conn[e * npe + b];
-  keys[t] = row * (uint64_t)n + col;
-  vals[t] = (int32_t)t;
+// ------------------------------------------------ Reissner-Mindlin plate ---
+// 9-node flat plate element with node DoFs (u, v, w, bx, by): membrane ("disc")
+// = the reference's plane-stress element (assembly.py:31-67), bending
+// kappa = [bx,x, by,y, bx,y + by,x] with D_b = E t^3/(12(1-nu^2)) (...), shear
+// gamma = [w,x + bx, w,y + by] with (5/6) G t at the 2x2 rule, consistent mass
+// rho t (u, v, w) and rho t^3/12 (bx, by).  One CTA per element, one thread per
+// (row, col) entry of the 45 x 45 matrices.
+constexpr int PL_NT = 128;
+
+__device__ __forceinline__ void quad9_geom(const double (*X)[2], const double* dN_ref, double* dNx,
+                                           double* wdet, double w, int* bad, int e) {
+  double J[2][2] = {{0, 0}, {0, 0}};
+  for (int i = 0; i < 9; ++i)
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) J[a][b] += dN_ref[i * 2 + a] * X[i][b];
+  const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  if (!(det > 0.0)) atomicMin(bad, e);
+  const double id = 1.0 / det;
+  const double iJ[2][2] = {{J[1][1] * id, -J[0][1] * id}, {-J[1][0] * id, J[0][0] * id}};
+  for (int i = 0; i < 9; ++i)
+    for (int b = 0; b < 2; ++b) dNx[i * 2 + b] = dN_ref[i * 2] * iJ[0][b] + dN_ref[i * 2 + 1] * iJ[1][b];
+  *wdet = w * det;
 }
 
-__global__ void head_flags_kernel(int64_t T, const uint64_t* __restrict__ keys, int32_t* __restrict__ head) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  head[t] = (t == 0 || keys[t] != keys[t - 1]) ? 1 : 0;
-}
-
-__global__ void emit_pattern_kernel(int64_t T, int n, const uint64_t* __restrict__ keys,
-                                    const int32_t* __restrict__ head, const int32_t* __restrict__ slot,
-                                    int32_t* __restrict__ indices, int64_t* __restrict__ gptr,
-                                    int32_t* __restrict__ row_count) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  if (head[t]) {
-    const int s = slot[t];
-    const uint64_t k = keys[t];
-    indices[s] = (int32_t)(k % (uint64_t)n);
-    gptr[s] = t;
-    atomicAdd(row_count + (int)(k / (uint64_t)n), 1);
+__global__ void __launch_bounds__(PL_NT) rm_plate_kernel(int n_elem, const double* __restrict__ xyz,
+                                                         const int32_t* __restrict__ conn, double E, double nu,
+                                                         double rho, double t, double* __restrict__ Ke,
+                                                         double* __restrict__ Me, int* __restrict__ bad) {
+  __shared__ double X[9][2];
+  __shared__ double dF[9][18], wF[9], NF[9][9];   // full 3x3 rule
+  __shared__ double dR[4][18], wR[4], NR[4][9];   // reduced 2x2 rule
+  const int tid = threadIdx.x;
+  const double cm = E * t / (1.0 - nu * nu), cb = E * t * t * t / (12.0 * (1.0 - nu * nu));
+  const double gs = 5.0 / 6.0 * E / (2.0 * (1.0 + nu)) * t;
+  const double mt = rho * t, mr = rho * t * t * t / 12.0;
+  for (int e = blockIdx.x; e < n_elem; e += gridDim.x) {
+    if (tid < 18) X[tid / 2][tid % 2] = xyz[(size_t)conn[(size_t)e * 9 + tid / 2] * 3 + tid % 2];
+    __syncthreads();
+    if (tid < 9) {
+      quad9_geom(X, &c_qdN[tid * 18], dF[tid], &wF[tid], c_qW[tid], bad, e);
+      for (int i = 0; i < 9; ++i) NF[tid][i] = c_qN[tid * 9 + i];
+    } else if (tid >= 32 && tid < 36) {
+      const int g = tid - 32;
+      quad9_geom(X, &c_rdN[g * 18], dR[g], &wR[g], c_rW[g], bad, e);
+      for (int i = 0; i < 9; ++i) NR[g][i] = c_rN[g * 9 + i];
+    }
+    __syncthreads();
+    for (int q = tid; q < 2025; q += PL_NT) {
+      const int A = q / 45, B = q - A * 45;
+      const int a = A / 5, pa = A - a * 5, b = B / 5, pb = B - b * 5;
+      double k = 0.0, m = 0.0;
+      const bool mem = pa < 2 && pb < 2, ben = pa >= 3 && pb >= 3;
+      if (mem || ben) {
+        // B column of (node, dof): [d/dx, 0, d/dy] for the x-type dof, [0, d/dy, d/dx] for the y-type dof
+        const int ta = mem ? pa : pa - 3, tb = mem ? pb : pb - 3;
+        const double c = mem ? cm : cb;
+        for (int g = 0; g < 9; ++g) {
+          const double ax = dF[g][a * 2], ay = dF[g][a * 2 + 1], bx = dF[g][b * 2], by = dF[g][b * 2 + 1];
+          double v;
+          if (ta == 0 && tb == 0) v = ax * bx + 0.5 * (1.0 - nu) * ay * by;
+          else if (ta == 1 && tb == 1) v = ay * by + 0.5 * (1.0 - nu) * ax * bx;
+          else if (ta == 0) v = nu * ax * by + 0.5 * (1.0 - nu) * ay * bx;
+          else v = nu * ay * bx + 0.5 * (1.0 - nu) * ax * by;
+          k += wF[g] * c * v;
+        }
+      }
+      if (pa >= 2 && pb >= 2) {  // transverse shear, reduced rule
+        for (int g = 0; g < 4; ++g) {
+          double sa0, sa1, sb0, sb1;
+          if (pa == 2) { sa0 = dR[g][a * 2]; sa1 = dR[g][a * 2 + 1]; }
+          else if (pa == 3) { sa0 = NR[g][a]; sa1 = 0.0; }
+          else { sa0 = 0.0; sa1 = NR[g][a]; }
+          if (pb == 2) { sb0 = dR[g][b * 2]; sb1 = dR[g][b * 2 + 1]; }
+          else if (pb == 3) { sb0 = NR[g][b]; sb1 = 0.0; }
+          else { sb0 = 0.0; sb1 = NR[g][b]; }
+          k += wR[g] * gs * (sa0 * sb0 + sa1 * sb1);
+        }
+      }
+      if (pa == pb) {
+        const double mc = pa >= 3 ? mr : mt;
+        for (int g = 0; g < 9; ++g) m += wF[g] * mc * NF[g][a] * NF[g][b];
+      }
+      Ke[(size_t)e * 2025 + q] = k;
+      Me[(size_t)e * 2025 + q] = m;
+    }
+    __syncthreads();
   }
 }
 
-__global__ void finish_gptr_kernel(int64_t T, const int32_t* nnz_dev, int64_t* gptr) {
-  gptr[*nnz_dev] = T;
+int rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, double E, double nu, double rho, double t,
+                      double* Ke, double* Me, int32_t* bad_elem_host, cudaStream_t stream) {
+  if (int rc = init_tables()) return rc;
+  int* bad = nullptr;
+  VB_CUDA(cudaMallocAsync(&bad, sizeof(int), stream));
+  const int big = 0x7fffffff;
+  VB_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, stream));
+  if (n_elem > 0) {
+    const int grid = n_elem < 148 * 16 ? n_elem : 148 * 16;
+    rm_plate_kernel<<<grid, PL_NT, 0, stream>>>(n_elem, xyz, conn, E, nu, rho, t, Ke, Me, bad);
+    VB_LAUNCHED("rm_plate_kernel");
+  }
+  int hb = big;
+  VB_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  VB_CUDA(cudaFreeAsync(bad, stream));
+  VB_CUDA(cudaStreamSynchronize(stream));
+  *bad_elem_host = hb == big ? -1 : hb;
+  return 0;
+}
+
+// ------------------------------------------------------------ pattern ---
+// Triplet t = e*nr*nc + a*nc + b of element e has row rdofs[e][a] and column
+// cdofs[e][b] (assembly.py:166-167: rows = repeat(dofs), cols = tile(dofs));
+// a negative DoF (eliminated, e.g. a clamped plate node) drops the triplet:
+// its key is the all-ones sentinel, which sorts after every real key.
+
+__global__ void make_keys_kernel(int64_t T, int nr, int nc, int ncols, const int32_t* __restrict__ rdofs,
+                                 const int32_t* __restrict__ cdofs, uint64_t KEY_DROP,
+                                 uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int64_t pe = (int64_t)nr * nc;
+  const int64_t e = t / pe;
+  const int a = (int)((t / nc) % nr), b = (int)(t % nc);
+  const int row = rdofs[e * nr + a], col = cdofs[e * nc + b];
+  keys[t] = (row < 0 || col < 0) ? KEY_DROP : (uint64_t)row * (uint64_t)ncols + (uint64_t)col;
+  vals[t] = (int32_t)t;
+}
+
+__global__ void head_flags_kernel(int64_t T, const uint64_t* __restrict__ keys, uint64_t KEY_DROP,
+                                  int32_t* __restrict__ head) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  head[t] = (keys[t] != KEY_DROP && (t == 0 || keys[t] != keys[t - 1])) ? 1 : 0;
+}
+
+__global__ void emit_pattern_kernel(int64_t T, int ncols, const uint64_t* __restrict__ keys, uint64_t KEY_DROP,
+                                    const int32_t* __restrict__ head, const int32_t* __restrict__ slot,
+                                    int32_t* __restrict__ indices, int64_t* __restrict__ gptr,
+                                    int32_t* __restrict__ row_count, int64_t* __restrict__ tvalid) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint64_t k = keys[t];
+  if (k != KEY_DROP && (t == T - 1 || keys[t + 1] == KEY_DROP)) *tvalid = t + 1;  // valid triplet count
+  if (head[t]) {
+    const int s = slot[t];
+    indices[s] = (int32_t)(k % (uint64_t)ncols);
+    gptr[s] = t;
+    atomicAdd(row_count + (int)(k / (uint64_t)ncols), 1);
+  }
+}
+
+__global__ void finish_gptr_kernel(const int32_t* nnz_dev, const int64_t* tvalid, int64_t* gptr) {
+  gptr[*nnz_dev] = *tvalid;
 }
 
 __global__ void nnz_kernel(int64_t T, const int32_t* head, const int32_t* slot, int32_t* nnz) {
@@ -259,7 +399,7 @@ __global__ void csr_gather_kernel(int64_t nnz, const int64_t* __restrict__ gptr,
 
 // ------------------------------------------------------------- host side ---
 struct PatternWs {
-  size_t keys_a, keys_b, vals_a, head, slot, cnt, nnz, cub;
+  size_t keys_a, keys_b, vals_a, head, slot, cnt, nnz, tvalid, cub;
   size_t total;
 };
 
@@ -279,6 +419,7 @@ static int pattern_ws(int64_t T, int n, PatternWs* w) {
   w->slot = off; off += align256(T * 4);
   w->cnt = off; off += align256((size_t)(n + 1) * 4);
   w->nnz = off; off += 256;
+  w->tvalid = off; off += 256;
   w->cub = off; off += align256(cub_sort > cub_scan ? cub_sort : cub_scan);
   w->total = off;
   return 0;
@@ -296,14 +437,15 @@ static int end_bit_for(uint64_t maxkey) {
   return b;
 }
 
-int csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, int32_t* indptr,
-                              int32_t* indices, int64_t* gptr, int32_t* gidx, int64_t* nnz_host,
-                              void* work, size_t work_bytes, cudaStream_t stream) {
-  const int64_t T = (int64_t)n_elem * npe * npe;
-  VB_CHECK_ARG(T > 0 && T < ((int64_t)1 << 31), "vb_csr_pattern_from_elements: triplet count out of range");
+int csr_pattern_from_blocks(int n_rows, int n_cols, int n_elem, int nr, int nc, const int32_t* rdofs,
+                            const int32_t* cdofs, int32_t* indptr, int32_t* indices, int64_t* gptr, int32_t* gidx,
+                            int64_t* nnz_host, void* work, size_t work_bytes, cudaStream_t stream) {
+  const int64_t T = (int64_t)n_elem * nr * nc;
+  VB_CHECK_ARG(T > 0 && T < ((int64_t)1 << 31), "vb_csr_pattern_from_blocks: triplet count out of range");
+  const int nmax = n_rows > n_cols ? n_rows : n_cols;
   PatternWs w;
-  if (int rc = pattern_ws(T, n, &w)) return rc;
-  VB_CHECK_ARG(work && work_bytes >= w.total, "vb_csr_pattern_from_elements: workspace too small");
+  if (int rc = pattern_ws(T, nmax, &w)) return rc;
+  VB_CHECK_ARG(work && work_bytes >= w.total, "vb_csr_pattern_from_blocks: workspace too small");
   char* base = (char*)work;
   uint64_t* ka = (uint64_t*)(base + w.keys_a);
   uint64_t* kb = (uint64_t*)(base + w.keys_b);
@@ -312,33 +454,44 @@ int csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, i
   int32_t* slot = (int32_t*)(base + w.slot);
   int32_t* cnt = (int32_t*)(base + w.cnt);
   int32_t* nnz_dev = (int32_t*)(base + w.nnz);
+  int64_t* tvalid = (int64_t*)(base + w.tvalid);
   void* cubtmp = base + w.cub;
   size_t cubbytes = work_bytes - w.cub;
   const int nt = 256;
   const unsigned nb = (unsigned)((T + nt - 1) / nt);
-  make_keys_kernel<<<nb, nt, 0, stream>>>(T, npe, n, conn, ka, va);
+  // keys need end_bit bits; the drop sentinel (all end_bit bits set) sorts last
+  const int eb = end_bit_for((uint64_t)n_rows * (uint64_t)n_cols) + 1;
+  const uint64_t drop = (eb >= 64) ? ~(uint64_t)0 : (((uint64_t)1 << eb) - 1);
+  make_keys_kernel<<<nb, nt, 0, stream>>>(T, nr, nc, n_cols, rdofs, cdofs, drop, ka, va);
   VB_LAUNCHED("make_keys_kernel");
-  const int eb = end_bit_for((uint64_t)n * (uint64_t)n);
   VB_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, cubbytes, ka, kb, va, gidx, T, 0, eb, stream));
   count_launches(1);
-  head_flags_kernel<<<nb, nt, 0, stream>>>(T, kb, head);
+  head_flags_kernel<<<nb, nt, 0, stream>>>(T, kb, drop, head);
   VB_LAUNCHED("head_flags_kernel");
   VB_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, cubbytes, head, slot, T, stream));
   count_launches(1);
-  VB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 4, stream));
-  emit_pattern_kernel<<<nb, nt, 0, stream>>>(T, n, kb, head, slot, indices, gptr, cnt);
+  VB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)(n_rows + 1) * 4, stream));
+  VB_CUDA(cudaMemsetAsync(tvalid, 0, sizeof(int64_t), stream));
+  emit_pattern_kernel<<<nb, nt, 0, stream>>>(T, n_cols, kb, drop, head, slot, indices, gptr, cnt, tvalid);
   VB_LAUNCHED("emit_pattern_kernel");
-  VB_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, cubbytes, cnt, indptr, n + 1, stream));
+  VB_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, cubbytes, cnt, indptr, n_rows + 1, stream));
   count_launches(1);
   nnz_kernel<<<1, 1, 0, stream>>>(T, head, slot, nnz_dev);
   VB_LAUNCHED("nnz_kernel");
-  finish_gptr_kernel<<<1, 1, 0, stream>>>(T, nnz_dev, gptr);
+  finish_gptr_kernel<<<1, 1, 0, stream>>>(nnz_dev, tvalid, gptr);
   VB_LAUNCHED("finish_gptr_kernel");
   int32_t nnz = 0;
   VB_CUDA(cudaMemcpyAsync(&nnz, nnz_dev, 4, cudaMemcpyDeviceToHost, stream));
   VB_CUDA(cudaStreamSynchronize(stream));
   *nnz_host = nnz;
   return 0;
+}
+
+int csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, int32_t* indptr,
+                              int32_t* indices, int64_t* gptr, int32_t* gidx, int64_t* nnz_host,
+                              void* work, size_t work_bytes, cudaStream_t stream) {
+  return csr_pattern_from_blocks(n, n, n_elem, npe, npe, conn, conn, indptr, indices, gptr, gidx, nnz_host, work,
+                                 work_bytes, stream);
 }
 
 int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv, double* vals,

@@ -82,6 +82,27 @@ int vb_csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn
                                        nnz_host, work, work_bytes, (cudaStream_t)stream);
 }
 
+size_t vb_csr_pattern_blocks_workspace_bytes(int n_rows, int n_cols, int n_elem, int nr, int nc) {
+  return vb::csr_pattern_workspace_bytes(n_rows > n_cols ? n_rows : n_cols, (int64_t)n_elem * nr * nc);
+}
+
+int vb_csr_pattern_from_blocks(int n_rows, int n_cols, int n_elem, int nr, int nc, const int32_t* row_dofs,
+                               const int32_t* col_dofs, int32_t* indptr, int32_t* indices, int64_t* gather_ptr,
+                               int32_t* gather_idx, int64_t* nnz_host, void* work, size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(n_rows > 0 && n_cols > 0 && n_elem > 0 && nr > 0 && nc > 0, "vb_csr_pattern_from_blocks: bad sizes");
+  VB_CHECK_ARG(row_dofs && col_dofs && indptr && indices && gather_ptr && gather_idx && nnz_host,
+               "vb_csr_pattern_from_blocks: null pointer");
+  return vb::csr_pattern_from_blocks(n_rows, n_cols, n_elem, nr, nc, row_dofs, col_dofs, indptr, indices, gather_ptr,
+                                     gather_idx, nnz_host, work, work_bytes, (cudaStream_t)stream);
+}
+
+int vb_rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, double E, double nu, double rho,
+                         double t, double* Ke, double* Me, int32_t* bad_elem_host, void* stream) {
+  VB_CHECK_ARG(n_elem >= 0 && xyz && conn && Ke && Me && bad_elem_host && t > 0,
+               "vb_rm_plate_elements: bad arguments");
+  return vb::rm_plate_elements(n_elem, xyz, conn, E, nu, rho, t, Ke, Me, bad_elem_host, (cudaStream_t)stream);
+}
+
 int vb_csr_gather(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx,
                   const double* triplet_vals, double* vals, void* stream) {
   VB_CHECK_ARG(nnz >= 0, "vb_csr_gather: bad nnz");

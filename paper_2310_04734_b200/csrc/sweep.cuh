@@ -31,6 +31,11 @@ size_t csr_pattern_workspace_bytes(int n, int64_t T);
 int csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, int32_t* indptr,
                               int32_t* indices, int64_t* gptr, int32_t* gidx, int64_t* nnz_host,
                               void* work, size_t work_bytes, cudaStream_t stream);
+int csr_pattern_from_blocks(int n_rows, int n_cols, int n_elem, int nr, int nc, const int32_t* rdofs,
+                            const int32_t* cdofs, int32_t* indptr, int32_t* indices, int64_t* gptr, int32_t* gidx,
+                            int64_t* nnz_host, void* work, size_t work_bytes, cudaStream_t stream);
+int rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, double E, double nu, double rho, double t,
+                      double* Ke, double* Me, int32_t* bad_elem_host, cudaStream_t stream);
 int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv, double* vals,
                cudaStream_t stream);
 int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* Ke, double* Me,

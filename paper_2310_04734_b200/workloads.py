@@ -166,3 +166,68 @@ def cfg3_model(seed: int = 3, box=CFG3_BOX, ne=CFG3_NE, n_src: int = CFG3_NSRC, 
     return fom, {"xyz": xyz, "conn": conn, "src": src, "rec": rec, "walls": Zs, "Kg": Kg, "Mn": Mn,
                  "freqs": np.arange(20.0, 300.0 + 1e-9, 0.25), "points": CFG3_POINTS,
                  "moments": CFG3_MOMENTS}
+
+
+# ---------------------------------------------------------------- cfg2 -----
+CFG2_PLATE = dict(E=60e9, nu=0.3, rho=1550.0, t=0.003)
+CFG2_BOX = (0.0, 0.0, 0.0, 0.8, 0.6, 0.5)
+CFG2_NE = (16, 12, 10)
+CFG2_THETA = math.radians(30.0)
+CFG2_POINTS = (60.0, 140.0, 220.0, 300.0, 380.0, 460.0)  # sextile midpoints of [20, 500]
+CFG2_MOMENTS = 10
+
+
+def cfg2_model(seed: int = 2, box=CFG2_BOX, ne=CFG2_NE, n_rec: int = CFG1_NREC, device=None):
+    """cfg2 (BASELINE configs[1]): clamped 0.8 x 0.6 m, 3 mm CFRP-like plate of
+    16 x 12 9-node Reissner-Mindlin + membrane elements on top of a 0.8 x 0.6 x 0.5 m
+    air cavity of 16 x 12 x 10 hex27 (conforming wet face), eta(f) = 0.01 + 2e-5 f
+    on the plate stiffness, unit plane-wave pressure at 30 deg incidence, 50
+    seeded cavity receivers, 20:0.5:500 Hz, 6 points x 10 moments.
+    DoFs: [plate free (u, v, w, bx, by) | cavity pressure]; n = 3,565 + 17,325."""
+    import torch
+    from . import assembly, plate
+    from .mor import AffineOperator, AffineTerm, FullOrderModel
+    dev = torch.device(device or "cuda")
+    nx, ny, nz = ne
+    x0, y0, z0, x1, y1, z1 = box
+    xyz_f, conn_f = assembly.hex27_box(box, *ne)
+    pxyz, pconn = plate.plate_mesh((x0, y0, x1, y1), nx, ny, z1)
+    dmap, n_p = plate.clamped_dof_map(nx, ny)
+    n_f = xyz_f.shape[0]
+    n = n_p + n_f
+    # cavity primitives in the global numbering (rows/cols offset by the plate DoFs)
+    conn_g = (conn_f + n_p).astype(np.int32)
+    xyz_d = torch.as_tensor(xyz_f, device=dev)
+    Ke, Me = assembly.hex27_helmholtz(xyz_d, torch.as_tensor(conn_f, device=dev))
+    Kg = plate.assemble_blocks(n, n, conn_g, conn_g, Ke, dev)
+    Mn = plate.assemble_blocks(n, n, conn_g, conn_g, Me, dev)
+    # plate
+    P = CFG2_PLATE
+    Kpe, Mpe = plate.plate_elements(torch.as_tensor(pxyz, device=dev), torch.as_tensor(pconn, device=dev),
+                                    P["E"], P["nu"], P["rho"], P["t"])
+    pd = dmap[pconn].reshape(len(pconn), 45)
+    Kp = plate.assemble_blocks(n, n, pd, pd, Kpe, dev)
+    Mp = plate.assemble_blocks(n, n, pd, pd, Mpe, dev)
+    # coupling on the wet face (plate element e <-> cavity top-face element e)
+    fconn = assembly.hex27_box_face(ne, "z1", conn_f)
+    Fe = assembly.face_mass(torch.as_tensor(pxyz, device=dev), torch.as_tensor(pconn, device=dev))
+    wd = dmap[pconn][:, :, 2]
+    Fsf = plate.assemble_blocks(n, n, wd, fconn + n_p, Fe, dev)
+    Ffs = plate.assemble_blocks(n, n, fconn + n_p, wd, Fe.transpose(1, 2).contiguous(), dev)
+    sgn = -1.0  # structure -> fluid normal is -z (cavity below the plate)
+    rng = np.random.default_rng(seed)
+    inner = assembly.interior_nodes(xyz_f, box)
+    rec = np.sort(rng.choice(inner, n_rec, replace=False)).astype(np.int64) + n_p
+    Cmat = np.zeros((n_rec, n))
+    Cmat[np.arange(n_rec), rec] = 1.0
+    load = plate.PlaneWaveLoad(pxyz, pconn, dmap, n, AIR_C, CFG2_THETA, 1.0, dev)
+    aff = AffineOperator(
+        K=[AffineTerm(Kg, 1.0 / AIR_RHO), AffineTerm(Kp, lambda f: 1.0 + 1j * plate.eta_cfg2(f)),
+           AffineTerm(Fsf, -sgn)],
+        M=[AffineTerm(Mn, 1.0 / (AIR_RHO * AIR_C * AIR_C)), AffineTerm(Mp, 1.0), AffineTerm(Ffs, AIR_RHO * sgn)],
+        D=[], load=load)
+    fom = FullOrderModel(c_out=Cmat, n=n, affine=aff)
+    return fom, {"n_plate": n_p, "n_fluid": n_f, "rec": rec, "dmap": dmap, "pxyz": pxyz, "pconn": pconn,
+                 "xyz_f": xyz_f, "conn_f": conn_f, "fconn": fconn, "Kg": Kg, "Mn": Mn, "Kp": Kp, "Mp": Mp,
+                 "Fsf": Fsf, "Ffs": Ffs, "load": load, "freqs": np.arange(20.0, 500.0 + 1e-9, 0.5),
+                 "points": CFG2_POINTS, "moments": CFG2_MOMENTS}
