@@ -66,95 +66,112 @@ struct __align__(64) Params {
   size_t cta_stride;  // workspace elements per CTA
 };
 
-__device__ __forceinline__ void block_argmax(double& v, int& idx, double* rv, int* ri) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  warp_argmax(v, idx);
-  if (lane == 0) { rv[warp] = v; ri[warp] = idx; }
-  __syncthreads();
-  if (warp == 0) {
-    v = lane < NT / 32 ? rv[lane] : -1.0;
-    idx = lane < NT / 32 ? ri[lane] : 0x7fffffff;
-    warp_argmax(v, idx);
-  }
+// izamax candidate carried through the reductions together with its value.
+struct Cand {
+  double v;
+  int i;
+  z_t val;
+};
+
+__device__ __forceinline__ void cand_better(Cand& a, const Cand& b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) a = b;
 }
 
-// Factor the inner panel rows [j0, r) x cols [j0, j0+wc) in shared memory
-// (unblocked zgetf2 order; the argmax for column jj+1 is fused into the
-// rank-1 update of column jj).
+// Block-wide izamax (max |Re|+|Im|, lowest row on ties): warp shuffles, one
+// barrier, then EVERY warp reduces the 8 partials itself (no second barrier).
+__device__ __forceinline__ Cand block_argmax(Cand c, double* rv, int* ri, z_t* rz) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand d;
+    d.v = __shfl_xor_sync(0xffffffffu, c.v, o);
+    d.i = __shfl_xor_sync(0xffffffffu, c.i, o);
+    d.val.x = __shfl_xor_sync(0xffffffffu, c.val.x, o);
+    d.val.y = __shfl_xor_sync(0xffffffffu, c.val.y, o);
+    cand_better(c, d);
+  }
+  if (lane == 0) { rv[warp] = c.v; ri[warp] = c.i; rz[warp] = c.val; }
+  __syncthreads();
+  Cand best{rv[0], ri[0], rz[0]};
+#pragma unroll
+  for (int q = 1; q < NT / 32; ++q) cand_better(best, Cand{rv[q], ri[q], rz[q]});
+  return best;
+}
+
+// Factor the inner panel rows [j0, r) x cols [j0, j0+wc) in shared memory,
+// unblocked zgetf2 order.  Rows are padded to w+1 complex (conflict-free
+// row-per-thread access), each thread owns whole rows, the pivot value travels
+// with the argmax, and the argmax for column jj+1 is fused into the update of
+// column jj: two barriers per column.
 __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* piv,
-                            int* s_info, double* rv, int* ri, int* s_p, z_t* s_pv) {
-  const int r = P.r, ldw = P.ldw, w = P.w;
+                            int* s_info, double* rv, int* ri, z_t* rz) {
+  const int r = P.r, ldw = P.ldw, lp = P.w + 1;
   const int H = r - j0;
   const int tid = threadIdx.x;
   for (int e = tid; e < H * wc; e += NT) {
     const int i = e / wc, c = e - i * wc;
-    Ps[i * w + c] = A[(size_t)(j0 + i) * ldw + j0 + c];
+    Ps[i * lp + c] = A[(size_t)(j0 + i) * ldw + j0 + c];
   }
   __syncthreads();
-  double v = -1.0;
-  int pi = 0x7fffffff;
+  Cand cd{-1.0, 0x7fffffff, zmake(0.0, 0.0)};
   for (int i = tid; i < H; i += NT) {
-    const double a = zabs1(Ps[i * w]);
-    if (a > v) { v = a; pi = i; }
+    const z_t x = Ps[i * lp];
+    const double a = zabs1(x);
+    if (a > cd.v) cd = Cand{a, i, x};
   }
-  block_argmax(v, pi, rv, ri);
+  Cand best = block_argmax(cd, rv, ri, rz);
   for (int jj = 0; jj < wc; ++jj) {
+    const bool zero = !(best.v > 0.0);
+    const int p = zero ? jj : best.i;
     if (tid == 0) {
-      if (v == 0.0) {
-        if (*s_info == 0) *s_info = j0 + jj + 1;
-        *s_p = -1;
-      } else {
-        *s_p = pi;
-        *s_pv = Ps[pi * w + jj];
-      }
-      piv[j0 - k0 + jj] = j0 + (v == 0.0 ? jj : pi);
+      if (zero && *s_info == 0) *s_info = j0 + jj + 1;  // LAPACK INFO: no interchange, no scaling
+      piv[j0 - k0 + jj] = j0 + p;
     }
-    __syncthreads();
-    const int p = *s_p;
     const int nc = wc - jj - 1;
-    v = -1.0;
-    pi = 0x7fffffff;
-    if (p >= 0) {
-      const z_t pv = *s_pv;
+    cd = Cand{-1.0, 0x7fffffff, zmake(0.0, 0.0)};
+    if (!zero) {
+      const z_t pv = best.val;
       const z_t pinv = zrecip(pv);
+      // phase A: multipliers (column jj read through the interchange) and the
+      // row interchange jj <-> p on the other columns
       for (int i = jj + 1 + tid; i < H; i += NT) {
         const int src = (i == p) ? jj : i;
-        Ps[i * w + jj] = zmul(Ps[src * w + jj], pinv);
+        Ps[i * lp + jj] = zmul(Ps[src * lp + jj], pinv);
       }
-      if (p != jj) {
-        for (int c = tid; c < wc; c += NT) {
-          if (c == jj) continue;
-          const z_t t = Ps[jj * w + c];
-          Ps[jj * w + c] = Ps[p * w + c];
-          Ps[p * w + c] = t;
-        }
-      }
+      if (p != jj)
+        for (int c = tid; c < wc; c += NT)
+          if (c != jj) {
+            const z_t t = Ps[jj * lp + c];
+            Ps[jj * lp + c] = Ps[p * lp + c];
+            Ps[p * lp + c] = t;
+          }
       __syncthreads();
-      if (tid == 0) Ps[jj * w + jj] = pv;
-      if (nc > 0) {
-        for (int e = tid; e < (H - jj - 1) * nc; e += NT) {
-          const int ii = e / nc, cc = e - ii * nc;
-          const int i = jj + 1 + ii, c = jj + 1 + cc;
-          const z_t nv = zfms(Ps[i * w + c], Ps[i * w + jj], Ps[jj * w + c]);
-          Ps[i * w + c] = nv;
-          if (cc == 0) {
+      if (tid == 0) Ps[jj * lp + jj] = pv;
+      // phase B: rank-1 update of the remaining columns, argmax of column jj+1
+      for (int i = jj + 1 + tid; i < H; i += NT) {
+        const z_t l = Ps[i * lp + jj];
+        for (int c = jj + 1; c < wc; ++c) {
+          const z_t nv = zfms(Ps[i * lp + c], l, Ps[jj * lp + c]);
+          Ps[i * lp + c] = nv;
+          if (c == jj + 1) {
             const double a = zabs1(nv);
-            if (a > v || (a == v && i < pi)) { v = a; pi = i; }
+            if (a > cd.v) cd = Cand{a, i, nv};
           }
         }
       }
     } else if (nc > 0) {
       for (int i = jj + 1 + tid; i < H; i += NT) {
-        const double a = zabs1(Ps[i * w + jj + 1]);
-        if (a > v) { v = a; pi = i; }
+        const z_t x = Ps[i * lp + jj + 1];
+        const double a = zabs1(x);
+        if (a > cd.v) cd = Cand{a, i, x};
       }
     }
-    if (nc > 0) block_argmax(v, pi, rv, ri);
+    if (nc > 0) best = block_argmax(cd, rv, ri, rz);
   }
   __syncthreads();
   for (int e = tid; e < H * wc; e += NT) {
     const int i = e / wc, c = e - i * wc;
-    A[(size_t)(j0 + i) * ldw + j0 + c] = Ps[i * w + c];
+    A[(size_t)(j0 + i) * ldw + j0 + c] = Ps[i * lp + c];
   }
   __syncthreads();
 }
@@ -339,8 +356,8 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
   __shared__ int piv[NB];
   __shared__ double rv[NT / 32];
   __shared__ int ri[NT / 32];
-  __shared__ int s_info, s_p;
-  __shared__ z_t s_pv;
+  __shared__ int s_info;
+  __shared__ z_t rz[NT / 32];
   __shared__ z_t alph[64];
   const int r = P.r, s = P.s, ldw = P.ldw, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -379,7 +396,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
       for (int l = 0; l < nleaves; ++l) {
         const int j0 = k0 + l * P.w;
         const int wc = min(P.w, k0 + nb - j0);
-        inner_panel(P, A, k0, j0, wc, smem, piv, &s_info, rv, ri, &s_p, &s_pv);
+        inner_panel(P, A, k0, j0, wc, smem, piv, &s_info, rv, ri, rz);
         apply_swaps(A, ldw, piv, k0, j0, j0 + wc, k0, j0);
         apply_swaps(A, ldw, piv, k0, j0, j0 + wc, j0 + wc, k0 + nb);
         __syncthreads();
@@ -453,7 +470,7 @@ static size_t smem_bytes(int r, int w) {
   m = m > GemmOut::SMEM ? m : GemmOut::SMEM;
   m = m > TRSM_SMEM ? m : TRSM_SMEM;
   m = m > BACK_SMEM ? m : BACK_SMEM;
-  const size_t ps = (size_t)r * w * sizeof(z_t);
+  const size_t ps = (size_t)r * (w + 1) * sizeof(z_t);  // padded panel rows
   return (m > ps ? m : ps) + 1024;  // + alignment slack for the 1024-B aligned base
 }
 
