@@ -231,6 +231,13 @@ int vb_scale_columns(int n, int m, vb_complex* W, int64_t ldw, const double* sca
  * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */
 int vb_probe_fp64_peak(double* tflops_host, void* stream);
 
+/* Profiling aid: per-phase SM-cycle totals of the blocked sweep kernel (16
+ * counters; non-zero only in a library built with -DVB_PHASE_TIMING).  Phases:
+ * form, leaf panel, in-panel TRSM+GEMM, interchanges, U12 TRSM, trailing GEMM,
+ * back substitution, outputs; then sub-phases leaf load, leaf factor, leaf
+ * interchanges, leaf TRSM. */
+int vb_debug_phase_cycles(unsigned long long* cycles_host, int reset);
+
 /* Number of this library's kernel launches since load (process-wide counter,
  * incremented on every successful launch). */
 int64_t vb_launch_count(void);

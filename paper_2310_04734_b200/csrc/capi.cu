@@ -200,4 +200,9 @@ int vb_hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1,
   return vb::hex27_box_csr(nx, ny, nz, K1, M1, maxnp, indptr, indices, Kvals, Mvals, (cudaStream_t)stream);
 }
 
+int vb_debug_phase_cycles(unsigned long long* cycles_host, int reset) {
+  VB_CHECK_ARG(cycles_host != nullptr, "vb_debug_phase_cycles: null output");
+  return vb::sweep_debug_phase_cycles(cycles_host, reset);
+}
+
 }  // extern "C"

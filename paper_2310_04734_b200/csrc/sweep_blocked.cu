@@ -47,6 +47,41 @@ constexpr size_t BACK_SMEM = (size_t)(NB * LDL + NB * LDY) * sizeof(z_t);
 
 using GemmT = tma::GemmTma<3>;
 
+// Optional per-phase cycle accounting (build with -DVB_PHASE_TIMING; read with
+// vb_debug_phase_cycles): thread 0 of every CTA adds the clock64() span of
+// each phase.  0 form, 1 leaf panel, 2 in-panel TRSM+GEMM, 3 swaps,
+// 4 U12 TRSM, 5 trailing GEMM, 6 back substitution, 7 outputs.
+__device__ unsigned long long g_phase_cycles[16];
+#ifdef VB_PHASE_TIMING
+#define PH_BEGIN long long _ph_t = clock64()
+#define PH_MARK(k)                                                                     \
+  do {                                                                                 \
+    if (threadIdx.x == 0) {                                                            \
+      const long long _n = clock64();                                                  \
+      atomicAdd(&g_phase_cycles[k], (unsigned long long)(_n - _ph_t));                 \
+      _ph_t = _n;                                                                      \
+    }                                                                                  \
+  } while (0)
+#define PH_SUB(k)                                                                      \
+  do {                                                                                 \
+    if (threadIdx.x == 0) {                                                            \
+      const long long _n = clock64();                                                  \
+      atomicAdd(&g_phase_cycles[k], (unsigned long long)(_n - _sub_t));                \
+      _sub_t = _n;                                                                     \
+    }                                                                                  \
+  } while (0)
+#define PH_SUB_BEGIN long long _sub_t = clock64()
+#else
+#define PH_BEGIN
+#define PH_SUB(k) \
+  do {            \
+  } while (0)
+#define PH_SUB_BEGIN
+#define PH_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 struct __align__(64) Params {
   tma::Maps maps;  // TMA descriptors over all CTAs' workspaces (must stay first: 64-B aligned)
   int r, nprim, s, n_out;
@@ -66,31 +101,35 @@ struct __align__(64) Params {
   size_t cta_stride;  // workspace elements per CTA
 };
 
-// izamax candidate carried through the reductions together with its value.
+// izamax candidate carried through the reductions together with its value:
+// key = (logical row << 16) | physical row, so that ties resolve to the lowest
+// LOGICAL row (izamax order) while the physical slot locates the row.
 struct Cand {
   double v;
-  int i;
+  int key;
   z_t val;
 };
 
 __device__ __forceinline__ void cand_better(Cand& a, const Cand& b) {
-  if (b.v > a.v || (b.v == a.v && b.i < a.i)) a = b;
+  if (b.v > a.v || (b.v == a.v && b.key < a.key)) a = b;
 }
 
-// Block-wide izamax (max |Re|+|Im|, lowest row on ties): warp shuffles, one
-// barrier, then EVERY warp reduces the 8 partials itself (no second barrier).
+// Block-wide izamax (max |Re|+|Im|, lowest logical row on ties): warp
+// shuffles, ONE barrier, then every warp reduces the 8 partials itself.  The
+// partial slots are double-buffered by the caller (column parity), so the next
+// column may overwrite the other buffer without a second barrier.
 __device__ __forceinline__ Cand block_argmax(Cand c, double* rv, int* ri, z_t* rz) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     Cand d;
     d.v = __shfl_xor_sync(0xffffffffu, c.v, o);
-    d.i = __shfl_xor_sync(0xffffffffu, c.i, o);
+    d.key = __shfl_xor_sync(0xffffffffu, c.key, o);
     d.val.x = __shfl_xor_sync(0xffffffffu, c.val.x, o);
     d.val.y = __shfl_xor_sync(0xffffffffu, c.val.y, o);
     cand_better(c, d);
   }
-  if (lane == 0) { rv[warp] = c.v; ri[warp] = c.i; rz[warp] = c.val; }
+  if (lane == 0) { rv[warp] = c.v; ri[warp] = c.key; rz[warp] = c.val; }
   __syncthreads();
   Cand best{rv[0], ri[0], rz[0]};
 #pragma unroll
@@ -98,31 +137,52 @@ __device__ __forceinline__ Cand block_argmax(Cand c, double* rv, int* ri, z_t* r
   return best;
 }
 
-// Factor the inner panel rows [j0, r) x cols [j0, j0+wc) in shared memory,
-// unblocked zgetf2 order.  Rows are padded to w+1 complex (conflict-free
-// row-per-thread access), each thread owns whole rows, the pivot value travels
-// with the argmax, and the argmax for column jj+1 is fused into the update of
-// column jj: two barriers per column.
-__device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* piv,
+// 1/a with one division: a is scaled by a power of two (exact) so that
+// |a|^2 neither overflows nor underflows.
+__device__ __forceinline__ z_t zrecip_fast(z_t a) {
+  const double m = fmax(fabs(a.x), fabs(a.y));
+  int e;
+  frexp(m, &e);
+  const double sc = ldexp(1.0, -e);
+  const double xr = a.x * sc, xi = a.y * sc;
+  const double inv = sc / (xr * xr + xi * xi);
+  return zmake(xr * inv, -xi * inv);
+}
+
+// Factor the inner panel rows [j0, r) x cols [j0, j0+wc) in shared memory
+// (zgetf2 order, LAPACK pivots).  Rows never move inside shared memory: each
+// physical row carries its LOGICAL position (lg[], touched only by the thread
+// owning the row), an interchange just exchanges two logical positions, and
+// the pivot row — read by every thread during the rank-1 update — is never
+// written in the same phase.  The update of column jj fuses the argmax of
+// column jj+1, so each column costs ONE block barrier.  Rows are written back
+// to global memory in logical order.
+__device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* lg, int* piv,
                             int* s_info, double* rv, int* ri, z_t* rz) {
   const int r = P.r, ldw = P.ldw, lp = P.w + 1;
   const int H = r - j0;
   const int tid = threadIdx.x;
+  PH_SUB_BEGIN;
   for (int e = tid; e < H * wc; e += NT) {
     const int i = e / wc, c = e - i * wc;
-    Ps[i * lp + c] = A[(size_t)(j0 + i) * ldw + j0 + c];
+    cp_async16(Ps + i * lp + c, A + (size_t)(j0 + i) * ldw + j0 + c, true);
   }
+  cp_commit();
+  for (int q = tid; q < H; q += NT) lg[q] = q;
+  cp_wait<0>();
   __syncthreads();
+  PH_SUB(8);
   Cand cd{-1.0, 0x7fffffff, zmake(0.0, 0.0)};
-  for (int i = tid; i < H; i += NT) {
-    const z_t x = Ps[i * lp];
+  for (int q = tid; q < H; q += NT) {
+    const z_t x = Ps[q * lp];
     const double a = zabs1(x);
-    if (a > cd.v) cd = Cand{a, i, x};
+    if (a > cd.v) cd = Cand{a, (q << 16) | q, x};
   }
   Cand best = block_argmax(cd, rv, ri, rz);
   for (int jj = 0; jj < wc; ++jj) {
     const bool zero = !(best.v > 0.0);
-    const int p = zero ? jj : best.i;
+    const int p = zero ? jj : (best.key >> 16);
+    const int b = best.key & 0xffff;
     if (tid == 0) {
       if (zero && *s_info == 0) *s_info = j0 + jj + 1;  // LAPACK INFO: no interchange, no scaling
       piv[j0 - k0 + jj] = j0 + p;
@@ -130,48 +190,44 @@ __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t
     const int nc = wc - jj - 1;
     cd = Cand{-1.0, 0x7fffffff, zmake(0.0, 0.0)};
     if (!zero) {
-      const z_t pv = best.val;
-      const z_t pinv = zrecip(pv);
-      // phase A: multipliers (column jj read through the interchange) and the
-      // row interchange jj <-> p on the other columns
-      for (int i = jj + 1 + tid; i < H; i += NT) {
-        const int src = (i == p) ? jj : i;
-        Ps[i * lp + jj] = zmul(Ps[src * lp + jj], pinv);
-      }
-      if (p != jj)
-        for (int c = tid; c < wc; c += NT)
-          if (c != jj) {
-            const z_t t = Ps[jj * lp + c];
-            Ps[jj * lp + c] = Ps[p * lp + c];
-            Ps[p * lp + c] = t;
-          }
-      __syncthreads();
-      if (tid == 0) Ps[jj * lp + jj] = pv;
-      // phase B: rank-1 update of the remaining columns, argmax of column jj+1
-      for (int i = jj + 1 + tid; i < H; i += NT) {
-        const z_t l = Ps[i * lp + jj];
+      const z_t pinv = zrecip_fast(best.val);
+      const z_t* prow = Ps + b * lp;
+      for (int q = tid; q < H; q += NT) {
+        int l = lg[q];
+        if (l < jj) continue;                       // finished (U) row
+        if (q == b) { lg[q] = jj; continue; }       // pivot row moves to logical jj
+        if (l == jj) { l = p; lg[q] = p; }          // displaced row takes the pivot's slot
+        z_t* row = Ps + q * lp;
+        const z_t m = zmul(row[jj], pinv);
+        row[jj] = m;
         for (int c = jj + 1; c < wc; ++c) {
-          const z_t nv = zfms(Ps[i * lp + c], l, Ps[jj * lp + c]);
-          Ps[i * lp + c] = nv;
+          const z_t nv = zfms(row[c], m, prow[c]);
+          row[c] = nv;
           if (c == jj + 1) {
             const double a = zabs1(nv);
-            if (a > cd.v) cd = Cand{a, i, nv};
+            if (a > cd.v || (a == cd.v && ((l << 16) | q) < cd.key)) cd = Cand{a, (l << 16) | q, nv};
           }
         }
       }
     } else if (nc > 0) {
-      for (int i = jj + 1 + tid; i < H; i += NT) {
-        const z_t x = Ps[i * lp + jj + 1];
+      for (int q = tid; q < H; q += NT) {
+        const int l = lg[q];
+        if (l <= jj) continue;
+        const z_t x = Ps[q * lp + jj + 1];
         const double a = zabs1(x);
-        if (a > cd.v) cd = Cand{a, i, x};
+        if (a > cd.v || (a == cd.v && ((l << 16) | q) < cd.key)) cd = Cand{a, (l << 16) | q, x};
       }
     }
-    if (nc > 0) best = block_argmax(cd, rv, ri, rz);
+    PH_SUB(12);
+    const int buf = (jj + 1) & 1;
+    if (nc > 0) best = block_argmax(cd, rv + buf * (NT / 32), ri + buf * (NT / 32), rz + buf * (NT / 32));
+    PH_SUB(14);
   }
   __syncthreads();
+  PH_SUB(9);
   for (int e = tid; e < H * wc; e += NT) {
-    const int i = e / wc, c = e - i * wc;
-    A[(size_t)(j0 + i) * ldw + j0 + c] = Ps[i * lp + c];
+    const int q = e / wc, c = e - q * wc;
+    A[(size_t)(j0 + lg[q]) * ldw + j0 + c] = Ps[q * lp + c];
   }
   __syncthreads();
 }
@@ -192,28 +248,42 @@ __device__ void apply_swaps(z_t* A, int ldw, const int* piv, int k0, int a, int 
 }
 
 // U = L^-1 U for rows [cl, cl+n1) (unit lower L = A[cl:cl+n1, cl:cl+n1], n1 <= 32)
-// on columns [c0, c1): L staged in shared memory; for long chains (n1 >= 16) one
-// WARP per column with the column's rows on the lanes (forward substitution by
-// shuffles), else one thread per column.
+// on columns [c0, c1) (c1 - c0 <= 32).  Short chains (n1 < 16): L and the
+// block are staged in shared memory with one round of independent loads and
+// solved one thread per column; long chains: one WARP per column with the
+// column's rows on the lanes (forward substitution by shuffles).
 __device__ void trsm_small(z_t* A, int ldw, int cl, int n1, int c0, int c1, z_t* smem) {
   constexpr int LD = 33;
   z_t* Ls = smem;
+  z_t* Xs = smem + 32 * LD;
+  const int nc = c1 - c0;
+  if (n1 < 16) {
+    for (int e = threadIdx.x; e < n1 * n1 + n1 * nc; e += NT) {
+      if (e < n1 * n1) {
+        const int i = e / n1, k = e - i * n1;
+        Ls[i * LD + k] = A[(size_t)(cl + i) * ldw + cl + k];
+      } else {
+        const int f = e - n1 * n1, i = f / nc, c = f - i * nc;
+        Xs[i * LD + c] = A[(size_t)(cl + i) * ldw + c0 + c];
+      }
+    }
+    __syncthreads();
+    const int c = threadIdx.x;
+    if (c < nc) {
+      for (int i = 1; i < n1; ++i) {
+        z_t x = Xs[i * LD + c];
+        for (int k = 0; k < i; ++k) x = zfms(x, Ls[i * LD + k], Xs[k * LD + c]);
+        Xs[i * LD + c] = x;
+        A[(size_t)(cl + i) * ldw + c0 + c] = x;
+      }
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < n1 * n1; e += NT) {
     const int i = e / n1, k = e - i * n1;
     Ls[i * LD + k] = A[(size_t)(cl + i) * ldw + cl + k];
   }
   __syncthreads();
-  if (n1 < 16) {  // short chains: one thread per column (coalesced across the warp)
-    for (int c = c0 + threadIdx.x; c < c1; c += NT) {
-      z_t* col = A + (size_t)cl * ldw + c;
-      for (int i = 1; i < n1; ++i) {
-        z_t acc = col[(size_t)i * ldw];
-        for (int k = 0; k < i; ++k) acc = zfms(acc, Ls[i * LD + k], col[(size_t)k * ldw]);
-        col[(size_t)i * ldw] = acc;
-      }
-    }
-    return;
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int c = c0 + warp; c < c1; c += NT / 32) {
     z_t x = zmake(0.0, 0.0);
@@ -354,10 +424,10 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
   double2* smem = (double2*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ GemmT::Bars bars;
   __shared__ int piv[NB];
-  __shared__ double rv[NT / 32];
-  __shared__ int ri[NT / 32];
+  __shared__ double rv[2 * (NT / 32)];
+  __shared__ int ri[2 * (NT / 32)];
   __shared__ int s_info;
-  __shared__ z_t rz[NT / 32];
+  __shared__ z_t rz[2 * (NT / 32)];
   __shared__ z_t alph[64];
   const int r = P.r, s = P.s, ldw = P.ldw, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -369,6 +439,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
     if (tid == 0) s_info = 0;
     __syncthreads();
     // ---- form [A | B] ----
+    PH_BEGIN;
     form_matrix(P, A, alph);
     const z_t* bf = P.b + f * P.b_stride_f;
     for (int idx = tid; idx < r * s; idx += NT) {
@@ -384,6 +455,8 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
     }
     __syncthreads();
 
+    __syncthreads();
+    PH_MARK(0);
     // ---- blocked right-looking LU on [A | B] ----
     for (int k0 = 0; k0 < r; k0 += NB) {
       const int nb = min(NB, r - k0);
@@ -396,10 +469,14 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
       for (int l = 0; l < nleaves; ++l) {
         const int j0 = k0 + l * P.w;
         const int wc = min(P.w, k0 + nb - j0);
-        inner_panel(P, A, k0, j0, wc, smem, piv, &s_info, rv, ri, rz);
+        inner_panel(P, A, k0, j0, wc, smem, (int*)(smem + (size_t)(r - j0) * (P.w + 1)), piv, &s_info, rv, ri,
+                    rz);
+        PH_MARK(1);
+        PH_SUB_BEGIN;
         apply_swaps(A, ldw, piv, k0, j0, j0 + wc, k0, j0);
         apply_swaps(A, ldw, piv, k0, j0, j0 + wc, j0 + wc, k0 + nb);
         __syncthreads();
+        PH_SUB(10);
         if (l + 1 < nleaves) {
           const int kk = __ffs(~l) - 1;           // trailing ones of l
           const int n1 = (1 << kk) * P.w;         // left subtree width
@@ -407,18 +484,23 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
           const int rc0 = j0 + wc, rc1 = min(rc0 + n1, k0 + nb);
           trsm_small(A, ldw, cl, n1, rc0, rc1, smem);
           __syncthreads();
+          PH_SUB(11);
           GemmT::run(&P.maps, A, ldw, rc0, cl, cl, rc0, r - rc0, rc1 - rc0, n1, (char*)smem, &bars,
                      blockIdx.x);
           __syncthreads();
+          PH_MARK(2);
         }
       }
       const int c0 = k0 + nb, c1 = r + s;
       apply_swaps(A, ldw, piv, k0, k0, k0 + nb, c0, c1);
       __syncthreads();
+      PH_MARK(3);
       panel_trsm(A, ldw, k0, nb, c0, c1, smem);
+      PH_MARK(4);
       if (c0 < r) {
         GemmT::run(&P.maps, A, ldw, c0, k0, k0, c0, r - c0, c1 - c0, nb, (char*)smem, &bars, blockIdx.x);
         __syncthreads();
+        PH_MARK(5);
       }
     }
 
@@ -433,6 +515,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
       }
     }
 
+    PH_MARK(6);
     // ---- outputs: x, y = C_R x (DMMA GEMM), SPL ----
     if (P.x) {
       z_t* xf = P.x + f * (int64_t)r * s;
@@ -458,6 +541,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
       }
     }
     if (tid == 0 && P.info) P.info[f] = s_info;
+    PH_MARK(7);
     __syncthreads();
   }
 }
@@ -465,12 +549,12 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
 static int ldw_of(int r, int s) { return (r + s + 3) & ~3; }
 
 static size_t smem_bytes(int r, int w) {
-  size_t m = GemmT::SMEM;
+  size_t m = GemmT::SMEM > GemmT::SMEM_SKINNY ? GemmT::SMEM : GemmT::SMEM_SKINNY;
   m = m > GemmNarrow::SMEM ? m : GemmNarrow::SMEM;
   m = m > GemmOut::SMEM ? m : GemmOut::SMEM;
   m = m > TRSM_SMEM ? m : TRSM_SMEM;
   m = m > BACK_SMEM ? m : BACK_SMEM;
-  const size_t ps = (size_t)r * (w + 1) * sizeof(z_t);  // padded panel rows
+  const size_t ps = (size_t)r * (w + 1) * sizeof(z_t) + (size_t)r * sizeof(int);  // padded rows + logical ids
   return (m > ps ? m : ps) + 1024;  // + alignment slack for the 1024-B aligned base
 }
 
@@ -521,6 +605,15 @@ static int encode_map(CUtensorMap* map, void* base, const cuuint64_t* dims, cons
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return 2;
+  }
+  return 0;
+}
+
+int sweep_debug_phase_cycles(unsigned long long* out_host, int reset) {
+  VB_CUDA(cudaMemcpyFromSymbol(out_host, blk::g_phase_cycles, sizeof(unsigned long long) * 16));
+  if (reset) {
+    unsigned long long z[16] = {};
+    VB_CUDA(cudaMemcpyToSymbol(blk::g_phase_cycles, z, sizeof(z)));
   }
   return 0;
 }

@@ -106,11 +106,113 @@ struct GemmTma {
     for (int b = 0; b < 4; ++b) tma_load_3d(Cs + b * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0, cta, bar);
   }
 
+  // Skinny updates (K <= KC, N <= 16: the in-panel updates of the recursive
+  // panel) are latency-bound on the C tile, so each ring stage carries a whole
+  // tile — A (64 x 16), B (16 x 16) AND C (64 x 16) — and STAGES-1 tiles are in
+  // flight while one computes.  8 warps x (8 rows x 16 columns).
+  static constexpr unsigned SK_B = 2 * 2048, SK_C = 2 * 8192;
+  static constexpr unsigned SK_STAGE = A_BYTES + SK_B + SK_C;
+  static constexpr size_t SMEM_SKINNY = (size_t)STAGES * SK_STAGE;
+
+  __device__ static __forceinline__ void issue_tile(const Maps* mp, char* st, uint64_t* bar, int cta, int ar0,
+                                                    int ac0, int br0, int bc0, int m0) {
+    mbar_expect_tx(bar, SK_STAGE);
+    tma_load_3d(st, &mp->a64, 2 * ac0, ar0 + m0, cta, bar);
+    tma_load_3d(st + 8192, &mp->a64, 2 * (ac0 + 8), ar0 + m0, cta, bar);
+    tma_load_3d(st + A_BYTES, &mp->b16, 2 * bc0, br0, cta, bar);
+    tma_load_3d(st + A_BYTES + 2048, &mp->b16, 2 * (bc0 + 8), br0, cta, bar);
+    tma_load_3d(st + A_BYTES + SK_B, &mp->a64, 2 * bc0, ar0 + m0, cta, bar);
+    tma_load_3d(st + A_BYTES + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), ar0 + m0, cta, bar);
+  }
+
+  __device__ static void run_skinny(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int M,
+                                    int N, int K, char* smem, Bars* bars, int cta) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ntiles = (M + TM - 1) / TM;
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&bars->full[s], 1);
+        mbar_init(&bars->empty[s], NT / 32);
+      }
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async_global();
+      for (int j = 0; j < STAGES - 1 && j < ntiles; ++j)
+        issue_tile(mp, smem + j * SK_STAGE, &bars->full[j], cta, ar0, ac0, br0, bc0, j * TM);
+    }
+    unsigned full_ph = 0, empty_ph = 0;
+    const int ak = lane & 3, prow = perm8(lane >> 2);
+    const int row = warp * 8 + prow;
+    const int k4n = (K + 3) >> 2;
+    for (int t = 0; t < ntiles; ++t) {
+      const int st = t % STAGES;
+      mbar_wait(&bars->full[st], (full_ph >> st) & 1);
+      full_ph ^= 1u << st;
+      const char* as = smem + st * SK_STAGE;
+      const char* bs = as + A_BYTES;
+      const char* cs = bs + SK_B;
+      double cr[2][2], ci[2][2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+      for (int kk = 0; kk < k4n; ++kk) {
+        const int kcol = kk * 4 + ak;
+        const bool kin = kcol < K;
+        z_t a = *(const z_t*)(as + (kcol >> 3) * 8192 + swz(row, kcol & 7));
+        if (!kin) a = zmake(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          z_t b = *(const z_t*)(bs + j * 2048 + swz(kcol, prow));
+          if (!kin) b = zmake(0.0, 0.0);
+          blk::dmma(cr[j][0], cr[j][1], a.x, b.x);
+          blk::dmma(cr[j][0], cr[j][1], a.y, -b.y);
+          blk::dmma(ci[j][0], ci[j][1], a.x, b.y);
+          blk::dmma(ci[j][0], ci[j][1], a.y, b.x);
+        }
+      }
+      const int m0 = t * TM;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int col = j * 8 + perm8(2 * ak + v);
+          if (m0 + row < M && col < N) {
+            const z_t c = *(const z_t*)(cs + j * 8192 + swz(row, col & 7));
+            Cg[(size_t)(ar0 + m0 + row) * ldw + bc0 + col] = zmake(c.x - cr[j][v], c.y - ci[j][v]);
+          }
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->empty[st]);
+      if (tid == 0 && t + STAGES - 1 < ntiles) {
+        const int s2 = (t + STAGES - 1) % STAGES;
+        if (t >= 1) {
+          mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
+          empty_ph ^= 1u << s2;
+        }
+        issue_tile(mp, smem + s2 * SK_STAGE, &bars->full[s2], cta, ar0, ac0, br0, bc0, (t + STAGES - 1) * TM);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_inval(&bars->full[s]);
+        mbar_inval(&bars->empty[s]);
+      }
+    }
+  }
+
   // ar0/ac0: A origin; br0/bc0: B origin; cr0/cc0: C origin (= (ar0, bc0)); ldw
   // for the generic-store epilogue.  smem must be 1024-byte aligned.
   __device__ static void run(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int M, int N,
                              int K, char* smem, Bars* bars, int cta) {
     if (M <= 0 || N <= 0 || K <= 0) return;
+    if (K <= KC && N <= 16) {
+      run_skinny(mp, Cg, ldw, ar0, ac0, br0, bc0, M, N, K, smem, bars, cta);
+      return;
+    }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
     const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
