@@ -39,10 +39,8 @@ using GemmNarrow = Gemm<64, 16, 8, 1, 2, EPI_SUB>; // back-substitution updates 
 using GemmOut = Gemm<64, 16, 8, 1, 2, EPI_SET>;   // y = C_R x
 
 constexpr int LDL = NB + 4;     // == 4 (mod 8): triangular inverse used as A operand
-constexpr int TRS_N = 32;       // U12 strip width
-constexpr int LDS_B = TRS_N + 2;
 constexpr int LDY = 16 + 2;
-constexpr size_t TRSM_SMEM = (size_t)(NB * LDL + NB * LDS_B) * sizeof(z_t);
+constexpr size_t TRSM_SMEM = (size_t)(NB * LDL) * sizeof(z_t);
 constexpr size_t BACK_SMEM = (size_t)(NB * LDL + NB * LDY) * sizeof(z_t);
 
 using GemmT = tma::GemmTma<3>;
@@ -296,12 +294,17 @@ __device__ void trsm_small(z_t* A, int ldw, int cl, int n1, int c0, int c1, z_t*
   }
 }
 
-// U12 = L11^-1 A12 in place for columns [c0, c1), L11^-1 formed explicitly
-// (identity-padded to 64) and applied with DMMA in 64 x 32 strips.
-__device__ void panel_trsm(z_t* A, int ldw, int k0, int nb, int c0, int c1, z_t* smem) {
-  z_t* Li = smem;             // NB x LDL
-  z_t* Bs = smem + NB * LDL;  // NB x LDS_B
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// U12 = L11^-1 A12 in place for columns [c0, c1): L11^-1 is formed explicitly
+// (identity-padded to 64) and its strictly lower part, negated, is written to
+// the CTA's scratch rows [r, r+64) so that the product runs through the TMA
+// GEMM as an update: U12 = A12 - N A12 with N = I - L11^-1 = -offdiag(L11^-1)
+// (the unit diagonal of L11^-1 is exact, so this equals L11^-1 A12).  Each C
+// tile is fully consumed as the B operand before its epilogue writes it.
+__device__ void panel_trsm(const Params& P, z_t* A, int k0, int nb, int c0, int c1, z_t* smem, GemmT::Bars* bars) {
+  const int ldw = P.ldw, r = P.r;
+  z_t* Li = smem;  // NB x LDL
+  z_t* Nsc = A + (size_t)r * ldw;
+  const int tid = threadIdx.x;
   for (int e = tid; e < NB * NB; e += NT) {
     const int i = e / NB, j = e - i * NB;
     z_t v = zmake(i == j ? 1.0 : 0.0, 0.0);
@@ -310,34 +313,14 @@ __device__ void panel_trsm(z_t* A, int ldw, int k0, int nb, int c0, int c1, z_t*
   }
   __syncthreads();
   tri_inv64<true>(Li, LDL);
-  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps over the 64 x 32 strip
-  const int k4 = (nb + 3) >> 2;
-  for (int cs = c0; cs < c1; cs += TRS_N) {
-    const int ncol = min(TRS_N, c1 - cs);
-    for (int e = tid; e < NB * TRS_N; e += NT) {
-      const int i = e / TRS_N, j = e - i * TRS_N;
-      Bs[i * LDS_B + j] = (i < nb && j < ncol) ? A[(size_t)(k0 + i) * ldw + cs + j] : zmake(0.0, 0.0);
-    }
-    __syncthreads();
-    double cr[2][2][2], ci[2][2][2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-    warp_cmma<2, 2, false>(cr, ci, Li + (wm * 16) * LDL, LDL, Bs + wn * 16, LDS_B, k4);
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int row = wm * 16 + i * 8 + (lane >> 2);
-          const int col = wn * 16 + j * 8 + 2 * (lane & 3) + v;
-          if (row < nb && col < ncol)
-            A[(size_t)(k0 + row) * ldw + cs + col] = zmake(cr[i][j][v], ci[i][j][v]);
-        }
-    __syncthreads();
+  for (int e = tid; e < NB * NB; e += NT) {
+    const int i = e / NB, j = e - i * NB;
+    const z_t v = Li[i * LDL + j];
+    Nsc[(size_t)i * ldw + j] = (j < i && i < nb) ? zmake(-v.x, -v.y) : zmake(0.0, 0.0);
   }
+  __syncthreads();
+  GemmT::run(&P.maps, A, ldw, r, 0, k0, c0, nb, c1 - c0, nb, (char*)smem, bars, blockIdx.x, k0);
+  __syncthreads();
 }
 
 // X = U_kk^-1 Y on the diagonal block rows [kb, kb+nb) of the RHS columns.
@@ -432,7 +415,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
   const int r = P.r, s = P.s, ldw = P.ldw, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   z_t* A = P.work + (size_t)blockIdx.x * P.cta_stride;
-  z_t* yscratch = A + (size_t)r * ldw;
+  z_t* yscratch = A + (size_t)(r + NB) * ldw;  // rows [r, r+NB): U12 scratch
 
   for (int64_t f = blockIdx.x; f < P.F; f += gridDim.x) {
     if (tid < P.nprim) alph[tid] = P.alpha[f * P.nprim + tid];
@@ -495,7 +478,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
       apply_swaps(A, ldw, piv, k0, k0, k0 + nb, c0, c1);
       __syncthreads();
       PH_MARK(3);
-      panel_trsm(A, ldw, k0, nb, c0, c1, smem);
+      panel_trsm(P, A, k0, nb, c0, c1, smem, &bars);
       PH_MARK(4);
       if (c0 < r) {
         GemmT::run(&P.maps, A, ldw, c0, k0, k0, c0, r - c0, c1 - c0, nb, (char*)smem, &bars, blockIdx.x);
@@ -546,7 +529,10 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
   }
 }
 
-static int ldw_of(int r, int s) { return (r + s + 3) & ~3; }
+static int ldw_of(int r, int s) {
+  const int l = (r + s + 3) & ~3;
+  return l > NB ? l : NB;  // the U12 scratch rows hold NB columns
+}
 
 static size_t smem_bytes(int r, int w) {
   size_t m = GemmT::SMEM > GemmT::SMEM_SKINNY ? GemmT::SMEM : GemmT::SMEM_SKINNY;
@@ -567,7 +553,7 @@ static int pick_w(int r) {
 }
 
 static size_t cta_stride(int r, int s, int n_out) {
-  return ((size_t)r * ldw_of(r, s) + (size_t)n_out * s + 7) & ~(size_t)7;
+  return ((size_t)(r + NB) * ldw_of(r, s) + (size_t)n_out * s + 7) & ~(size_t)7;
 }
 
 }  // namespace blk
@@ -638,7 +624,7 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
   P.cta_stride = blk::cta_stride(r, s, n_out);
   {
     const int grid = blocked_grid(F);
-    const cuuint64_t dims[3] = {(cuuint64_t)2 * P.ldw, (cuuint64_t)r, (cuuint64_t)grid};
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * P.ldw, (cuuint64_t)(r + blk::NB), (cuuint64_t)grid};
     const cuuint64_t strides[2] = {(cuuint64_t)P.ldw * 16, (cuuint64_t)P.cta_stride * 16};
     const cuuint32_t box64[3] = {16, 64, 1}, box16[3] = {16, 16, 1}, es[3] = {1, 1, 1};
     if (int rc = encode_map(&P.maps.a64, work, dims, strides, box64, es)) return rc;

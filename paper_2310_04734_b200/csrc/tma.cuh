@@ -115,18 +115,18 @@ struct GemmTma {
   static constexpr size_t SMEM_SKINNY = (size_t)STAGES * SK_STAGE;
 
   __device__ static __forceinline__ void issue_tile(const Maps* mp, char* st, uint64_t* bar, int cta, int ar0,
-                                                    int ac0, int br0, int bc0, int m0) {
+                                                    int ac0, int br0, int bc0, int cr0, int m0) {
     mbar_expect_tx(bar, SK_STAGE);
     tma_load_3d(st, &mp->a64, 2 * ac0, ar0 + m0, cta, bar);
     tma_load_3d(st + 8192, &mp->a64, 2 * (ac0 + 8), ar0 + m0, cta, bar);
     tma_load_3d(st + A_BYTES, &mp->b16, 2 * bc0, br0, cta, bar);
     tma_load_3d(st + A_BYTES + 2048, &mp->b16, 2 * (bc0 + 8), br0, cta, bar);
-    tma_load_3d(st + A_BYTES + SK_B, &mp->a64, 2 * bc0, ar0 + m0, cta, bar);
-    tma_load_3d(st + A_BYTES + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), ar0 + m0, cta, bar);
+    tma_load_3d(st + A_BYTES + SK_B, &mp->a64, 2 * bc0, cr0 + m0, cta, bar);
+    tma_load_3d(st + A_BYTES + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), cr0 + m0, cta, bar);
   }
 
-  __device__ static void run_skinny(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int M,
-                                    int N, int K, char* smem, Bars* bars, int cta) {
+  __device__ static void run_skinny(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int cr0,
+                                    int M, int N, int K, char* smem, Bars* bars, int cta) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ntiles = (M + TM - 1) / TM;
     if (tid == 0) {
@@ -141,7 +141,7 @@ struct GemmTma {
     if (tid == 0) {
       fence_proxy_async_global();
       for (int j = 0; j < STAGES - 1 && j < ntiles; ++j)
-        issue_tile(mp, smem + j * SK_STAGE, &bars->full[j], cta, ar0, ac0, br0, bc0, j * TM);
+        issue_tile(mp, smem + j * SK_STAGE, &bars->full[j], cta, ar0, ac0, br0, bc0, cr0, j * TM);
     }
     unsigned full_ph = 0, empty_ph = 0;
     const int ak = lane & 3, prow = perm8(lane >> 2);
@@ -180,7 +180,7 @@ struct GemmTma {
           const int col = j * 8 + perm8(2 * ak + v);
           if (m0 + row < M && col < N) {
             const z_t c = *(const z_t*)(cs + j * 8192 + swz(row, col & 7));
-            Cg[(size_t)(ar0 + m0 + row) * ldw + bc0 + col] = zmake(c.x - cr[j][v], c.y - ci[j][v]);
+            Cg[(size_t)(cr0 + m0 + row) * ldw + bc0 + col] = zmake(c.x - cr[j][v], c.y - ci[j][v]);
           }
         }
       __syncwarp();
@@ -191,7 +191,8 @@ struct GemmTma {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
           empty_ph ^= 1u << s2;
         }
-        issue_tile(mp, smem + s2 * SK_STAGE, &bars->full[s2], cta, ar0, ac0, br0, bc0, (t + STAGES - 1) * TM);
+        issue_tile(mp, smem + s2 * SK_STAGE, &bars->full[s2], cta, ar0, ac0, br0, bc0, cr0,
+                   (t + STAGES - 1) * TM);
       }
     }
     __syncthreads();
@@ -204,24 +205,27 @@ struct GemmTma {
     }
   }
 
-  // ar0/ac0: A origin; br0/bc0: B origin; cr0/cc0: C origin (= (ar0, bc0)); ldw
-  // for the generic-store epilogue.  smem must be 1024-byte aligned.
+  // ar0/ac0: A origin; br0/bc0: B origin; C origin (cr0, bc0) with cr0 = ar0
+  // unless given; ldw for the generic-store epilogue.  smem must be 1024-byte
+  // aligned.
   __device__ static void run(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int M, int N,
-                             int K, char* smem, Bars* bars, int cta) {
+                             int K, char* smem, Bars* bars, int cta, int cr0_ = -1) {
     if (M <= 0 || N <= 0 || K <= 0) return;
+    const int cr0 = cr0_ < 0 ? ar0 : cr0_;
     if (K <= KC && N <= 16) {
-      run_skinny(mp, Cg, ldw, ar0, ac0, br0, bc0, M, N, K, smem, bars, cta);
+      run_skinny(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
       return;
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
     const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
-    const int ntiles = ((M + TM - 1) / TM) * ntn;
+    const int ntm = (M + TM - 1) / TM;
+    const int ntiles = ntm * ntn;
     const int T = ntiles * nk;
     char* As = smem;
     char* Bs = smem + STAGES * A_BYTES;
     char* Cs = Bs + STAGES * B_BYTES;
-    const int cr0 = ar0, cc0 = bc0;
+    const int cc0 = bc0;
     if (tid == 0) {
 #pragma unroll
       for (int s = 0; s < STAGES; ++s) {
