@@ -551,13 +551,23 @@ namespace vb {
 // indices and both value arrays with consecutive lanes on consecutive slots:
 // the kernel writes exactly the algorithmic bytes of the assembly.
 // band tables: [d][i][o] with o = j - i + 2 in 0..4, for d = x, y, z.
-__global__ void hex27_box_csr_kernel(int nx, int ny, int nz, const double* __restrict__ K1,
-                                     const double* __restrict__ M1, int maxnp, int32_t* __restrict__ indptr,
-                                     int32_t* __restrict__ indices, double* __restrict__ Kv,
-                                     double* __restrict__ Mv) {
+__global__ void __launch_bounds__(256) hex27_box_csr_kernel(int nx, int ny, int nz, const double* __restrict__ K1,
+                                                            const double* __restrict__ M1, int maxnp,
+                                                            int32_t* __restrict__ indptr,
+                                                            int32_t* __restrict__ indices, double* __restrict__ Kv,
+                                                            double* __restrict__ Mv) {
+  // Kronecker form per entry: K = kx (my mz) + mx (ky mz + kz my), M = mx (my mz).
+  // The (y, z) factors P = my mz, Q = ky mz + kz my and the column bases of the
+  // <= 25 neighbour lines are set up once per line task in shared memory; the x
+  // factors once per row.  Each row's entries are one contiguous run of
+  // cx*cy*cz slots (qz slowest, qx fastest) that the warp's lanes stride, so
+  // every store instruction writes 32 consecutive entries.
+  __shared__ double2 sPQ[8][25];
+  __shared__ int sCol[8][25];
+  __shared__ double2 sKX[8][8][5];  // (kx, mx) band rows of the task's 8 x-rows
   const int npx = 2 * nx + 1, npy = 2 * ny + 1, npz = 2 * nz + 1;
-  const int lane = threadIdx.x & 31;
-  const int64_t Tx = 8LL * nx + 1, Ty = 8LL * ny + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int Tx = 8 * nx + 1, Ty = 8 * ny + 1;  // nnz < 2^31 is checked by the launcher
   const int nlines = npy * npz;
   constexpr int SEG = 8;  // rows per warp task (enough tasks to fill the GPU)
   const int nseg = (npx + SEG - 1) / SEG;
@@ -579,50 +589,60 @@ __global__ void hex27_box_csr_kernel(int nx, int ny, int nz, const double* __res
     const int pz = iz < 1 ? 0 : 3 * iz + 2 * min(nz - 1, (iz - 1) >> 1);
     const int ix0 = seg * SEG, ix1 = min(npx, ix0 + SEG);
     const int px = ix0 < 1 ? 0 : 3 * ix0 + 2 * min(nx - 1, (ix0 - 1) >> 1);
-    int64_t start = (int64_t)pz * Ty * Tx + (int64_t)cz * ((int64_t)py * Tx + (int64_t)cy * px);
-    // rows of this segment; when a y-x neighbour plane has <= 16 slots (cy = 3),
-    // the two half-warps take two consecutive rows at once
-    const int half = (cy == 3) ? 16 : 32;
-    const int sub = lane / half, hl = lane - sub * half;
-    for (int ixb = ix0; ixb < ix1; ixb += (half == 16 ? 2 : 1)) {
-      const int ixa = ixb;
-      // offsets of the (up to) two rows of this step
-      const int cxa = (ixa & 1) ? 3 : (min(npx - 1, ixa + 2) - max(0, ixa - 2) + 1);
-      const int ix = ixa + sub;
-      const bool active = ix < ix1 && (half == 32 ? sub == 0 : true);
+    int start = pz * Ty * Tx + cz * (py * Tx + cy * px);
+    // one round of table loads per task: (y, z) factors and the 8 rows' x bands
+    __syncwarp();
+    if (lane < cy * cz) {
+      const int qz = lane / cy, qy = lane - qz * cy;
+      const int jy = ylo + qy, jz = zlo + qz;
+      const double ky = __ldg(Ky + iy * 5 + jy - iy + 2), my = __ldg(My + iy * 5 + jy - iy + 2);
+      const double kz = __ldg(Kz + iz * 5 + jz - iz + 2), mz = __ldg(Mz + iz * 5 + jz - iz + 2);
+      sPQ[w][lane] = make_double2(my * mz, ky * mz + kz * my);
+      sCol[w][lane] = (jz * npy + jy) * npx;
+    }
+    for (int t = lane; t < (ix1 - ix0) * 5; t += 32) {
+      const int rr = t / 5, o = t - rr * 5, ix = ix0 + rr;
+      sKX[w][rr][o] = make_double2(__ldg(Kx + ix * 5 + o), __ldg(Mx + ix * 5 + o));
+    }
+    __syncwarp();
+    for (int ix = ix0; ix < ix1; ++ix) {
       const int xlo = (ix & 1) ? ix - 1 : max(0, ix - 2), xhi = (ix & 1) ? ix + 1 : min(npx - 1, ix + 2);
-      const int cx = xhi - xlo + 1;
-      const int cxy = cx * cy, cnt = cxy * cz;
-      const int64_t rstart = start + (sub == 1 ? (int64_t)cxa * cy * cz : 0);
-      const int64_t row = (int64_t)line * npx + ix;
-      if (active && hl == 0) indptr[row] = (int32_t)rstart;
-      if (active && hl < cxy) {  // (qy, qx) of the y-x plane of neighbours, loop over qz
-        const int qy = hl / cx, qx = hl - qy * cx;
-        const int jx = xlo + qx, jy = ylo + qy;
-        const int ox = jx - ix + 2, oy = jy - iy + 2;
-        const double kx = __ldg(Kx + ix * 5 + ox), mx = __ldg(Mx + ix * 5 + ox);
-        const double ky = __ldg(Ky + iy * 5 + oy), my = __ldg(My + iy * 5 + oy);
-        const double kxy = my * kx + ky * mx, mxy = my * mx;
-        const int64_t col0 = (int64_t)jy * npx + jx;
-        for (int qz = 0; qz < cz; ++qz) {
-          const int jz = zlo + qz, oz = jz - iz + 2;
-          const double kz = __ldg(Kz + iz * 5 + oz), mz = __ldg(Mz + iz * 5 + oz);
-          const int64_t s = rstart + (int64_t)qz * cxy + hl;
-          indices[s] = (int32_t)((int64_t)jz * npy * npx + col0);
-          Kv[s] = mz * kxy + kz * mxy;
-          Mv[s] = mz * mxy;
+      const int cx = xhi - xlo + 1, cnt = cx * cy * cz;
+      if (lane == 0) indptr[(int64_t)line * npx + ix] = start;
+      const double2* km_row = &sKX[w][ix - ix0][xlo - ix + 2];
+      // entry e of the row: column, K and M values
+      auto entry = [&](int e, int& col, double& kv, double& mv) {
+        // p = e / cx (cx is 3 or 5 except on 1-element lines)
+        const int p = cx == 3 ? (e * 43691) >> 17 : (cx == 5 ? (e * 52429) >> 18 : e / cx);
+        const int qx = e - p * cx;
+        const double2 pq = sPQ[w][p], km = km_row[qx];
+        col = sCol[w][p] + xlo + qx;
+        kv = km.x * pq.x + km.y * pq.y;
+        mv = km.y * pq.x;
+      };
+      // 16-byte (value) / 8-byte (index) stores on the even-aligned body of the run
+      const int head = start & 1;
+      if (head && lane == 0) {
+        int c; double kv, mv;
+        entry(0, c, kv, mv);
+        indices[start] = c; Kv[start] = kv; Mv[start] = mv;
+      }
+      for (int e = head + 2 * lane; e < cnt; e += 64) {
+        int c0, c1 = 0; double k0, m0, k1 = 0.0, m1 = 0.0;
+        entry(e, c0, k0, m0);
+        const int sidx = start + e;
+        if (e + 1 < cnt) {
+          entry(e + 1, c1, k1, m1);
+          *reinterpret_cast<int2*>(indices + sidx) = make_int2(c0, c1);
+          *reinterpret_cast<double2*>(Kv + sidx) = make_double2(k0, k1);
+          *reinterpret_cast<double2*>(Mv + sidx) = make_double2(m0, m1);
+        } else {
+          indices[sidx] = c0; Kv[sidx] = k0; Mv[sidx] = m0;
         }
       }
-      // advance past the rows handled in this step
-      start += (int64_t)cxa * cy * cz;
-      if (half == 16 && ixa + 1 < ix1) {
-        const int ixn = ixa + 1;
-        const int cxn = (ixn & 1) ? 3 : (min(npx - 1, ixn + 2) - max(0, ixn - 2) + 1);
-        start += (int64_t)cxn * cy * cz;
-      }
-      (void)cnt;
+      start += cnt;
     }
-    if (line == nlines - 1 && ix1 == npx && lane == 0) indptr[(int64_t)nlines * npx] = (int32_t)start;
+    if (line == nlines - 1 && ix1 == npx && lane == 0) indptr[(int64_t)nlines * npx] = start;
   }
 }
 

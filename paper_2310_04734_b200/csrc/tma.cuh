@@ -20,6 +20,27 @@
 namespace vb {
 namespace tma {
 
+// Profiling aid (-DVB_PHASE_TIMING): SM cycles of the general GEMM path split
+// into wait-full / compute / release+produce / epilogue for warp 1 (a pure
+// consumer) and thread 0 (consumer + producer); vb_debug_phase_cycles 16..23.
+__device__ unsigned long long g_gemm_cycles[8];
+#ifdef VB_PHASE_TIMING
+#define GT_BEGIN long long _gt = clock64()
+#define GT_MARK(k)                                                                  \
+  do {                                                                              \
+    if ((threadIdx.x & 31) == 0 && threadIdx.x < 64) {                              \
+      const long long _n = clock64();                                               \
+      atomicAdd(&g_gemm_cycles[(k) + (threadIdx.x ? 0 : 4)], (unsigned long long)(_n - _gt)); \
+      _gt = _n;                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define GT_BEGIN
+#define GT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 using blk::NT;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -257,10 +278,12 @@ struct GemmTma {
     const int ar = lane >> 2, ak = lane & 3;
     const int prow = perm8(ar);
     int t = 0, kc = 0;
+    GT_BEGIN;
     for (int it = 0; it < T; ++it) {
       const int st = it % STAGES;
       mbar_wait(&bars->full[st], (full_ph >> st) & 1);
       full_ph ^= 1u << st;
+      GT_MARK(0);
       const char* as = As + st * A_BYTES;
       const char* bs = Bs + st * B_BYTES;
       const int kvalid = min(KC, K - kc * KC);
@@ -293,6 +316,7 @@ struct GemmTma {
         }
       }
       __syncwarp();
+      GT_MARK(1);
       if (lane == 0) mbar_arrive(&bars->empty[st]);
       // refill the stage consumed in the previous iteration
       if (tid == 0 && it + STAGES - 1 < T) {
@@ -305,6 +329,7 @@ struct GemmTma {
                     (pt / ntn) * TM, (pt % ntn) * TN, pk * KC);
         if (++pk == nk) { pk = 0; ++pt; }
       }
+      GT_MARK(2);
       if (kc == nk - 1) {
         const int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
         mbar_wait(&bars->cfull, c_ph);
@@ -333,6 +358,7 @@ struct GemmTma {
           fence_proxy_async_global();
           issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, ((t + 1) / ntn) * TM, ((t + 1) % ntn) * TN);
         }
+        GT_MARK(3);
         kc = 0;
         ++t;
       } else {
