@@ -597,11 +597,11 @@ static int encode_map(CUtensorMap* map, void* base, const cuuint64_t* dims, cons
 
 int sweep_debug_phase_cycles(unsigned long long* out_host, int reset) {
   VB_CUDA(cudaMemcpyFromSymbol(out_host, blk::g_phase_cycles, sizeof(unsigned long long) * 16));
-  VB_CUDA(cudaMemcpyFromSymbol(out_host + 16, tma::g_gemm_cycles, sizeof(unsigned long long) * 8));
+  VB_CUDA(cudaMemcpyFromSymbol(out_host + 16, tma::g_gemm_cycles, sizeof(unsigned long long) * 16));
   if (reset) {
     unsigned long long z[16] = {};
     VB_CUDA(cudaMemcpyToSymbol(blk::g_phase_cycles, z, sizeof(z)));
-    VB_CUDA(cudaMemcpyToSymbol(tma::g_gemm_cycles, z, 8 * sizeof(unsigned long long)));
+    VB_CUDA(cudaMemcpyToSymbol(tma::g_gemm_cycles, z, 16 * sizeof(unsigned long long)));
   }
   return 0;
 }

@@ -23,7 +23,7 @@ namespace tma {
 // Profiling aid (-DVB_PHASE_TIMING): SM cycles of the general GEMM path split
 // into wait-full / compute / release+produce / epilogue for warp 1 (a pure
 // consumer) and thread 0 (consumer + producer); vb_debug_phase_cycles 16..23.
-__device__ unsigned long long g_gemm_cycles[8];
+__device__ unsigned long long g_gemm_cycles[16];
 #ifdef VB_PHASE_TIMING
 #define GT_BEGIN long long _gt = clock64()
 #define GT_MARK(k)                                                                  \
@@ -34,9 +34,20 @@ __device__ unsigned long long g_gemm_cycles[8];
       _gt = _n;                                                                     \
     }                                                                               \
   } while (0)
+#define GS_MARK(k)                                                                  \
+  do {                                                                              \
+    if (threadIdx.x == 32) {                                                        \
+      const long long _n = clock64();                                               \
+      atomicAdd(&g_gemm_cycles[8 + (k)], (unsigned long long)(_n - _gt));           \
+      _gt = _n;                                                                     \
+    }                                                                               \
+  } while (0)
 #else
 #define GT_BEGIN
 #define GT_MARK(k) \
+  do {             \
+  } while (0)
+#define GS_MARK(k) \
   do {             \
   } while (0)
 #endif
@@ -150,6 +161,7 @@ struct GemmTma {
                                     int M, int N, int K, char* smem, Bars* bars, int cta) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ntiles = (M + TM - 1) / TM;
+    GT_BEGIN;
     if (tid == 0) {
 #pragma unroll
       for (int s = 0; s < STAGES; ++s) {
@@ -168,10 +180,12 @@ struct GemmTma {
     const int ak = lane & 3, prow = perm8(lane >> 2);
     const int row = warp * 8 + prow;
     const int k4n = (K + 3) >> 2;
+    GS_MARK(0);
     for (int t = 0; t < ntiles; ++t) {
       const int st = t % STAGES;
       mbar_wait(&bars->full[st], (full_ph >> st) & 1);
       full_ph ^= 1u << st;
+      if (t == 0) GS_MARK(1); else GS_MARK(2);
       const char* as = smem + st * SK_STAGE;
       const char* bs = as + A_BYTES;
       const char* cs = bs + SK_B;
@@ -205,6 +219,7 @@ struct GemmTma {
           }
         }
       __syncwarp();
+      GS_MARK(3);
       if (lane == 0) mbar_arrive(&bars->empty[st]);
       if (tid == 0 && t + STAGES - 1 < ntiles) {
         const int s2 = (t + STAGES - 1) % STAGES;
@@ -215,8 +230,10 @@ struct GemmTma {
         issue_tile(mp, smem + s2 * SK_STAGE, &bars->full[s2], cta, ar0, ac0, br0, bc0, cr0,
                    (t + STAGES - 1) * TM);
       }
+      GS_MARK(4);
     }
     __syncthreads();
+    GS_MARK(5);
     if (tid == 0) {
 #pragma unroll
       for (int s = 0; s < STAGES; ++s) {

@@ -33,7 +33,7 @@ for r in [int(x) for x in sys.argv[1:]] or [1024]:
     f = torch.from_numpy(w.freqs[:nf]).cuda()
     rs.sweep_device(f)
     torch.cuda.synchronize()
-    buf = (C.c_uint64 * 16)()
+    buf = (C.c_uint64 * 32)()
     lib.vb_debug_phase_cycles(buf, 1)
     rs.sweep_device(f)
     torch.cuda.synchronize()
@@ -47,8 +47,15 @@ for r in [int(x) for x in sys.argv[1:]] or [1024]:
     print(f"r={r} F={nf}: {t0.elapsed_time(t1):.2f} ms per launch")
     v = np.array(list(buf), dtype=float)
     print("total Mcycles per CTA-freq", v[:8].sum() / nf / 1e6)
-    sub = v[8:]
+    sub = v[8:16]
+    gm = v[16:24]
+    sk = v[24:32]
+    skn = ["setup", "first tile wait", "tile waits", "compute+epilogue", "release/produce", "final barrier"]
+    print(f"r={r}: skinny warp1 " + ", ".join(f"{n} {100 * x / v[:8].sum():.1f}%" for n, x in zip(skn, sk)))
     v = v[:8]
+    gn = ["wait full", "compute", "release/produce", "epilogue"]
+    print(f"r={r}: gemm warp1 " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(gn, gm[:4])))
+    print(f"r={r}: gemm thr0  " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(gn, gm[4:])))
     subn = ["leaf load", "leaf factor", "leaf swaps", "leaf trsm_small", "colA", "colB", "colArgmax"]
     print(f"r={r}: sub-phases " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(subn, sub)))
     print(f"r={r}: " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(names, v)))
