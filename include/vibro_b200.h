@@ -239,6 +239,12 @@ int vb_probe_fp64_peak(double* tflops_host, void* stream);
  * 24..29 the skinny (in-panel) GEMM split. */
 int vb_debug_phase_cycles(unsigned long long* cycles_host, int reset);
 
+/* Give back the L2 set-aside that vb_rom_sweep reserves for the reduced
+ * primitives (persisting-access window): resets persisting lines and the
+ * device's persisting-L2 limit to 0, so later bandwidth-bound work gets the
+ * whole L2.  The next blocked sweep launch re-reserves it. */
+int vb_release_l2_persistence(void);
+
 /* Number of this library's kernel launches since load (process-wide counter,
  * incremented on every successful launch). */
 int64_t vb_launch_count(void);

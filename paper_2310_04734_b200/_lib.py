@@ -31,6 +31,7 @@ _SIGS = {
     "vb_version": (C.c_char_p, []),
     "vb_last_error": (C.c_char_p, []),
     "vb_launch_count": (C.c_int64, []),
+    "vb_release_l2_persistence": (C.c_int, []),
     "vb_debug_phase_cycles": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
     "vb_rom_sweep_path": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "vb_set_sweep_path_override": (None, [C.c_int]),

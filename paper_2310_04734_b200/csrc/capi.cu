@@ -40,6 +40,12 @@ const char* vb_last_error(void) { return vb::g_last_error.c_str(); }
 
 int64_t vb_launch_count(void) { return vb::g_launches.load(); }
 
+int vb_release_l2_persistence(void) {
+  VB_CUDA(cudaCtxResetPersistingL2Cache());
+  VB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+  return 0;
+}
+
 int vb_rom_sweep_path(int r, int nprim, int s, int n_out) { return vb::sweep_path(r, nprim, s, n_out); }
 
 void vb_set_sweep_path_override(int path) { vb::sweep_set_override(path); }

@@ -28,6 +28,8 @@ def timed(fn, reps=3):
 
 
 def measure():
+    # a preceding blocked sweep leaves part of L2 set aside for its primitives
+    _lib.check(_lib.load().vb_release_l2_persistence(), "vb_release_l2_persistence")
     dev = torch.device("cuda")
     peak_hbm = json.load(open(Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"))["hbm_gbs"] \
         if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6650.0
