@@ -231,12 +231,13 @@ int vb_scale_columns(int n, int m, vb_complex* W, int64_t ldw, const double* sca
  * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */
 int vb_probe_fp64_peak(double* tflops_host, void* stream);
 
-/* Profiling aid: per-phase SM-cycle totals of the blocked sweep kernel (32
+/* Profiling aid: per-phase SM-cycle totals of the blocked sweep kernel (36
  * counters; non-zero only in a library built with -DVB_PHASE_TIMING).  Phases:
  * form, leaf panel, in-panel TRSM+GEMM, interchanges, U12 TRSM, trailing GEMM,
  * back substitution, outputs; 8..15 leaf sub-phases; 16..23 the TMA GEMM's
  * wait/compute/epilogue split for a consumer warp and for the producer thread;
- * 24..29 the skinny (in-panel) GEMM split. */
+ * 24..29 the skinny (in-panel) GEMM split; 32..35 vb_zgetrf's panel / swaps /
+ * TRSM / GEMM phases (CTA 0). */
 int vb_debug_phase_cycles(unsigned long long* cycles_host, int reset);
 
 /* Give back the L2 set-aside that vb_rom_sweep reserves for the reduced

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "mma.cuh"
 #include "sweep.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -30,14 +31,42 @@ using blk::KC;
 using blk::NB;
 using blk::NT;
 
-using GemmLU = blk::Gemm<64, 64, 2, 4, 3, blk::EPI_SUB>;
+// Trailing update: the TMA + mbarrier DMMA GEMM of the blocked sweep
+// (csrc/tma.cuh) over a 2-D tensor map of the matrix, tiles spread over CTAs.
+using GemmT = tma::GemmTma<3>;
+
+// Profiling aid (-DVB_PHASE_TIMING): CTA 0's SM cycles in panel / swaps /
+// TRSM / GEMM (each phase ends at a grid barrier), vb_debug_phase_cycles 32..35.
+__device__ unsigned long long g_lu_cycles[4];
+#ifdef VB_PHASE_TIMING
+#define LU_MARK(k)                                                              \
+  do {                                                                          \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                  \
+      const long long _n = clock64();                                           \
+      g_lu_cycles[k] += (unsigned long long)(_n - _lt);                         \
+      _lt = _n;                                                                 \
+    }                                                                           \
+  } while (0)
+#define LU_BEGIN long long _lt = clock64()
+#else
+#define LU_MARK(k) \
+  do {             \
+  } while (0)
+#define LU_BEGIN
+#endif
 constexpr int LDL = NB + 4;
 constexpr int TRS_N = 32;
 constexpr int LDS_B = TRS_N + 2;
 constexpr size_t TRSM_SMEM = (size_t)(NB * LDL + NB * LDS_B) * sizeof(z_t);
-constexpr size_t LU_SMEM = GemmLU::SMEM > TRSM_SMEM ? GemmLU::SMEM : TRSM_SMEM;
+constexpr size_t LU_SMEM = (GemmT::SMEM > TRSM_SMEM ? GemmT::SMEM : TRSM_SMEM) + 1024;  // + 1024-B alignment
+// + the CTA's panel rows (ceil(n / grid) x (NB + 1) complex)
+inline size_t lu_smem(int n, int grid) {
+  const size_t rows = (size_t)((n + grid - 1) / grid) * (NB + 1) * sizeof(z_t) + 1024;
+  return rows > LU_SMEM ? rows : LU_SMEM;
+}
 
-struct LuParams {
+struct __align__(64) LuParams {
+  tma::Maps maps;  // over the matrix (must stay first: 64-B aligned)
   int n;
   z_t* A;
   int64_t lda;
@@ -78,9 +107,11 @@ __device__ void load_diag_block(const z_t* A, int64_t lda, int k0, int nb, z_t* 
   blk::tri_inv64<LOWER>(T, LDL);
 }
 
-__global__ void __launch_bounds__(NT, 1) zgetrf_kernel(LuParams P) {
+__global__ void __launch_bounds__(NT, 1) zgetrf_kernel(const __grid_constant__ LuParams P) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(1024) char smem_raw[];
+  double2* smem = (double2*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ GemmT::Bars bars;
   __shared__ z_t s_prow[NB];
   __shared__ z_t s_rowj[NB];
   __shared__ double rv[NT / 32];
@@ -94,16 +125,28 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(LuParams P) {
   int lo, hi;
   row_range(n, lo, hi);
   if (c == 0 && tid == 0) *P.info = 0;
+  LU_BEGIN;
 
   for (int k0 = 0; k0 < n; k0 += NB) {
     const int nb = min(NB, n - k0), kend = k0 + nb;
     // ------------------------------------------------------------ panel
+    // The CTA's own panel rows [plo, hi) live in shared memory for the 64
+    // column steps (one round of loads, one write-back): only the pivot search
+    // partials, the candidate rows and row j travel through global scratch.
+    const int plo = max(lo, k0), pn = max(0, hi - plo);
+    constexpr int LP = NB + 1;  // padded row (conflict-free row-per-thread access)
+    z_t* Ps = smem;
+    for (int e = tid; e < pn * nb; e += NT) {
+      const int i = e / nb, t = e - i * nb;
+      Ps[i * LP + t] = __ldcg(A + (int64_t)(plo + i) * lda + k0 + t);
+    }
+    __syncthreads();
     for (int j = k0; j < kend; ++j) {
-      const int buf = j & 1;
+      const int buf = j & 1, jj = j - k0;
       double v = -1.0;
       int pi = 0x7fffffff;
-      for (int i = max(lo, j) + tid; i < hi; i += NT) {
-        const double a = zabs1(A[(int64_t)i * lda + j]);
+      for (int i = max(plo, j) + tid; i < hi; i += NT) {
+        const double a = zabs1(Ps[(i - plo) * LP + jj]);
         if (a > v) { v = a; pi = i; }
       }
       warp_argmax(v, pi);
@@ -121,10 +164,9 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(LuParams P) {
         P.pidx[buf * G + c] = s_idx;
       }
       if (s_val >= 0.0)
-        for (int t = tid; t < nb; t += NT)
-          P.prow[((int64_t)buf * G + c) * NB + t] = A[(int64_t)s_idx * lda + k0 + t];
-      if (j >= lo && j < hi)
-        for (int t = tid; t < nb; t += NT) P.rowj[buf * NB + t] = A[(int64_t)j * lda + k0 + t];
+        for (int t = tid; t < nb; t += NT) P.prow[((int64_t)buf * G + c) * NB + t] = Ps[(s_idx - plo) * LP + t];
+      if (j >= plo && j < hi)
+        for (int t = tid; t < nb; t += NT) P.rowj[buf * NB + t] = Ps[(j - plo) * LP + t];
       grid.sync();
       // every CTA resolves the same pivot from the published partials
       if (warp == 0) {
@@ -164,35 +206,37 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(LuParams P) {
       }
       if (c == 0 && tid == 0) P.ipiv[j] = p;
       __syncthreads();
-      const int jj = j - k0;
       const z_t pinv = zrecip(s_prow[jj]);
-      if (p != j) {
-        if (j >= lo && j < hi)
-          for (int t = tid; t < nb; t += NT) A[(int64_t)j * lda + k0 + t] = s_prow[t];
-      }
+      if (p != j && j >= plo && j < hi)
+        for (int t = tid; t < nb; t += NT) Ps[(j - plo) * LP + t] = s_prow[t];
       // eliminate own rows i > j; row p (if swapped) now holds the old row j
-      const int r0 = max(lo, j + 1);
+      const int r0 = max(plo, j + 1);
       const int nrows = hi - r0, ncols = nb - jj - 1;
       if (nrows > 0) {
         // multipliers first (column j), then the rank-1 update of the panel
         for (int i = r0 + tid; i < hi; i += NT) {
-          const z_t aij = (i == p) ? s_rowj[jj] : A[(int64_t)i * lda + j];
-          A[(int64_t)i * lda + j] = zmul(aij, pinv);
+          const z_t aij = (i == p) ? s_rowj[jj] : Ps[(i - plo) * LP + jj];
+          Ps[(i - plo) * LP + jj] = zmul(aij, pinv);
         }
         if (p != j && p >= r0 && p < hi)
           for (int t = tid; t < nb; t += NT)
-            if (t != jj) A[(int64_t)p * lda + k0 + t] = s_rowj[t];
+            if (t != jj) Ps[(p - plo) * LP + t] = s_rowj[t];
         __syncthreads();
         if (ncols > 0)
           for (int e = tid; e < nrows * ncols; e += NT) {
             const int ii = e / ncols, t = jj + 1 + (e - ii * ncols);
-            const int64_t off = (int64_t)(r0 + ii) * lda;
-            A[off + k0 + t] = zfms(A[off + k0 + t], A[off + j], s_prow[t]);
+            z_t* row = Ps + (r0 - plo + ii) * LP;
+            row[t] = zfms(row[t], row[jj], s_prow[t]);
           }
       }
       __syncthreads();
     }
+    for (int e = tid; e < pn * nb; e += NT) {
+      const int i = e / nb, t = e - i * nb;
+      A[(int64_t)(plo + i) * lda + k0 + t] = Ps[i * LP + t];
+    }
     grid.sync();
+    LU_MARK(0);
     // ------------------------------------------------------------ swaps
     {
       const int64_t ncol = (int64_t)n - nb;
@@ -209,6 +253,7 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(LuParams P) {
       }
     }
     grid.sync();
+    LU_MARK(1);
     // ------------------------------------------------------------ TRSM
     {
       z_t* Li = smem;
@@ -254,13 +299,13 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(LuParams P) {
       }
     }
     grid.sync();
+    LU_MARK(2);
     // ------------------------------------------------------------ GEMM
     if (kend < n) {
-      GemmLU::run(A + (int64_t)kend * lda + kend, (int)lda, A + (int64_t)kend * lda + k0, (int)lda,
-                  A + (int64_t)k0 * lda + kend, (int)lda, n - kend, n - kend, nb, smem,
-                  zmake(1.0, 0.0), zmake(0.0, 0.0), c, G);
+      GemmT::run(&P.maps, A, (int)lda, kend, k0, k0, kend, n - kend, n - kend, nb, (char*)smem, &bars, 0, -1, c, G);
     }
     grid.sync();
+    LU_MARK(3);
   }
   // final permutation from the interchange sequence (LAPACK ipiv semantics)
   if (c == 0) {
@@ -401,6 +446,8 @@ constexpr size_t SOLVE_SMEM = (size_t)(NB * (NB + 1) + NB * MAXRHS) * sizeof(z_t
 static int coop_grid(const void* kern, size_t smem, int* grid) {
   int dev = 0, nsm = 0, per = 0, coop = 0;
   VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared));
   VB_CUDA(cudaGetDevice(&dev));
   VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   VB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
@@ -419,9 +466,19 @@ static int coop_grid(const void* kern, size_t smem, int* grid) {
 
 }  // namespace lu
 
+int lu_debug_cycles(unsigned long long* out, int reset) {
+  VB_CUDA(cudaMemcpyFromSymbol(out, lu::g_lu_cycles, 4 * sizeof(unsigned long long)));
+  if (reset) {
+    unsigned long long z[4] = {};
+    VB_CUDA(cudaMemcpyToSymbol(lu::g_lu_cycles, z, sizeof(z)));
+  }
+  return 0;
+}
+
 size_t zgetrf_workspace_bytes(int n) {
-  int grid = 148;
-  lu::coop_grid((const void*)lu::zgetrf_kernel, lu::LU_SMEM, &grid);
+  int grid = 148, dev = 0;  // one CTA per SM (see coop_grid; no attribute side effects here)
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev);
   const int nblk = (n + lu::NB - 1) / lu::NB;
   size_t b = 0;
   b += 2 * (size_t)grid * sizeof(double);
@@ -446,6 +503,9 @@ int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size
   VB_CHECK_ARG(aux && aux_bytes >= zgetrf_aux_bytes(n), "vb_zgetrf: aux too small");
   int grid = 0;
   if (int rc = lu::coop_grid((const void*)lu::zgetrf_kernel, lu::LU_SMEM, &grid)) return rc;
+  const size_t smem = lu::lu_smem(n, grid);
+  VB_CHECK_ARG(smem <= 227 * 1024, "vb_zgetrf: n too large for the shared-memory panel rows");
+  if (int rc = lu::coop_grid((const void*)lu::zgetrf_kernel, smem, &grid)) return rc;
   const int nblk = (n + lu::NB - 1) / lu::NB;
   VB_CHECK_ARG(work && work_bytes >= zgetrf_workspace_bytes(n), "vb_zgetrf: workspace too small");
   lu::LuParams P;
@@ -460,8 +520,28 @@ int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size
   P.Linv = (z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
   P.Uinv = (z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
   P.perm = (int*)x;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * lda, (cuuint64_t)n, 1};
+    const cuuint64_t strides[2] = {(cuuint64_t)lda * 16, (cuuint64_t)lda * 16 * n};
+    const cuuint32_t box64[3] = {16, 64, 1}, box16[3] = {16, 16, 1}, es[3] = {1, 1, 1};
+    if (int rc = tma_encode_map(&P.maps.a64, A, dims, strides, box64, es)) return rc;
+    if (int rc = tma_encode_map(&P.maps.b16, A, dims, strides, box16, es)) return rc;
+  }
   void* args[] = {&P};
-  VB_CUDA(cudaLaunchCooperativeKernel((const void*)lu::zgetrf_kernel, grid, lu::NT, args, lu::LU_SMEM, st));
+  {
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)lu::zgetrf_kernel, grid, lu::NT, args, smem, st);
+    if (e != cudaSuccess) {
+      int per = -1;
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, (const void*)lu::zgetrf_kernel);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lu::zgetrf_kernel, lu::NT, smem);
+      set_error(std::string("vb_zgetrf launch: ") + cudaGetErrorString(e) + " (grid " + std::to_string(grid) +
+                ", dyn smem " + std::to_string(smem) + ", static " + std::to_string(fa.sharedSizeBytes) +
+                ", max dyn " + std::to_string(fa.maxDynamicSharedSizeBytes) + ", regs " +
+                std::to_string(fa.numRegs) + ", blocks/SM " + std::to_string(per) + ")");
+      return 2;
+    }
+  }
   VB_LAUNCHED("zgetrf_kernel");
   return 0;
 }

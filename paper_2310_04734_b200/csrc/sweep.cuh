@@ -1,8 +1,14 @@
 // Internal interface of the reduced-sweep kernels (dispatch in sweep.cu).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace vb {
+
+// 3-D FP64 tensor map (doubles x rows x slabs, 128B swizzle) for the TMA GEMMs.
+int tma_encode_map(CUtensorMap* map, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box, const cuuint32_t* es);
 
 size_t sweep_small_smem_bytes(int r, int nprim, int s, int n_out);
 int sweep_small_launch(int r, int nprim, int s, int n_out, int64_t F, const z_t* prims,
@@ -21,6 +27,7 @@ int probe_fp64_peak(double* tflops, cudaStream_t stream);
 size_t sweep_blocked_workspace_bytes(int r, int s, int n_out, int64_t F);
 int sweep_blocked_supported(int r, int s, int n_out);
 int sweep_debug_phase_cycles(unsigned long long* out_host, int reset);
+int lu_debug_cycles(unsigned long long* out, int reset);
 int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_t* prims,
                          const z_t* alpha, const z_t* b, int64_t b_stride_f, const z_t* c_r, z_t* y,
                          double* spl, z_t* x, int* info, void* work, size_t work_bytes,

@@ -574,8 +574,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static int encode_map(CUtensorMap* map, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
-                      const cuuint32_t* box, const cuuint32_t* es) {
+int tma_encode_map(CUtensorMap* map, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box, const cuuint32_t* es) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -598,6 +598,7 @@ static int encode_map(CUtensorMap* map, void* base, const cuuint64_t* dims, cons
 int sweep_debug_phase_cycles(unsigned long long* out_host, int reset) {
   VB_CUDA(cudaMemcpyFromSymbol(out_host, blk::g_phase_cycles, sizeof(unsigned long long) * 16));
   VB_CUDA(cudaMemcpyFromSymbol(out_host + 16, tma::g_gemm_cycles, sizeof(unsigned long long) * 16));
+  if (int rc = lu_debug_cycles(out_host + 32, reset)) return rc;
   if (reset) {
     unsigned long long z[16] = {};
     VB_CUDA(cudaMemcpyToSymbol(blk::g_phase_cycles, z, sizeof(z)));
@@ -629,8 +630,8 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
     const cuuint64_t dims[3] = {(cuuint64_t)2 * P.ldw, (cuuint64_t)(r + blk::NB), (cuuint64_t)grid};
     const cuuint64_t strides[2] = {(cuuint64_t)P.ldw * 16, (cuuint64_t)P.cta_stride * 16};
     const cuuint32_t box64[3] = {16, 64, 1}, box16[3] = {16, 16, 1}, es[3] = {1, 1, 1};
-    if (int rc = encode_map(&P.maps.a64, work, dims, strides, box64, es)) return rc;
-    if (int rc = encode_map(&P.maps.b16, work, dims, strides, box16, es)) return rc;
+    if (int rc = tma_encode_map(&P.maps.a64, work, dims, strides, box64, es)) return rc;
+    if (int rc = tma_encode_map(&P.maps.b16, work, dims, strides, box16, es)) return rc;
   }
   const size_t smem = blk::smem_bytes(r, w);
   VB_CUDA(cudaFuncSetAttribute(blk::rom_sweep_blocked_kernel,

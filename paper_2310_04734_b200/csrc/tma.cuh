@@ -246,11 +246,14 @@ struct GemmTma {
   // ar0/ac0: A origin; br0/bc0: B origin; C origin (cr0, bc0) with cr0 = ar0
   // unless given; ldw for the generic-store epilogue.  smem must be 1024-byte
   // aligned.
+  // t_first / t_step: this CTA computes tiles t_first, t_first + t_step, ...
+  // of the row-major tile grid (several CTAs sharing one GEMM).
   __device__ static void run(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int M, int N,
-                             int K, char* smem, Bars* bars, int cta, int cr0_ = -1) {
+                             int K, char* smem, Bars* bars, int cta, int cr0_ = -1, int t_first = 0,
+                             int t_step = 1) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int cr0 = cr0_ < 0 ? ar0 : cr0_;
-    if (K <= KC && N <= 16) {
+    if (K <= KC && N <= 16 && t_step == 1) {
       run_skinny(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
       return;
     }
@@ -258,8 +261,13 @@ struct GemmTma {
     const int wm = warp >> 1, wn = warp & 1;
     const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
     const int ntm = (M + TM - 1) / TM;
-    const int ntiles = ntm * ntn;
+    const int ntiles_all = ntm * ntn;
+    if (t_first >= ntiles_all) return;
+    const int ntiles = (ntiles_all - 1 - t_first) / t_step + 1;  // this CTA's tiles
     const int T = ntiles * nk;
+    // local tile l -> (m0, n0)
+    auto tm0 = [&](int l) { return ((t_first + l * t_step) / ntn) * TM; };
+    auto tn0 = [&](int l) { return ((t_first + l * t_step) % ntn) * TN; };
     char* As = smem;
     char* Bs = smem + STAGES * A_BYTES;
     char* Cs = Bs + STAGES * B_BYTES;
@@ -279,10 +287,10 @@ struct GemmTma {
     int pt = 0, pk = 0;
     if (tid == 0) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
-      issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, 0, 0);
+      issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(0), tn0(0));
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
         issue_chunk(mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], cta, ar0, ac0, br0, bc0,
-                    (pt / ntn) * TM, (pt % ntn) * TN, pk * KC);
+                    tm0(pt), tn0(pt), pk * KC);
         if (++pk == nk) { pk = 0; ++pt; }
       }
     }
@@ -343,12 +351,12 @@ struct GemmTma {
           empty_ph ^= 1u << s2;
         }
         issue_chunk(mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], cta, ar0, ac0, br0, bc0,
-                    (pt / ntn) * TM, (pt % ntn) * TN, pk * KC);
+                    tm0(pt), tn0(pt), pk * KC);
         if (++pk == nk) { pk = 0; ++pt; }
       }
       GT_MARK(2);
       if (kc == nk - 1) {
-        const int m0 = (t / ntn) * TM, n0 = (t % ntn) * TN;
+        const int m0 = tm0(t), n0 = tn0(t);
         mbar_wait(&bars->cfull, c_ph);
         c_ph ^= 1;
 #pragma unroll
@@ -373,7 +381,7 @@ struct GemmTma {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
           fence_proxy_async_global();
-          issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, ((t + 1) / ntn) * TM, ((t + 1) % ntn) * TN);
+          issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(t + 1), tn0(t + 1));
         }
         GT_MARK(3);
         kc = 0;

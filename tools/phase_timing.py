@@ -33,7 +33,7 @@ for r in [int(x) for x in sys.argv[1:]] or [1024]:
     f = torch.from_numpy(w.freqs[:nf]).cuda()
     rs.sweep_device(f)
     torch.cuda.synchronize()
-    buf = (C.c_uint64 * 32)()
+    buf = (C.c_uint64 * 36)()
     lib.vb_debug_phase_cycles(buf, 1)
     rs.sweep_device(f)
     torch.cuda.synchronize()
