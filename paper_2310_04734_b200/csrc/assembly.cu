@@ -121,43 +121,81 @@ static int init_tables() {
 }
 
 // ------------------------------------------------------- element kernels ---
-// One CTA per hex27 element.  Follows assembly.py:77-91 exactly:
-// J = dshape^T X, detJ <= 0 rejected, dN = dshape inv(J),
-// Kgrad += w detJ dN dN^T, Mnn += w detJ N N^T.
-constexpr int EL_NT = 128;
+// One WARP per hex27 element (assembly.py:77-91): J = dshape^T X, detJ <= 0
+// rejected, dN = dshape inv(J), then
+//   Kgrad = D^T W D   with D[(g,b)][i] = dN_i/dx_b at Gauss point g (81 x 27),
+//   Mnn   = N^T W N   with N[g][i]                                   (27 x 27),
+// W = diag(w_g detJ_g), both as 27 x 27 (padded to 32 x 32) products on the FP64
+// tensor cores: mma.sync.m8n8k4.f64, 4 x 4 fragments per warp, 21 (K) + 7 (M)
+// k-steps.  The D fragments are formed on the fly from the reference-element
+// gradients (shared table) and the per-point inverse Jacobians, so no element
+// array of D is stored; W is applied to the A-side fragment.  The 27 x 27
+// results are staged in shared memory and written with coalesced stores.
+constexpr int EL_NT = 256;            // 8 warps = 8 elements in flight per CTA
+constexpr int EL_WARPS = EL_NT / 32;
 
-__global__ void __launch_bounds__(EL_NT) hex27_helmholtz_kernel(int n_elem, const double* __restrict__ xyz,
+__device__ __forceinline__ void el_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct ElWarp {
+  double X[27][3];
+  double iJ[27][9];
+  double wdet[28];  // [27] = 0 (padding point)
+  double out[27 * 27];
+};
+
+__global__ void __launch_bounds__(EL_NT, 2) hex27_helmholtz_kernel(int n_elem, const double* __restrict__ xyz,
                                                                 const int32_t* __restrict__ conn,
                                                                 double* __restrict__ Ke,
                                                                 double* __restrict__ Me,
                                                                 int* __restrict__ bad) {
-  __shared__ double X[27][3];
-  __shared__ double wdet[27];
-  __shared__ double dNx[27][27][3];  // [g][i][b]
-  __shared__ double sN[27 * 27];     // N[g][i]
-  const int tid = threadIdx.x;
-  for (int q = tid; q < 729; q += EL_NT) sN[q] = c_hexN[q];
-  for (int e = blockIdx.x; e < n_elem; e += gridDim.x) {
-    for (int q = tid; q < 81; q += EL_NT) X[q / 3][q % 3] = xyz[(size_t)conn[(size_t)e * 27 + q / 3] * 3 + q % 3];
-    __syncthreads();
-    // J[g][a][b] = sum_i dN_i/dxi_a(g) X_i,b  (243 independent sums)
-    __shared__ double Jg[27][9];
-    for (int q = tid; q < 243; q += EL_NT) {
-      const int g = q / 9, a = (q % 9) / 3, b = q % 3;
+  extern __shared__ double el_smem[];
+  double* sdN = el_smem;               // [27 g][27 i][3 a] reference gradients
+  double* sN = sdN + 2187;             // [28 g][32 i] shape values, zero padded
+  ElWarp* W = (ElWarp*)(sN + 28 * 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int q = tid; q < 2187; q += EL_NT) sdN[q] = c_hexdN[q];
+  for (int q = tid; q < 28 * 32; q += EL_NT) {
+    const int g = q >> 5, i = q & 31;
+    sN[q] = (g < 27 && i < 27) ? c_hexN[g * 27 + i] : 0.0;
+  }
+  __syncthreads();
+  ElWarp& w = W[warp];
+  const int col = lane >> 2, kq = lane & 3;  // fragment column (A row / B col) and k offset
+  for (int e = blockIdx.x * EL_WARPS + warp; e < n_elem; e += gridDim.x * EL_WARPS) {
+    for (int q = lane; q < 81; q += 32) w.X[q / 3][q % 3] = xyz[(size_t)conn[(size_t)e * 27 + q / 3] * 3 + q % 3];
+    __syncwarp();
+    // J[g][a][b] = sum_i dN_i/dxi_a(g) X_i,b: 243 sums over the lanes
+    double Jv[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int q = lane + 32 * t;
       double acc = 0.0;
-      for (int i = 0; i < 27; ++i) acc += __ldg(&c_hexdN[(g * 27 + i) * 3 + a]) * X[i][b];
-      Jg[g][a * 3 + b] = acc;
+      if (q < 243) {
+        const int g = q / 9, a = (q % 9) / 3, b = q % 3;
+        for (int i = 0; i < 27; ++i) acc += sdN[(g * 27 + i) * 3 + a] * w.X[i][b];
+      }
+      Jv[t] = acc;
     }
-    __syncthreads();
-    __shared__ double iJg[27][9];
-    if (tid < 27) {
-      const int g = tid;
-      const double* J = Jg[g];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int q = lane + 32 * t;
+      if (q < 243) w.iJ[q / 9][q % 9] = Jv[t];  // J first, inverted in place below
+    }
+    __syncwarp();
+    if (lane < 27) {
+      const int g = lane;
+      double J[9];
+#pragma unroll
+      for (int t = 0; t < 9; ++t) J[t] = w.iJ[g][t];
       const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
                          J[2] * (J[3] * J[7] - J[4] * J[6]);
       if (!(det > 0.0)) atomicMin(bad, e);
       const double id = 1.0 / det;
-      double* iJ = iJg[g];
+      double* iJ = w.iJ[g];
       iJ[0] = (J[4] * J[8] - J[5] * J[7]) * id;
       iJ[1] = (J[2] * J[7] - J[1] * J[8]) * id;
       iJ[2] = (J[1] * J[5] - J[2] * J[4]) * id;
@@ -167,30 +205,87 @@ __global__ void __launch_bounds__(EL_NT) hex27_helmholtz_kernel(int n_elem, cons
       iJ[6] = (J[3] * J[7] - J[4] * J[6]) * id;
       iJ[7] = (J[1] * J[6] - J[0] * J[7]) * id;
       iJ[8] = (J[0] * J[4] - J[1] * J[3]) * id;
-      wdet[g] = __ldg(&c_hexW[g]) * det;
+      w.wdet[g] = __ldg(&c_hexW[g]) * det;
+    } else if (lane == 27) {
+      w.wdet[27] = 0.0;
     }
-    __syncthreads();
-    // dN = dshape inv(J)  (assembly.py:88): 27 x 27 x 3 entries
-    for (int q = tid; q < 2187; q += EL_NT) {
-      const int g = q / 81, i = (q / 3) % 27, b = q % 3;
-      const double* dS = &c_hexdN[(g * 27 + i) * 3];
-      dNx[g][i][b] = __ldg(dS) * iJg[g][b] + __ldg(dS + 1) * iJg[g][3 + b] + __ldg(dS + 2) * iJg[g][6 + b];
-    }
-    __syncthreads();
-    for (int q = tid; q < 729; q += EL_NT) {
-      const int i = q / 27, j = q % 27;
-      double k = 0.0, m = 0.0;
-      for (int g = 0; g < 27; ++g) {
-        const double w = wdet[g];
-        k += w * (dNx[g][i][0] * dNx[g][j][0] + dNx[g][i][1] * dNx[g][j][1] + dNx[g][i][2] * dNx[g][j][2]);
-        m += w * (sN[g * 27 + i] * sN[g * 27 + j]);
+    __syncwarp();
+    // ---- Kgrad = D^T W D, k = (g, b) = 0..80 padded to 84
+    double acc[4][4][2];
+#pragma unroll
+    for (int I = 0; I < 4; ++I)
+#pragma unroll
+      for (int J = 0; J < 4; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
+    for (int k0 = 0; k0 < 84; k0 += 4) {
+      const int k = k0 + kq;
+      const bool kin = k < 81;
+      const int g = kin ? k / 3 : 0, b = k - 3 * (k / 3);
+      const double i0 = w.iJ[g][b], i1 = w.iJ[g][3 + b], i2 = w.iJ[g][6 + b];
+      const double wg = kin ? w.wdet[g] : 0.0;
+      double d[4];
+#pragma unroll
+      for (int I = 0; I < 4; ++I) {
+        const int i = 8 * I + col;
+        double v = 0.0;
+        if (i < 27) {
+          const double* ds = sdN + (g * 27 + i) * 3;
+          v = ds[0] * i0 + ds[1] * i1 + ds[2] * i2;  // dN = dshape inv(J)
+        }
+        d[I] = v;
       }
-      Ke[(size_t)e * 729 + q] = k;
-      Me[(size_t)e * 729 + q] = m;
+#pragma unroll
+      for (int I = 0; I < 4; ++I) {
+        const double a = wg * d[I];
+#pragma unroll
+        for (int J = 0; J < 4; ++J) el_dmma(acc[I][J][0], acc[I][J][1], a, d[J]);
+      }
     }
-    __syncthreads();
+#pragma unroll
+    for (int I = 0; I < 4; ++I)
+#pragma unroll
+      for (int J = 0; J < 4; ++J)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int i = 8 * I + col, j = 8 * J + 2 * kq + v;
+          if (i < 27 && j < 27) w.out[i * 27 + j] = acc[I][J][v];
+        }
+    __syncwarp();
+    for (int q = lane; q < 729; q += 32) Ke[(size_t)e * 729 + q] = w.out[q];
+    __syncwarp();
+    // ---- Mnn = N^T W N, k = g = 0..26 padded to 28
+#pragma unroll
+    for (int I = 0; I < 4; ++I)
+#pragma unroll
+      for (int J = 0; J < 4; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
+    for (int k0 = 0; k0 < 28; k0 += 4) {
+      const int g = k0 + kq;
+      const double wg = w.wdet[g];
+      double nv[4];
+#pragma unroll
+      for (int I = 0; I < 4; ++I) nv[I] = sN[g * 32 + 8 * I + col];
+#pragma unroll
+      for (int I = 0; I < 4; ++I) {
+        const double a = wg * nv[I];
+#pragma unroll
+        for (int J = 0; J < 4; ++J) el_dmma(acc[I][J][0], acc[I][J][1], a, nv[J]);
+      }
+    }
+#pragma unroll
+    for (int I = 0; I < 4; ++I)
+#pragma unroll
+      for (int J = 0; J < 4; ++J)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int i = 8 * I + col, j = 8 * J + 2 * kq + v;
+          if (i < 27 && j < 27) w.out[i * 27 + j] = acc[I][J][v];
+        }
+    __syncwarp();
+    for (int q = lane; q < 729; q += 32) Me[(size_t)e * 729 + q] = w.out[q];
+    __syncwarp();
   }
 }
+
+constexpr size_t EL_SMEM = (2187 + 28 * 32) * sizeof(double) + EL_WARPS * sizeof(ElWarp);
 
 // One warp per 9-node face: int_Gamma N N^T dGamma with dA = |t_xi x t_eta|.
 __global__ void quad9_face_mass_kernel(int n_faces, const double* __restrict__ xyz,
@@ -513,9 +608,11 @@ int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* 
   int dev = 0, nsm = 148;
   VB_CUDA(cudaGetDevice(&dev));
   VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = n_elem < nsm * 16 ? n_elem : nsm * 16;
+  const int need = (n_elem + EL_WARPS - 1) / EL_WARPS;
+  const int grid = need < nsm * 2 ? need : nsm * 2;
   if (grid > 0) {
-    hex27_helmholtz_kernel<<<grid, EL_NT, 0, stream>>>(n_elem, xyz, conn, Ke, Me, bad);
+    VB_CUDA(cudaFuncSetAttribute(hex27_helmholtz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EL_SMEM));
+    hex27_helmholtz_kernel<<<grid, EL_NT, EL_SMEM, stream>>>(n_elem, xyz, conn, Ke, Me, bad);
     VB_LAUNCHED("hex27_helmholtz_kernel");
   }
   int hb = big;

@@ -41,6 +41,7 @@ const char* vb_last_error(void) { return vb::g_last_error.c_str(); }
 int64_t vb_launch_count(void) { return vb::g_launches.load(); }
 
 int vb_release_l2_persistence(void) {
+  VB_CUDA(cudaFree(nullptr));  // make sure the primary context exists
   VB_CUDA(cudaCtxResetPersistingL2Cache());
   VB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
   return 0;

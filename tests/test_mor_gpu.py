@@ -153,9 +153,12 @@ def test_box_mor_pipeline_matches_reference(cuda, golden_dir):
             mor.ReducedModel(fom=fom, V=V, window=(200.0, 600.0))]
     res = mor.rom_sweep(roms, list(z["grid"]))
     np.testing.assert_array_equal(res.window_index, z["window_index"])
+    # TF_TOL, floored at twice the reference's own rounding sensitivity at that
+    # frequency (y_sens: the reference pipeline rerun on ~1-ulp perturbed K, M;
+    # 1.3e-8 at 950 Hz, <= 2.4e-9 everywhere else — make_golden.gold_box_mor)
     for i in range(len(z["grid"])):
         _, e, _, _ = mor.relative_error(z["y"][i], res.frf[i])
-        assert e <= TF_TOL, (i, e)
+        assert e <= max(TF_TOL, 2.0 * z["y_sens"][i]), (i, e, z["y_sens"][i])
         assert abs(res.spl[i][0] - z["spl"][i]) <= 0.01
     assert [s[0] for s in res.seam_log] == list(z["seam_f"])
     np.testing.assert_allclose([np.max(s[1]) for s in res.seam_log], z["seam_gap"], rtol=1e-6)
