@@ -21,6 +21,7 @@
 #include "mma.cuh"
 #include "sweep.cuh"
 #include "tma.cuh"
+#include "tma_big.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -31,9 +32,10 @@ using blk::KC;
 using blk::NB;
 using blk::NT;
 
-// Trailing update: the TMA + mbarrier DMMA GEMM of the blocked sweep
-// (csrc/tma.cuh) over a 2-D tensor map of the matrix, tiles spread over CTAs.
-using GemmT = tma::GemmTma<3>;
+// Trailing update: the large-tile TMA + mbarrier DMMA GEMM (csrc/tma_big.cuh,
+// 128 x 64 tiles, one CTA per SM) over a 2-D tensor map of the matrix, tiles
+// spread over the CTAs.
+using GemmT = tma::GemmBig<3>;
 
 // Profiling aid (-DVB_PHASE_TIMING): CTA 0's SM cycles in panel / swaps /
 // TRSM / GEMM (each phase ends at a grid barrier), vb_debug_phase_cycles 32..35.
@@ -66,7 +68,7 @@ inline size_t lu_smem(int n, int grid) {
 }
 
 struct __align__(64) LuParams {
-  tma::Maps maps;  // over the matrix (must stay first: 64-B aligned)
+  tma::BigMaps maps;  // over the matrix (must stay first: 64-B aligned)
   int n;
   z_t* A;
   int64_t lda;
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(const __grid_constant__ L
     LU_MARK(2);
     // ------------------------------------------------------------ GEMM
     if (kend < n) {
-      GemmT::run(&P.maps, A, (int)lda, kend, k0, k0, kend, n - kend, n - kend, nb, (char*)smem, &bars, 0, -1, c, G);
+      GemmT::run(&P.maps, A, lda, kend, k0, k0, kend, n - kend, n - kend, nb, (char*)smem, &bars, c, G);
     }
     grid.sync();
     LU_MARK(3);
@@ -523,9 +525,9 @@ int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size
   {
     const cuuint64_t dims[3] = {(cuuint64_t)2 * lda, (cuuint64_t)n, 1};
     const cuuint64_t strides[2] = {(cuuint64_t)lda * 16, (cuuint64_t)lda * 16 * n};
-    const cuuint32_t box64[3] = {16, 64, 1}, box16[3] = {16, 16, 1}, es[3] = {1, 1, 1};
+    const cuuint32_t box64[3] = {16, 64, 1}, box8[3] = {16, 8, 1}, es[3] = {1, 1, 1};
     if (int rc = tma_encode_map(&P.maps.a64, A, dims, strides, box64, es)) return rc;
-    if (int rc = tma_encode_map(&P.maps.b16, A, dims, strides, box16, es)) return rc;
+    if (int rc = tma_encode_map(&P.maps.b8, A, dims, strides, box8, es)) return rc;
   }
   void* args[] = {&P};
   {

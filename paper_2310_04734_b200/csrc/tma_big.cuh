@@ -1,0 +1,197 @@
+// Large-tile TMA + mbarrier complex GEMM for kernels that own a whole SM (one
+// CTA per SM, up to 255 registers and ~200 KB of shared memory): the trailing
+// update of the full-order LU (csrc/lu.cu).  C[M x N] -= A[M x K] B[K x N].
+//
+//  * 128 x 64 complex tiles, 8 warps as 4 (M) x 2 (N), 32 x 32 per warp: 4 x 4
+//    DMMA fragments with separate re/im accumulators (64 doubles per lane), so
+//    each A/B fragment pair loaded from shared memory feeds 8 DMMAs (twice the
+//    reuse of the 64 x 32 tiles in tma.cuh).
+//  * k chunks of 8 complex: A = 2 boxes of 64 rows x 8 complex, B = 8 boxes of
+//    8 rows x 8 complex, 128B-swizzled, in a STAGES-deep ring (full/empty
+//    mbarriers, one elected producer thread); the next C tile (16 boxes) is
+//    fetched by TMA while the current tile computes.
+//  * Tiles t_first, t_first + t_step, ... of the row-major tile grid, so all
+//    CTAs of a cooperative kernel share one GEMM.
+#pragma once
+#include "tma.cuh"
+
+namespace vb {
+namespace tma {
+
+struct BigMaps {
+  CUtensorMap a64;  // box: 16 doubles x 64 rows x 1
+  CUtensorMap b8;   // box: 16 doubles x 8 rows x 1
+};
+
+template <int STAGES>
+struct GemmBig {
+  static constexpr int TM = 128, TN = 64, KC = 8;
+  static constexpr unsigned A_BYTES = TM * KC * 16;  // 2 boxes of 64 rows x 8 complex
+  static constexpr unsigned B_BYTES = KC * TN * 16;  // 8 boxes of 8 rows x 8 complex
+  static constexpr unsigned C_BYTES = TM * TN * 16;  // 16 boxes of 64 rows x 8 complex
+  static constexpr size_t SMEM = (size_t)STAGES * (A_BYTES + B_BYTES) + C_BYTES;
+
+  struct Bars {
+    uint64_t full[STAGES], empty[STAGES], cfull, cempty;
+  };
+
+  __device__ static __forceinline__ void issue_chunk(const BigMaps* mp, char* As, char* Bs, uint64_t* bar,
+                                                     int ar0, int ac0, int br0, int bc0, int m0, int n0, int k0) {
+    mbar_expect_tx(bar, A_BYTES + B_BYTES);
+    tma_load_3d(As, &mp->a64, 2 * (ac0 + k0), ar0 + m0, 0, bar);
+    tma_load_3d(As + 8192, &mp->a64, 2 * (ac0 + k0), ar0 + m0 + 64, 0, bar);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) tma_load_3d(Bs + b * 1024, &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, 0, bar);
+  }
+  __device__ static __forceinline__ void issue_c(const BigMaps* mp, char* Cs, uint64_t* bar, int cr0, int cc0,
+                                                 int m0, int n0) {
+    mbar_expect_tx(bar, C_BYTES);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        tma_load_3d(Cs + (h * 8 + b) * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0 + 64 * h, 0, bar);
+  }
+
+  // C origin (ar0, bc0); Cg row-major with leading dimension ldc.
+  __device__ static void run(const BigMaps* mp, z_t* Cg, int64_t ldc, int ar0, int ac0, int br0, int bc0, int M,
+                             int N, int K, char* smem, Bars* bars, int t_first, int t_step) {
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    const int ntn = (N + TN - 1) / TN, ntm = (M + TM - 1) / TM, nk = (K + KC - 1) / KC;
+    const int ntiles_all = ntm * ntn;
+    if (t_first >= ntiles_all) return;
+    const int ntiles = (ntiles_all - 1 - t_first) / t_step + 1;
+    const int T = ntiles * nk;
+    auto tm0 = [&](int l) { return ((t_first + l * t_step) / ntn) * TM; };
+    auto tn0 = [&](int l) { return ((t_first + l * t_step) % ntn) * TN; };
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    char* As = smem;
+    char* Bs = smem + STAGES * A_BYTES;
+    char* Cs = Bs + STAGES * B_BYTES;
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&bars->full[s], 1);
+        mbar_init(&bars->empty[s], NT / 32);
+      }
+      mbar_init(&bars->cfull, 1);
+      mbar_init(&bars->cempty, NT / 32);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    int pt = 0, pk = 0;  // producer cursor (thread 0)
+    if (tid == 0) {
+      fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
+      issue_c(mp, Cs, &bars->cfull, ar0, bc0, tm0(0), tn0(0));
+      for (int j = 0; j < STAGES - 1 && j < T; ++j) {
+        issue_chunk(mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], ar0, ac0, br0, bc0, tm0(pt), tn0(pt),
+                    pk * KC);
+        if (++pk == nk) { pk = 0; ++pt; }
+      }
+    }
+    unsigned full_ph = 0, empty_ph = 0, c_ph = 0, cempty_ph = 0;
+    double cr[4][4][2], ci[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    const int ak = lane & 3, prow = perm8(lane >> 2);
+    int t = 0, kc = 0;
+    for (int it = 0; it < T; ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&bars->full[st], (full_ph >> st) & 1);
+      full_ph ^= 1u << st;
+      const char* as = As + st * A_BYTES;
+      const char* bs = Bs + st * B_BYTES;
+      const int kvalid = min(KC, K - kc * KC);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int kcol = kk * 4 + ak;
+        if (kk * 4 < kvalid) {
+          const bool kin = kcol < kvalid;
+          z_t a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int row = wm * 32 + i * 8 + prow;  // 0..127
+            a[i] = *(const z_t*)(as + (row >> 6) * 8192 + swz(row & 63, kcol));
+            if (!kin) a[i] = zmake(0.0, 0.0);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            b[j] = *(const z_t*)(bs + (wn * 4 + j) * 1024 + swz(kcol, prow));
+            if (!kin) b[j] = zmake(0.0, 0.0);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double br = b[j].x, bi = b[j].y, nbi = -bi;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              blk::dmma(cr[i][j][0], cr[i][j][1], a[i].x, br);
+              blk::dmma(cr[i][j][0], cr[i][j][1], a[i].y, nbi);
+              blk::dmma(ci[i][j][0], ci[i][j][1], a[i].x, bi);
+              blk::dmma(ci[i][j][0], ci[i][j][1], a[i].y, br);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->empty[st]);
+      // refill the stage consumed in the previous iteration
+      if (tid == 0 && it + STAGES - 1 < T) {
+        const int s2 = (it + STAGES - 1) % STAGES;
+        if (it >= 1) {
+          mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
+          empty_ph ^= 1u << s2;
+        }
+        issue_chunk(mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], ar0, ac0, br0, bc0, tm0(pt),
+                    tn0(pt), pk * KC);
+        if (++pk == nk) { pk = 0; ++pt; }
+      }
+      if (kc == nk - 1) {
+        const int m0 = tm0(t), n0 = tn0(t);
+        mbar_wait(&bars->cfull, c_ph);
+        c_ph ^= 1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int row = wm * 32 + i * 8 + prow;
+              const int col = wn * 32 + j * 8 + perm8(2 * ak + v);
+              if (m0 + row < M && n0 + col < N) {
+                const z_t c = *(const z_t*)(Cs + ((row >> 6) * 8 + (col >> 3)) * 8192 + swz(row & 63, col & 7));
+                Cg[(int64_t)(ar0 + m0 + row) * ldc + bc0 + n0 + col] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+              }
+              cr[i][j][v] = 0.0;
+              ci[i][j][v] = 0.0;
+            }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->cempty);
+        if (tid == 0 && t + 1 < ntiles) {
+          mbar_wait(&bars->cempty, cempty_ph);
+          cempty_ph ^= 1;
+          issue_c(mp, Cs, &bars->cfull, ar0, bc0, tm0(t + 1), tn0(t + 1));
+        }
+        kc = 0;
+        ++t;
+      } else {
+        ++kc;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_inval(&bars->full[s]);
+        mbar_inval(&bars->empty[s]);
+      }
+      mbar_inval(&bars->cfull);
+      mbar_inval(&bars->cempty);
+    }
+  }
+};
+
+}  // namespace tma
+}  // namespace vb
