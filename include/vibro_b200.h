@@ -162,6 +162,18 @@ int vb_csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const
                 const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha,
                 vb_complex beta, void* stream);
 
+/* Y = alpha * Op X + beta * Y for the assembled primitives of a uniform hex27
+ * box WITHOUT the CSR: Op = Kx(x)My(x)Mz + Mx(x)Ky(x)Mz + Mx(x)My(x)Kz
+ * (stiff = 1, Kgrad) or Mx(x)My(x)Mz (stiff = 0, Mnn), the exact Kronecker
+ * form of the element sums; K1/M1 are the [3][maxnp][5] band tables of the 1D
+ * assembled matrices (x, y, z; entry o couples nodes i and i+o-2), the same
+ * tables vb_hex27_box_csr takes, so Op equals that CSR to rounding.  Grid of
+ * npx x npy x npz nodes, row (z npy + y) npx + x; X, Y complex n x k row-major.
+ * Replaces `P @ V` (mor.py:81-85, 117) for box primitives. */
+int vb_kron3_apply(int npx, int npy, int npz, const double* K1, const double* M1, int maxnp, int stiff, int k,
+                   vb_complex alpha, const vb_complex* X, int64_t ldx, vb_complex beta, vb_complex* Y,
+                   int64_t ldy, void* stream);
+
 /* D += alpha * A: scatter a scaled real CSR primitive into a dense complex
  * matrix (row-major, ldd) — assembles K - w^2 M + i w D at an expansion point
  * (vibrofem/mor.py:41-46) for the dense full-order LU. */

@@ -69,14 +69,31 @@ def interior_nodes(xyz: np.ndarray, box, tol=1e-12):
 
 # ----------------------------------------------------------------- CSR -----
 @dataclass
+class KronBox:
+    """Kronecker form of a uniform-box primitive (vb_kron3_apply): node grid,
+    [3][maxnp][5] band tables of the 1D stiffness/mass, stiff = Kgrad (1) or Mnn (0)."""
+
+    npx: int
+    npy: int
+    npz: int
+    K1: torch.Tensor
+    M1: torch.Tensor
+    maxnp: int
+    stiff: int
+
+
+@dataclass
 class DeviceCSR:
     """Square CSR on the device: int32 indptr/indices, float64 values (one
-    primitive) — the scipy canonical layout of assembly.py:172-173."""
+    primitive) — the scipy canonical layout of assembly.py:172-173.  `kron`,
+    when set, is the same operator in Kronecker form (uniform boxes): products
+    with it run matrix-free (linalg.spmm)."""
 
     n: int
     indptr: torch.Tensor
     indices: torch.Tensor
     data: torch.Tensor
+    kron: KronBox | None = None
 
     @property
     def nnz(self) -> int:
@@ -217,4 +234,6 @@ def assemble_helmholtz_box(box, ne, device=None):
     _lib.check(lib.vb_hex27_box_csr(nx, ny, nz, _lib.ptr(K1d), _lib.ptr(M1d), maxnp, _lib.ptr(indptr),
                                     _lib.ptr(indices), _lib.ptr(Kv), _lib.ptr(Mv), _lib.stream_handle()),
                "vb_hex27_box_csr")
-    return DeviceCSR(n, indptr, indices, Kv), DeviceCSR(n, indptr, indices, Mv)
+    grid = (2 * nx + 1, 2 * ny + 1, 2 * nz + 1)
+    return (DeviceCSR(n, indptr, indices, Kv, KronBox(*grid, K1d, M1d, maxnp, 1)),
+            DeviceCSR(n, indptr, indices, Mv, KronBox(*grid, K1d, M1d, maxnp, 0)))

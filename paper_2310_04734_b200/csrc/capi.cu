@@ -207,6 +207,14 @@ int vb_hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1,
   return vb::hex27_box_csr(nx, ny, nz, K1, M1, maxnp, indptr, indices, Kvals, Mvals, (cudaStream_t)stream);
 }
 
+int vb_kron3_apply(int npx, int npy, int npz, const double* K1, const double* M1, int maxnp, int stiff, int k,
+                   vb_complex alpha, const vb_complex* X, int64_t ldx, vb_complex beta, vb_complex* Y,
+                   int64_t ldy, void* stream) {
+  VB_CHECK_ARG(K1 && M1 && X && Y, "vb_kron3_apply: null pointer");
+  return vb::kron3_apply(npx, npy, npz, K1, M1, maxnp, stiff, k, zc(alpha), (const z_t*)X, ldx, zc(beta),
+                         (z_t*)Y, ldy, (cudaStream_t)stream);
+}
+
 int vb_debug_phase_cycles(unsigned long long* cycles_host, int reset) {
   VB_CHECK_ARG(cycles_host != nullptr, "vb_debug_phase_cycles: null output");
   return vb::sweep_debug_phase_cycles(cycles_host, reset);

@@ -28,6 +28,8 @@ size_t sweep_blocked_workspace_bytes(int r, int s, int n_out, int64_t F);
 int sweep_blocked_supported(int r, int s, int n_out);
 int sweep_debug_phase_cycles(unsigned long long* out_host, int reset);
 int lu_debug_cycles(unsigned long long* out, int reset);
+int kron3_apply(int npx, int npy, int npz, const double* K1, const double* M1, int maxnp, int stiff, int k,
+                z_t alpha, const z_t* X, int64_t ldx, z_t beta, z_t* Y, int64_t ldy, cudaStream_t st);
 int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_t* prims,
                          const z_t* alpha, const z_t* b, int64_t b_stride_f, const z_t* c_r, z_t* y,
                          double* spl, z_t* x, int* info, void* work, size_t work_bytes,

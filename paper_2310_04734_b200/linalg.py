@@ -25,7 +25,9 @@ def _cols(t: torch.Tensor) -> int:
 
 
 def spmm(A: DeviceCSR, X: torch.Tensor, alpha=1.0, beta=0.0, Y: torch.Tensor | None = None):
-    """Y = alpha A X + beta Y (A real CSR, X/Y complex)."""
+    """Y = alpha A X + beta Y (A real CSR, X/Y complex).  Uniform-box primitives
+    (A.kron set) with k >= 2 columns take the matrix-free Kronecker apply
+    (vb_kron3_apply; same operator to rounding), everything else the CSR SpMM."""
     lib = _lib.load()
     k = _cols(X)
     if Y is None:
@@ -33,6 +35,12 @@ def spmm(A: DeviceCSR, X: torch.Tensor, alpha=1.0, beta=0.0, Y: torch.Tensor | N
         beta = 0.0
     ldx = _ld(X) if X.dim() == 2 else 1
     ldy = _ld(Y) if Y.dim() == 2 else 1
+    kb = getattr(A, "kron", None)
+    if kb is not None and k >= 2:  # uniform-box primitive: matrix-free Kronecker apply
+        _lib.check(lib.vb_kron3_apply(kb.npx, kb.npy, kb.npz, _lib.ptr(kb.K1), _lib.ptr(kb.M1), kb.maxnp,
+                                      kb.stiff, k, _lib.zc(alpha), C_ptr(X), ldx, _lib.zc(beta), C_ptr(Y), ldy,
+                                      _lib.stream_handle()), "vb_kron3_apply")
+        return Y
     _lib.check(lib.vb_csr_spmm(A.n, _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(A.data), k,
                                C_ptr(X), ldx, C_ptr(Y), ldy, _lib.zc(alpha), _lib.zc(beta),
                                _lib.stream_handle()), "vb_csr_spmm")

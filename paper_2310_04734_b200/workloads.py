@@ -150,7 +150,10 @@ def cfg3_model(seed: int = 3, box=CFG3_BOX, ne=CFG3_NE, n_src: int = CFG3_NSRC, 
     src = np.sort(rng.choice(inner, n_src, replace=False)).astype(np.int64)
     rec = np.sort(rng.choice(np.setdiff1d(inner, src), n_rec, replace=False)).astype(np.int64)
     Zs = {w: AIR_RHO * AIR_C * float(rng.uniform(2.0, 10.0)) for w in CFG3_WALLS}
-    Kg, Mn = assembly.assemble_helmholtz(xyz, conn, device)
+    # structured box: the vb_hex27_box_csr CSR (same pattern as the general
+    # assembly, values to rounding) carrying the Kronecker form, so the
+    # projections P V run matrix-free (vb_kron3_apply)
+    Kg, Mn = assembly.assemble_helmholtz_box(box, ne, device)
     n = xyz.shape[0]
     D_terms = []
     for w, Z in Zs.items():

@@ -77,6 +77,17 @@ def measure():
         out[f"spmm_k{k}_ms"] = t
         out[f"spmm_k{k}_GBps"] = alg / (t * 1e-3) / 1e9
         out[f"spmm_k{k}_frac_hbm"] = out[f"spmm_k{k}_GBps"] / peak_hbm
+    # matrix-free Kronecker apply of the same primitive (uniform box): reads X and
+    # writes Y once (+ x-y halo); bytes = X + Y (the CSR is not read)
+    Kbox, _ = assembly.assemble_helmholtz_box(box, ne)
+    for k in (32, 400):
+        X = torch.randn(n, k, dtype=torch.complex128, device=dev)
+        t = timed(lambda: linalg.spmm(Kbox, X))
+        alg = 2 * n * k * 16
+        out[f"kron_k{k}_ms"] = t
+        out[f"kron_k{k}_GBps"] = alg / (t * 1e-3) / 1e9
+        out[f"kron_k{k}_frac_hbm"] = out[f"kron_k{k}_GBps"] / peak_hbm
+        out[f"kron_k{k}_speedup_vs_csr"] = out[f"spmm_k{k}_ms"] / t
     V = torch.randn(n, 400, dtype=torch.complex128, device=dev)
     W = torch.randn(n, 400, dtype=torch.complex128, device=dev)
     t = timed(lambda: linalg.zgemm("C", V, W))
