@@ -126,6 +126,11 @@ int vb_rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, dou
 int vb_csr_gather(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx,
                   const double* triplet_vals, double* vals, void* stream);
 
+/* The same for two primitives sharing the pattern (Kgrad, Mnn): one pass over
+ * the gather map. */
+int vb_csr_gather2(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx, const double* tv0,
+                   const double* tv1, double* vals0, double* vals1, void* stream);
+
 /* Unscaled Helmholtz integrals of 27-node hexahedra (vibrofem/assembly.py:77-91
  * generalised to 3D: J = dshape^T X, dN = dshape inv(J), 3x3x3 Gauss):
  *  xyz [n_nodes][3], conn [n_elem][27] (local node a + 3b + 9c),

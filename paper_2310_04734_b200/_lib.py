@@ -49,6 +49,8 @@ _SIGS = {
     "vb_rm_plate_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p]),
     "vb_csr_gather": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vb_csr_gather2": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p]),
     "vb_hex27_helmholtz_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.POINTER(C.c_int32), C.c_void_p]),
     "vb_hex27_box_nnz": (C.c_int64, [C.c_int, C.c_int, C.c_int]),

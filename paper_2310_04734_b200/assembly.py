@@ -128,6 +128,16 @@ class Pattern:
                                      _lib.stream_handle()), "vb_csr_gather")
         return DeviceCSR(self.n, self.indptr, self.indices, vals)
 
+    def gather2(self, tv0: torch.Tensor, tv1: torch.Tensor):
+        """Two primitives on this pattern in one pass over the gather map."""
+        lib = _lib.load()
+        v0 = torch.empty(self.nnz, dtype=torch.float64, device=self.indptr.device)
+        v1 = torch.empty_like(v0)
+        _lib.check(lib.vb_csr_gather2(self.nnz, _lib.ptr(self.gather_ptr), _lib.ptr(self.gather_idx),
+                                      _lib.ptr(tv0.contiguous()), _lib.ptr(tv1.contiguous()), _lib.ptr(v0),
+                                      _lib.ptr(v1), _lib.stream_handle()), "vb_csr_gather2")
+        return (DeviceCSR(self.n, self.indptr, self.indices, v0), DeviceCSR(self.n, self.indptr, self.indices, v1))
+
 
 def pattern_from_elements(n: int, conn_dev: torch.Tensor) -> Pattern:
     """vb_csr_pattern_from_elements: canonical CSR pattern + element-order gather map."""
@@ -183,7 +193,7 @@ def assemble_helmholtz(xyz, conn, device=None):
     conn_d = torch.as_tensor(np.ascontiguousarray(conn, dtype=np.int32), device=dev)
     pat = pattern_from_elements(xyz.shape[0], conn_d)
     Ke, Me = hex27_helmholtz(xyz_d, conn_d)
-    return pat.gather(Ke), pat.gather(Me)
+    return pat.gather2(Ke, Me)
 
 
 def assemble_face_mass(xyz, face_conn, device=None) -> DeviceCSR:

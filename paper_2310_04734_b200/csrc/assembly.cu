@@ -411,23 +411,47 @@ __global__ void __launch_bounds__(PL_NT) rm_plate_kernel(int n_elem, const doubl
   }
 }
 
+// Device flag for the "non-positive Jacobian" check (lowest bad element id):
+// one device int + one pinned host int for the whole process, reset with a
+// memset (0x7f7f7f7f > any element id) — no per-call allocation.
+__device__ int g_bad_elem;
+static int* bad_flag_dev() {
+  static int* p = nullptr;
+  if (!p) cudaGetSymbolAddress((void**)&p, g_bad_elem);
+  return p;
+}
+static int* bad_flag_host() {
+  static int* h = nullptr;
+  if (!h) cudaHostAlloc((void**)&h, sizeof(int), cudaHostAllocDefault);
+  return h;
+}
+static int bad_flag_reset(cudaStream_t stream) {
+  int* d = bad_flag_dev();
+  if (!d || !bad_flag_host()) {
+    set_error("bad-element flag allocation failed");
+    return 2;
+  }
+  VB_CUDA(cudaMemsetAsync(d, 0x7f, sizeof(int), stream));
+  return 0;
+}
+static int bad_flag_read(cudaStream_t stream, int32_t* out) {
+  int* h = bad_flag_host();
+  VB_CUDA(cudaMemcpyAsync(h, bad_flag_dev(), sizeof(int), cudaMemcpyDeviceToHost, stream));
+  VB_CUDA(cudaStreamSynchronize(stream));
+  *out = *h == 0x7f7f7f7f ? -1 : *h;
+  return 0;
+}
+
 int rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, double E, double nu, double rho, double t,
                       double* Ke, double* Me, int32_t* bad_elem_host, cudaStream_t stream) {
   if (int rc = init_tables()) return rc;
-  int* bad = nullptr;
-  VB_CUDA(cudaMallocAsync(&bad, sizeof(int), stream));
-  const int big = 0x7fffffff;
-  VB_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, stream));
+  if (int rc = bad_flag_reset(stream)) return rc;
   if (n_elem > 0) {
     const int grid = n_elem < 148 * 16 ? n_elem : 148 * 16;
-    rm_plate_kernel<<<grid, PL_NT, 0, stream>>>(n_elem, xyz, conn, E, nu, rho, t, Ke, Me, bad);
+    rm_plate_kernel<<<grid, PL_NT, 0, stream>>>(n_elem, xyz, conn, E, nu, rho, t, Ke, Me, bad_flag_dev());
     VB_LAUNCHED("rm_plate_kernel");
   }
-  int hb = big;
-  VB_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  VB_CUDA(cudaFreeAsync(bad, stream));
-  VB_CUDA(cudaStreamSynchronize(stream));
-  *bad_elem_host = hb == big ? -1 : hb;
+  if (int rc = bad_flag_read(stream, bad_elem_host)) return rc;
   return 0;
 }
 
@@ -490,6 +514,25 @@ __global__ void csr_gather_kernel(int64_t nnz, const int64_t* __restrict__ gptr,
   const int64_t b = gptr[s], e = gptr[s + 1];
   for (int64_t t = b; t < e; ++t) acc += __ldg(tv + gidx[t]);
   vals[s] = acc;
+}
+
+// Two primitives sharing one pattern (Kgrad and Mnn): the gather map is read
+// once for both.
+__global__ void csr_gather2_kernel(int64_t nnz, const int64_t* __restrict__ gptr,
+                                   const int32_t* __restrict__ gidx, const double* __restrict__ tv0,
+                                   const double* __restrict__ tv1, double* __restrict__ v0,
+                                   double* __restrict__ v1) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nnz) return;
+  double a0 = 0.0, a1 = 0.0;
+  const int64_t b = __ldg(gptr + s), e = __ldg(gptr + s + 1);
+  for (int64_t t = b; t < e; ++t) {
+    const int32_t g = __ldg(gidx + t);
+    a0 += __ldg(tv0 + g);
+    a1 += __ldg(tv1 + g);
+  }
+  v0[s] = a0;
+  v1[s] = a1;
 }
 
 // ------------------------------------------------------------- host side ---
@@ -589,6 +632,15 @@ int csr_pattern_from_elements(int n, int n_elem, int npe, const int32_t* conn, i
                                  work_bytes, stream);
 }
 
+int csr_gather2(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv0, const double* tv1,
+                double* v0, double* v1, cudaStream_t stream) {
+  if (nnz <= 0) return 0;
+  const int nt = 256;
+  csr_gather2_kernel<<<(unsigned)((nnz + nt - 1) / nt), nt, 0, stream>>>(nnz, gptr, gidx, tv0, tv1, v0, v1);
+  VB_LAUNCHED("csr_gather2_kernel");
+  return 0;
+}
+
 int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv, double* vals,
                cudaStream_t stream) {
   if (nnz <= 0) return 0;
@@ -601,10 +653,7 @@ int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const doub
 int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* Ke, double* Me,
                     int32_t* bad_elem_host, cudaStream_t stream) {
   if (int rc = init_tables()) return rc;
-  int* bad = nullptr;
-  VB_CUDA(cudaMallocAsync(&bad, sizeof(int), stream));
-  const int big = 0x7fffffff;
-  VB_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, stream));
+  if (int rc = bad_flag_reset(stream)) return rc;
   int dev = 0, nsm = 148;
   VB_CUDA(cudaGetDevice(&dev));
   VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -612,14 +661,10 @@ int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* 
   const int grid = need < nsm * 2 ? need : nsm * 2;
   if (grid > 0) {
     VB_CUDA(cudaFuncSetAttribute(hex27_helmholtz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EL_SMEM));
-    hex27_helmholtz_kernel<<<grid, EL_NT, EL_SMEM, stream>>>(n_elem, xyz, conn, Ke, Me, bad);
+    hex27_helmholtz_kernel<<<grid, EL_NT, EL_SMEM, stream>>>(n_elem, xyz, conn, Ke, Me, bad_flag_dev());
     VB_LAUNCHED("hex27_helmholtz_kernel");
   }
-  int hb = big;
-  VB_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  VB_CUDA(cudaFreeAsync(bad, stream));
-  VB_CUDA(cudaStreamSynchronize(stream));
-  *bad_elem_host = hb == big ? -1 : hb;
+  if (int rc = bad_flag_read(stream, bad_elem_host)) return rc;
   return 0;
 }
 

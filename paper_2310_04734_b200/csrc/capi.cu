@@ -110,6 +110,12 @@ int vb_rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, dou
   return vb::rm_plate_elements(n_elem, xyz, conn, E, nu, rho, t, Ke, Me, bad_elem_host, (cudaStream_t)stream);
 }
 
+int vb_csr_gather2(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx, const double* tv0,
+                   const double* tv1, double* vals0, double* vals1, void* stream) {
+  VB_CHECK_ARG(nnz >= 0, "vb_csr_gather2: bad nnz");
+  return vb::csr_gather2(nnz, gather_ptr, gather_idx, tv0, tv1, vals0, vals1, (cudaStream_t)stream);
+}
+
 int vb_csr_gather(int64_t nnz, const int64_t* gather_ptr, const int32_t* gather_idx,
                   const double* triplet_vals, double* vals, void* stream) {
   VB_CHECK_ARG(nnz >= 0, "vb_csr_gather: bad nnz");

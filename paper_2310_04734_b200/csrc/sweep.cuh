@@ -46,6 +46,8 @@ int csr_pattern_from_blocks(int n_rows, int n_cols, int n_elem, int nr, int nc, 
                             int64_t* nnz_host, void* work, size_t work_bytes, cudaStream_t stream);
 int rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, double E, double nu, double rho, double t,
                       double* Ke, double* Me, int32_t* bad_elem_host, cudaStream_t stream);
+int csr_gather2(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv0, const double* tv1,
+                double* v0, double* v1, cudaStream_t stream);
 int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const double* tv, double* vals,
                cudaStream_t stream);
 int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* Ke, double* Me,
