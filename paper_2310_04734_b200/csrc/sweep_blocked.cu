@@ -632,6 +632,8 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
     const cuuint32_t box64[3] = {16, 64, 1}, box16[3] = {16, 16, 1}, es[3] = {1, 1, 1};
     if (int rc = tma_encode_map(&P.maps.a64, work, dims, strides, box64, es)) return rc;
     if (int rc = tma_encode_map(&P.maps.b16, work, dims, strides, box16, es)) return rc;
+    const cuuint32_t box8[3] = {16, 8, 1};
+    if (int rc = tma_encode_map(&P.maps.b8, work, dims, strides, box8, es)) return rc;
   }
   const size_t smem = blk::smem_bytes(r, w);
   VB_CUDA(cudaFuncSetAttribute(blk::rom_sweep_blocked_kernel,

@@ -106,15 +106,19 @@ __device__ __forceinline__ unsigned swz(int row, int chunk) {
 struct Maps {
   CUtensorMap a64;  // box: 16 doubles x 64 rows x 1 CTA
   CUtensorMap b16;  // box: 16 doubles x 16 rows x 1 CTA
+  CUtensorMap b8;   // box: 16 doubles x 8 rows x 1 CTA
 };
 
 // C[M x N] -= A[M x K] B[K x N]; operand origins are (row, col) coordinates in
-// the CTA's workspace matrix.  TM = 64, TN = 32, KC = 16, 8 warps as 4 x 2.
-template <int STAGES>
+// the CTA's workspace matrix.  TM = 64, TN = 32, k chunks of KC_ (16 or 8)
+// complex, 8 warps as 4 x 2.
+template <int STAGES, int KC_ = 16>
 struct GemmTma {
-  static constexpr int TM = 64, TN = 32, KC = 16;
-  static constexpr unsigned A_BYTES = TM * KC * 16;   // 2 boxes of 64 rows x 8 complex
-  static constexpr unsigned B_BYTES = KC * TN * 16;   // 4 boxes of 16 rows x 8 complex
+  static constexpr int TM = 64, TN = 32, KC = KC_;
+  static_assert(KC == 16 || KC == 8, "k chunk of 8 or 16 complex");
+  static constexpr unsigned A_BYTES = TM * KC * 16;   // KC/8 boxes of 64 rows x 8 complex
+  static constexpr unsigned BBOX = KC * 128;          // B box: KC rows x 8 complex
+  static constexpr unsigned B_BYTES = KC * TN * 16;   // 4 boxes
   static constexpr unsigned C_BYTES = TM * TN * 16;   // 4 boxes of 64 rows x 8 complex
   static constexpr size_t SMEM = (size_t)STAGES * (A_BYTES + B_BYTES) + C_BYTES;
 
@@ -126,10 +130,11 @@ struct GemmTma {
   __device__ static __forceinline__ void issue_chunk(const Maps* mp, char* As, char* Bs, uint64_t* bar, int cta,
                                                      int ar0, int ac0, int br0, int bc0, int m0, int n0, int k0) {
     mbar_expect_tx(bar, A_BYTES + B_BYTES);
-    tma_load_3d(As, &mp->a64, 2 * (ac0 + k0), ar0 + m0, cta, bar);
-    tma_load_3d(As + 8192, &mp->a64, 2 * (ac0 + k0 + 8), ar0 + m0, cta, bar);
 #pragma unroll
-    for (int b = 0; b < 4; ++b) tma_load_3d(Bs + b * 2048, &mp->b16, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
+    for (int h = 0; h < KC / 8; ++h) tma_load_3d(As + h * 8192, &mp->a64, 2 * (ac0 + k0 + 8 * h), ar0 + m0, cta, bar);
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      tma_load_3d(Bs + b * BBOX, KC == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
   }
   __device__ static __forceinline__ void issue_c(const Maps* mp, char* Cs, uint64_t* bar, int cta, int cr0, int cc0,
                                                  int m0, int n0) {
@@ -142,19 +147,20 @@ struct GemmTma {
   // panel) are latency-bound on the C tile, so each ring stage carries a whole
   // tile — A (64 x 16), B (16 x 16) AND C (64 x 16) — and STAGES-1 tiles are in
   // flight while one computes.  8 warps x (8 rows x 16 columns).
-  static constexpr unsigned SK_B = 2 * 2048, SK_C = 2 * 8192;
-  static constexpr unsigned SK_STAGE = A_BYTES + SK_B + SK_C;
-  static constexpr size_t SMEM_SKINNY = (size_t)STAGES * SK_STAGE;
+  static constexpr unsigned SK_A = 2 * 8192, SK_B = 2 * 2048, SK_C = 2 * 8192;
+  static constexpr unsigned SK_STAGE = SK_A + SK_B + SK_C;
+  static constexpr int SK_STAGES = 3;
+  static constexpr size_t SMEM_SKINNY = (size_t)SK_STAGES * SK_STAGE;
 
   __device__ static __forceinline__ void issue_tile(const Maps* mp, char* st, uint64_t* bar, int cta, int ar0,
                                                     int ac0, int br0, int bc0, int cr0, int m0) {
     mbar_expect_tx(bar, SK_STAGE);
     tma_load_3d(st, &mp->a64, 2 * ac0, ar0 + m0, cta, bar);
     tma_load_3d(st + 8192, &mp->a64, 2 * (ac0 + 8), ar0 + m0, cta, bar);
-    tma_load_3d(st + A_BYTES, &mp->b16, 2 * bc0, br0, cta, bar);
-    tma_load_3d(st + A_BYTES + 2048, &mp->b16, 2 * (bc0 + 8), br0, cta, bar);
-    tma_load_3d(st + A_BYTES + SK_B, &mp->a64, 2 * bc0, cr0 + m0, cta, bar);
-    tma_load_3d(st + A_BYTES + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), cr0 + m0, cta, bar);
+    tma_load_3d(st + SK_A, &mp->b16, 2 * bc0, br0, cta, bar);
+    tma_load_3d(st + SK_A + 2048, &mp->b16, 2 * (bc0 + 8), br0, cta, bar);
+    tma_load_3d(st + SK_A + SK_B, &mp->a64, 2 * bc0, cr0 + m0, cta, bar);
+    tma_load_3d(st + SK_A + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), cr0 + m0, cta, bar);
   }
 
   __device__ static void run_skinny(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int cr0,
@@ -164,7 +170,7 @@ struct GemmTma {
     GT_BEGIN;
     if (tid == 0) {
 #pragma unroll
-      for (int s = 0; s < STAGES; ++s) {
+      for (int s = 0; s < SK_STAGES; ++s) {
         mbar_init(&bars->full[s], 1);
         mbar_init(&bars->empty[s], NT / 32);
       }
@@ -173,7 +179,7 @@ struct GemmTma {
     __syncthreads();
     if (tid == 0) {
       fence_proxy_async_global();
-      for (int j = 0; j < STAGES - 1 && j < ntiles; ++j)
+      for (int j = 0; j < SK_STAGES - 1 && j < ntiles; ++j)
         issue_tile(mp, smem + j * SK_STAGE, &bars->full[j], cta, ar0, ac0, br0, bc0, cr0, j * TM);
     }
     unsigned full_ph = 0, empty_ph = 0;
@@ -182,12 +188,12 @@ struct GemmTma {
     const int k4n = (K + 3) >> 2;
     GS_MARK(0);
     for (int t = 0; t < ntiles; ++t) {
-      const int st = t % STAGES;
+      const int st = t % SK_STAGES;
       mbar_wait(&bars->full[st], (full_ph >> st) & 1);
       full_ph ^= 1u << st;
       if (t == 0) GS_MARK(1); else GS_MARK(2);
       const char* as = smem + st * SK_STAGE;
-      const char* bs = as + A_BYTES;
+      const char* bs = as + SK_A;
       const char* cs = bs + SK_B;
       double cr[2][2], ci[2][2];
 #pragma unroll
@@ -221,14 +227,14 @@ struct GemmTma {
       __syncwarp();
       GS_MARK(3);
       if (lane == 0) mbar_arrive(&bars->empty[st]);
-      if (tid == 0 && t + STAGES - 1 < ntiles) {
-        const int s2 = (t + STAGES - 1) % STAGES;
+      if (tid == 0 && t + SK_STAGES - 1 < ntiles) {
+        const int s2 = (t + SK_STAGES - 1) % SK_STAGES;
         if (t >= 1) {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
           empty_ph ^= 1u << s2;
         }
         issue_tile(mp, smem + s2 * SK_STAGE, &bars->full[s2], cta, ar0, ac0, br0, bc0, cr0,
-                   (t + STAGES - 1) * TM);
+                   (t + SK_STAGES - 1) * TM);
       }
       GS_MARK(4);
     }
@@ -236,7 +242,7 @@ struct GemmTma {
     GS_MARK(5);
     if (tid == 0) {
 #pragma unroll
-      for (int s = 0; s < STAGES; ++s) {
+      for (int s = 0; s < SK_STAGES; ++s) {
         mbar_inval(&bars->full[s]);
         mbar_inval(&bars->empty[s]);
       }
@@ -253,7 +259,7 @@ struct GemmTma {
                              int t_step = 1) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int cr0 = cr0_ < 0 ? ar0 : cr0_;
-    if (K <= KC && N <= 16 && t_step == 1) {
+    if (K <= 16 && N <= 16 && t_step == 1) {
       run_skinny(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
       return;
     }
@@ -325,7 +331,7 @@ struct GemmTma {
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          b[j] = *(const z_t*)(bs + (wn * 2 + j) * 2048 + swz(kcol, prow));
+          b[j] = *(const z_t*)(bs + (wn * 2 + j) * BBOX + swz(kcol, prow));
           if (!kin) b[j] = zmake(0.0, 0.0);
         }
 #pragma unroll
