@@ -96,6 +96,28 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Warp-collective forms: called by ALL lanes of one warp with identical
+// operands; one elected lane performs the operation.  Keeping the producer in
+// warp-uniform control flow lets ptxas hold the coordinates in uniform
+// registers (a single-thread `if (tid == 0)` producer compiles every UTMALDG
+// into an R2UR waterfall loop, ~140 cycles per box).
+__device__ __forceinline__ void mbar_expect_tx_w(uint64_t* b, unsigned bytes) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b64 st;\n elect.sync _|p, 0xffffffff;\n"
+      " @p mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(b)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_w(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                              uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+      " @p cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n}\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ int perm8(int x) { return (x >> 1) | ((x & 1) << 2); }
 
 // byte offset of complex element (row, chunk) inside a 128B-swizzled box
@@ -129,18 +151,18 @@ struct GemmTma {
   // issue the A and B boxes of chunk (m0, n0, k0) into stage st
   __device__ static __forceinline__ void issue_chunk(const Maps* mp, char* As, char* Bs, uint64_t* bar, int cta,
                                                      int ar0, int ac0, int br0, int bc0, int m0, int n0, int k0) {
-    mbar_expect_tx(bar, A_BYTES + B_BYTES);
+    mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
 #pragma unroll
-    for (int h = 0; h < KC / 8; ++h) tma_load_3d(As + h * 8192, &mp->a64, 2 * (ac0 + k0 + 8 * h), ar0 + m0, cta, bar);
+    for (int h = 0; h < KC / 8; ++h) tma_load_3d_w(As + h * 8192, &mp->a64, 2 * (ac0 + k0 + 8 * h), ar0 + m0, cta, bar);
 #pragma unroll
     for (int b = 0; b < 4; ++b)
-      tma_load_3d(Bs + b * BBOX, KC == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
+      tma_load_3d_w(Bs + b * BBOX, KC == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
   }
   __device__ static __forceinline__ void issue_c(const Maps* mp, char* Cs, uint64_t* bar, int cta, int cr0, int cc0,
                                                  int m0, int n0) {
-    mbar_expect_tx(bar, C_BYTES);
+    mbar_expect_tx_w(bar, C_BYTES);
 #pragma unroll
-    for (int b = 0; b < 4; ++b) tma_load_3d(Cs + b * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0, cta, bar);
+    for (int b = 0; b < 4; ++b) tma_load_3d_w(Cs + b * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0, cta, bar);
   }
 
   // Skinny updates (K <= KC, N <= 16: the in-panel updates of the recursive
@@ -154,13 +176,13 @@ struct GemmTma {
 
   __device__ static __forceinline__ void issue_tile(const Maps* mp, char* st, uint64_t* bar, int cta, int ar0,
                                                     int ac0, int br0, int bc0, int cr0, int m0) {
-    mbar_expect_tx(bar, SK_STAGE);
-    tma_load_3d(st, &mp->a64, 2 * ac0, ar0 + m0, cta, bar);
-    tma_load_3d(st + 8192, &mp->a64, 2 * (ac0 + 8), ar0 + m0, cta, bar);
-    tma_load_3d(st + SK_A, &mp->b16, 2 * bc0, br0, cta, bar);
-    tma_load_3d(st + SK_A + 2048, &mp->b16, 2 * (bc0 + 8), br0, cta, bar);
-    tma_load_3d(st + SK_A + SK_B, &mp->a64, 2 * bc0, cr0 + m0, cta, bar);
-    tma_load_3d(st + SK_A + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), cr0 + m0, cta, bar);
+    mbar_expect_tx_w(bar, SK_STAGE);
+    tma_load_3d_w(st, &mp->a64, 2 * ac0, ar0 + m0, cta, bar);
+    tma_load_3d_w(st + 8192, &mp->a64, 2 * (ac0 + 8), ar0 + m0, cta, bar);
+    tma_load_3d_w(st + SK_A, &mp->b16, 2 * bc0, br0, cta, bar);
+    tma_load_3d_w(st + SK_A + 2048, &mp->b16, 2 * (bc0 + 8), br0, cta, bar);
+    tma_load_3d_w(st + SK_A + SK_B, &mp->a64, 2 * bc0, cr0 + m0, cta, bar);
+    tma_load_3d_w(st + SK_A + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), cr0 + m0, cta, bar);
   }
 
   __device__ static void run_skinny(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int cr0,
@@ -177,7 +199,7 @@ struct GemmTma {
       mbar_fence_init();
     }
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {  // warp-collective producer (see tma_load_3d_w)
       fence_proxy_async_global();
       for (int j = 0; j < SK_STAGES - 1 && j < ntiles; ++j)
         issue_tile(mp, smem + j * SK_STAGE, &bars->full[j], cta, ar0, ac0, br0, bc0, cr0, j * TM);
@@ -227,7 +249,7 @@ struct GemmTma {
       __syncwarp();
       GS_MARK(3);
       if (lane == 0) mbar_arrive(&bars->empty[st]);
-      if (tid == 0 && t + SK_STAGES - 1 < ntiles) {
+      if (warp == 0 && t + SK_STAGES - 1 < ntiles) {
         const int s2 = (t + SK_STAGES - 1) % SK_STAGES;
         if (t >= 1) {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
@@ -289,9 +311,9 @@ struct GemmTma {
       mbar_fence_init();
     }
     __syncthreads();
-    // producer cursor (thread 0 only)
+    // producer cursor (warp 0, warp-collective issue)
     int pt = 0, pk = 0;
-    if (tid == 0) {
+    if (warp == 0) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
       issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(0), tn0(0));
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
@@ -350,7 +372,7 @@ struct GemmTma {
       GT_MARK(1);
       if (lane == 0) mbar_arrive(&bars->empty[st]);
       // refill the stage consumed in the previous iteration
-      if (tid == 0 && it + STAGES - 1 < T) {
+      if (warp == 0 && it + STAGES - 1 < T) {
         const int s2 = (it + STAGES - 1) % STAGES;
         if (it >= 1) {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
@@ -383,7 +405,7 @@ struct GemmTma {
             }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->cempty);
-        if (tid == 0 && t + 1 < ntiles) {
+        if (warp == 0 && t + 1 < ntiles) {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
           fence_proxy_async_global();

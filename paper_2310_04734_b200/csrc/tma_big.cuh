@@ -37,20 +37,20 @@ struct GemmBig {
 
   __device__ static __forceinline__ void issue_chunk(const BigMaps* mp, char* As, char* Bs, uint64_t* bar,
                                                      int ar0, int ac0, int br0, int bc0, int m0, int n0, int k0) {
-    mbar_expect_tx(bar, A_BYTES + B_BYTES);
-    tma_load_3d(As, &mp->a64, 2 * (ac0 + k0), ar0 + m0, 0, bar);
-    tma_load_3d(As + 8192, &mp->a64, 2 * (ac0 + k0), ar0 + m0 + 64, 0, bar);
+    mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
+    tma_load_3d_w(As, &mp->a64, 2 * (ac0 + k0), ar0 + m0, 0, bar);
+    tma_load_3d_w(As + 8192, &mp->a64, 2 * (ac0 + k0), ar0 + m0 + 64, 0, bar);
 #pragma unroll
-    for (int b = 0; b < 8; ++b) tma_load_3d(Bs + b * 1024, &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, 0, bar);
+    for (int b = 0; b < 8; ++b) tma_load_3d_w(Bs + b * 1024, &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, 0, bar);
   }
   __device__ static __forceinline__ void issue_c(const BigMaps* mp, char* Cs, uint64_t* bar, int cr0, int cc0,
                                                  int m0, int n0) {
-    mbar_expect_tx(bar, C_BYTES);
+    mbar_expect_tx_w(bar, C_BYTES);
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int b = 0; b < 8; ++b)
-        tma_load_3d(Cs + (h * 8 + b) * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0 + 64 * h, 0, bar);
+        tma_load_3d_w(Cs + (h * 8 + b) * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0 + 64 * h, 0, bar);
   }
 
   // C origin (ar0, bc0); Cg row-major with leading dimension ldc.
@@ -80,8 +80,8 @@ struct GemmBig {
       mbar_fence_init();
     }
     __syncthreads();
-    int pt = 0, pk = 0;  // producer cursor (thread 0)
-    if (tid == 0) {
+    int pt = 0, pk = 0;  // producer cursor (warp 0, warp-collective issue)
+    if (warp == 0) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
       issue_c(mp, Cs, &bars->cfull, ar0, bc0, tm0(0), tn0(0));
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
@@ -138,7 +138,7 @@ struct GemmBig {
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->empty[st]);
       // refill the stage consumed in the previous iteration
-      if (tid == 0 && it + STAGES - 1 < T) {
+      if (warp == 0 && it + STAGES - 1 < T) {
         const int s2 = (it + STAGES - 1) % STAGES;
         if (it >= 1) {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
@@ -169,7 +169,7 @@ struct GemmBig {
             }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->cempty);
-        if (tid == 0 && t + 1 < ntiles) {
+        if (warp == 0 && t + 1 < ntiles) {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
           issue_c(mp, Cs, &bars->cfull, ar0, bc0, tm0(t + 1), tn0(t + 1));
