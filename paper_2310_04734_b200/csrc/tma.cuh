@@ -148,15 +148,23 @@ struct GemmTma {
     uint64_t full[STAGES], empty[STAGES], cfull, cempty;
   };
 
-  // issue the A and B boxes of chunk (m0, n0, k0) into stage st
-  __device__ static __forceinline__ void issue_chunk(const Maps* mp, char* As, char* Bs, uint64_t* bar, int cta,
-                                                     int ar0, int ac0, int br0, int bc0, int m0, int n0, int k0) {
-    mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
+  // issue the A and B boxes of chunk (m0, n0, k0) into stage st.  Split over
+  // two producer warps: warp 0 arms the barrier with the whole stage's bytes and
+  // loads A, warp 1 loads B (a complete-tx may precede the expect-tx: the phase
+  // cannot complete before warp 0's arrival).
+  __device__ static __forceinline__ void issue_chunk_part(int part, const Maps* mp, char* As, char* Bs,
+                                                          uint64_t* bar, int cta, int ar0, int ac0, int br0, int bc0,
+                                                          int m0, int n0, int k0) {
+    if (part == 0) {
+      mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
 #pragma unroll
-    for (int h = 0; h < KC / 8; ++h) tma_load_3d_w(As + h * 8192, &mp->a64, 2 * (ac0 + k0 + 8 * h), ar0 + m0, cta, bar);
+      for (int h = 0; h < KC / 8; ++h)
+        tma_load_3d_w(As + h * 8192, &mp->a64, 2 * (ac0 + k0 + 8 * h), ar0 + m0, cta, bar);
+    } else {
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-      tma_load_3d_w(Bs + b * BBOX, KC == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
+      for (int b = 0; b < 4; ++b)
+        tma_load_3d_w(Bs + b * BBOX, KC == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
+    }
   }
   __device__ static __forceinline__ void issue_c(const Maps* mp, char* Cs, uint64_t* bar, int cta, int cr0, int cc0,
                                                  int m0, int n0) {
@@ -311,14 +319,14 @@ struct GemmTma {
       mbar_fence_init();
     }
     __syncthreads();
-    // producer cursor (warp 0, warp-collective issue)
+    // producer cursor (warps 0 and 1, warp-collective issue)
     int pt = 0, pk = 0;
-    if (warp == 0) {
+    if (warp <= 1) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
-      issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(0), tn0(0));
+      if (warp == 0) issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(0), tn0(0));
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
-        issue_chunk(mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], cta, ar0, ac0, br0, bc0,
-                    tm0(pt), tn0(pt), pk * KC);
+        issue_chunk_part(warp, mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], cta, ar0, ac0, br0, bc0,
+                         tm0(pt), tn0(pt), pk * KC);
         if (++pk == nk) { pk = 0; ++pt; }
       }
     }
@@ -372,14 +380,14 @@ struct GemmTma {
       GT_MARK(1);
       if (lane == 0) mbar_arrive(&bars->empty[st]);
       // refill the stage consumed in the previous iteration
-      if (warp == 0 && it + STAGES - 1 < T) {
+      if (warp <= 1 && it + STAGES - 1 < T) {
         const int s2 = (it + STAGES - 1) % STAGES;
         if (it >= 1) {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
           empty_ph ^= 1u << s2;
         }
-        issue_chunk(mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], cta, ar0, ac0, br0, bc0,
-                    tm0(pt), tn0(pt), pk * KC);
+        issue_chunk_part(warp, mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], cta, ar0, ac0, br0, bc0,
+                         tm0(pt), tn0(pt), pk * KC);
         if (++pk == nk) { pk = 0; ++pt; }
       }
       GT_MARK(2);
