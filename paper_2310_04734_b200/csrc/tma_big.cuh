@@ -8,8 +8,9 @@
 //    reuse of the 64 x 32 tiles in tma.cuh).
 //  * k chunks of 8 complex: A = 2 boxes of 64 rows x 8 complex, B = 8 boxes of
 //    8 rows x 8 complex, 128B-swizzled, in a STAGES-deep ring (full/empty
-//    mbarriers, one elected producer thread); the next C tile (16 boxes) is
-//    fetched by TMA while the current tile computes.
+//    mbarriers; the box issue is spread over 4 producer warps, each issuing
+//    warp-collectively); the next C tile (16 boxes) is fetched by TMA while
+//    the current tile computes.
 //  * Tiles t_first, t_first + t_step, ... of the row-major tile grid, so all
 //    CTAs of a cooperative kernel share one GEMM.
 #pragma once
@@ -35,22 +36,29 @@ struct GemmBig {
     uint64_t full[STAGES], empty[STAGES], cfull, cempty;
   };
 
-  __device__ static __forceinline__ void issue_chunk(const BigMaps* mp, char* As, char* Bs, uint64_t* bar,
-                                                     int ar0, int ac0, int br0, int bc0, int m0, int n0, int k0) {
-    mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
-    tma_load_3d_w(As, &mp->a64, 2 * (ac0 + k0), ar0 + m0, 0, bar);
-    tma_load_3d_w(As + 8192, &mp->a64, 2 * (ac0 + k0), ar0 + m0 + 64, 0, bar);
-#pragma unroll
-    for (int b = 0; b < 8; ++b) tma_load_3d_w(Bs + b * 1024, &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, 0, bar);
+  // Producer work split over PW warps (warp-collective issue; warp 0 arms the
+  // barrier with the whole transfer, a complete-tx may precede it).
+  static constexpr int PW = 4;
+  __device__ static __forceinline__ void issue_chunk(int part, const BigMaps* mp, char* As, char* Bs,
+                                                     uint64_t* bar, int ar0, int ac0, int br0, int bc0, int m0,
+                                                     int n0, int k0) {
+    if (part == 0) {
+      mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
+      tma_load_3d_w(As, &mp->a64, 2 * (ac0 + k0), ar0 + m0, 0, bar);
+      tma_load_3d_w(As + 8192, &mp->a64, 2 * (ac0 + k0), ar0 + m0 + 64, 0, bar);
+    } else {
+      // warps 1..3: B boxes part-1, part+2, ... (8 boxes of 8 rows x 8 complex)
+      for (int b = part - 1; b < 8; b += PW - 1)
+        tma_load_3d_w(Bs + b * 1024, &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, 0, bar);
+    }
   }
-  __device__ static __forceinline__ void issue_c(const BigMaps* mp, char* Cs, uint64_t* bar, int cr0, int cc0,
-                                                 int m0, int n0) {
-    mbar_expect_tx_w(bar, C_BYTES);
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        tma_load_3d_w(Cs + (h * 8 + b) * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0 + 64 * h, 0, bar);
+  __device__ static __forceinline__ void issue_c(int part, const BigMaps* mp, char* Cs, uint64_t* bar, int cr0,
+                                                 int cc0, int m0, int n0) {
+    if (part == 0) mbar_expect_tx_w(bar, C_BYTES);
+    for (int q = part; q < 16; q += PW) {  // 16 boxes of 64 rows x 8 complex
+      const int h = q >> 3, b = q & 7;
+      tma_load_3d_w(Cs + q * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0 + 64 * h, 0, bar);
+    }
   }
 
   // C origin (ar0, bc0); Cg row-major with leading dimension ldc.
@@ -80,13 +88,13 @@ struct GemmBig {
       mbar_fence_init();
     }
     __syncthreads();
-    int pt = 0, pk = 0;  // producer cursor (warp 0, warp-collective issue)
-    if (warp == 0) {
+    int pt = 0, pk = 0;  // producer cursor (warps 0..PW-1, warp-collective issue)
+    if (warp < PW) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
-      issue_c(mp, Cs, &bars->cfull, ar0, bc0, tm0(0), tn0(0));
+      issue_c(warp, mp, Cs, &bars->cfull, ar0, bc0, tm0(0), tn0(0));
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
-        issue_chunk(mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], ar0, ac0, br0, bc0, tm0(pt), tn0(pt),
-                    pk * KC);
+        issue_chunk(warp, mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], ar0, ac0, br0, bc0, tm0(pt),
+                    tn0(pt), pk * KC);
         if (++pk == nk) { pk = 0; ++pt; }
       }
     }
@@ -138,13 +146,13 @@ struct GemmBig {
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->empty[st]);
       // refill the stage consumed in the previous iteration
-      if (warp == 0 && it + STAGES - 1 < T) {
+      if (warp < PW && it + STAGES - 1 < T) {
         const int s2 = (it + STAGES - 1) % STAGES;
         if (it >= 1) {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
           empty_ph ^= 1u << s2;
         }
-        issue_chunk(mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], ar0, ac0, br0, bc0, tm0(pt),
+        issue_chunk(warp, mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], ar0, ac0, br0, bc0, tm0(pt),
                     tn0(pt), pk * KC);
         if (++pk == nk) { pk = 0; ++pt; }
       }
@@ -169,10 +177,10 @@ struct GemmBig {
             }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->cempty);
-        if (warp == 0 && t + 1 < ntiles) {
+        if (warp < PW && t + 1 < ntiles) {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
-          issue_c(mp, Cs, &bars->cfull, ar0, bc0, tm0(t + 1), tn0(t + 1));
+          issue_c(warp, mp, Cs, &bars->cfull, ar0, bc0, tm0(t + 1), tn0(t + 1));
         }
         kc = 0;
         ++t;
