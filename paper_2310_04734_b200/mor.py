@@ -106,6 +106,7 @@ class FullOrderModel:
     affine: AffineOperator | None = None
     fdm: object = None            # fdm.BoxFDM for structured boxes (cfg3-size solves)
     prefer_fdm: bool = False
+    schur: object = None  # schur.CoupledBoxSchur: structure + box cavity (cfg2)
 
     def __post_init__(self):
         if self.affine is not None:
@@ -162,10 +163,13 @@ class FullOrderModel:
         return b.view(-1, 1) if b.dim() == 1 else b.contiguous()
 
     def factor(self, f: float):
-        """GPU factorisation of A(f): dense LU (n <= DENSE_MAX_N) or the
-        fast-diagonalisation solver of a structured box (any n)."""
+        """GPU factorisation of A(f): dense LU (n <= DENSE_MAX_N), the
+        fast-diagonalisation solver of a structured box (any n), or a Schur
+        complement on a structure coupled to a box cavity (schur.py)."""
         if self.fdm is not None and (self.prefer_fdm or self.n > DENSE_MAX_N):
             return self.fdm.factor(f, self)
+        if self.schur is not None:  # Schur complement on the structure, FDM cavity
+            return RefinedSolver(self.schur.factor(f), self, f)
         if self.n > DENSE_MAX_N:
             raise RuntimeError(f"n = {self.n} exceeds the dense GPU LU limit ({DENSE_MAX_N}); "
                                "attach a BoxFDM solver (FullOrderModel.fdm)")

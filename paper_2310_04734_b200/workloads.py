@@ -180,7 +180,8 @@ CFG2_POINTS = (60.0, 140.0, 220.0, 300.0, 380.0, 460.0)  # sextile midpoints of 
 CFG2_MOMENTS = 10
 
 
-def cfg2_model(seed: int = 2, box=CFG2_BOX, ne=CFG2_NE, n_rec: int = CFG1_NREC, device=None):
+def cfg2_model(seed: int = 2, box=CFG2_BOX, ne=CFG2_NE, n_rec: int = CFG1_NREC, device=None,
+               use_schur: bool = True):
     """cfg2 (BASELINE configs[1]): clamped 0.8 x 0.6 m, 3 mm CFRP-like plate of
     16 x 12 9-node Reissner-Mindlin + membrane elements on top of a 0.8 x 0.6 x 0.5 m
     air cavity of 16 x 12 x 10 hex27 (conforming wet face), eta(f) = 0.01 + 2e-5 f
@@ -229,7 +230,11 @@ def cfg2_model(seed: int = 2, box=CFG2_BOX, ne=CFG2_NE, n_rec: int = CFG1_NREC, 
            AffineTerm(Fsf, -sgn)],
         M=[AffineTerm(Mn, 1.0 / (AIR_RHO * AIR_C * AIR_C)), AffineTerm(Mp, 1.0), AffineTerm(Ffs, AIR_RHO * sgn)],
         D=[], load=load)
-    fom = FullOrderModel(c_out=Cmat, n=n, affine=aff)
+    # cavity block = box operator with rigid walls -> Schur complement on the plate
+    from .fdm import BoxFDM
+    from .schur import CoupledBoxSchur
+    schur = CoupledBoxSchur(aff, n_p, BoxFDM(box, ne, AIR_RHO, AIR_C, {}), dev) if use_schur else None
+    fom = FullOrderModel(c_out=Cmat, n=n, affine=aff, schur=schur)
     return fom, {"n_plate": n_p, "n_fluid": n_f, "rec": rec, "dmap": dmap, "pxyz": pxyz, "pconn": pconn,
                  "xyz_f": xyz_f, "conn_f": conn_f, "fconn": fconn, "Kg": Kg, "Mn": Mn, "Kp": Kp, "Mp": Mp,
                  "Fsf": Fsf, "Ffs": Ffs, "load": load, "freqs": np.arange(20.0, 500.0 + 1e-9, 0.5),

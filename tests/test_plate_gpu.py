@@ -73,10 +73,18 @@ def test_cfg2_small_chain_matches_oracle(cuda):
     rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 500.0))
     grid = list(np.arange(20.0, 500.1, 40.0))
     res = mor.rom_sweep([rom], grid)
+    # the oracle's own rounding sensitivity on these inputs: the same reduction
+    # with V perturbed by ~1 ulp (2 seeded trials); near the coupled system's
+    # resonances it reaches the 1e-8 level (cond(A) ~ 2e12), so the tolerance is
+    # floored at 4x that noise
+    rng = np.random.default_rng(0)
+    Vp = [Vh * (1 + 2.2e-16 * (rng.standard_normal(Vh.shape) + 1j * rng.standard_normal(Vh.shape)))
+          for _ in range(2)]
     for i, f in enumerate(grid):
         yo = omor.reduced_output(ofom, Vh, f)
+        sens = max(omor.relative_error(yo, omor.reduced_output(ofom, V2, f))[1] for V2 in Vp)
         _, e, _, _ = omor.relative_error(yo, res.frf[i])
-        assert e <= 1e-8, (f, e)
+        assert e <= max(1e-8, 4.0 * sens), (f, e, sens)
         assert abs(omor.mean_spl(yo) - res.spl[i][0]) <= 0.01
     # moment matching: the ROM reproduces the FOM at the expansion points, to the
     # accuracy the unscaled coupled operator allows (cond(A) ~ 2e12: measured
@@ -130,3 +138,22 @@ def test_cfg2_full_size_fom_and_rom(cuda):
         _, e, _, _ = mor.relative_error(yf, res.frf[i])
         worst = max(worst, e)
     assert worst <= 5e-2, worst
+
+
+def test_cfg2_schur_solver_matches_dense_lu(cuda):
+    """Schur complement on the plate + fast-diagonalisation cavity == the dense
+    whole-system LU (both refined to ||b - A x|| / ||b|| <= 1e-10)."""
+    import torch
+    from paper_2310_04734_b200 import workloads
+    box, ne = SMALL
+    fom_s, lay = workloads.cfg2_model(box=box, ne=ne, n_rec=12)
+    fom_d, _ = workloads.cfg2_model(box=box, ne=ne, n_rec=12, use_schur=False)
+    assert fom_s.schur is not None and fom_d.schur is None
+    g = torch.Generator(device="cuda").manual_seed(5)
+    B = torch.randn(fom_s.n, 3, dtype=torch.complex128, device="cuda", generator=g)
+    for f in (33.0, 250.0, 487.5):
+        fs, fd = fom_s.factor(f), fom_d.factor(f)
+        Xs, Xd = fs.solve(B), fd.solve(B)
+        assert fs.last_residual <= 1e-10 and fd.last_residual <= 1e-10
+        rel = float((Xs - Xd).abs().max() / Xd.abs().max())
+        assert rel <= 1e-8, (f, rel)
