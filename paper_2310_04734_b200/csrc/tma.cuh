@@ -152,25 +152,25 @@ struct GemmTma {
   // two producer warps: warp 0 arms the barrier with the whole stage's bytes and
   // loads A, warp 1 loads B (a complete-tx may precede the expect-tx: the phase
   // cannot complete before warp 0's arrival).
+  // PW producer warps share the KC/8 + 4 boxes of a chunk (box q by warp q % PW).
+  static constexpr int PW = KC / 8 + 4;
   __device__ static __forceinline__ void issue_chunk_part(int part, const Maps* mp, char* As, char* Bs,
                                                           uint64_t* bar, int cta, int ar0, int ac0, int br0, int bc0,
                                                           int m0, int n0, int k0) {
-    if (part == 0) {
-      mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
-#pragma unroll
-      for (int h = 0; h < KC / 8; ++h)
-        tma_load_3d_w(As + h * 8192, &mp->a64, 2 * (ac0 + k0 + 8 * h), ar0 + m0, cta, bar);
+    if (part == 0) mbar_expect_tx_w(bar, A_BYTES + B_BYTES);
+    if (part < KC / 8) {
+      tma_load_3d_w(As + part * 8192, &mp->a64, 2 * (ac0 + k0 + 8 * part), ar0 + m0, cta, bar);
     } else {
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        tma_load_3d_w(Bs + b * BBOX, KC == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
+      const int b = part - KC / 8;
+      tma_load_3d_w(Bs + b * BBOX, KC == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + n0 + 8 * b), br0 + k0, cta, bar);
     }
   }
-  __device__ static __forceinline__ void issue_c(const Maps* mp, char* Cs, uint64_t* bar, int cta, int cr0, int cc0,
-                                                 int m0, int n0) {
-    mbar_expect_tx_w(bar, C_BYTES);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) tma_load_3d_w(Cs + b * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * b), cr0 + m0, cta, bar);
+  // C tile: 4 boxes, box b by warp b (warp 0 arms the barrier)
+  __device__ static __forceinline__ void issue_c(int part, const Maps* mp, char* Cs, uint64_t* bar, int cta,
+                                                 int cr0, int cc0, int m0, int n0) {
+    if (part == 0) mbar_expect_tx_w(bar, C_BYTES);
+    if (part < 4)
+      tma_load_3d_w(Cs + part * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * part), cr0 + m0, cta, bar);
   }
 
   // Skinny updates (K <= KC, N <= 16: the in-panel updates of the recursive
@@ -319,11 +319,11 @@ struct GemmTma {
       mbar_fence_init();
     }
     __syncthreads();
-    // producer cursor (warps 0 and 1, warp-collective issue)
+    // producer cursor (warps 0..PW-1, warp-collective issue)
     int pt = 0, pk = 0;
-    if (warp <= 1) {
+    if (warp < PW) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
-      if (warp == 0) issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(0), tn0(0));
+      if (warp < 4) issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(0), tn0(0));
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
         issue_chunk_part(warp, mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], cta, ar0, ac0, br0, bc0,
                          tm0(pt), tn0(pt), pk * KC);
@@ -380,7 +380,7 @@ struct GemmTma {
       GT_MARK(1);
       if (lane == 0) mbar_arrive(&bars->empty[st]);
       // refill the stage consumed in the previous iteration
-      if (warp <= 1 && it + STAGES - 1 < T) {
+      if (warp < PW && it + STAGES - 1 < T) {
         const int s2 = (it + STAGES - 1) % STAGES;
         if (it >= 1) {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
@@ -413,11 +413,11 @@ struct GemmTma {
             }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->cempty);
-        if (warp == 0 && t + 1 < ntiles) {
+        if (warp < 4 && t + 1 < ntiles) {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
           fence_proxy_async_global();
-          issue_c(mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(t + 1), tn0(t + 1));
+          issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(t + 1), tn0(t + 1));
         }
         GT_MARK(3);
         kc = 0;
