@@ -146,6 +146,7 @@ struct GemmTma {
 
   struct Bars {
     uint64_t full[STAGES], empty[STAGES], cfull, cempty;
+    uint64_t sfull[8], sempty[8];  // skinny ring (up to 8 stages)
   };
 
   // issue the A and B boxes of chunk (m0, n0, k0) into stage st.  Split over
@@ -173,44 +174,55 @@ struct GemmTma {
       tma_load_3d_w(Cs + part * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * part), cr0 + m0, cta, bar);
   }
 
-  // Skinny updates (K <= KC, N <= 16: the in-panel updates of the recursive
+  // Skinny updates (K, N <= NW = 8 or 16: the in-panel updates of the recursive
   // panel) are latency-bound on the C tile, so each ring stage carries a whole
-  // tile — A (64 x 16), B (16 x 16) AND C (64 x 16) — and STAGES-1 tiles are in
-  // flight while one computes.  8 warps x (8 rows x 16 columns).
-  static constexpr unsigned SK_A = 2 * 8192, SK_B = 2 * 2048, SK_C = 2 * 8192;
-  static constexpr unsigned SK_STAGE = SK_A + SK_B + SK_C;
-  static constexpr int SK_STAGES = 3;
-  static constexpr size_t SMEM_SKINNY = (size_t)SK_STAGES * SK_STAGE;
+  // tile — A (64 x NW), B (NW x NW) AND C (64 x NW) — and all but one stage are
+  // in flight while one computes: 3 stages of 36 KB for NW = 16, 6 stages of
+  // 17 KB for NW = 8.  8 warps x (8 rows x NW columns).
+  static constexpr unsigned SK_BUDGET = 3 * (2 * 8192 + 2 * 2048 + 2 * 8192);
+  template <int NW>
+  struct Sk {
+    static constexpr int NBX = NW / 8;
+    static constexpr unsigned A = NBX * 8192, BBX = NW * 128, B = NBX * BBX, C = NBX * 8192;
+    static constexpr unsigned STAGE = A + B + C;
+    static constexpr int NSTG = (int)(SK_BUDGET / STAGE);
+  };
+  static constexpr size_t SMEM_SKINNY = SK_BUDGET;
 
+  template <int NW>
   __device__ static __forceinline__ void issue_tile(const Maps* mp, char* st, uint64_t* bar, int cta, int ar0,
                                                     int ac0, int br0, int bc0, int cr0, int m0) {
-    mbar_expect_tx_w(bar, SK_STAGE);
-    tma_load_3d_w(st, &mp->a64, 2 * ac0, ar0 + m0, cta, bar);
-    tma_load_3d_w(st + 8192, &mp->a64, 2 * (ac0 + 8), ar0 + m0, cta, bar);
-    tma_load_3d_w(st + SK_A, &mp->b16, 2 * bc0, br0, cta, bar);
-    tma_load_3d_w(st + SK_A + 2048, &mp->b16, 2 * (bc0 + 8), br0, cta, bar);
-    tma_load_3d_w(st + SK_A + SK_B, &mp->a64, 2 * bc0, cr0 + m0, cta, bar);
-    tma_load_3d_w(st + SK_A + SK_B + 8192, &mp->a64, 2 * (bc0 + 8), cr0 + m0, cta, bar);
+    using S = Sk<NW>;
+    mbar_expect_tx_w(bar, S::STAGE);
+#pragma unroll
+    for (int h = 0; h < S::NBX; ++h) {
+      tma_load_3d_w(st + h * 8192, &mp->a64, 2 * (ac0 + 8 * h), ar0 + m0, cta, bar);
+      tma_load_3d_w(st + S::A + h * S::BBX, NW == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + 8 * h), br0, cta, bar);
+      tma_load_3d_w(st + S::A + S::B + h * 8192, &mp->a64, 2 * (bc0 + 8 * h), cr0 + m0, cta, bar);
+    }
   }
 
+  template <int NW>
   __device__ static void run_skinny(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int cr0,
                                     int M, int N, int K, char* smem, Bars* bars, int cta) {
+    using S = Sk<NW>;
+    constexpr int NST = S::NSTG;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ntiles = (M + TM - 1) / TM;
     GT_BEGIN;
     if (tid == 0) {
 #pragma unroll
-      for (int s = 0; s < SK_STAGES; ++s) {
-        mbar_init(&bars->full[s], 1);
-        mbar_init(&bars->empty[s], NT / 32);
+      for (int s = 0; s < NST; ++s) {
+        mbar_init(&bars->sfull[s], 1);
+        mbar_init(&bars->sempty[s], NT / 32);
       }
       mbar_fence_init();
     }
     __syncthreads();
     if (warp == 0) {  // warp-collective producer (see tma_load_3d_w)
       fence_proxy_async_global();
-      for (int j = 0; j < SK_STAGES - 1 && j < ntiles; ++j)
-        issue_tile(mp, smem + j * SK_STAGE, &bars->full[j], cta, ar0, ac0, br0, bc0, cr0, j * TM);
+      for (int j = 0; j < NST - 1 && j < ntiles; ++j)
+        issue_tile<NW>(mp, smem + j * S::STAGE, &bars->sfull[j], cta, ar0, ac0, br0, bc0, cr0, j * TM);
     }
     unsigned full_ph = 0, empty_ph = 0;
     const int ak = lane & 3, prow = perm8(lane >> 2);
@@ -218,24 +230,24 @@ struct GemmTma {
     const int k4n = (K + 3) >> 2;
     GS_MARK(0);
     for (int t = 0; t < ntiles; ++t) {
-      const int st = t % SK_STAGES;
-      mbar_wait(&bars->full[st], (full_ph >> st) & 1);
+      const int st = t % NST;
+      mbar_wait(&bars->sfull[st], (full_ph >> st) & 1);
       full_ph ^= 1u << st;
       if (t == 0) GS_MARK(1); else GS_MARK(2);
-      const char* as = smem + st * SK_STAGE;
-      const char* bs = as + SK_A;
-      const char* cs = bs + SK_B;
-      double cr[2][2], ci[2][2];
+      const char* as = smem + st * S::STAGE;
+      const char* bs = as + S::A;
+      const char* cs = bs + S::B;
+      double cr[S::NBX][2], ci[S::NBX][2];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+      for (int j = 0; j < S::NBX; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
       for (int kk = 0; kk < k4n; ++kk) {
         const int kcol = kk * 4 + ak;
         const bool kin = kcol < K;
         z_t a = *(const z_t*)(as + (kcol >> 3) * 8192 + swz(row, kcol & 7));
         if (!kin) a = zmake(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          z_t b = *(const z_t*)(bs + j * 2048 + swz(kcol, prow));
+        for (int j = 0; j < S::NBX; ++j) {
+          z_t b = *(const z_t*)(bs + j * S::BBX + swz(kcol, prow));
           if (!kin) b = zmake(0.0, 0.0);
           blk::dmma(cr[j][0], cr[j][1], a.x, b.x);
           blk::dmma(cr[j][0], cr[j][1], a.y, -b.y);
@@ -245,7 +257,7 @@ struct GemmTma {
       }
       const int m0 = t * TM;
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < S::NBX; ++j)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int col = j * 8 + perm8(2 * ak + v);
@@ -256,15 +268,15 @@ struct GemmTma {
         }
       __syncwarp();
       GS_MARK(3);
-      if (lane == 0) mbar_arrive(&bars->empty[st]);
-      if (warp == 0 && t + SK_STAGES - 1 < ntiles) {
-        const int s2 = (t + SK_STAGES - 1) % SK_STAGES;
+      if (lane == 0) mbar_arrive(&bars->sempty[st]);
+      if (warp == 0 && t + NST - 1 < ntiles) {
+        const int s2 = (t + NST - 1) % NST;
         if (t >= 1) {
-          mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
+          mbar_wait(&bars->sempty[s2], (empty_ph >> s2) & 1);
           empty_ph ^= 1u << s2;
         }
-        issue_tile(mp, smem + s2 * SK_STAGE, &bars->full[s2], cta, ar0, ac0, br0, bc0, cr0,
-                   (t + SK_STAGES - 1) * TM);
+        issue_tile<NW>(mp, smem + s2 * S::STAGE, &bars->sfull[s2], cta, ar0, ac0, br0, bc0, cr0,
+                       (t + NST - 1) * TM);
       }
       GS_MARK(4);
     }
@@ -272,9 +284,9 @@ struct GemmTma {
     GS_MARK(5);
     if (tid == 0) {
 #pragma unroll
-      for (int s = 0; s < SK_STAGES; ++s) {
-        mbar_inval(&bars->full[s]);
-        mbar_inval(&bars->empty[s]);
+      for (int s = 0; s < NST; ++s) {
+        mbar_inval(&bars->sfull[s]);
+        mbar_inval(&bars->sempty[s]);
       }
     }
   }
@@ -289,8 +301,12 @@ struct GemmTma {
                              int t_step = 1) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int cr0 = cr0_ < 0 ? ar0 : cr0_;
+    if (K <= 8 && N <= 8 && t_step == 1) {
+      run_skinny<8>(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
+      return;
+    }
     if (K <= 16 && N <= 16 && t_step == 1) {
-      run_skinny(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
+      run_skinny<16>(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
       return;
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
