@@ -465,11 +465,19 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
           const int n1 = (1 << kk) * P.w;         // left subtree width
           const int cl = j0 + wc - n1;            // left subtree start column
           const int rc0 = j0 + wc, rc1 = min(rc0 + n1, k0 + nb);
-          trsm_small(A, ldw, cl, n1, rc0, rc1, smem);
-          __syncthreads();
-          PH_SUB(11);
-          GemmT::run(&P.maps, A, ldw, rc0, cl, cl, rc0, r - rc0, rc1 - rc0, n1, (char*)smem, &bars,
-                     blockIdx.x);
+          if (n1 <= 8 && rc1 - rc0 <= 8) {  // TRSM fused into the skinny update
+            GemmT::run_skinny_trsm<8>(&P.maps, A, ldw, rc0, cl, cl, rc0, rc0, r - rc0, rc1 - rc0, n1, (char*)smem,
+                                      &bars, blockIdx.x);
+          } else if (n1 <= 16 && rc1 - rc0 <= 16) {
+            GemmT::run_skinny_trsm<16>(&P.maps, A, ldw, rc0, cl, cl, rc0, rc0, r - rc0, rc1 - rc0, n1,
+                                       (char*)smem, &bars, blockIdx.x);
+          } else {
+            trsm_small(A, ldw, cl, n1, rc0, rc1, smem);
+            __syncthreads();
+            PH_SUB(11);
+            GemmT::run(&P.maps, A, ldw, rc0, cl, cl, rc0, r - rc0, rc1 - rc0, n1, (char*)smem, &bars,
+                       blockIdx.x);
+          }
           __syncthreads();
           PH_MARK(2);
         }

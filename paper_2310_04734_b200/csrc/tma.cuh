@@ -174,41 +174,51 @@ struct GemmTma {
       tma_load_3d_w(Cs + part * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * part), cr0 + m0, cta, bar);
   }
 
-  // Skinny updates (K, N <= NW = 8 or 16: the in-panel updates of the recursive
-  // panel) are latency-bound on the C tile, so each ring stage carries a whole
-  // tile — A (64 x NW), B (NW x NW) AND C (64 x NW) — and all but one stage are
-  // in flight while one computes: 3 stages of 36 KB for NW = 16, 6 stages of
-  // 17 KB for NW = 8.  8 warps x (8 rows x NW columns).
+  // Skinny in-panel updates of the recursive panel, fused with their TRSM:
+  //   U = L^-1 X   (L = unit lower n1 x n1 block, X = the n1 x N block above C),
+  //   C -= A U     (A: M x n1, C: M x N, n1, N <= NW = 8 or 16).
+  // They are latency-bound on the C tile, so each ring stage carries a whole
+  // tile — A (64 x NW) and C (64 x NW) — and all but one stage are in flight
+  // while one computes (3 x 32 KB for NW = 16, 6 x 16 KB for NW = 8).  U is
+  // solved in shared memory (one thread per column) while the first tiles load
+  // and written back once; the tiles read it from shared memory.  8 warps x
+  // (8 rows x NW columns).
   static constexpr unsigned SK_BUDGET = 3 * (2 * 8192 + 2 * 2048 + 2 * 8192);
+  static constexpr int SK_LD = 17;                                  // odd stride
+  static constexpr unsigned SK_TRI = 2 * 16 * SK_LD * 16;           // L and U blocks
   template <int NW>
   struct Sk {
     static constexpr int NBX = NW / 8;
-    static constexpr unsigned A = NBX * 8192, BBX = NW * 128, B = NBX * BBX, C = NBX * 8192;
-    static constexpr unsigned STAGE = A + B + C;
-    static constexpr int NSTG = (int)(SK_BUDGET / STAGE);
+    static constexpr unsigned A = NBX * 8192, C = NBX * 8192;
+    static constexpr unsigned STAGE = A + C;
+    static constexpr int NSTG = (int)((SK_BUDGET - SK_TRI) / STAGE) < 8 ? (int)((SK_BUDGET - SK_TRI) / STAGE) : 8;
   };
   static constexpr size_t SMEM_SKINNY = SK_BUDGET;
 
   template <int NW>
   __device__ static __forceinline__ void issue_tile(const Maps* mp, char* st, uint64_t* bar, int cta, int ar0,
-                                                    int ac0, int br0, int bc0, int cr0, int m0) {
+                                                    int ac0, int bc0, int cr0, int m0) {
     using S = Sk<NW>;
     mbar_expect_tx_w(bar, S::STAGE);
 #pragma unroll
     for (int h = 0; h < S::NBX; ++h) {
       tma_load_3d_w(st + h * 8192, &mp->a64, 2 * (ac0 + 8 * h), ar0 + m0, cta, bar);
-      tma_load_3d_w(st + S::A + h * S::BBX, NW == 16 ? &mp->b16 : &mp->b8, 2 * (bc0 + 8 * h), br0, cta, bar);
-      tma_load_3d_w(st + S::A + S::B + h * 8192, &mp->a64, 2 * (bc0 + 8 * h), cr0 + m0, cta, bar);
+      tma_load_3d_w(st + S::A + h * 8192, &mp->a64, 2 * (bc0 + 8 * h), cr0 + m0, cta, bar);
     }
   }
 
+  // In-panel update with its TRSM: L = Ag[br0.., ac0..] (n1 x n1 unit lower),
+  // X = Ag[br0.., bc0..] (n1 x N) is replaced by U = L^-1 X, then
+  // C = Ag[cr0.., bc0..] -= Ag[ar0.., ac0..] U for M rows.
   template <int NW>
-  __device__ static void run_skinny(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int cr0,
-                                    int M, int N, int K, char* smem, Bars* bars, int cta) {
+  __device__ static void run_skinny_trsm(const Maps* mp, z_t* Ag, int ldw, int ar0, int ac0, int br0, int bc0,
+                                         int cr0, int M, int N, int K, char* smem, Bars* bars, int cta) {
     using S = Sk<NW>;
     constexpr int NST = S::NSTG;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ntiles = (M + TM - 1) / TM;
+    z_t* Ls = (z_t*)(smem + NST * S::STAGE);
+    z_t* Us = Ls + 16 * SK_LD;
     GT_BEGIN;
     if (tid == 0) {
 #pragma unroll
@@ -222,8 +232,25 @@ struct GemmTma {
     if (warp == 0) {  // warp-collective producer (see tma_load_3d_w)
       fence_proxy_async_global();
       for (int j = 0; j < NST - 1 && j < ntiles; ++j)
-        issue_tile<NW>(mp, smem + j * S::STAGE, &bars->sfull[j], cta, ar0, ac0, br0, bc0, cr0, j * TM);
+        issue_tile<NW>(mp, smem + j * S::STAGE, &bars->sfull[j], cta, ar0, ac0, bc0, cr0, j * TM);
     }
+    // TRSM while the first tiles land: U = L^-1 X (zero-padded to NW x NW)
+    for (int e = tid; e < NW * NW; e += NT) {
+      const int i = e / NW, c = e % NW;
+      Ls[i * SK_LD + c] = (i < K && c < i) ? Ag[(size_t)(br0 + i) * ldw + ac0 + c] : zmake(0.0, 0.0);
+      Us[i * SK_LD + c] = (i < K && c < N) ? Ag[(size_t)(br0 + i) * ldw + bc0 + c] : zmake(0.0, 0.0);
+    }
+    __syncthreads();
+    if (tid < N) {
+      const int c = tid;
+      for (int i = 1; i < K; ++i) {
+        z_t x = Us[i * SK_LD + c];
+        for (int k = 0; k < i; ++k) x = zfms(x, Ls[i * SK_LD + k], Us[k * SK_LD + c]);
+        Us[i * SK_LD + c] = x;
+        Ag[(size_t)(br0 + i) * ldw + bc0 + c] = x;
+      }
+    }
+    __syncthreads();
     unsigned full_ph = 0, empty_ph = 0;
     const int ak = lane & 3, prow = perm8(lane >> 2);
     const int row = warp * 8 + prow;
@@ -235,20 +262,17 @@ struct GemmTma {
       full_ph ^= 1u << st;
       if (t == 0) GS_MARK(1); else GS_MARK(2);
       const char* as = smem + st * S::STAGE;
-      const char* bs = as + S::A;
-      const char* cs = bs + S::B;
+      const char* cs = as + S::A;
       double cr[S::NBX][2], ci[S::NBX][2];
 #pragma unroll
       for (int j = 0; j < S::NBX; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
       for (int kk = 0; kk < k4n; ++kk) {
         const int kcol = kk * 4 + ak;
-        const bool kin = kcol < K;
         z_t a = *(const z_t*)(as + (kcol >> 3) * 8192 + swz(row, kcol & 7));
-        if (!kin) a = zmake(0.0, 0.0);
+        if (kcol >= K) a = zmake(0.0, 0.0);
 #pragma unroll
         for (int j = 0; j < S::NBX; ++j) {
-          z_t b = *(const z_t*)(bs + j * S::BBX + swz(kcol, prow));
-          if (!kin) b = zmake(0.0, 0.0);
+          const z_t b = Us[kcol * SK_LD + j * 8 + prow];  // zero rows/cols beyond K, N
           blk::dmma(cr[j][0], cr[j][1], a.x, b.x);
           blk::dmma(cr[j][0], cr[j][1], a.y, -b.y);
           blk::dmma(ci[j][0], ci[j][1], a.x, b.y);
@@ -263,7 +287,7 @@ struct GemmTma {
           const int col = j * 8 + perm8(2 * ak + v);
           if (m0 + row < M && col < N) {
             const z_t c = *(const z_t*)(cs + j * 8192 + swz(row, col & 7));
-            Cg[(size_t)(cr0 + m0 + row) * ldw + bc0 + col] = zmake(c.x - cr[j][v], c.y - ci[j][v]);
+            Ag[(size_t)(cr0 + m0 + row) * ldw + bc0 + col] = zmake(c.x - cr[j][v], c.y - ci[j][v]);
           }
         }
       __syncwarp();
@@ -275,8 +299,7 @@ struct GemmTma {
           mbar_wait(&bars->sempty[s2], (empty_ph >> s2) & 1);
           empty_ph ^= 1u << s2;
         }
-        issue_tile<NW>(mp, smem + s2 * S::STAGE, &bars->sfull[s2], cta, ar0, ac0, br0, bc0, cr0,
-                       (t + NST - 1) * TM);
+        issue_tile<NW>(mp, smem + s2 * S::STAGE, &bars->sfull[s2], cta, ar0, ac0, bc0, cr0, (t + NST - 1) * TM);
       }
       GS_MARK(4);
     }
@@ -301,14 +324,7 @@ struct GemmTma {
                              int t_step = 1) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int cr0 = cr0_ < 0 ? ar0 : cr0_;
-    if (K <= 8 && N <= 8 && t_step == 1) {
-      run_skinny<8>(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
-      return;
-    }
-    if (K <= 16 && N <= 16 && t_step == 1) {
-      run_skinny<16>(mp, Cg, ldw, ar0, ac0, br0, bc0, cr0, M, N, K, smem, bars, cta);
-      return;
-    }
+
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
     const int ntn = (N + TN - 1) / TN, nk = (K + KC - 1) / KC;
