@@ -319,7 +319,7 @@ __device__ void panel_trsm(const Params& P, z_t* A, int k0, int nb, int c0, int 
     Nsc[(size_t)i * ldw + j] = (j < i && i < nb) ? zmake(-v.x, -v.y) : zmake(0.0, 0.0);
   }
   __syncthreads();
-  GemmT::run(&P.maps, A, ldw, r, 0, k0, c0, nb, c1 - c0, nb, (char*)smem, bars, blockIdx.x, k0);
+  GemmT::run(&P.maps, A, ldw, r, 0, k0, c0, nb, c1 - c0, nb, (char*)smem, bars, blockIdx.x, k0, 0, 1, true);
   __syncthreads();
 }
 

@@ -318,10 +318,12 @@ struct GemmTma {
   // unless given; ldw for the generic-store epilogue.  smem must be 1024-byte
   // aligned.
   // t_first / t_step: this CTA computes tiles t_first, t_first + t_step, ...
-  // of the row-major tile grid (several CTAs sharing one GEMM).
+  // of the row-major tile grid (several CTAs sharing one GEMM).  a_lower: A is
+  // strictly lower triangular and M <= TM (the U12 product): zero k chunks are
+  // skipped per warp.
   __device__ static void run(const Maps* mp, z_t* Cg, int ldw, int ar0, int ac0, int br0, int bc0, int M, int N,
                              int K, char* smem, Bars* bars, int cta, int cr0_ = -1, int t_first = 0,
-                             int t_step = 1) {
+                             int t_step = 1, bool a_lower = false) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int cr0 = cr0_ < 0 ? ar0 : cr0_;
 
@@ -380,7 +382,9 @@ struct GemmTma {
       const char* as = As + st * A_BYTES;
       const char* bs = Bs + st * B_BYTES;
       const int kvalid = min(KC, K - kc * KC);
-      const int k4n = (kvalid + 3) >> 2;
+      // a_lower: A strictly lower triangular within a single 64-row tile, so
+      // k chunk kc only reaches this warp's rows [16 wm, 16 wm + 16) if kc <= wm
+      const int k4n = (a_lower && kc * KC >= 16 * (wm + 1)) ? 0 : (kvalid + 3) >> 2;
       for (int kk = 0; kk < k4n; ++kk) {
         const int kcol = kk * 4 + ak;
         const bool kin = kcol < kvalid;
