@@ -156,3 +156,46 @@ def test_blocked_pivoting_and_singular(cuda, force_blocked):
     P2[0, :r - 1, :r - 1] = np.eye(r - 1)
     out = _run(cuda, P2, alpha, b, c_r)
     assert out.info.cpu().tolist() == [r, r]
+
+
+@pytest.mark.parametrize("r,nf", [(1024, 6), (2048, 2)])
+def test_cfg5_full_size_sample(cuda, r, nf):
+    """BASELINE cfg5 at its full reduced orders: a seeded sample of the 100k grid
+    against the oracle (numpy zgesv), TF <= 1e-8 and |dSPL| <= 0.01 dB."""
+    from paper_2310_04734_b200 import workloads
+    w = workloads.cfg5(r=r, n_freq=100_000)
+    idx = np.random.default_rng(r).choice(100_000, nf, replace=False)
+    f = w.freqs[np.sort(idx)]
+    alpha = w.alpha(f)
+    y_ref, spl_ref = omor.affine_sweep(w.prims, alpha, w.b, w.c_r)
+    out = _run(cuda, w.prims, alpha, w.b, w.c_r)
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+
+
+def test_cfg5_r1024_residuals_and_determinism(cuda):
+    """Size-independent properties on a full launch (2 x #SM frequencies at
+    r = 1024): backward-stable residuals ||A x - b|| / (||A|| ||x||) for every
+    frequency, and bit-identical results for the same frequency at different
+    batch positions (one CTA per frequency, fixed reduction orders)."""
+    import torch
+    from paper_2310_04734_b200 import sweep, workloads
+    w = workloads.cfg5(r=1024, n_freq=100_000)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    F = 2 * nsm
+    f = w.freqs[np.linspace(0, 99_999, F).astype(int)]
+    f[-1] = f[0]  # same frequency in the first and the last slot
+    alpha = w.alpha(f)
+    out = _run(cuda, w.prims, alpha, w.b, w.c_r, want_x=True)
+    assert int(out.info.abs().sum()) == 0
+    assert torch.equal(out.x[0], out.x[-1]) and torch.equal(out.y[0], out.y[-1])
+    P = sweep.as_ctensor(w.prims, cuda)
+    B = sweep.as_ctensor(w.b, cuda)
+    Al = sweep.as_ctensor(alpha, cuda)
+    worst = 0.0
+    for i in range(0, F, 37):
+        A = torch.einsum("k,kij->ij", Al[i], P)
+        X = out.x[i]
+        R = A @ X - B
+        rel = float(torch.linalg.matrix_norm(R) / (torch.linalg.matrix_norm(A) * torch.linalg.matrix_norm(X)))
+        worst = max(worst, rel)
+    assert worst <= 1e-14, worst
