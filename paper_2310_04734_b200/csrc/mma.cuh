@@ -288,68 +288,57 @@ __device__ __noinline__ void tri_inv64(z_t* T, int ld) {
     }
   }
   __syncthreads();
+  // doubling levels on the FP64 tensor cores: each h x h off-diagonal block is
+  // two complex GEMMs of 8x8 fragments (warp_cmma); h/2 fragments per level,
+  // at most two per warp.  Results are held in registers across the barrier
+  // that separates the reads of a pass from its in-place writes.
+  const int lane8 = lane >> 2, lq = lane & 3;
 #pragma unroll 1
   for (int h = 8; h < 64; h *= 2) {
-    const int hh = h * h, nel = (64 / (2 * h)) * hh;  // = 32 h <= 1024
-    z_t tv[4];
-    // step 1: T = C A^-1 (lower) or T = B D^-1 (upper), into the off-diagonal block
+    const int nf = h / 8, per_blk = nf * nf, nfr = (64 / (2 * h)) * per_blk;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      double rr[2][2], ri[2][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + q * NT;
-      if (e < nel) {
-        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
-        const int o = pn * 2 * h;
-        z_t acc = zmake(0.0, 0.0);
-        if (LOWER) {
-          for (int k = j; k < h; ++k) acc = zfma(acc, T[(o + h + i) * ld + o + k], T[(o + k) * ld + o + j]);
-        } else {
-          for (int k = 0; k <= j; ++k)
-            acc = zfma(acc, T[(o + i) * ld + o + h + k], T[(o + h + k) * ld + o + h + j]);
+      for (int q = 0; q < 2; ++q) {
+        const int fr = warp + q * (NT / 32);
+        rr[q][0] = rr[q][1] = ri[q][0] = ri[q][1] = 0.0;
+        if (fr < nfr) {
+          const int pb = fr / per_blk, fi = (fr % per_blk) / nf, fj = fr % nf, o = pb * 2 * h;
+          double cr[1][1][2] = {{{0.0, 0.0}}}, ci[1][1][2] = {{{0.0, 0.0}}};
+          if (pass == 0) {  // T = C A^-1 (lower) or T = B D^-1 (upper)
+            if (LOWER)
+              warp_cmma<1, 1, false>(cr, ci, T + (o + h + fi * 8) * ld + o, ld, T + o * ld + o + fj * 8, ld, h / 4);
+            else
+              warp_cmma<1, 1, false>(cr, ci, T + (o + fi * 8) * ld + o + h, ld, T + (o + h) * ld + o + h + fj * 8,
+                                     ld, h / 4);
+          } else {          // X = -D^-1 T (lower) or X = -A^-1 T (upper)
+            if (LOWER)
+              warp_cmma<1, 1, true>(cr, ci, T + (o + h + fi * 8) * ld + o + h, ld, T + (o + h) * ld + o + fj * 8,
+                                    ld, h / 4);
+            else
+              warp_cmma<1, 1, true>(cr, ci, T + (o + fi * 8) * ld + o, ld, T + o * ld + o + h + fj * 8, ld, h / 4);
+          }
+          rr[q][0] = cr[0][0][0];
+          rr[q][1] = cr[0][0][1];
+          ri[q][0] = ci[0][0][0];
+          ri[q][1] = ci[0][0][1];
         }
-        tv[q] = acc;
       }
-    }
-    __syncthreads();
+      __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + q * NT;
-      if (e < nel) {
-        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
-        const int o = pn * 2 * h;
-        if (LOWER) T[(o + h + i) * ld + o + j] = tv[q];
-        else T[(o + i) * ld + o + h + j] = tv[q];
-      }
-    }
-    __syncthreads();
-    // step 2: X = -D^-1 T (lower) or X = -A^-1 T (upper)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + q * NT;
-      if (e < nel) {
-        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
-        const int o = pn * 2 * h;
-        z_t acc = zmake(0.0, 0.0);
-        if (LOWER) {
-          for (int k = 0; k <= i; ++k)
-            acc = zfma(acc, T[(o + h + i) * ld + o + h + k], T[(o + h + k) * ld + o + j]);
-        } else {
-          for (int k = i; k < h; ++k) acc = zfma(acc, T[(o + i) * ld + o + k], T[(o + k) * ld + o + h + j]);
+      for (int q = 0; q < 2; ++q) {
+        const int fr = warp + q * (NT / 32);
+        if (fr < nfr) {
+          const int pb = fr / per_blk, fi = (fr % per_blk) / nf, fj = fr % nf, o = pb * 2 * h;
+          const int row = (LOWER ? o + h : o) + fi * 8 + lane8;
+          const int col = (LOWER ? o : o + h) + fj * 8 + 2 * lq;
+          T[row * ld + col] = zmake(rr[q][0], ri[q][0]);
+          T[row * ld + col + 1] = zmake(rr[q][1], ri[q][1]);
         }
-        tv[q] = zmake(-acc.x, -acc.y);
       }
+      __syncthreads();
     }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + q * NT;
-      if (e < nel) {
-        const int pn = e / hh, rem = e - pn * hh, i = rem / h, j = rem - (rem / h) * h;
-        const int o = pn * 2 * h;
-        if (LOWER) T[(o + h + i) * ld + o + j] = tv[q];
-        else T[(o + i) * ld + o + h + j] = tv[q];
-      }
-    }
-    __syncthreads();
   }
 }
 
