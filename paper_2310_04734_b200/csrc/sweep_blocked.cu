@@ -155,9 +155,10 @@ __device__ __forceinline__ z_t zrecip_fast(z_t a) {
 // written in the same phase.  The update of column jj fuses the argmax of
 // column jj+1, so each column costs ONE block barrier.  Rows are written back
 // to global memory in logical order.
-__device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* lg, int* piv,
-                            int* s_info, double* rv, int* ri, z_t* rz) {
-  const int r = P.r, ldw = P.ldw, lp = P.w + 1;
+template <int W>
+__device__ void inner_panel_w(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* lg, int* piv,
+                              int* s_info, double* rv, int* ri, z_t* rz) {
+  const int r = P.r, ldw = P.ldw, lp = W + 1;
   const int H = r - j0;
   const int tid = threadIdx.x;
   PH_SUB_BEGIN;
@@ -198,12 +199,16 @@ __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t
         z_t* row = Ps + q * lp;
         const z_t m = zmul(row[jj], pinv);
         row[jj] = m;
-        for (int c = jj + 1; c < wc; ++c) {
-          const z_t nv = zfms(row[c], m, prow[c]);
-          row[c] = nv;
-          if (c == jj + 1) {
-            const double a = zabs1(nv);
-            if (a > cd.v || (a == cd.v && ((l << 16) | q) < cd.key)) cd = Cand{a, (l << 16) | q, nv};
+        // compile-time column loop: all loads of the row issue back to back
+#pragma unroll
+        for (int c = 1; c < W; ++c) {
+          if (c > jj && c < wc) {
+            const z_t nv = zfms(row[c], m, prow[c]);
+            row[c] = nv;
+            if (c == jj + 1) {
+              const double a = zabs1(nv);
+              if (a > cd.v || (a == cd.v && ((l << 16) | q) < cd.key)) cd = Cand{a, (l << 16) | q, nv};
+            }
           }
         }
       }
@@ -228,6 +233,17 @@ __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t
     A[(size_t)(j0 + lg[q]) * ldw + j0 + c] = Ps[q * lp + c];
   }
   __syncthreads();
+}
+
+__device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* lg, int* piv,
+                            int* s_info, double* rv, int* ri, z_t* rz) {
+  switch (P.w) {
+    case 16: inner_panel_w<16>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
+    case 8: inner_panel_w<8>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
+    case 4: inner_panel_w<4>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
+    case 2: inner_panel_w<2>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
+    default: inner_panel_w<1>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
+  }
 }
 
 // Row interchanges piv[a..b) (global row ids, relative to panel base k0) applied
