@@ -108,8 +108,14 @@ struct Cand {
   z_t val;
 };
 
+// |Re|+|Im| >= 0 (or -1 for "no candidate"): the IEEE bit patterns order like
+// the values when read as signed 64-bit integers, so the comparisons run on the
+// integer pipe instead of waiting for the FP64 pipe the co-resident CTA's DMMAs
+// keep busy.
+__device__ __forceinline__ long long vbits(double v) { return __double_as_longlong(v); }
 __device__ __forceinline__ void cand_better(Cand& a, const Cand& b) {
-  if (b.v > a.v || (b.v == a.v && b.key < a.key)) a = b;
+  const long long vb = vbits(b.v), va = vbits(a.v);
+  if (vb > va || (vb == va && b.key < a.key)) a = b;
 }
 
 // Block-wide izamax (max |Re|+|Im|, lowest logical row on ties): warp
@@ -137,13 +143,25 @@ __device__ __forceinline__ Cand block_argmax(Cand c, double* rv, int* ri, z_t* r
 
 // 1/a with one division: a is scaled by a power of two (exact) so that
 // |a|^2 neither overflows nor underflows.
+// 1/a: a is scaled by a power of two (exact, from the exponent bits) so that
+// d = |a|^2 lies in [1, 8); 1/d by the MUFU reciprocal estimate and two
+// Newton steps (a few ulp, not correctly rounded — well inside the sweep's
+// tolerance) instead of a full IEEE division on the contended FP64 pipe.
 __device__ __forceinline__ z_t zrecip_fast(z_t a) {
   const double m = fmax(fabs(a.x), fabs(a.y));
-  int e;
-  frexp(m, &e);
-  const double sc = ldexp(1.0, -e);
+  // sc = 2^(1023 - eb) from the biased exponent eb of m, so m sc lies in [1, 2)
+  long long eb = (__double_as_longlong(m) >> 52) & 0x7ff;
+  eb = eb < 1 ? 1 : (eb > 2045 ? 2045 : eb);
+  const double sc = __longlong_as_double((2046 - eb) << 52);
   const double xr = a.x * sc, xi = a.y * sc;
-  const double inv = sc / (xr * xr + xi * xi);
+  const double d = xr * xr + xi * xi;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  const double inv = sc * y;
   return zmake(xr * inv, -xi * inv);
 }
 
@@ -190,6 +208,7 @@ __device__ void inner_panel_w(const Params& P, z_t* A, int k0, int j0, int wc, z
     cd = Cand{-1.0, 0x7fffffff, zmake(0.0, 0.0)};
     if (!zero) {
       const z_t pinv = zrecip_fast(best.val);
+      PH_SUB(13);
       const z_t* prow = Ps + b * lp;
       for (int q = tid; q < H; q += NT) {
         int l = lg[q];

@@ -56,6 +56,6 @@ for r in [int(x) for x in sys.argv[1:]] or [1024]:
     gn = ["wait full", "compute", "release/produce", "epilogue"]
     print(f"r={r}: gemm warp1 " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(gn, gm[:4])))
     print(f"r={r}: gemm thr0  " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(gn, gm[4:])))
-    subn = ["leaf load", "leaf factor", "leaf swaps", "leaf trsm_small", "colA", "colB", "colArgmax"]
+    subn = ["leaf load", "leaf factor", "leaf swaps", "leaf trsm_small", "col update", "col pivot-recip", "col argmax"]
     print(f"r={r}: sub-phases " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(subn, sub)))
     print(f"r={r}: " + ", ".join(f"{n} {100 * x / v.sum():.1f}%" for n, x in zip(names, v)))
