@@ -336,8 +336,20 @@ struct GemmTma {
     const int ntiles = (ntiles_all - 1 - t_first) / t_step + 1;  // this CTA's tiles
     const int T = ntiles * nk;
     // local tile l -> (m0, n0)
-    auto tm0 = [&](int l) { return ((t_first + l * t_step) / ntn) * TM; };
-    auto tn0 = [&](int l) { return ((t_first + l * t_step) % ntn) * TN; };
+    // tile coordinates walked incrementally (no integer division per chunk):
+    // a cursor (row tile, col tile) advanced by t_step tiles at a time
+    struct Cur {
+      int m, n;
+    };
+    auto start = [&]() { return Cur{t_first / ntn, t_first % ntn}; };
+    auto advance = [&](Cur c) {
+      c.n += t_step;
+      if (c.n >= ntn) {
+        c.m += c.n / ntn;
+        c.n %= ntn;
+      }
+      return c;
+    };
     char* As = smem;
     char* Bs = smem + STAGES * A_BYTES;
     char* Cs = Bs + STAGES * B_BYTES;
@@ -354,14 +366,15 @@ struct GemmTma {
     }
     __syncthreads();
     // producer cursor (warps 0..PW-1, warp-collective issue)
-    int pt = 0, pk = 0;
+    int pk = 0;
+    Cur pc = start();  // producer's tile
     if (warp < PW) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
-      if (warp < 4) issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(0), tn0(0));
+      if (warp < 4) issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, pc.m * TM, pc.n * TN);
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
         issue_chunk_part(warp, mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], cta, ar0, ac0, br0, bc0,
-                         tm0(pt), tn0(pt), pk * KC);
-        if (++pk == nk) { pk = 0; ++pt; }
+                         pc.m * TM, pc.n * TN, pk * KC);
+        if (++pk == nk) { pk = 0; pc = advance(pc); }
       }
     }
     unsigned full_ph = 0, empty_ph = 0, c_ph = 0, cempty_ph = 0;
@@ -373,6 +386,7 @@ struct GemmTma {
     const int ar = lane >> 2, ak = lane & 3;
     const int prow = perm8(ar);
     int t = 0, kc = 0;
+    Cur cc = start();  // consumer's tile
     GT_BEGIN;
     for (int it = 0; it < T; ++it) {
       const int st = it % STAGES;
@@ -423,12 +437,12 @@ struct GemmTma {
           empty_ph ^= 1u << s2;
         }
         issue_chunk_part(warp, mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], cta, ar0, ac0, br0, bc0,
-                         tm0(pt), tn0(pt), pk * KC);
-        if (++pk == nk) { pk = 0; ++pt; }
+                         pc.m * TM, pc.n * TN, pk * KC);
+        if (++pk == nk) { pk = 0; pc = advance(pc); }
       }
       GT_MARK(2);
       if (kc == nk - 1) {
-        const int m0 = tm0(t), n0 = tn0(t);
+        const int m0 = cc.m * TM, n0 = cc.n * TN;
         mbar_wait(&bars->cfull, c_ph);
         c_ph ^= 1;
 #pragma unroll
@@ -453,11 +467,13 @@ struct GemmTma {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
           fence_proxy_async_global();
-          issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, tm0(t + 1), tn0(t + 1));
+          const Cur nx = advance(cc);
+          issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, nx.m * TM, nx.n * TN);
         }
         GT_MARK(3);
         kc = 0;
         ++t;
+        cc = advance(cc);
       } else {
         ++kc;
       }

@@ -70,8 +70,19 @@ struct GemmBig {
     if (t_first >= ntiles_all) return;
     const int ntiles = (ntiles_all - 1 - t_first) / t_step + 1;
     const int T = ntiles * nk;
-    auto tm0 = [&](int l) { return ((t_first + l * t_step) / ntn) * TM; };
-    auto tn0 = [&](int l) { return ((t_first + l * t_step) % ntn) * TN; };
+    // tile coordinates walked incrementally (one division per tile at most)
+    struct Cur {
+      int m, n;
+    };
+    auto advance = [&](Cur c) {
+      c.n += t_step;
+      if (c.n >= ntn) {
+        c.m += c.n / ntn;
+        c.n %= ntn;
+      }
+      return c;
+    };
+    const Cur c0 = {t_first / ntn, t_first % ntn};
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
     char* As = smem;
@@ -88,14 +99,15 @@ struct GemmBig {
       mbar_fence_init();
     }
     __syncthreads();
-    int pt = 0, pk = 0;  // producer cursor (warps 0..PW-1, warp-collective issue)
+    int pk = 0;  // producer cursor (warps 0..PW-1, warp-collective issue)
+    Cur pc = c0;
     if (warp < PW) {
       fence_proxy_async_global();  // generic writes before this GEMM -> visible to TMA
-      issue_c(warp, mp, Cs, &bars->cfull, ar0, bc0, tm0(0), tn0(0));
+      issue_c(warp, mp, Cs, &bars->cfull, ar0, bc0, pc.m * TM, pc.n * TN);
       for (int j = 0; j < STAGES - 1 && j < T; ++j) {
-        issue_chunk(warp, mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], ar0, ac0, br0, bc0, tm0(pt),
-                    tn0(pt), pk * KC);
-        if (++pk == nk) { pk = 0; ++pt; }
+        issue_chunk(warp, mp, As + j * A_BYTES, Bs + j * B_BYTES, &bars->full[j], ar0, ac0, br0, bc0, pc.m * TM,
+                    pc.n * TN, pk * KC);
+        if (++pk == nk) { pk = 0; pc = advance(pc); }
       }
     }
     unsigned full_ph = 0, empty_ph = 0, c_ph = 0, cempty_ph = 0;
@@ -106,6 +118,7 @@ struct GemmBig {
       for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
     const int ak = lane & 3, prow = perm8(lane >> 2);
     int t = 0, kc = 0;
+    Cur cc = c0;  // consumer's tile
     for (int it = 0; it < T; ++it) {
       const int st = it % STAGES;
       mbar_wait(&bars->full[st], (full_ph >> st) & 1);
@@ -152,12 +165,12 @@ struct GemmBig {
           mbar_wait(&bars->empty[s2], (empty_ph >> s2) & 1);
           empty_ph ^= 1u << s2;
         }
-        issue_chunk(warp, mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], ar0, ac0, br0, bc0, tm0(pt),
-                    tn0(pt), pk * KC);
-        if (++pk == nk) { pk = 0; ++pt; }
+        issue_chunk(warp, mp, As + s2 * A_BYTES, Bs + s2 * B_BYTES, &bars->full[s2], ar0, ac0, br0, bc0,
+                    pc.m * TM, pc.n * TN, pk * KC);
+        if (++pk == nk) { pk = 0; pc = advance(pc); }
       }
       if (kc == nk - 1) {
-        const int m0 = tm0(t), n0 = tn0(t);
+        const int m0 = cc.m * TM, n0 = cc.n * TN;
         mbar_wait(&bars->cfull, c_ph);
         c_ph ^= 1;
 #pragma unroll
@@ -180,10 +193,12 @@ struct GemmBig {
         if (warp < PW && t + 1 < ntiles) {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
-          issue_c(warp, mp, Cs, &bars->cfull, ar0, bc0, tm0(t + 1), tn0(t + 1));
+          const Cur nx = advance(cc);
+          issue_c(warp, mp, Cs, &bars->cfull, ar0, bc0, nx.m * TM, nx.n * TN);
         }
         kc = 0;
         ++t;
+        cc = advance(cc);
       } else {
         ++kc;
       }
