@@ -398,10 +398,11 @@ struct GemmTma {
       const int kvalid = min(KC, K - kc * KC);
       // a_lower: A strictly lower triangular within a single 64-row tile, so
       // k chunk kc only reaches this warp's rows [16 wm, 16 wm + 16) if kc <= wm
-      const int k4n = (a_lower && kc * KC >= 16 * (wm + 1)) ? 0 : (kvalid + 3) >> 2;
-      for (int kk = 0; kk < k4n; ++kk) {
+      const bool skip = a_lower && kc * KC >= 16 * (wm + 1);
+      // one k step of 4: fragment loads (masked past kvalid when MASK) + 16 DMMAs
+      auto kstep = [&](int kk, bool mask) {
         const int kcol = kk * 4 + ak;
-        const bool kin = kcol < kvalid;
+        const bool kin = !mask || kcol < kvalid;
         z_t a[2], b[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -424,6 +425,15 @@ struct GemmTma {
             blk::dmma(ci[i][j][0], ci[i][j][1], a[i].x, bi);
             blk::dmma(ci[i][j][0], ci[i][j][1], a[i].y, br);
           }
+        }
+      };
+      if (!skip) {
+        if (kvalid == KC) {  // full chunk: unmasked, fully unrolled
+#pragma unroll
+          for (int kk = 0; kk < KC / 4; ++kk) kstep(kk, false);
+        } else {
+          const int k4n = (kvalid + 3) >> 2;
+          for (int kk = 0; kk < k4n; ++kk) kstep(kk, true);
         }
       }
       __syncwarp();
