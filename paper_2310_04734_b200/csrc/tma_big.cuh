@@ -126,11 +126,12 @@ struct GemmBig {
       const char* as = As + st * A_BYTES;
       const char* bs = Bs + st * B_BYTES;
       const int kvalid = min(KC, K - kc * KC);
+      const bool full = kvalid == KC;  // full chunk: no masking
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
         const int kcol = kk * 4 + ak;
-        if (kk * 4 < kvalid) {
-          const bool kin = kcol < kvalid;
+        if (full || kk * 4 < kvalid) {
+          const bool kin = full || kcol < kvalid;
           z_t a[4], b[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
