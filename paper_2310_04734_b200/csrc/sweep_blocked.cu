@@ -393,6 +393,17 @@ __device__ void diag_backsolve(z_t* A, int ldw, int r, int s, int kb, int nb, z_
 // A = sum_k alpha_k P_k into the workspace.  Bandwidth-bound: each thread keeps
 // KP x 4 independent 16-byte loads in flight (the primitives are shared by all
 // CTAs and pinned in L2 when they fit, see sweep_blocked_launch).
+// 256-bit global accesses (sm_100: LDG/STG.256): two complex per instruction
+__device__ __forceinline__ void ld256(const z_t* p, z_t& a, z_t& b) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+               : "l"(p));
+}
+__device__ __forceinline__ void st256(z_t* p, z_t a, z_t b) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+               : "memory");
+}
+
 template <int KP>
 __device__ __forceinline__ void form_quads(const Params& P, z_t* A, const z_t* alph) {
   const int r = P.r, ldw = P.ldw;
@@ -403,17 +414,21 @@ __device__ __forceinline__ void form_quads(const Params& P, z_t* A, const z_t* a
   for (int64_t q = threadIdx.x; q < nq; q += NT) {
     z_t v[KP][4];
 #pragma unroll
-    for (int k = 0; k < KP; ++k)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[k][e] = __ldg(P.prims + k * rr + 4 * q + e);
+    for (int k = 0; k < KP; ++k) {  // 64 B of each primitive in two 256-bit loads
+      ld256(P.prims + k * rr + 4 * q, v[k][0], v[k][1]);
+      ld256(P.prims + k * rr + 4 * q + 2, v[k][2], v[k][3]);
+    }
     const int64_t i = (4 * q) / r, j = 4 * q - i * r;
+    z_t o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       z_t acc = zmul(a[0], v[0][e]);
 #pragma unroll
       for (int k = 1; k < KP; ++k) acc = zfma(acc, a[k], v[k][e]);
-      A[i * ldw + j + e] = acc;
+      o[e] = acc;
     }
+    st256(A + i * ldw + j, o[0], o[1]);
+    st256(A + i * ldw + j + 2, o[2], o[3]);
   }
 }
 
