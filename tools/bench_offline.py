@@ -50,6 +50,14 @@ def measure():
     out["gather_ms"] = timed(lambda: P.gather2(Ke, Me))
     Kg = P.gather(Ke)
     out["box_fastpath_ms"] = timed(lambda: assembly.assemble_helmholtz_box(box, ne))
+    ne_ = conn.shape[0]
+    T = ne_ * 729
+    # the scatter (fused K+M gather) on its own traffic: gather map + triplet values + CSR values
+    gbytes = (nnz + 1) * 8 + T * 4 + 2 * T * 8 + 2 * nnz * 8
+    out["gather_GBps"] = gbytes / (out["gather_ms"] * 1e-3) / 1e9
+    out["gather_frac_hbm"] = out["gather_GBps"] / peak_hbm
+    # element integrals on DMMA: 32x32 padded products, 21 + 7 k-steps of 8x8x4 per element
+    out["element_dmma_TFLOPs"] = ne_ * (16 * (21 + 7) * 512) / (out["element_ms"] * 1e-3) / 1e12  # 512 flop/DMMA
     alg_asm = nnz * (8 * 2 + 4) + (n + 1) * 4 + xyz.nbytes + conn.nbytes
     t_val = out["element_ms"] + out["gather_ms"]
     out["assembly_values_GBps"] = alg_asm / (t_val * 1e-3) / 1e9
