@@ -125,19 +125,19 @@ __device__ __forceinline__ void cand_better(Cand& a, const Cand& b) {
 __device__ __forceinline__ Cand block_argmax(Cand c, double* rv, int* ri, z_t* rz) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = 16; o > 0; o >>= 1) {  // (value, key) only: the pivot value is re-read from its row
     Cand d;
     d.v = __shfl_xor_sync(0xffffffffu, c.v, o);
     d.key = __shfl_xor_sync(0xffffffffu, c.key, o);
-    d.val.x = __shfl_xor_sync(0xffffffffu, c.val.x, o);
-    d.val.y = __shfl_xor_sync(0xffffffffu, c.val.y, o);
+    d.val = zmake(0.0, 0.0);
     cand_better(c, d);
   }
-  if (lane == 0) { rv[warp] = c.v; ri[warp] = c.key; rz[warp] = c.val; }
+  (void)rz;
+  if (lane == 0) { rv[warp] = c.v; ri[warp] = c.key; }
   __syncthreads();
-  Cand best{rv[0], ri[0], rz[0]};
+  Cand best{rv[0], ri[0], zmake(0.0, 0.0)};
 #pragma unroll
-  for (int q = 1; q < NT / 32; ++q) cand_better(best, Cand{rv[q], ri[q], rz[q]});
+  for (int q = 1; q < NT / 32; ++q) cand_better(best, Cand{rv[q], ri[q], zmake(0.0, 0.0)});
   return best;
 }
 
@@ -207,7 +207,7 @@ __device__ void inner_panel_w(const Params& P, z_t* A, int k0, int j0, int wc, z
     const int nc = wc - jj - 1;
     cd = Cand{-1.0, 0x7fffffff, zmake(0.0, 0.0)};
     if (!zero) {
-      const z_t pinv = zrecip_fast(best.val);
+      const z_t pinv = zrecip_fast(Ps[b * lp + jj]);  // pivot value from its (unmoved) row
       PH_SUB(13);
       const z_t* prow = Ps + b * lp;
       for (int q = tid; q < H; q += NT) {
