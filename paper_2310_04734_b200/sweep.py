@@ -84,6 +84,8 @@ def rom_sweep_affine(prims: torch.Tensor, alpha: torch.Tensor, b: torch.Tensor, 
     for t in (prims, alpha, b) + ((c_r,) if n_out else ()):
         if t.dtype != CDT or not t.is_cuda or not t.is_contiguous():
             raise ValueError("rom_sweep_affine expects contiguous complex128 CUDA tensors")
+    if s > MAX_RHS_BLOCKED and lib.vb_rom_sweep_path(r, K, s, n_out) == 1:
+        return _sweep_rhs_groups(prims, alpha, b, c_r, want_y, want_spl, want_x, stream, out)
     if out is None:
         out = SweepOut(
             y=torch.empty((F, n_out, s), dtype=CDT, device=dev) if want_y and n_out else None,
@@ -97,6 +99,38 @@ def rom_sweep_affine(prims: torch.Tensor, alpha: torch.Tensor, b: torch.Tensor, 
                           _lib.ptr(out.x), _lib.ptr(out.info), _lib.ptr(work), wbytes,
                           _lib.stream_handle(stream))
     _lib.check(rc, "vb_rom_sweep")
+    return out
+
+
+MAX_RHS_BLOCKED = 16  # right-hand sides per launch on the blocked path
+
+
+def _sweep_rhs_groups(prims, alpha, b, c_r, want_y, want_spl, want_x, stream, out):
+    """More than 16 right-hand sides on the blocked path: one launch per group
+    of 16 columns (each column's outputs and SPL are independent; every group
+    refactors A(f), so the result equals one launch over all columns)."""
+    F, r = alpha.shape[0], prims.shape[1]
+    s = b.shape[-1]
+    n_out = c_r.shape[0] if c_r is not None else 0
+    dev = prims.device
+    if out is None:
+        out = SweepOut(
+            y=torch.empty((F, n_out, s), dtype=CDT, device=dev) if want_y and n_out else None,
+            spl=torch.empty((F, s), dtype=torch.float64, device=dev) if want_spl and n_out else None,
+            x=torch.empty((F, r, s), dtype=CDT, device=dev) if want_x else None,
+            info=torch.empty((F,), dtype=torch.int32, device=dev))
+    for g0 in range(0, s, MAX_RHS_BLOCKED):
+        g1 = min(s, g0 + MAX_RHS_BLOCKED)
+        bg = b[..., g0:g1].contiguous()
+        o = rom_sweep_affine(prims, alpha, bg, c_r, want_y, want_spl, want_x, stream)
+        if out.y is not None:
+            out.y[:, :, g0:g1] = o.y
+        if out.spl is not None:
+            out.spl[:, g0:g1] = o.spl
+        if out.x is not None:
+            out.x[:, :, g0:g1] = o.x
+        if g0 == 0:
+            out.info.copy_(o.info)
     return out
 
 

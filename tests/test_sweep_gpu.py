@@ -199,3 +199,19 @@ def test_cfg5_r1024_residuals_and_determinism(cuda):
         rel = float(torch.linalg.matrix_norm(R) / (torch.linalg.matrix_norm(A) * torch.linalg.matrix_norm(X)))
         worst = max(worst, rel)
     assert worst <= 1e-14, worst
+
+
+def test_blocked_path_more_than_16_rhs(cuda):
+    """s > 16 right-hand sides on the blocked path run as groups of 16 (the
+    reference's numpy.linalg.solve takes any number of columns)."""
+    rng = np.random.default_rng(33)
+    r, s, n_out, K, F = 150, 37, 20, 3, 9
+    prims = rng.standard_normal((K, r, r)) + 1j * rng.standard_normal((K, r, r))
+    alpha = rng.standard_normal((F, K)) + 1j * rng.standard_normal((F, K))
+    b = rng.standard_normal((r, s)) + 1j * rng.standard_normal((r, s))
+    c_r = rng.standard_normal((n_out, r)) + 1j * rng.standard_normal((n_out, r))
+    y_ref, spl_ref = omor.affine_sweep(prims, alpha, b, c_r)
+    out = _run(cuda, prims, alpha, b, c_r, want_x=True)
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+    x_ref = np.stack([np.linalg.solve(np.tensordot(alpha[i], prims, 1), b) for i in range(F)])
+    assert np.abs(out.x.cpu().numpy() - x_ref).max() <= 1e-9 * np.abs(x_ref).max()
