@@ -39,6 +39,7 @@ using GemmNarrow = Gemm<64, 16, 8, 1, 2, EPI_SUB>; // back-substitution updates 
 using GemmOut = Gemm<64, 16, 8, 1, 2, EPI_SET>;   // y = C_R x
 
 constexpr int LDL = NB + 4;     // == 4 (mod 8): triangular inverse used as A operand
+constexpr int DEEP_MIN_R = 640; // deferred 128-deep trailing updates from this order on
 constexpr int LDY = 16 + 2;
 constexpr size_t TRSM_SMEM = (size_t)(NB * LDL) * sizeof(z_t);
 constexpr size_t BACK_SMEM = (size_t)(NB * LDL + NB * LDY) * sizeof(z_t);
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
   // 1024-byte aligned base (128B-swizzled TMA boxes)
   double2* smem = (double2*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ GemmT::Bars bars;
-  __shared__ int piv[NB];
+  __shared__ int piv[2 * NB];  // the two panels of an outer 128-column step
   __shared__ double rv[2 * (NT / 32)];
   __shared__ int ri[2 * (NT / 32)];
   __shared__ int s_info;
@@ -491,30 +492,29 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
     __syncthreads();
     PH_MARK(0);
     // ---- blocked right-looking LU on [A | B] ----
-    for (int k0 = 0; k0 < r; k0 += NB) {
-      const int nb = min(NB, r - k0);
-      // Recursive (zgetrf2-order) panel: leaves of w columns are factored in
-      // shared memory; after leaf l the right sibling of the largest completed
-      // left subtree (size 2^k leaves, k = trailing ones of l) is updated with
-      // one TRSM + one GEMM of depth 2^k w.  In-panel traffic ~ r NB log2(NB/w)
-      // instead of r NB^2 / w for rank-w updates after every leaf.
-      const int nleaves = (nb + P.w - 1) / P.w;
+    // Recursive (zgetrf2-order) panel of pnb columns from pk0: leaves of w
+    // columns are factored in shared memory; after leaf l the right sibling of
+    // the largest completed left subtree (2^k leaves, k = trailing ones of l) is
+    // updated with one TRSM + one GEMM of depth 2^k w.  Pivots go to
+    // piv[j - pbase].
+    auto factor_panel = [&](int pk0, int pnb, int pbase) {
+      const int nleaves = (pnb + P.w - 1) / P.w;
       for (int l = 0; l < nleaves; ++l) {
-        const int j0 = k0 + l * P.w;
-        const int wc = min(P.w, k0 + nb - j0);
-        inner_panel(P, A, k0, j0, wc, smem, (int*)(smem + (size_t)(r - j0) * (P.w + 1)), piv, &s_info, rv, ri,
-                    rz);
+        const int j0 = pk0 + l * P.w;
+        const int wc = min(P.w, pk0 + pnb - j0);
+        inner_panel(P, A, pbase, j0, wc, smem, (int*)(smem + (size_t)(r - j0) * (P.w + 1)), piv, &s_info, rv,
+                    ri, rz);
         PH_MARK(1);
         PH_SUB_BEGIN;
-        apply_swaps(A, ldw, piv, k0, j0, j0 + wc, k0, j0);
-        apply_swaps(A, ldw, piv, k0, j0, j0 + wc, j0 + wc, k0 + nb);
+        apply_swaps(A, ldw, piv, pbase, j0, j0 + wc, pk0, j0);
+        apply_swaps(A, ldw, piv, pbase, j0, j0 + wc, j0 + wc, pk0 + pnb);
         __syncthreads();
         PH_SUB(10);
         if (l + 1 < nleaves) {
           const int kk = __ffs(~l) - 1;           // trailing ones of l
           const int n1 = (1 << kk) * P.w;         // left subtree width
           const int cl = j0 + wc - n1;            // left subtree start column
-          const int rc0 = j0 + wc, rc1 = min(rc0 + n1, k0 + nb);
+          const int rc0 = j0 + wc, rc1 = min(rc0 + n1, pk0 + pnb);
           if (n1 <= 8 && rc1 - rc0 <= 8) {  // TRSM fused into the skinny update
             GemmT::run_skinny_trsm<8>(&P.maps, A, ldw, rc0, cl, cl, rc0, rc0, r - rc0, rc1 - rc0, n1, (char*)smem,
                                       &bars, blockIdx.x);
@@ -532,14 +532,45 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
           PH_MARK(2);
         }
       }
-      const int c0 = k0 + nb, c1 = r + s;
-      apply_swaps(A, ldw, piv, k0, k0, k0 + nb, c0, c1);
+    };
+    // Outer steps of two 64-column panels with a deferred trailing update of
+    // depth 128 (half the C-tile passes, twice the work per C tile): panel 2 is
+    // brought up to date by panel 1 (its 64 columns only) and factored; then
+    // both panels' interchanges hit the right columns, U12 is solved by block
+    // forward substitution (U_a = La^-1 A_top, A_bot -= L21' U_a,
+    // U_b = Lb^-1 A_bot) and A22 -= L21 U12 runs once with K = 128.  Row
+    // exchanges commute with the deferred row updates because panel 2's
+    // exchanges are also applied to panel 1's L columns.
+    // (Small orders keep one panel per step: the extra calls of the deferred
+    // scheme cost more latency than the deeper trailing GEMM saves.)
+    const int step = r >= DEEP_MIN_R ? 2 * NB : NB;
+    for (int K0 = 0; K0 < r; K0 += step) {
+      const int nb1 = min(NB, r - K0), nb2 = step == NB ? 0 : max(0, min(NB, r - K0 - nb1)), nbt = nb1 + nb2;
+      factor_panel(K0, nb1, K0);
+      if (nb2 > 0) {
+        apply_swaps(A, ldw, piv, K0, K0, K0 + nb1, K0 + nb1, K0 + nbt);
+        __syncthreads();
+        panel_trsm(P, A, K0, nb1, K0 + nb1, K0 + nbt, smem, &bars);
+        GemmT::run(&P.maps, A, ldw, K0 + nb1, K0, K0, K0 + nb1, r - K0 - nb1, nb2, nb1, (char*)smem, &bars,
+                   blockIdx.x);
+        __syncthreads();
+        factor_panel(K0 + nb1, nb2, K0);
+        apply_swaps(A, ldw, piv, K0, K0 + nb1, K0 + nbt, K0, K0 + nb1);
+        __syncthreads();
+      }
+      const int c0 = K0 + nbt, c1 = r + s;
+      apply_swaps(A, ldw, piv, K0, K0, K0 + nbt, c0, c1);
       __syncthreads();
       PH_MARK(3);
-      panel_trsm(P, A, k0, nb, c0, c1, smem, &bars);
+      panel_trsm(P, A, K0, nb1, c0, c1, smem, &bars);
+      if (nb2 > 0) {
+        GemmT::run(&P.maps, A, ldw, K0 + nb1, K0, K0, c0, nb2, c1 - c0, nb1, (char*)smem, &bars, blockIdx.x);
+        __syncthreads();
+        panel_trsm(P, A, K0 + nb1, nb2, c0, c1, smem, &bars);
+      }
       PH_MARK(4);
       if (c0 < r) {
-        GemmT::run(&P.maps, A, ldw, c0, k0, k0, c0, r - c0, c1 - c0, nb, (char*)smem, &bars, blockIdx.x);
+        GemmT::run(&P.maps, A, ldw, c0, K0, K0, c0, r - c0, c1 - c0, nbt, (char*)smem, &bars, blockIdx.x);
         __syncthreads();
         PH_MARK(5);
       }
