@@ -39,7 +39,8 @@ using GemmNarrow = Gemm<64, 16, 8, 1, 2, EPI_SUB>; // back-substitution updates 
 using GemmOut = Gemm<64, 16, 8, 1, 2, EPI_SET>;   // y = C_R x
 
 constexpr int LDL = NB + 4;     // == 4 (mod 8): triangular inverse used as A operand
-constexpr int DEEP_MIN_R = 640; // deferred 128-deep trailing updates from this order on
+constexpr int DEEP_MIN_R = 640;   // outer steps of 2 panels (trailing K = 128) from this order on
+constexpr int DEEP4_MIN_R = 1536; // ... of 4 panels (K = 256)
 constexpr int LDY = 16 + 2;
 constexpr size_t TRSM_SMEM = (size_t)(NB * LDL) * sizeof(z_t);
 constexpr size_t BACK_SMEM = (size_t)(NB * LDL + NB * LDY) * sizeof(z_t);
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
   // 1024-byte aligned base (128B-swizzled TMA boxes)
   double2* smem = (double2*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ GemmT::Bars bars;
-  __shared__ int piv[2 * NB];  // the two panels of an outer 128-column step
+  __shared__ int piv[4 * NB];  // the panels of an outer step (up to 4)
   __shared__ double rv[2 * (NT / 32)];
   __shared__ int ri[2 * (NT / 32)];
   __shared__ int s_info;
@@ -543,33 +544,41 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
     // exchanges are also applied to panel 1's L columns.
     // (Small orders keep one panel per step: the extra calls of the deferred
     // scheme cost more latency than the deeper trailing GEMM saves.)
-    const int step = r >= DEEP_MIN_R ? 2 * NB : NB;
-    for (int K0 = 0; K0 < r; K0 += step) {
-      const int nb1 = min(NB, r - K0), nb2 = step == NB ? 0 : max(0, min(NB, r - K0 - nb1)), nbt = nb1 + nb2;
-      factor_panel(K0, nb1, K0);
-      if (nb2 > 0) {
-        apply_swaps(A, ldw, piv, K0, K0, K0 + nb1, K0 + nb1, K0 + nbt);
-        __syncthreads();
-        panel_trsm(P, A, K0, nb1, K0 + nb1, K0 + nbt, smem, &bars);
-        GemmT::run(&P.maps, A, ldw, K0 + nb1, K0, K0, K0 + nb1, r - K0 - nb1, nb2, nb1, (char*)smem, &bars,
-                   blockIdx.x);
-        __syncthreads();
-        factor_panel(K0 + nb1, nb2, K0);
-        apply_swaps(A, ldw, piv, K0, K0 + nb1, K0 + nbt, K0, K0 + nb1);
-        __syncthreads();
+    const int mp = r >= DEEP4_MIN_R ? 4 : (r >= DEEP_MIN_R ? 2 : 1);  // panels per outer step
+    for (int K0 = 0; K0 < r; K0 += mp * NB) {
+      const int nbt = min(mp * NB, r - K0), npan = (nbt + NB - 1) / NB;
+      // right-looking LU of the step's columns [K0, K0 + nbt), panel by panel
+      for (int pj = 0; pj < npan; ++pj) {
+        const int pk0 = K0 + pj * NB, pnb = min(NB, K0 + nbt - pk0), pe = pk0 + pnb;
+        factor_panel(pk0, pnb, K0);
+        if (pj > 0) {  // this panel's interchanges on the step's earlier L columns
+          apply_swaps(A, ldw, piv, K0, pk0, pe, K0, pk0);
+          __syncthreads();
+        }
+        if (pe < K0 + nbt) {  // bring the step's later columns up to date with this panel
+          apply_swaps(A, ldw, piv, K0, pk0, pe, pe, K0 + nbt);
+          __syncthreads();
+          panel_trsm(P, A, pk0, pnb, pe, K0 + nbt, smem, &bars);
+          GemmT::run(&P.maps, A, ldw, pe, pk0, pk0, pe, r - pe, K0 + nbt - pe, pnb, (char*)smem, &bars,
+                     blockIdx.x);
+          __syncthreads();
+        }
       }
       const int c0 = K0 + nbt, c1 = r + s;
-      apply_swaps(A, ldw, piv, K0, K0, K0 + nbt, c0, c1);
+      apply_swaps(A, ldw, piv, K0, K0, c0, c0, c1);
       __syncthreads();
       PH_MARK(3);
-      panel_trsm(P, A, K0, nb1, c0, c1, smem, &bars);
-      if (nb2 > 0) {
-        GemmT::run(&P.maps, A, ldw, K0 + nb1, K0, K0, c0, nb2, c1 - c0, nb1, (char*)smem, &bars, blockIdx.x);
-        __syncthreads();
-        panel_trsm(P, A, K0 + nb1, nb2, c0, c1, smem, &bars);
+      // U12 = L11^-1 A12 by block forward substitution over the step's panels
+      for (int pj = 0; pj < npan; ++pj) {
+        const int pk0 = K0 + pj * NB, pnb = min(NB, c0 - pk0), pe = pk0 + pnb;
+        panel_trsm(P, A, pk0, pnb, c0, c1, smem, &bars);
+        if (pe < c0) {
+          GemmT::run(&P.maps, A, ldw, pe, pk0, pk0, c0, c0 - pe, c1 - c0, pnb, (char*)smem, &bars, blockIdx.x);
+          __syncthreads();
+        }
       }
       PH_MARK(4);
-      if (c0 < r) {
+      if (c0 < r) {  // A22 -= L21 U12 with K = the whole step
         GemmT::run(&P.maps, A, ldw, c0, K0, K0, c0, r - c0, c1 - c0, nbt, (char*)smem, &bars, blockIdx.x);
         __syncthreads();
         PH_MARK(5);
