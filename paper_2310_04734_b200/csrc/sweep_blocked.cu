@@ -97,7 +97,8 @@ struct __align__(64) Params {
   int* info;
   z_t* work;
   int ldw;            // leading dimension of the augmented matrix
-  int w;              // inner panel width
+  int w;              // inner panel width for the full height r
+  int leaf_bytes;     // shared memory available to a leaf (rows + logical ids)
   size_t cta_stride;  // workspace elements per CTA
 };
 
@@ -257,8 +258,8 @@ __device__ void inner_panel_w(const Params& P, z_t* A, int k0, int j0, int wc, z
 }
 
 __device__ void inner_panel(const Params& P, z_t* A, int k0, int j0, int wc, z_t* Ps, int* lg, int* piv,
-                            int* s_info, double* rv, int* ri, z_t* rz) {
-  switch (P.w) {
+                            int* s_info, double* rv, int* ri, z_t* rz, int pw) {
+  switch (pw) {
     case 16: inner_panel_w<16>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
     case 8: inner_panel_w<8>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
     case 4: inner_panel_w<4>(P, A, k0, j0, wc, Ps, lg, piv, s_info, rv, ri, rz); return;
@@ -499,12 +500,18 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
     // updated with one TRSM + one GEMM of depth 2^k w.  Pivots go to
     // piv[j - pbase].
     auto factor_panel = [&](int pk0, int pnb, int pbase) {
-      const int nleaves = (pnb + P.w - 1) / P.w;
+      // leaf width: the widest of 16 / 8 / P.w whose rows (r - pk0 of them)
+      // fit in shared memory — lower panels get wider leaves
+      const int H = r - pk0;
+      int pw = P.w;
+      if (pw < 16 && (size_t)H * (17 * sizeof(z_t) + sizeof(int)) <= (size_t)P.leaf_bytes) pw = 16;
+      else if (pw < 8 && (size_t)H * (9 * sizeof(z_t) + sizeof(int)) <= (size_t)P.leaf_bytes) pw = 8;
+      const int nleaves = (pnb + pw - 1) / pw;
       for (int l = 0; l < nleaves; ++l) {
-        const int j0 = pk0 + l * P.w;
-        const int wc = min(P.w, pk0 + pnb - j0);
-        inner_panel(P, A, pbase, j0, wc, smem, (int*)(smem + (size_t)(r - j0) * (P.w + 1)), piv, &s_info, rv,
-                    ri, rz);
+        const int j0 = pk0 + l * pw;
+        const int wc = min(pw, pk0 + pnb - j0);
+        inner_panel(P, A, pbase, j0, wc, smem, (int*)(smem + (size_t)(r - j0) * (pw + 1)), piv, &s_info, rv,
+                    ri, rz, pw);
         PH_MARK(1);
         PH_SUB_BEGIN;
         apply_swaps(A, ldw, piv, pbase, j0, j0 + wc, pk0, j0);
@@ -513,7 +520,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
         PH_SUB(10);
         if (l + 1 < nleaves) {
           const int kk = __ffs(~l) - 1;           // trailing ones of l
-          const int n1 = (1 << kk) * P.w;         // left subtree width
+          const int n1 = (1 << kk) * pw;          // left subtree width
           const int cl = j0 + wc - n1;            // left subtree start column
           const int rc0 = j0 + wc, rc1 = min(rc0 + n1, pk0 + pnb);
           if (n1 <= 8 && rc1 - rc0 <= 8) {  // TRSM fused into the skinny update
@@ -722,6 +729,7 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
   P.prims = prims; P.alpha = alpha; P.b = b; P.b_stride_f = b_stride_f; P.c_r = c_r;
   P.y = y; P.spl = spl; P.x = x; P.info = info;
   P.work = (z_t*)work; P.ldw = blk::ldw_of(r, s); P.w = w;
+  P.leaf_bytes = (int)(blk::smem_bytes(r, w) - 1024);
   P.cta_stride = blk::cta_stride(r, s, n_out);
   {
     const int grid = blocked_grid(F);
