@@ -195,44 +195,86 @@ __global__ void __launch_bounds__(NT) zgemm_nn_kernel(int m, int n, int k, z_t a
               gridDim.x);
 }
 
-// Split-K C_part[s] = A_s^H B_s over k-chunks s (A: k x m, B: k x n, row-major),
-// A^H staged transposed+conjugated in shared memory; one (tile, chunk) per CTA.
-constexpr int CN_TM = 64, CN_TN = 32, CN_KCH = 512;
-constexpr int CN_LDA = KC + 4, CN_LDB = CN_TN + 2;
+// Split-K C_part[s] = A_s^H B_s over k-chunks s (A: k x m, B: k x n, row-major):
+// one (tile, chunk) per CTA, 64 x 32 tiles.  Both operands stream through a
+// 3-stage cp.async ring in their natural [k][.] layout (A is NOT transposed on
+// the way in: the A^H fragments are read column-wise from the [k][i] tile, row
+// stride == 2 (mod 8) 16-byte units so the 8 lanes of a quarter-warp hit 8
+// distinct bank groups) and conjugated in registers.
+constexpr int CN_TM = 64, CN_TN = 32, CN_KCH = 512, CN_ST = 3;
+constexpr int CN_LDA = CN_TM + 2, CN_LDB = CN_TN + 2;
+constexpr size_t CN_SMEM = (size_t)CN_ST * KC * (CN_LDA + CN_LDB) * sizeof(z_t);
 
 __global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int k, const z_t* __restrict__ A,
                                                               int64_t lda, const z_t* __restrict__ B,
                                                               int64_t ldb, z_t* __restrict__ part) {
-  __shared__ z_t As[CN_TM * CN_LDA];
-  __shared__ z_t Bs[KC * CN_LDB];
+  extern __shared__ double2 cn_smem[];
+  z_t (*As)[KC * CN_LDA] = reinterpret_cast<z_t (*)[KC * CN_LDA]>(cn_smem);                       // [k][i]
+  z_t (*Bs)[KC * CN_LDB] = reinterpret_cast<z_t (*)[KC * CN_LDB]>(cn_smem + CN_ST * KC * CN_LDA);  // [k][j]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps, 16 x 16 each
   const int ntn = (n + CN_TN - 1) / CN_TN, ntm = (m + CN_TM - 1) / CN_TM;
   const int tile = blockIdx.x % (ntm * ntn), split = blockIdx.x / (ntm * ntn);
   const int m0 = (tile / ntn) * CN_TM, n0 = (tile % ntn) * CN_TN;
   const int kb = split * CN_KCH, ke = min(k, kb + CN_KCH);
+  const int nch = (ke - kb + KC - 1) / KC;
+  auto load = [&](int c, int st) {
+    const int k0 = kb + c * KC;
+#pragma unroll
+    for (int q = 0; q < (KC * CN_TM) / NT; ++q) {  // 4 per thread
+      const int e = tid + q * NT, kk = e / CN_TM, i = e - kk * CN_TM;
+      const bool ok = k0 + kk < ke && m0 + i < m;
+      blk::cp_async16(&As[st][kk * CN_LDA + i], ok ? (const void*)(A + (int64_t)(k0 + kk) * lda + m0 + i) : A, ok);
+    }
+#pragma unroll
+    for (int q = 0; q < (KC * CN_TN) / NT; ++q) {  // 2 per thread
+      const int e = tid + q * NT, kk = e / CN_TN, j = e - kk * CN_TN;
+      const bool ok = k0 + kk < ke && n0 + j < n;
+      blk::cp_async16(&Bs[st][kk * CN_LDB + j], ok ? (const void*)(B + (int64_t)(k0 + kk) * ldb + n0 + j) : B, ok);
+    }
+  };
   double cr[2][2][2], ci[2][2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-  for (int k0 = kb; k0 < ke; k0 += KC) {
-    for (int e = tid; e < KC * CN_TM; e += NT) {
-      const int kk = e / CN_TM, i = e - kk * CN_TM;
-      z_t v = zmake(0.0, 0.0);
-      if (k0 + kk < ke && m0 + i < m) v = A[(int64_t)(k0 + kk) * lda + m0 + i];
-      As[i * CN_LDA + kk] = zmake(v.x, -v.y);
-    }
-    for (int e = tid; e < KC * CN_TN; e += NT) {
-      const int kk = e / CN_TN, j = e - kk * CN_TN;
-      z_t v = zmake(0.0, 0.0);
-      if (k0 + kk < ke && n0 + j < n) v = B[(int64_t)(k0 + kk) * ldb + n0 + j];
-      Bs[kk * CN_LDB + j] = v;
-    }
-    __syncthreads();
-    blk::warp_cmma<2, 2, false>(cr, ci, As + (wm * 16) * CN_LDA, CN_LDA, Bs + wn * 16, CN_LDB, KC / 4);
-    __syncthreads();
+#pragma unroll
+  for (int c = 0; c < CN_ST - 1; ++c) {
+    if (c < nch) load(c, c);
+    blk::cp_commit();
   }
+  const int ar = lane >> 2, ak = lane & 3;
+  for (int c = 0; c < nch; ++c) {
+    blk::cp_wait<CN_ST - 2>();
+    __syncthreads();
+    if (c + CN_ST - 1 < nch) load(c + CN_ST - 1, (c + CN_ST - 1) % CN_ST);
+    blk::cp_commit();
+    const z_t* as = As[c % CN_ST];
+    const z_t* bs = Bs[c % CN_ST];
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const int kr = kk * 4 + ak;
+      z_t a[2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = as[kr * CN_LDA + wm * 16 + i * 8 + ar];  // A^H[i][k] = conj(A[k][i])
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = bs[kr * CN_LDB + wn * 16 + j * 8 + ar];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const double br = b[j].x, bi = b[j].y, nbi = -bi;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          // conj(a) b: re = ar br + ai bi ; im = ar bi - ai br
+          const double nai = -a[i].y;
+          blk::dmma(cr[i][j][0], cr[i][j][1], a[i].x, br);
+          blk::dmma(cr[i][j][0], cr[i][j][1], nai, nbi);
+          blk::dmma(ci[i][j][0], ci[i][j][1], a[i].x, bi);
+          blk::dmma(ci[i][j][0], ci[i][j][1], nai, br);
+        }
+      }
+    }
+  }
+  blk::cp_wait<0>();
   z_t* P = part + (int64_t)split * m * n;
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -292,7 +334,8 @@ int zgemm(char transa, int m, int n, int k, z_t alpha, const z_t* A, int64_t lda
   VB_CHECK_ARG(k > 0, "vb_zgemm: k must be positive");
   VB_CHECK_ARG(work && work_bytes >= zgemm_workspace_bytes(transa, m, n, k), "vb_zgemm: workspace too small");
   const int ntiles = ((m + CN_TM - 1) / CN_TM) * ((n + CN_TN - 1) / CN_TN);
-  zgemm_cn_partial_kernel<<<(unsigned)(ntiles * nsplit), NT, 0, st>>>(m, n, k, A, lda, B, ldb, (z_t*)work);
+  VB_CUDA(cudaFuncSetAttribute(zgemm_cn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CN_SMEM));
+  zgemm_cn_partial_kernel<<<(unsigned)(ntiles * nsplit), NT, CN_SMEM, st>>>(m, n, k, A, lda, B, ldb, (z_t*)work);
   VB_LAUNCHED("zgemm_cn_partial_kernel");
   const int64_t mn = (int64_t)m * n;
   zgemm_cn_reduce_kernel<<<(unsigned)((mn + 255) / 256), 256, 0, st>>>(m, n, nsplit, (const z_t*)work,
