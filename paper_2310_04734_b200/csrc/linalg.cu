@@ -185,52 +185,81 @@ using blk::NT;
 using blk::KC;
 
 // C = alpha A B + beta C, A (m x k), B (k x n): DMMA tiles over the grid.
+// n <= 16 (W -= V G in the basis orthogonalisation: V streamed once, G tiny)
+// uses 128 x 16 tiles so the padded DMMA work stays below the HBM time.
 using GemmNN = blk::Gemm<64, 32, 4, 2, 3, blk::EPI_AXPBY>;
+using GemmNN16 = blk::Gemm<128, 16, 8, 1, 3, blk::EPI_AXPBY>;
 
+template <class G>
 __global__ void __launch_bounds__(NT) zgemm_nn_kernel(int m, int n, int k, z_t alpha, const z_t* A,
                                                       int64_t lda, const z_t* B, int64_t ldb,
                                                       z_t beta, z_t* C, int64_t ldc) {
   extern __shared__ double2 smem[];
-  GemmNN::run(C, (int)ldc, A, (int)lda, B, (int)ldb, m, n, k, smem, alpha, beta, blockIdx.x,
-              gridDim.x);
+  G::run(C, (int)ldc, A, (int)lda, B, (int)ldb, m, n, k, smem, alpha, beta, blockIdx.x, gridDim.x);
+}
+
+template <class G, int TM, int TN>
+static int launch_nn(int m, int n, int k, z_t alpha, const z_t* A, int64_t lda, const z_t* B, int64_t ldb,
+                     z_t beta, z_t* C, int64_t ldc, cudaStream_t st) {
+  const int ntiles = ((m + TM - 1) / TM) * ((n + TN - 1) / TN);
+  int dev = 0, nsm = 148, per_sm = 1;
+  VB_CUDA(cudaGetDevice(&dev));
+  VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  VB_CUDA(cudaFuncSetAttribute(zgemm_nn_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+  VB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zgemm_nn_kernel<G>, NT, G::SMEM));
+  if (per_sm < 1) per_sm = 1;
+  const int grid = ntiles < per_sm * nsm ? ntiles : per_sm * nsm;
+  zgemm_nn_kernel<G><<<grid, NT, G::SMEM, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  VB_LAUNCHED("zgemm_nn_kernel");
+  return 0;
 }
 
 // Split-K C_part[s] = A_s^H B_s over k-chunks s (A: k x m, B: k x n, row-major):
-// one (tile, chunk) per CTA, 64 x 32 tiles.  Both operands stream through a
-// 3-stage cp.async ring in their natural [k][.] layout (A is NOT transposed on
-// the way in: the A^H fragments are read column-wise from the [k][i] tile, row
-// stride == 2 (mod 8) 16-byte units so the 8 lanes of a quarter-warp hit 8
-// distinct bank groups) and conjugated in registers.
-constexpr int CN_TM = 64, CN_TN = 32, CN_KCH = 512, CN_ST = 3;
-constexpr int CN_LDA = CN_TM + 2, CN_LDB = CN_TN + 2;
-constexpr size_t CN_SMEM = (size_t)CN_ST * KC * (CN_LDA + CN_LDB) * sizeof(z_t);
+// one (tile, chunk) per CTA, TM x TN tiles (64 x 32, or 128 x 16 when n <= 16:
+// the tall-skinny V^H W of the basis orthogonalisation, where padding n = 10 to
+// 32 made the kernel DMMA-bound at 3x the useful work).  Both operands stream
+// through a 3-stage cp.async ring in their natural [k][.] layout (A is NOT
+// transposed on the way in: the A^H fragments are read column-wise from the
+// [k][i] tile, row stride == 2 (mod 8) 16-byte units so the 8 lanes of a
+// quarter-warp hit 8 distinct bank groups) and conjugated in registers.
+constexpr int CN_KCH = 512, CN_ST = 3;
+template <int TM, int TN>
+struct CnCfg {
+  static constexpr int WN = TN / 16, WM = (NT / 32) / WN;  // warps, 16 x 16 each
+  static_assert(WM * 16 == TM, "warp grid");
+  static constexpr int LDA = TM + 2, LDB = TN + 2;
+  static constexpr size_t SMEM = (size_t)CN_ST * KC * (LDA + LDB) * sizeof(z_t);
+};
 
+template <int TM, int TN>
 __global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int k, const z_t* __restrict__ A,
                                                               int64_t lda, const z_t* __restrict__ B,
                                                               int64_t ldb, z_t* __restrict__ part) {
+  using Cfg = CnCfg<TM, TN>;
+  constexpr int LDA = Cfg::LDA, LDB = Cfg::LDB;
   extern __shared__ double2 cn_smem[];
-  z_t (*As)[KC * CN_LDA] = reinterpret_cast<z_t (*)[KC * CN_LDA]>(cn_smem);                       // [k][i]
-  z_t (*Bs)[KC * CN_LDB] = reinterpret_cast<z_t (*)[KC * CN_LDB]>(cn_smem + CN_ST * KC * CN_LDA);  // [k][j]
+  z_t (*As)[KC * LDA] = reinterpret_cast<z_t (*)[KC * LDA]>(cn_smem);                    // [k][i]
+  z_t (*Bs)[KC * LDB] = reinterpret_cast<z_t (*)[KC * LDB]>(cn_smem + CN_ST * KC * LDA);  // [k][j]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps, 16 x 16 each
-  const int ntn = (n + CN_TN - 1) / CN_TN, ntm = (m + CN_TM - 1) / CN_TM;
+  const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
+  const int ntn = (n + TN - 1) / TN, ntm = (m + TM - 1) / TM;
   const int tile = blockIdx.x % (ntm * ntn), split = blockIdx.x / (ntm * ntn);
-  const int m0 = (tile / ntn) * CN_TM, n0 = (tile % ntn) * CN_TN;
+  const int m0 = (tile / ntn) * TM, n0 = (tile % ntn) * TN;
   const int kb = split * CN_KCH, ke = min(k, kb + CN_KCH);
   const int nch = (ke - kb + KC - 1) / KC;
   auto load = [&](int c, int st) {
     const int k0 = kb + c * KC;
 #pragma unroll
-    for (int q = 0; q < (KC * CN_TM) / NT; ++q) {  // 4 per thread
-      const int e = tid + q * NT, kk = e / CN_TM, i = e - kk * CN_TM;
+    for (int q = 0; q < (KC * TM) / NT; ++q) {
+      const int e = tid + q * NT, kk = e / TM, i = e - kk * TM;
       const bool ok = k0 + kk < ke && m0 + i < m;
-      blk::cp_async16(&As[st][kk * CN_LDA + i], ok ? (const void*)(A + (int64_t)(k0 + kk) * lda + m0 + i) : A, ok);
+      blk::cp_async16(&As[st][kk * LDA + i], ok ? (const void*)(A + (int64_t)(k0 + kk) * lda + m0 + i) : A, ok);
     }
 #pragma unroll
-    for (int q = 0; q < (KC * CN_TN) / NT; ++q) {  // 2 per thread
-      const int e = tid + q * NT, kk = e / CN_TN, j = e - kk * CN_TN;
+    for (int q = 0; q < (KC * TN) / NT; ++q) {
+      const int e = tid + q * NT, kk = e / TN, j = e - kk * TN;
       const bool ok = k0 + kk < ke && n0 + j < n;
-      blk::cp_async16(&Bs[st][kk * CN_LDB + j], ok ? (const void*)(B + (int64_t)(k0 + kk) * ldb + n0 + j) : B, ok);
+      blk::cp_async16(&Bs[st][kk * LDB + j], ok ? (const void*)(B + (int64_t)(k0 + kk) * ldb + n0 + j) : B, ok);
     }
   };
   double cr[2][2][2], ci[2][2][2];
@@ -256,9 +285,9 @@ __global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int 
       const int kr = kk * 4 + ak;
       z_t a[2], b[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) a[i] = as[kr * CN_LDA + wm * 16 + i * 8 + ar];  // A^H[i][k] = conj(A[k][i])
+      for (int i = 0; i < 2; ++i) a[i] = as[kr * LDA + wm * 16 + i * 8 + ar];  // A^H[i][k] = conj(A[k][i])
 #pragma unroll
-      for (int j = 0; j < 2; ++j) b[j] = bs[kr * CN_LDB + wn * 16 + j * 8 + ar];
+      for (int j = 0; j < 2; ++j) b[j] = bs[kr * LDB + wn * 16 + j * 8 + ar];
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const double br = b[j].x, bi = b[j].y, nbi = -bi;
@@ -288,20 +317,109 @@ __global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int 
       }
 }
 
-__global__ void zgemm_cn_reduce_kernel(int m, int n, int nsplit, const z_t* __restrict__ part, z_t alpha,
-                                       z_t beta, z_t* __restrict__ C, int64_t ldc) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)m * n) return;
+template <int TM, int TN>
+static int launch_cn_partial(int m, int n, int k, const z_t* A, int64_t lda, const z_t* B, int64_t ldb, z_t* work,
+                             int nsplit, cudaStream_t st) {
+  const int ntiles = ((m + TM - 1) / TM) * ((n + TN - 1) / TN);
+  const size_t smem = CnCfg<TM, TN>::SMEM;
+  VB_CUDA(cudaFuncSetAttribute(zgemm_cn_partial_kernel<TM, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  zgemm_cn_partial_kernel<TM, TN><<<(unsigned)(ntiles * nsplit), NT, smem, st>>>(m, n, k, A, lda, B, ldb, work);
+  VB_LAUNCHED("zgemm_cn_partial_kernel");
+  return 0;
+}
+
+// C = alpha sum_s C_part[s] + beta C: a CTA owns 32 consecutive outputs (one
+// per lane, coalesced split rows), its 8 warps take splits w, w + 8, ... and
+// combine their partial sums in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) zgemm_cn_reduce_kernel(int m, int n, int nsplit,
+                                                              const z_t* __restrict__ part, z_t alpha, z_t beta,
+                                                              z_t* __restrict__ C, int64_t ldc) {
+  __shared__ z_t red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t mn = (int64_t)m * n;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
   z_t acc = zmake(0.0, 0.0);
-  for (int s = 0; s < nsplit; ++s) acc = zadd(acc, part[(int64_t)s * m * n + e]);  // fixed order
-  const int64_t i = e / n, j = e - i * n;
-  z_t out = zmul(alpha, acc);
-  if (beta.x != 0.0 || beta.y != 0.0) out = zfma(out, beta, C[i * ldc + j]);
-  C[i * ldc + j] = out;
+  if (e < mn)
+    for (int s = warp; s < nsplit; s += 8) acc = zadd(acc, part[(int64_t)s * mn + e]);
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && e < mn) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) acc = zadd(acc, red[w][lane]);
+    const int64_t i = e / n, j = e - i * n;
+    z_t out = zmul(alpha, acc);
+    if (beta.x != 0.0 || beta.y != 0.0) out = zfma(out, beta, C[i * ldc + j]);
+    C[i * ldc + j] = out;
+  }
+}
+
+// ------------------------------------------------- narrow GEMV (n == 1) ---
+// The in-block Gram-Schmidt of the basis orthogonalisation projects one column
+// w against the j <= 64 columns already kept: y = A^H w and w -= A y.  On the
+// DMMA tile kernels these are > 99 % padding; here they are HBM streams on the
+// CUDA cores: a warp per row, lanes over the (<= 64) columns.  Fixed row
+// partition (GV_GRID CTAs) + fixed-order reductions -> deterministic.
+constexpr int GV_GRID = 4 * 148, GV_MAXM = 64;
+
+__global__ void __launch_bounds__(256) zgemv_cn_partial_kernel(int k, int m, const z_t* __restrict__ A, int64_t lda,
+                                                               const z_t* __restrict__ x, int64_t ldx,
+                                                               z_t* __restrict__ part) {
+  __shared__ z_t red[8][GV_MAXM];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t chunk = ((int64_t)k + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min((int64_t)k, r0 + chunk);
+  z_t a0 = zmake(0.0, 0.0), a1 = zmake(0.0, 0.0);
+  const bool c0 = lane < m, c1 = lane + 32 < m;
+#pragma unroll 4
+  for (int64_t r = r0 + warp; r < r1; r += 8) {
+    const z_t xv = x[r * ldx];
+    const z_t* Ar = A + r * lda;
+    if (c0) { const z_t a = Ar[lane]; a0 = zmake(a0.x + a.x * xv.x + a.y * xv.y, a0.y + a.x * xv.y - a.y * xv.x); }
+    if (c1) { const z_t a = Ar[lane + 32]; a1 = zmake(a1.x + a.x * xv.x + a.y * xv.y, a1.y + a.x * xv.y - a.y * xv.x); }
+  }
+  red[warp][lane] = a0;
+  red[warp][lane + 32] = a1;
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      a0 = zadd(a0, red[w][lane]);
+      a1 = zadd(a1, red[w][lane + 32]);
+    }
+    if (c0) part[(int64_t)blockIdx.x * m + lane] = a0;
+    if (c1) part[(int64_t)blockIdx.x * m + lane + 32] = a1;
+  }
+}
+
+// y = alpha A g + beta y  (A: rows x k, k <= 64; g, y single columns): a
+// thread per row (its k loads are independent and hit the same L1 lines as
+// its warp neighbours'), g broadcast from shared memory.
+__global__ void __launch_bounds__(256) zgemv_nn_kernel(int rows, int k, z_t alpha, const z_t* __restrict__ A,
+                                                       int64_t lda, const z_t* __restrict__ g, int64_t ldg, z_t beta,
+                                                       z_t* __restrict__ y, int64_t ldy) {
+  __shared__ z_t gs[GV_MAXM];
+  if (threadIdx.x < k) gs[threadIdx.x] = g[threadIdx.x * ldg];
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const z_t* Ar = A + r * lda;
+  z_t acc0 = zmake(0.0, 0.0), acc1 = zmake(0.0, 0.0);
+  int c = 0;
+#pragma unroll 4
+  for (; c + 1 < k; c += 2) {
+    acc0 = zfma(acc0, Ar[c], gs[c]);
+    acc1 = zfma(acc1, Ar[c + 1], gs[c + 1]);
+  }
+  if (c < k) acc0 = zfma(acc0, Ar[c], gs[c]);
+  z_t out = zmul(alpha, zadd(acc0, acc1));
+  if (beta.x != 0.0 || beta.y != 0.0) out = zfma(out, beta, y[r * ldy]);
+  y[r * ldy] = out;
 }
 
 size_t zgemm_workspace_bytes(char transa, int m, int n, int k) {
   if (transa == 'N' || transa == 'n') return 0;
+  if (n == 1 && m <= GV_MAXM) return (size_t)GV_GRID * m * sizeof(z_t);
   const int64_t nsplit = (k + CN_KCH - 1) / CN_KCH;
   return (size_t)nsplit * m * n * sizeof(z_t);
 }
@@ -315,30 +433,34 @@ int zgemm(char transa, int m, int n, int k, z_t alpha, const z_t* A, int64_t lda
       set_error("vb_zgemm: k must be positive");
       return 1;
     }
-    const int ntiles = ((m + 63) / 64) * ((n + 31) / 32);
-    int dev = 0, nsm = 148;
-    VB_CUDA(cudaGetDevice(&dev));
-    VB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const int grid = ntiles < 2 * nsm ? ntiles : 2 * nsm;
-    VB_CUDA(cudaFuncSetAttribute(zgemm_nn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)GemmNN::SMEM));
-    zgemm_nn_kernel<<<grid, NT, GemmNN::SMEM, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-    VB_LAUNCHED("zgemm_nn_kernel");
-    return 0;
+    if (n == 1 && k <= GV_MAXM) {
+      zgemv_nn_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, k, alpha, A, lda, B, ldb, beta, C, ldc);
+      VB_LAUNCHED("zgemv_nn_kernel");
+      return 0;
+    }
+    if (n <= 16) return launch_nn<GemmNN16, 128, 16>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, st);
+    return launch_nn<GemmNN, 64, 32>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, st);
   }
   if (transa != 'C' && transa != 'c') {
     set_error("vb_zgemm: transa must be 'N' or 'C'");
     return 1;
   }
-  const int nsplit = (k + CN_KCH - 1) / CN_KCH;
   VB_CHECK_ARG(k > 0, "vb_zgemm: k must be positive");
   VB_CHECK_ARG(work && work_bytes >= zgemm_workspace_bytes(transa, m, n, k), "vb_zgemm: workspace too small");
-  const int ntiles = ((m + CN_TM - 1) / CN_TM) * ((n + CN_TN - 1) / CN_TN);
-  VB_CUDA(cudaFuncSetAttribute(zgemm_cn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CN_SMEM));
-  zgemm_cn_partial_kernel<<<(unsigned)(ntiles * nsplit), NT, CN_SMEM, st>>>(m, n, k, A, lda, B, ldb, (z_t*)work);
-  VB_LAUNCHED("zgemm_cn_partial_kernel");
+  if (n == 1 && m <= GV_MAXM) {
+    zgemv_cn_partial_kernel<<<GV_GRID, 256, 0, st>>>(k, m, A, lda, B, ldb, (z_t*)work);
+    VB_LAUNCHED("zgemv_cn_partial_kernel");
+    zgemm_cn_reduce_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(m, 1, GV_GRID, (const z_t*)work, alpha, beta,
+                                                                      C, ldc);
+    VB_LAUNCHED("zgemm_cn_reduce_kernel");
+    return 0;
+  }
+  const int nsplit = (k + CN_KCH - 1) / CN_KCH;
+  const int rc = n <= 16 ? launch_cn_partial<128, 16>(m, n, k, A, lda, B, ldb, (z_t*)work, nsplit, st)
+                         : launch_cn_partial<64, 32>(m, n, k, A, lda, B, ldb, (z_t*)work, nsplit, st);
+  if (rc) return rc;
   const int64_t mn = (int64_t)m * n;
-  zgemm_cn_reduce_kernel<<<(unsigned)((mn + 255) / 256), 256, 0, st>>>(m, n, nsplit, (const z_t*)work,
+  zgemm_cn_reduce_kernel<<<(unsigned)((mn + 31) / 32), 256, 0, st>>>(m, n, nsplit, (const z_t*)work,
                                                                          alpha, beta, C, ldc);
   VB_LAUNCHED("zgemm_cn_reduce_kernel");
   return 0;

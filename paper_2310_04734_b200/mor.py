@@ -493,6 +493,35 @@ def _polish(bases, w: torch.Tensor, nw: float, ref: float):
     return w, float(linalg.column_norms(w).item())
 
 
+# Bases grow in place: _orthonormalise returns the leading columns of a
+# row-major buffer with spare column capacity (a view with unit column stride,
+# leading dimension = capacity; every linalg entry point takes the leading
+# dimension).  The next call appends into the spare columns iff its V is the
+# newest view of that buffer, so an older view a caller kept (a best-so-far
+# basis) never sees its columns change; anything else is copied into a new
+# buffer.  data_ptr -> (width, capacity, rows) of the newest view.
+_BASIS_BUFS: dict[int, tuple[int, int, int]] = {}
+_BASIS_GROWTH = 1.5
+
+
+def _basis_append_view(Vd, n: int, k: int, dev) -> torch.Tensor:
+    """(n x (r + k)) view whose first r columns are Vd, reusing Vd's buffer
+    when it has room and Vd is its newest view."""
+    r = Vd.shape[1] if Vd is not None else 0
+    if Vd is not None and Vd.stride(1) == 1 and Vd.storage_offset() == 0:
+        cap = Vd.stride(0)
+        if (_BASIS_BUFS.get(Vd.data_ptr()) == (r, cap, n) and cap >= r + k
+                and Vd.untyped_storage().nbytes() >= n * cap * 16):
+            return Vd.as_strided((n, r + k), (cap, 1))
+    cap = max(r + k, int(math.ceil((r + k) * _BASIS_GROWTH)))
+    buf = torch.empty((n, cap), dtype=CDT, device=dev)
+    if r:
+        buf[:, :r].copy_(Vd)
+    if len(_BASIS_BUFS) > 16:
+        _BASIS_BUFS.pop(next(iter(_BASIS_BUFS)))
+    return buf[:, :r + k]
+
+
 def _orthonormalise(V, block):
     """Append the columns of `block` to V, twice-orthogonalised; columns that
     become negligible after projection are dropped (mor.py:122-135):
@@ -500,11 +529,11 @@ def _orthonormalise(V, block):
     is_np = not isinstance(block, torch.Tensor) and (V is None or not isinstance(V, torch.Tensor))
     dev = V.device if isinstance(V, torch.Tensor) else (block.device if isinstance(block, torch.Tensor) else _device())
     B = _as_dev(block, dev)
-    n = B.shape[0]
+    n, kb = B.shape
     if V is None:
         Vd = None
     elif isinstance(V, torch.Tensor):
-        Vd = V.contiguous() if V.numel() else None
+        Vd = (V if V.dim() == 2 and V.stride(1) == 1 else V.contiguous()) if V.numel() else None
     else:
         Vd = _as_dev(V, dev) if V.size else None
     refs = linalg.column_norms(B).cpu().numpy()
@@ -516,35 +545,39 @@ def _orthonormalise(V, block):
             linalg.zgemm("N", Vd, G, -1.0, 1.0, X)
 
     # pass 1: project on V (two CGS sweeps = the reference's two MGS passes),
-    # then Gram-Schmidt inside the block with the reference drop rule
+    # then Gram-Schmidt inside the block with the reference drop rule; kept
+    # columns go to Qb[:, :nk] (views, no per-column concatenation)
     if Vd is not None:
         against_V(W)
-    cols = []
-    for j in range(W.shape[1]):
-        w = W[:, j:j + 1].contiguous()
-        if cols:
-            w = _cgs2_against(torch.cat(cols, 1).contiguous(), w)
+    Qb = torch.empty((n, max(kb, 1)), dtype=CDT, device=dev)
+    nk = 0
+    for j in range(kb):
+        w = W[:, j:j + 1]
+        if nk:
+            w = _cgs2_against(Qb[:, :nk], w)
         nw = float(linalg.column_norms(w).item())
         if refs[j] > 0 and nw > ORTH_DROP_TOL * refs[j]:
-            w, nw = _polish((torch.cat(cols, 1).contiguous() if cols else None,), w, nw, refs[j])
-            cols.append(w / nw)
-    # pass 2 (block CGS2, Barlow-Smoktunowicz): re-project the kept, now
-    # orthonormal columns on V and re-orthonormalise inside the block.  Strong
-    # cancellation inside the block in pass 1 amplifies the rounding-level V
-    # components of a column; this pass removes them at block cost.
-    if Vd is not None and cols:
-        Q1 = torch.cat(cols, 1).contiguous()
-        against_V(Q1)
-        cols2 = []
-        for j in range(Q1.shape[1]):
-            w = Q1[:, j:j + 1].contiguous()
-            if cols2:
-                w = _cgs2_against(torch.cat(cols2, 1).contiguous(), w)
-            cols2.append(w / float(linalg.column_norms(w).item()))
-        cols = cols2
-    newV = torch.cat([Vd] + [c for c in cols], dim=1) if Vd is not None else (
-        torch.cat(cols, dim=1) if cols else torch.zeros((n, 0), dtype=CDT, device=dev))
-    newV = newV.contiguous()
+            w, nw = _polish((Qb[:, :nk] if nk else None,), w, nw, refs[j])
+            torch.mul(w, 1.0 / nw, out=Qb[:, nk:nk + 1])
+            nk += 1
+    r = Vd.shape[1] if Vd is not None else 0
+    newV = _basis_append_view(Vd, n, nk, dev)
+    if nk:
+        Q1 = newV[:, r:r + nk]
+        Q1.copy_(Qb[:, :nk])
+        # pass 2 (block CGS2, Barlow-Smoktunowicz): re-project the kept, now
+        # orthonormal columns on V and re-orthonormalise inside the block.
+        # Strong cancellation inside the block in pass 1 amplifies the
+        # rounding-level V components of a column; this pass removes them at
+        # block cost.  In place in the basis buffer; norms stay on the device.
+        if Vd is not None:
+            against_V(Q1)
+            for j in range(nk):
+                w = Q1[:, j:j + 1]
+                if j:
+                    _cgs2_against(Q1[:, :j], w)
+                w.div_(linalg.column_norms(w))
+    _BASIS_BUFS[newV.data_ptr()] = (r + nk, newV.stride(0), n)
     return newV.cpu().numpy() if is_np else newV
 
 

@@ -49,7 +49,8 @@ def test_axpy_dense(cuda):
     np.testing.assert_allclose(Dd.cpu().numpy(), D0 + (2 - 1j) * A.toarray(), rtol=1e-14, atol=1e-14)
 
 
-@pytest.mark.parametrize("m,n,k", [(32, 32, 4641), (76, 76, 8102), (5, 1, 1000), (400, 40, 3000), (1, 7, 13)])
+@pytest.mark.parametrize("m,n,k", [(32, 32, 4641), (76, 76, 8102), (5, 1, 1000), (400, 40, 3000), (1, 7, 13),
+                                   (33, 1, 5000), (64, 1, 100), (65, 1, 300), (300, 10, 20000), (17, 16, 2000)])
 def test_zgemm_conj(cuda, m, n, k):
     import torch
     from paper_2310_04734_b200 import linalg
@@ -61,7 +62,8 @@ def test_zgemm_conj(cuda, m, n, k):
     np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-12, atol=1e-10 * np.abs(ref).max())
 
 
-@pytest.mark.parametrize("m,n,k", [(4641, 8, 32), (100, 33, 70), (1, 1, 1), (257, 16, 513)])
+@pytest.mark.parametrize("m,n,k", [(4641, 8, 32), (100, 33, 70), (1, 1, 1), (257, 16, 513),
+                                   (20000, 1, 33), (5000, 1, 64), (300, 1, 65), (20000, 10, 300)])
 def test_zgemm_nn(cuda, m, n, k):
     import torch
     from paper_2310_04734_b200 import linalg
@@ -73,6 +75,24 @@ def test_zgemm_nn(cuda, m, n, k):
     np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-12, atol=1e-11 * np.abs(ref).max())
     out = linalg.zgemm("N", torch.as_tensor(A, device=cuda), torch.as_tensor(B, device=cuda))
     np.testing.assert_allclose(out.cpu().numpy(), A @ B, rtol=1e-12, atol=1e-11 * np.abs(ref).max())
+
+
+def test_zgemm_strided_views(cuda):
+    """Column slices of a wider buffer (ld > columns), as the basis build uses."""
+    import torch
+    from paper_2310_04734_b200 import linalg
+    rng = np.random.default_rng(7)
+    Vb = torch.as_tensor(_c(rng, 3000, 48), device=cuda)
+    Xb = torch.as_tensor(_c(rng, 3000, 12), device=cuda)
+    for nv, nx in ((40, 1), (40, 10), (9, 1)):
+        V, X = Vb[:, :nv], Xb[:, 2:2 + nx]
+        G = linalg.zgemm("C", V, X)
+        ref = V.conj().T @ X
+        assert float((G - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+        Y = X.clone()
+        linalg.zgemm("N", V, G, -1.0, 1.0, Y)
+        ref2 = X - V @ G
+        assert float((Y - ref2).abs().max()) <= 1e-12 * float(ref2.abs().max())
 
 
 def test_column_norms_and_scale(cuda):
