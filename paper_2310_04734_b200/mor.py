@@ -647,38 +647,46 @@ def krylov_blocks_mimo_dev(fom: FullOrderModel, f_j: float, m: int, second_order
     nv = linalg.column_norms(Vb).cpu().numpy()
     if np.any(nv == 0):
         raise ValueError("zero load at expansion point")
-    cols = [[Vb[:, j:j + 1] / nv[j]] for j in range(s)]
+    # per-source bases grow in place in (n x m) buffers; cnt[j] columns kept
+    Qs = [torch.empty((Vb.shape[0], m), dtype=CDT, device=Vb.device) for _ in range(s)]
+    for j in range(s):
+        torch.mul(Vb[:, j:j + 1], 1.0 / nv[j], out=Qs[j][:, 0:1])
+    cnt = [1] * s
     alive = [True] * s
     use2 = second_order and fom.damping is not None
     w0 = 2.0 * math.pi * f_j
-    prev = [torch.zeros_like(c[0]) for c in cols]
+    prev = [None] * s
     for _ in range(1, m):
         act = [j for j in range(s) if alive[j]]
         if not act:
             break
-        cur = torch.cat([cols[j][-1] for j in act], 1).contiguous()
+        cur = torch.cat([Qs[j][:, cnt[j] - 1:cnt[j]] for j in act], 1)
         if use2:
-            P = torch.cat([prev[j] for j in act], 1).contiguous()
+            P = torch.cat([prev[j] if prev[j] is not None else torch.zeros_like(cur[:, :1]) for j in act], 1)
             rhs = fom.apply("D", f_j, cur)
             fom.apply("M", f_j, cur, scale=2j * w0, out=rhs, beta=1.0)
             fom.apply("M", f_j, P, out=rhs, beta=1.0)
             for j in act:
-                prev[j] = cols[j][-1]
+                prev[j] = Qs[j][:, cnt[j] - 1:cnt[j]]
         else:
             rhs = fom.apply("M", f_j, cur)
         W = lu.solve(rhs)
         W.neg_()
         refs = linalg.column_norms(W).cpu().numpy()
+        # two CGS sweeps per source against its own basis (all sources queued),
+        # then ONE norm read for the drop decisions of the whole moment
         for q, j in enumerate(act):
-            Qb = torch.cat(cols[j], 1).contiguous()
-            w = _cgs2_against(Qb, W[:, q:q + 1].contiguous())
-            nw = float(linalg.column_norms(w).item())
+            _cgs2_against(Qs[j][:, :cnt[j]], W[:, q:q + 1])
+        nws = linalg.column_norms(W).cpu().numpy()
+        for q, j in enumerate(act):
+            nw = float(nws[q])
             if refs[q] == 0 or nw <= ORTH_DROP_TOL * refs[q]:
                 alive[j] = False
                 continue
-            w, nw = _polish((Qb,), w, nw, refs[q])
-            cols[j].append(w / nw)
-    return [(torch.cat(c, 1).contiguous(), not alive[j]) for j, c in enumerate(cols)]
+            w, nw = _polish((Qs[j][:, :cnt[j]],), W[:, q:q + 1], nw, refs[q])
+            torch.mul(w, 1.0 / nw, out=Qs[j][:, cnt[j]:cnt[j] + 1])
+            cnt[j] += 1
+    return [(Qs[j][:, :cnt[j]].contiguous(), not alive[j]) for j in range(s)]
 
 
 # ------------------------------------------------------ certification ----
