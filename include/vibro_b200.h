@@ -234,6 +234,17 @@ int vb_axis_apply(int n2, int n1, int n0, int nrhs, int axis, const vb_complex* 
                   vb_complex* Y, void* stream);
 int vb_fdm_diag(int n2, int n1, int n0, int nrhs, const vb_complex* lz, const vb_complex* ly,
                 const vb_complex* lx, vb_complex sigma, vb_complex* X, void* stream);
+/*  vb_fdm_solve: X = A^-1 B in one call on the FP64 tensor cores (the three
+ *  1-D transforms each way as DMMA GEMMs in an internal RHS-slowest layout,
+ *  transposed in and out).  V_d / VT_d: n_d x n_d row-major eigenvectors and
+ *  their transposes; B, X: n x nrhs row-major with leading dimensions;
+ *  work >= vb_fdm_solve_workspace_bytes (2 n nrhs complex).  Replaces the
+ *  per-column scipy splu solve (vibrofem/mor.py:48-49, 153-156) on boxes. */
+size_t vb_fdm_solve_workspace_bytes(int n2, int n1, int n0, int nrhs);
+int vb_fdm_solve(int n2, int n1, int n0, int nrhs, const vb_complex* Vx, const vb_complex* Vy, const vb_complex* Vz,
+                 const vb_complex* VTx, const vb_complex* VTy, const vb_complex* VTz, const vb_complex* lx,
+                 const vb_complex* ly, const vb_complex* lz, vb_complex sigma, const vb_complex* B, int64_t ldb,
+                 vb_complex* X, int64_t ldx, void* work, size_t work_bytes, void* stream);
 
 /* norms[j] = ||W[:, j]||_2 for an n x m complex row-major W (deterministic). */
 size_t vb_column_norms_workspace_bytes(int n, int m);

@@ -79,6 +79,9 @@ _SIGS = {
                             C.c_void_p, C.c_size_t, C.c_void_p]),
     "vb_axis_apply": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _z, _z, _z, C.c_void_p]),
     "vb_fdm_diag": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _z, _z, _z, VbComplex, _z, C.c_void_p]),
+    "vb_fdm_solve_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "vb_fdm_solve": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _z, _z, _z, _z, _z, _z, _z, _z, _z, VbComplex,
+                               _z, C.c_int64, _z, C.c_int64, C.c_void_p, C.c_size_t, C.c_void_p]),
     "vb_rom_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _z, _z, _z, C.c_int64,
                                _z, _z, C.c_void_p, _z, C.c_void_p, C.c_void_p, C.c_size_t,
                                C.c_void_p]),

@@ -205,6 +205,22 @@ int vb_fdm_diag(int n2, int n1, int n0, int nrhs, const vb_complex* lz, const vb
                       (cudaStream_t)stream);
 }
 
+size_t vb_fdm_solve_workspace_bytes(int n2, int n1, int n0, int nrhs) {
+  return vb::fdm_solve_workspace_bytes(n2, n1, n0, nrhs);
+}
+
+int vb_fdm_solve(int n2, int n1, int n0, int nrhs, const vb_complex* Vx, const vb_complex* Vy, const vb_complex* Vz,
+                 const vb_complex* VTx, const vb_complex* VTy, const vb_complex* VTz, const vb_complex* lx,
+                 const vb_complex* ly, const vb_complex* lz, vb_complex sigma, const vb_complex* B, int64_t ldb,
+                 vb_complex* X, int64_t ldx, void* work, size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(Vx && Vy && Vz && VTx && VTy && VTz && lx && ly && lz, "vb_fdm_solve: null factor pointer");
+  VB_CHECK_ARG(ldb >= nrhs && ldx >= nrhs, "vb_fdm_solve: leading dimension smaller than nrhs");
+  const z_t* V[3] = {(const z_t*)Vx, (const z_t*)Vy, (const z_t*)Vz};
+  const z_t* VT[3] = {(const z_t*)VTx, (const z_t*)VTy, (const z_t*)VTz};
+  return vb::fdm_solve(n2, n1, n0, nrhs, V, VT, (const z_t*)lx, (const z_t*)ly, (const z_t*)lz, zc(sigma),
+                       (const z_t*)B, ldb, (z_t*)X, ldx, work, work_bytes, (cudaStream_t)stream);
+}
+
 int64_t vb_hex27_box_nnz(int nx, int ny, int nz) { return vb::hex27_box_nnz(nx, ny, nz); }
 
 int vb_hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1, int maxnp, int32_t* indptr,

@@ -85,6 +85,10 @@ int zgetrs(int n, int nrhs, const z_t* LU, int64_t lda, const void* aux, const z
 
 // fdm.cu
 int axis_apply(int n2, int n1, int n0, int nrhs, int axis, const z_t* S, const z_t* X, z_t* Y, cudaStream_t st);
+size_t fdm_solve_workspace_bytes(int n2, int n1, int n0, int nrhs);
+int fdm_solve(int n2, int n1, int n0, int nrhs, const z_t* const V[3], const z_t* const VT[3], const z_t* lx,
+              const z_t* ly, const z_t* lz, z_t sigma, const z_t* B, int64_t ldb, z_t* X, int64_t ldx, void* work,
+              size_t work_bytes, cudaStream_t st);
 int fdm_diag(int n2, int n1, int n0, int nrhs, const z_t* lz, const z_t* ly, const z_t* lx, z_t sigma, z_t* X,
              cudaStream_t st);
 
