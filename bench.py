@@ -126,6 +126,28 @@ def cpu_sweep_rate(w, freqs_sample):
     return len(freqs_sample) / dt, dt
 
 
+def cpu_literal_rate(w, n_freq: int = 3):
+    """SURVEY §8(d) CPU baseline (1): the literal reference path,
+    ReducedModel.output (mor.py:73-98: per-frequency re-projection V^H K V,
+    V^H M V, V^H D V, then zgesv) with FOM providers that return the dense
+    reduced matrices and V = I (the tests/test_mor.py:119-125 construction).
+    Reported for completeness next to the affine-sweep port (baseline (2))."""
+    from oracle import mor as omor
+    K, D, M = (np.asarray(p) for p in w.prims)
+    r = K.shape[0]
+    fom = omor.Fom(stiffness=lambda f: K, mass=lambda f: M, load=lambda f: w.b, c_out=w.c_r, n=r,
+                   damping=lambda f: D)
+    V = np.eye(r, dtype=complex)
+    rng = np.random.default_rng(13)
+    fs = w.freqs[np.sort(rng.choice(len(w.freqs), n_freq, replace=False))]
+    omor.reduced_output(fom, V, float(fs[0]))  # warm-up
+    t0 = time.perf_counter()
+    for f in fs:
+        omor.reduced_output(fom, V, float(f))
+    dt = time.perf_counter() - t0
+    return n_freq / dt, dt, n_freq
+
+
 def cpu_sample_size(w, budget_s: float) -> int:
     """Number of frequencies the CPU port finishes in about budget_s seconds
     (pilot of 8 frequencies after a warm-up call)."""
@@ -371,6 +393,10 @@ def run_ours(args):
         cpu = {"value": rate, "unit": UNIT, "cores": blas_threads(), "kind": "port",
                "sample": f"{n} random grid frequencies in {dt:.1f} s, oracle.mor.affine_sweep "
                          f"(numpy.linalg.solve = LAPACK zgesv per frequency, BLAS threads)"}
+        lrate, ldt, ln = cpu_literal_rate(w)
+        cpu["literal_path"] = {"value": lrate, "unit": UNIT, "sample": f"{ln} random grid frequencies in "
+                               f"{ldt:.1f} s", "path": "oracle.mor.reduced_output = ReducedModel.output "
+                               "(mor.py:73-98) with dense reduced providers and V = I"}
 
     offline = None
     if ws == 1 and not args.no_offline:
