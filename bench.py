@@ -219,6 +219,18 @@ def offline_measurements(w):
                         "181-frequency sweep + SPL, wall clock incl. host orchestration")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    fom, lay = workloads.cfg1_model(fdm=True)
+    V = None
+    for f0 in lay["points"]:
+        Q, _ = mor.krylov_block_dev(fom, f0, lay["moments"], second_order=True)
+        V = mor._orthonormalise(V, Q)
+    rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 200.0))
+    res = mor.rom_sweep([rom], list(lay["freqs"]))
+    torch.cuda.synchronize()
+    out["cfg1_pipeline_fdm_s"] = time.perf_counter() - t0
+    out["cfg1_fdm_r"] = int(V.shape[1])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     fom, lay = workloads.cfg2_model()
     V = None
     for f0 in lay["points"]:

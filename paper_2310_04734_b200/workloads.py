@@ -99,11 +99,15 @@ def cfg1_layout(seed: int = 1, box=CFG1_BOX, ne=CFG1_NE, n_rec: int = CFG1_NREC)
     return xyz, conn, src, rec
 
 
-def cfg1_model(seed: int = 1, box=CFG1_BOX, ne=CFG1_NE, n_rec: int = CFG1_NREC, device=None):
+def cfg1_model(seed: int = 1, box=CFG1_BOX, ne=CFG1_NE, n_rec: int = CFG1_NREC, device=None,
+               fdm: bool = False):
     """cfg1 (BASELINE configs[0]): rigid air box 2.0 x 1.6 x 1.2 m, 10 x 8 x 6
     hex27 Helmholtz elements (n = 4641), floor impedance Z = rho c (5 + 1i),
     unit point source, 50 receivers.  All primitives assembled on the GPU;
-    returns (FullOrderModel with an affine operator, layout dict)."""
+    returns (FullOrderModel with an affine operator, layout dict).  Full-order
+    solves use the dense GPU LU (the reference's direct solve, mor.py:48-49)
+    or, with `fdm`, the box fast-diagonalisation solver (one impedance wall:
+    exact Kronecker sum) refined to the same 1e-10 residual contract."""
     import torch
     from . import assembly
     from .mor import AffineOperator, AffineTerm, FullOrderModel
@@ -118,7 +122,11 @@ def cfg1_model(seed: int = 1, box=CFG1_BOX, ne=CFG1_NE, n_rec: int = CFG1_NREC, 
     aff = AffineOperator(K=[AffineTerm(Kg, 1.0 / AIR_RHO)],
                          M=[AffineTerm(Mn, 1.0 / (AIR_RHO * AIR_C * AIR_C))],
                          D=[AffineTerm(F, 1.0 / CFG1_Z)], load=b)
-    fom = FullOrderModel(c_out=C, n=n, affine=aff)
+    fdm_solver = None
+    if fdm:
+        from .fdm import BoxFDM
+        fdm_solver = BoxFDM(box, ne, AIR_RHO, AIR_C, {"z0": CFG1_Z})
+    fom = FullOrderModel(c_out=C, n=n, affine=aff, fdm=fdm_solver, prefer_fdm=fdm)
     return fom, {"xyz": xyz, "conn": conn, "src": src, "rec": rec, "Kg": Kg, "Mn": Mn, "F": F,
                  "freqs": np.arange(20.0, 200.5, 1.0), "points": CFG1_POINTS,
                  "moments": CFG1_MOMENTS}

@@ -218,14 +218,15 @@ def test_local_roms_tie_rule_and_seam(cuda):
         mor.rom_sweep(roms, [200.0])
 
 
-def test_cfg1_end_to_end_matches_oracle(cuda):
+@pytest.mark.parametrize("fdm", [False, True])
+def test_cfg1_end_to_end_matches_oracle(cuda, fdm):
     """cfg1 (n = 4641, 4 points x 8 moments, second order, 50 receivers, 181
-    frequencies): GPU assembly -> GPU LU -> Krylov -> CGS2 -> projection ->
-    batched sweep -> SPL, against the oracle running the reference algorithm
-    (splu, MGS2, literal per-frequency re-projection, zgesv) on the oracle's own
-    assembly of the same box."""
+    frequencies): GPU assembly -> GPU LU (or the box FDM solver) -> Krylov ->
+    CGS2 -> projection -> batched sweep -> SPL, against the oracle running the
+    reference algorithm (splu, MGS2, literal per-frequency re-projection, zgesv)
+    on the oracle's own assembly of the same box."""
     from paper_2310_04734_b200 import mor, workloads
-    fom, lay = workloads.cfg1_model()
+    fom, lay = workloads.cfg1_model(fdm=fdm)
     V = None
     for f0 in lay["points"]:
         Q, _ = mor.krylov_block_dev(fom, f0, lay["moments"], second_order=True)
