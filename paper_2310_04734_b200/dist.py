@@ -69,3 +69,81 @@ def max_over_ranks(x: float, device=None) -> float:
 def barrier():
     if dist.is_available() and dist.is_initialized():
         dist.barrier()
+
+
+def gather_blocks(local: list, counts: list[int], n_rows: int, max_cols: int, dtype, device) -> list:
+    """All-gather variable-width column blocks: rank q contributes `counts[q]`
+    blocks (n_rows x w, w <= max_cols, row-major); every rank receives all
+    sum(counts) blocks in rank order.  One padded all_gather_into_tensor for
+    the payload and one for the widths (complex payloads travel as real
+    pairs, which every backend supports)."""
+    ws = len(counts)
+    if ws == 1:
+        return list(local)
+    cmax = max(max(counts), 1)
+    buf = torch.zeros((cmax, n_rows, max_cols), dtype=dtype, device=device)
+    widths = torch.zeros(cmax, dtype=torch.int64, device=device)
+    for i, b in enumerate(local):
+        b2 = b if b.dim() == 2 else b.view(-1, 1)
+        buf[i, :, : b2.shape[1]] = b2
+        widths[i] = b2.shape[1]
+    real = torch.view_as_real(buf) if buf.is_complex() else buf
+    out = torch.empty((ws * cmax,) + tuple(real.shape[1:]), dtype=real.dtype, device=device)
+    dist.all_gather_into_tensor(out, real.contiguous())
+    wout = torch.empty(ws * cmax, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(wout, widths)
+    full = torch.view_as_complex(out) if buf.is_complex() else out
+    wl = wout.cpu().tolist()
+    return [full[q * cmax + i, :, : wl[q * cmax + i]] for q in range(ws) for i in range(counts[q])]
+
+
+def krylov_basis_sharded(fom, points, moments: int, second_order: bool = False):
+    """Offline phase sharded by expansion point: each rank
+    factors the FOM and builds the Krylov blocks of its contiguous share of
+    `points` (mor.krylov_block, mor.py:138-180, per load column for a block
+    RHS), the blocks are all-gathered, and every rank appends them with
+    mor._orthonormalise in point order — the serial build's sequence, so every
+    rank holds the same basis.  Returns V (n x r, device)."""
+    from . import mor
+    rank, ws, _ = world()
+    if ws > 1 and not (dist.is_available() and dist.is_initialized()):
+        raise RuntimeError("krylov_basis_sharded: call dist.init() first")
+    points = list(points)
+    lo, hi = shard_range(len(points), rank, ws)
+    mine = []
+    n_load = None
+    for f in points[lo:hi]:
+        blocks = mor.krylov_blocks_mimo_dev(fom, f, moments, second_order=second_order)
+        n_load = len(blocks)
+        mine += [Q for Q, _ in blocks]
+    if n_load is None:  # a rank without points still needs the per-point block count
+        n_load = int(fom.load_dev(points[0], mor._device()).shape[1]) if points else 0
+    counts = [(b - a) * n_load for a, b in (shard_range(len(points), q, ws) for q in range(ws))]
+    dev = mor._device()
+    allq = gather_blocks(mine, counts, fom.n, moments, mor.CDT, dev)
+    V = None
+    for Q in allq:
+        V = mor._orthonormalise(V, Q.contiguous())
+    return V
+
+
+def sweep_sharded(rs, freqs: torch.Tensor, want_y: bool = False):
+    """Reduced sweep sharded by frequency: rank q sweeps its
+    contiguous block of `freqs` with `rs` (sweep.ReducedSweep, primitives
+    already on its GPU), then the SPL rows (and optionally the outputs y) are
+    all-gathered; returns (spl (F, s), y (F, n_out, s) or None) on every rank."""
+    from .sweep import raise_if_singular
+    rank, ws, _ = world()
+    F = int(freqs.shape[0])
+    lo, hi = shard_range(F, rank, ws)
+    s, n_out = int(rs.b.shape[-1]), int(rs.c.shape[0])
+    if hi > lo:
+        out = rs.sweep_device(freqs[lo:hi], want_y=want_y)
+        raise_if_singular(out.info)
+        spl_l, y_l = out.spl, out.y
+    else:  # more ranks than frequencies
+        spl_l = torch.empty((0, s), dtype=torch.float64, device=rs.device)
+        y_l = torch.empty((0, n_out, s), dtype=torch.complex128, device=rs.device) if want_y else None
+    spl = gather_rows(spl_l, F, ws)
+    y = gather_rows(y_l, F, ws) if want_y else None
+    return spl, y

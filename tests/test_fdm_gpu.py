@@ -129,3 +129,19 @@ def test_cfg3_mor_chain(cuda):
         _, e, _, _ = omor.relative_error(yf.ravel(), yg[0].ravel() if False else y.cpu().numpy()[i].ravel())
         worst = max(worst, e)
     assert worst <= 5e-2, worst
+
+
+def test_sharded_krylov_basis_world1_matches_serial(cuda):
+    """dist.krylov_basis_sharded (expansion points sharded over ranks, blocks
+    all-gathered, replicated orthonormalisation) at world size 1 is the serial
+    MIMO build bit for bit."""
+    import torch
+    from paper_2310_04734_b200 import dist as vdist, mor
+    fom, _ = _small_box(cuda)
+    pts = (80.0, 190.0, 300.0)
+    V1 = vdist.krylov_basis_sharded(fom, pts, 4, second_order=True)
+    V2 = None
+    for f0 in pts:
+        for Q, _ in mor.krylov_blocks_mimo_dev(fom, f0, 4, second_order=True):
+            V2 = mor._orthonormalise(V2, Q)
+    assert V1.shape == V2.shape and torch.equal(V1, V2)

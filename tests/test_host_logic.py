@@ -105,3 +105,41 @@ def test_frequency_shards_gather_over_gloo(n):
             lo, hi = shard_range(n, r, ws)
             np.testing.assert_array_equal(full[lo:hi, 0], np.arange(lo, hi) * 10 + r)
         assert t == 2.0
+
+
+def _blocks_worker(rank, ws, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(ws), LOCAL_RANK=str(rank))
+    from paper_2310_04734_b200 import dist as vdist
+    vdist.init(backend="gloo")
+    counts = [3, 2]
+    g = torch.Generator().manual_seed(100 + rank)
+    local = [torch.randn((6, 1 + (rank + i) % 4), dtype=torch.complex128, generator=g) for i in range(counts[rank])]
+    full = vdist.gather_blocks(local, counts, 6, 4, torch.complex128, torch.device("cpu"))
+    q.put((rank, [b.numpy().copy() for b in local], [b.numpy().copy() for b in full]))
+    dist.destroy_process_group()
+
+
+def test_gather_variable_width_blocks_over_gloo():
+    """Offline sharding by expansion point: Krylov blocks of different widths
+    (breakdowns) all-gathered in rank order on every rank."""
+    ws = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blocks_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(ws):
+        rank, local, full = q.get(timeout=120)
+        out[rank] = (local, full)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = out[0][0] + out[1][0]
+    for rank in range(ws):
+        full = out[rank][1]
+        assert len(full) == 5
+        for a, b in zip(full, expect):
+            np.testing.assert_array_equal(a, b)

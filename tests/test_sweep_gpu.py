@@ -215,3 +215,16 @@ def test_blocked_path_more_than_16_rhs(cuda):
     _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
     x_ref = np.stack([np.linalg.solve(np.tensordot(alpha[i], prims, 1), b) for i in range(F)])
     assert np.abs(out.x.cpu().numpy() - x_ref).max() <= 1e-9 * np.abs(x_ref).max()
+
+
+def test_sharded_sweep_world1_matches_direct(cuda):
+    """dist.sweep_sharded (frequency shards + SPL/y gather) at world size 1
+    returns exactly the direct sweep."""
+    import torch
+    from paper_2310_04734_b200 import dist as vdist, sweep, workloads
+    w = workloads.cfg5(r=256, n_freq=500)
+    rs = sweep.ReducedSweep(w.prims, w.b, w.c_r, kinds=w.kinds)
+    f = torch.as_tensor(w.freqs, device=cuda)
+    spl, y = vdist.sweep_sharded(rs, f, want_y=True)
+    out = rs.sweep_device(f)
+    assert torch.equal(spl, out.spl) and torch.equal(y, out.y)
