@@ -108,6 +108,22 @@ class FullOrderModel:
     prefer_fdm: bool = False
     schur: object = None  # schur.CoupledBoxSchur: structure + box cavity (cfg2)
 
+    def c_out_adjoint_dev(self, device) -> torch.Tensor:
+        """C^H (n x n_out, complex) on the device, uploaded once per c_out and
+        cached: the output map of every projection.  A real c_out travels as
+        float64 (half the bytes) and is made complex on the device."""
+        key = (str(device), id(self.c_out))
+        cache = getattr(self, "_cH_cache", None)
+        if cache is None or cache[0] != key:
+            c = np.atleast_2d(np.asarray(self.c_out))
+            if np.iscomplexobj(c) and np.any(c.imag):
+                h = torch.from_numpy(np.ascontiguousarray(c, dtype=np.complex128)).to(device)
+            else:
+                h = torch.from_numpy(np.ascontiguousarray(c.real, dtype=np.float64)).to(device)
+            cache = (key, _rowmajor(h.conj().T if h.is_complex() else h.T))
+            self._cH_cache = cache
+        return cache[1]
+
     def __post_init__(self):
         if self.affine is not None:
             a = self.affine
@@ -264,10 +280,45 @@ def _host_sum(terms, f):
     return A
 
 
+def _rowmajor(t: torch.Tensor) -> torch.Tensor:
+    """Dense row-major complex copy (standard strides even for size-1 dims;
+    conjugate views resolved)."""
+    out = torch.empty(tuple(t.shape), dtype=CDT, device=t.device)
+    out.copy_(t)
+    return out
+
+
 def _as_dev(V, device=None) -> torch.Tensor:
     if isinstance(V, torch.Tensor):
         return V.to(device=device or V.device, dtype=CDT).contiguous()
     return torch.as_tensor(np.ascontiguousarray(V, dtype=complex), device=device or _device())
+
+
+ROW_SUPPORT_MAX = 0.5  # compact a primitive whose nonempty rows are at most this share
+
+
+def _row_support(P):
+    """(row ids R, row-compacted CSR) of a primitive whose nonempty rows are a
+    small share of n (impedance face masses: the wall nodes), else None.  The
+    compacted CSR keeps P's index/value arrays (skipped rows own no entries),
+    so V^H P V = V[R]^H (P V)[R] costs |R| / n of the full product.  Cached on
+    the primitive."""
+    if getattr(P, "kron", None) is not None:
+        return None
+    cached = getattr(P, "_row_support", False)
+    if cached is not False:
+        return cached
+    lens = P.indptr[1:] - P.indptr[:-1]
+    ridx = torch.nonzero(lens > 0).flatten()
+    sup = None
+    if ridx.numel() <= ROW_SUPPORT_MAX * P.n:
+        ip = torch.cat([P.indptr[ridx], P.indptr[-1:]]).to(torch.int32).contiguous()
+        sup = (ridx, DeviceCSR(int(ridx.numel()), ip, P.indices, P.data))
+    try:
+        P._row_support = sup
+    except AttributeError:
+        pass
+    return sup
 
 
 @dataclass
@@ -303,14 +354,24 @@ class ReducedModel:
             prims, kinds = [], []
             for kind, terms in (("K", fom.affine.K), ("D", fom.affine.D), ("M", fom.affine.M)):
                 for t in terms:
-                    W = linalg.spmm(t.P, Vd)                       # P_k V      (SpMM)
-                    prims.append(linalg.zgemm("C", Vd, W))          # V^H P_k V  (DMMA)
+                    sup = _row_support(t.P)
+                    if sup is None:
+                        W = linalg.spmm(t.P, Vd)                   # P_k V      (SpMM)
+                        prims.append(linalg.zgemm("C", Vd, W))      # V^H P_k V  (DMMA)
+                    else:  # boundary primitive: only its nonempty rows R contribute
+                        ridx, Pc = sup
+                        if ridx.numel() == 0:
+                            prims.append(torch.zeros((Vd.shape[1],) * 2, dtype=CDT, device=Vd.device))
+                        else:
+                            W = linalg.spmm(Pc, Vd)                # (P_k V)[R]
+                            prims.append(linalg.zgemm("C", Vd.index_select(0, ridx), W))  # V[R]^H (P V)[R]
                     kinds.append((kind, t))
             b = fom.affine.load_block(0.0, Vd.device) if fom.affine.constant_load else None
             br = linalg.zgemm("C", Vd, b) if b is not None else None
             self._proj = (torch.stack(prims).contiguous(), kinds, br)
-        c = np.atleast_2d(self.fom.c_out)
-        self._cR = linalg.zgemm("N", _as_dev(c.astype(complex), Vd.device), Vd)
+        # C_R = C V as (V^H C^H)^H: split-K over the n rows instead of an
+        # n_out x r tile grid with an n-long k loop
+        self._cR = _rowmajor(linalg.zgemm("C", Vd, self.fom.c_out_adjoint_dev(Vd.device)).conj().T)
         self._Vd = Vd
         self._cache_key = key
         return self._proj
