@@ -126,7 +126,7 @@ def cpu_sweep_rate(w, freqs_sample):
     return len(freqs_sample) / dt, dt
 
 
-def cpu_literal_rate(w, n_freq: int = 3):
+def cpu_literal_rate(w, n_freq: int = 20):
     """SURVEY §8(d) CPU baseline (1): the literal reference path,
     ReducedModel.output (mor.py:73-98: per-frequency re-projection V^H K V,
     V^H M V, V^H D V, then zgesv) with FOM providers that return the dense
