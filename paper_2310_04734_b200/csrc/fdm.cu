@@ -79,7 +79,7 @@ int fdm_diag(int n2, int n1, int n0, int nrhs, const z_t* lz, const z_t* ly, con
 // the 1-D transforms run at tensor-core rate instead of re-reading X from
 // L2 once per 1-D coefficient (axis_apply_kernel).  B (n x nrhs, RHS fastest)
 // is transposed in and the result transposed out through 32 x 32 tiles.
-using GemmF = blk::Gemm<64, 32, 4, 2, 3, blk::EPI_SET>;
+using GemmF = blk::Gemm<64, 32, 4, 2, 3, blk::EPI_SET, 16, true>;  // 3M products
 
 __global__ void __launch_bounds__(blk::NT) fdm_gemm_kernel(int m, int n, int k, const z_t* A, int lda, int64_t sA,
                                                            const z_t* B, int ldb, int64_t sB, z_t* C, int ldc,

@@ -187,8 +187,8 @@ using blk::KC;
 // C = alpha A B + beta C, A (m x k), B (k x n): DMMA tiles over the grid.
 // n <= 16 (W -= V G in the basis orthogonalisation: V streamed once, G tiny)
 // uses 128 x 16 tiles so the padded DMMA work stays below the HBM time.
-using GemmNN = blk::Gemm<64, 32, 4, 2, 3, blk::EPI_AXPBY>;
-using GemmNN16 = blk::Gemm<128, 16, 8, 1, 3, blk::EPI_AXPBY>;
+using GemmNN = blk::Gemm<64, 32, 4, 2, 3, blk::EPI_AXPBY, 16, true>;     // 3M products
+using GemmNN16 = blk::Gemm<128, 16, 8, 1, 3, blk::EPI_AXPBY, 16, true>;
 
 template <class G>
 __global__ void __launch_bounds__(NT) zgemm_nn_kernel(int m, int n, int k, z_t alpha, const z_t* A,
@@ -262,11 +262,14 @@ __global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int 
       blk::cp_async16(&Bs[st][kk * LDB + j], ok ? (const void*)(B + (int64_t)(k0 + kk) * ldb + n0 + j) : B, ok);
     }
   };
-  double cr[2][2][2], ci[2][2][2];
+  // 3M (Gauss) conjugate product: t1 = ar br, t2 = ai bi, t3 = (ar - ai)(br + bi);
+  // Re = t1 + t2, Im = t3 - t1 + t2 (3 DMMAs per fragment pair instead of 4)
+  double cr[2][2][2], ci[2][2][2], c2[2][2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < 2; ++j)
+      cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = c2[i][j][0] = c2[i][j][1] = 0.0;
 #pragma unroll
   for (int c = 0; c < CN_ST - 1; ++c) {
     if (c < nch) load(c, c);
@@ -288,19 +291,19 @@ __global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int 
       for (int i = 0; i < 2; ++i) a[i] = as[kr * LDA + wm * 16 + i * 8 + ar];  // A^H[i][k] = conj(A[k][i])
 #pragma unroll
       for (int j = 0; j < 2; ++j) b[j] = bs[kr * LDB + wn * 16 + j * 8 + ar];
+      double sa[2], sb[2];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const double br = b[j].x, bi = b[j].y, nbi = -bi;
+      for (int i = 0; i < 2; ++i) sa[i] = a[i].x - a[i].y;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) sb[j] = b[j].x + b[j].y;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          // conj(a) b: re = ar br + ai bi ; im = ar bi - ai br
-          const double nai = -a[i].y;
-          blk::dmma(cr[i][j][0], cr[i][j][1], a[i].x, br);
-          blk::dmma(cr[i][j][0], cr[i][j][1], nai, nbi);
-          blk::dmma(ci[i][j][0], ci[i][j][1], a[i].x, bi);
-          blk::dmma(ci[i][j][0], ci[i][j][1], nai, br);
+          blk::dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+          blk::dmma(c2[i][j][0], c2[i][j][1], a[i].y, b[j].y);
+          blk::dmma(ci[i][j][0], ci[i][j][1], sa[i], sb[j]);
         }
-      }
     }
   }
   blk::cp_wait<0>();
@@ -313,7 +316,8 @@ __global__ void __launch_bounds__(NT) zgemm_cn_partial_kernel(int m, int n, int 
       for (int v = 0; v < 2; ++v) {
         const int row = m0 + wm * 16 + i * 8 + (lane >> 2);
         const int col = n0 + wn * 16 + j * 8 + 2 * (lane & 3) + v;
-        if (row < m && col < n) P[(int64_t)row * n + col] = zmake(cr[i][j][v], ci[i][j][v]);
+        if (row < m && col < n)
+          P[(int64_t)row * n + col] = zmake(cr[i][j][v] + c2[i][j][v], ci[i][j][v] - cr[i][j][v] + c2[i][j][v]);
       }
 }
 

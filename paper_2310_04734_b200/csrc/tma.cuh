@@ -17,6 +17,13 @@
 #include "common.cuh"
 #include "mma.cuh"
 
+#ifndef VB_GEMM_3M
+#define VB_GEMM_3M 1
+#endif
+#ifndef VB_SKINNY_3M
+#define VB_SKINNY_3M 0
+#endif
+
 namespace vb {
 namespace tma {
 
@@ -266,19 +273,43 @@ struct GemmTma {
       double cr[S::NBX][2], ci[S::NBX][2];
 #pragma unroll
       for (int j = 0; j < S::NBX; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+#if VB_SKINNY_3M
+      double c2[S::NBX][2];
+#pragma unroll
+      for (int j = 0; j < S::NBX; ++j) c2[j][0] = c2[j][1] = 0.0;
+#endif
       for (int kk = 0; kk < k4n; ++kk) {
         const int kcol = kk * 4 + ak;
         z_t a = *(const z_t*)(as + (kcol >> 3) * 8192 + swz(row, kcol & 7));
         if (kcol >= K) a = zmake(0.0, 0.0);
+#if VB_SKINNY_3M
+        const double sa = a.x + a.y;
+#endif
 #pragma unroll
         for (int j = 0; j < S::NBX; ++j) {
           const z_t b = Us[kcol * SK_LD + j * 8 + prow];  // zero rows/cols beyond K, N
+#if VB_SKINNY_3M
+          blk::dmma(cr[j][0], cr[j][1], a.x, b.x);
+          blk::dmma(c2[j][0], c2[j][1], a.y, b.y);
+          blk::dmma(ci[j][0], ci[j][1], sa, b.x + b.y);
+#else
           blk::dmma(cr[j][0], cr[j][1], a.x, b.x);
           blk::dmma(cr[j][0], cr[j][1], a.y, -b.y);
           blk::dmma(ci[j][0], ci[j][1], a.x, b.y);
           blk::dmma(ci[j][0], ci[j][1], a.y, b.x);
+#endif
         }
       }
+#if VB_SKINNY_3M
+#pragma unroll
+      for (int j = 0; j < S::NBX; ++j)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const double t1 = cr[j][v], t2 = c2[j][v];
+          cr[j][v] = t1 - t2;
+          ci[j][v] = ci[j][v] - t1 - t2;
+        }
+#endif
       const int m0 = t * TM;
 #pragma unroll
       for (int j = 0; j < S::NBX; ++j)
@@ -379,6 +410,13 @@ struct GemmTma {
     }
     unsigned full_ph = 0, empty_ph = 0, c_ph = 0, cempty_ph = 0;
     double cr[2][2][2], ci[2][2][2];
+#if VB_GEMM_3M
+    double c2[2][2][2];  // 3M: cr = sum ar br, c2 = sum ai bi, ci = sum (ar + ai)(br + bi)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) c2[i][j][0] = c2[i][j][1] = 0.0;
+#endif
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -415,6 +453,24 @@ struct GemmTma {
           b[j] = *(const z_t*)(bs + (wn * 2 + j) * BBOX + swz(kcol, prow));
           if (!kin) b[j] = zmake(0.0, 0.0);
         }
+#if VB_GEMM_3M
+        // Gauss / 3M complex product: 3 real DMMAs per fragment pair instead
+        // of 4 (the operand sums cost 4 DADDs per k step, the recombination
+        // is in the epilogue)
+        double sa[2], sb[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) sa[i] = a[i].x + a[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sb[j] = b[j].x + b[j].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            blk::dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+            blk::dmma(c2[i][j][0], c2[i][j][1], a[i].y, b[j].y);
+            blk::dmma(ci[i][j][0], ci[i][j][1], sa[i], sb[j]);
+          }
+#else
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const double br = b[j].x, bi = b[j].y, nbi = -bi;
@@ -426,6 +482,7 @@ struct GemmTma {
             blk::dmma(ci[i][j][0], ci[i][j][1], a[i].y, br);
           }
         }
+#endif
       };
       if (!skip) {
         if (kvalid == KC) {  // full chunk: unmasked, fully unrolled
@@ -466,10 +523,18 @@ struct GemmTma {
               const int col = wn * 16 + j * 8 + perm8(cfrag);
               if (m0 + row < M && n0 + col < N) {
                 const z_t c = *(const z_t*)(Cs + (col >> 3) * 8192 + swz(row, col & 7));
+#if VB_GEMM_3M
+                const double pr = cr[i][j][v] - c2[i][j][v], pi = ci[i][j][v] - cr[i][j][v] - c2[i][j][v];
+                Cg[(size_t)(cr0 + m0 + row) * ldw + cc0 + n0 + col] = zmake(c.x - pr, c.y - pi);
+#else
                 Cg[(size_t)(cr0 + m0 + row) * ldw + cc0 + n0 + col] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+#endif
               }
               cr[i][j][v] = 0.0;
               ci[i][j][v] = 0.0;
+#if VB_GEMM_3M
+              c2[i][j][v] = 0.0;
+#endif
             }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->cempty);

@@ -116,6 +116,13 @@ struct GemmBig {
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+#if VB_GEMM_3M
+    double c2[4][4][2];  // 3M: cr = sum ar br, c2 = sum ai bi, ci = sum (ar + ai)(br + bi)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c2[i][j][0] = c2[i][j][1] = 0.0;
+#endif
     const int ak = lane & 3, prow = perm8(lane >> 2);
     int t = 0, kc = 0;
     Cur cc = c0;  // consumer's tile
@@ -144,6 +151,21 @@ struct GemmBig {
             b[j] = *(const z_t*)(bs + (wn * 4 + j) * 1024 + swz(kcol, prow));
             if (!kin) b[j] = zmake(0.0, 0.0);
           }
+#if VB_GEMM_3M
+          double sa[4], sb[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) sa[i] = a[i].x + a[i].y;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sb[j] = b[j].x + b[j].y;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              blk::dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+              blk::dmma(c2[i][j][0], c2[i][j][1], a[i].y, b[j].y);
+              blk::dmma(ci[i][j][0], ci[i][j][1], sa[i], sb[j]);
+            }
+#else
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const double br = b[j].x, bi = b[j].y, nbi = -bi;
@@ -155,6 +177,7 @@ struct GemmBig {
               blk::dmma(ci[i][j][0], ci[i][j][1], a[i].y, br);
             }
           }
+#endif
         }
       }
       __syncwarp();
@@ -184,10 +207,18 @@ struct GemmBig {
               const int col = wn * 32 + j * 8 + perm8(2 * ak + v);
               if (m0 + row < M && n0 + col < N) {
                 const z_t c = *(const z_t*)(Cs + ((row >> 6) * 8 + (col >> 3)) * 8192 + swz(row & 63, col & 7));
+#if VB_GEMM_3M
+                const double pr = cr[i][j][v] - c2[i][j][v], pi = ci[i][j][v] - cr[i][j][v] - c2[i][j][v];
+                Cg[(int64_t)(ar0 + m0 + row) * ldc + bc0 + n0 + col] = zmake(c.x - pr, c.y - pi);
+#else
                 Cg[(int64_t)(ar0 + m0 + row) * ldc + bc0 + n0 + col] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+#endif
               }
               cr[i][j][v] = 0.0;
               ci[i][j][v] = 0.0;
+#if VB_GEMM_3M
+              c2[i][j][v] = 0.0;
+#endif
             }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->cempty);
