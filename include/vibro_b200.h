@@ -167,6 +167,31 @@ int vb_csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const
                 const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha,
                 vb_complex beta, void* stream);
 
+/* Row-group form of a CSR pattern for the many-column SpMM (HOST pointers,
+ * one-off per pattern; same call sites as vb_csr_spmm).  Greedy in row order:
+ * an ungrouped row becomes a group leader and adopts up to 7 ungrouped rows
+ * among its columns whose column sets are subsets of its own.  Outputs (sized
+ * by the caller for the worst case: n_rows groups, nnz union slots):
+ *   g_leader[G], g_rows[G][8] (member rows, -1 padded), g_uoff[G] (offset of
+ *   the group's union = the leader's CSR row in the union space),
+ *   masks[U] (bit i: member i has that column), vmap[U][8] (CSR position of
+ *   (member i, union column j), -1 absent); *n_groups = G, *n_union = U. */
+int vb_csr_row_groups(int n_rows, const int32_t* indptr_host, const int32_t* indices_host, int32_t* g_leader_host,
+                      int32_t* g_rows_host, int32_t* g_uoff_host, uint8_t* masks_host, int32_t* vmap_host,
+                      int* n_groups_host, int64_t* n_union_host);
+
+/* gvals[U][8] = vmap >= 0 ? vals[vmap] : 0 (device): the values of one
+ * primitive on its pattern's row groups. */
+int vb_rg_gather_values(int64_t n_union, const int32_t* vmap, const double* vals, double* gvals, void* stream);
+
+/* Y = alpha * A X + beta * Y through the row groups of A (device pointers;
+ * indptr/indices are A's CSR arrays, which hold each group's union).  Equal
+ * to vb_csr_spmm to rounding (dense 8-row blocks on the FP64 tensor cores). */
+int vb_rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
+               const int32_t* indptr, const int32_t* indices, const uint8_t* masks, const double* gvals, int k,
+               const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha, vb_complex beta,
+               void* stream);
+
 /* Y = alpha * Op X + beta * Y for the assembled primitives of a uniform hex27
  * box WITHOUT the CSR: Op = Kx(x)My(x)Mz + Mx(x)Ky(x)Mz + Mx(x)My(x)Kz
  * (stiff = 1, Kgrad) or Mx(x)My(x)Mz (stiff = 0, Mnn), the exact Kronecker

@@ -59,6 +59,12 @@ _SIGS = {
     "vb_quad9_face_mass": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vb_csr_spmm": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _z, C.c_int64, _z,
                               C.c_int64, VbComplex, VbComplex, C.c_void_p]),
+    "vb_csr_row_groups": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
+    "vb_rg_gather_values": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vb_rg_spmm": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.c_void_p, C.c_int, _z, C.c_int64, _z, C.c_int64, VbComplex, VbComplex,
+                             C.c_void_p]),
     "vb_kron3_apply": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                  VbComplex, _z, C.c_int64, VbComplex, _z, C.c_int64, C.c_void_p]),
     "vb_csr_axpy_dense": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, VbComplex, _z, C.c_int64,

@@ -145,6 +145,32 @@ int vb_csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const
                       zc(beta), (cudaStream_t)stream);
 }
 
+int vb_csr_row_groups(int n_rows, const int32_t* indptr, const int32_t* indices, int32_t* g_leader,
+                      int32_t* g_rows, int32_t* g_uoff, uint8_t* masks, int32_t* vmap, int* n_groups,
+                      int64_t* n_union) {
+  VB_CHECK_ARG(n_rows >= 0 && indptr && indices && g_leader && g_rows && g_uoff && masks && vmap && n_groups &&
+                   n_union,
+               "vb_csr_row_groups: bad arguments");
+  VB_CHECK_ARG(vb::csr_row_groups(n_rows, indptr, indices, g_leader, g_rows, g_uoff, masks, vmap, n_groups,
+                                  n_union) == 0,
+               "vb_csr_row_groups: union space exceeds int32");
+  return 0;
+}
+
+int vb_rg_gather_values(int64_t n_union, const int32_t* vmap, const double* vals, double* gvals, void* stream) {
+  VB_CHECK_ARG(n_union >= 0, "vb_rg_gather_values: bad sizes");
+  return vb::rg_gather_values(n_union, vmap, vals, gvals, (cudaStream_t)stream);
+}
+
+int vb_rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
+               const int32_t* indptr, const int32_t* indices, const uint8_t* masks, const double* gvals, int k,
+               const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha, vb_complex beta,
+               void* stream) {
+  VB_CHECK_ARG(n_groups >= 0 && k >= 0, "vb_rg_spmm: bad sizes");
+  return vb::rg_spmm(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals, k, (const z_t*)X, ldx,
+                     (z_t*)Y, ldy, zc(alpha), zc(beta), (cudaStream_t)stream);
+}
+
 int vb_csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
                       vb_complex alpha, vb_complex* D, int64_t ldd, void* stream) {
   VB_CHECK_ARG(n_rows >= 0 && D, "vb_csr_axpy_dense: bad arguments");

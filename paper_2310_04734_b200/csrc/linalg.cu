@@ -9,146 +9,7 @@
 
 namespace vb {
 
-// ------------------------------------------------------------------ SpMM ---
-// Y = alpha * A X + beta * Y, A real CSR (n_rows x *), X/Y complex row-major.
-// k > 1: one warp per row, lanes over the k columns (coalesced X rows), the
-// row's (value, index) pairs fetched 32 at a time and broadcast by shuffle.
-__global__ void spmm_kernel(int n_rows, const int32_t* __restrict__ indptr,
-                            const int32_t* __restrict__ indices, const double* __restrict__ vals,
-                            int k, const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y,
-                            int64_t ldy, z_t alpha, z_t beta) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
-  for (int64_t row = warp; row < n_rows; row += nwarps) {
-    const int b = indptr[row], e = indptr[row + 1];
-    for (int c0 = 0; c0 < k; c0 += 32) {
-      const int c = c0 + lane;
-      z_t acc = zmake(0.0, 0.0);
-      for (int j0 = b; j0 < e; j0 += 32) {
-        double v = 0.0;
-        int col = 0;
-        if (j0 + lane < e) {
-          v = vals[j0 + lane];
-          col = indices[j0 + lane];
-        }
-        const int cnt = min(32, e - j0);
-        for (int q = 0; q < cnt; ++q) {
-          const double a = __shfl_sync(0xffffffffu, v, q);
-          const int cc = __shfl_sync(0xffffffffu, col, q);
-          if (c < k) {
-            const z_t x = X[(int64_t)cc * ldx + c];
-            acc.x += a * x.x;
-            acc.y += a * x.y;
-          }
-        }
-      }
-      if (c < k) {
-        z_t out = zmul(alpha, acc);
-        if (!beta0) out = zfma(out, beta, Y[row * ldy + c]);
-        Y[row * ldy + c] = out;
-      }
-    }
-  }
-}
-
-// k == 1 (SpMV): lanes split the row's nonzeros, warp reduction in a fixed order.
-__global__ void spmv_kernel(int n_rows, const int32_t* __restrict__ indptr,
-                            const int32_t* __restrict__ indices, const double* __restrict__ vals,
-                            const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y, int64_t ldy,
-                            z_t alpha, z_t beta) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
-  for (int64_t row = warp; row < n_rows; row += nwarps) {
-    const int b = indptr[row], e = indptr[row + 1];
-    double re = 0.0, im = 0.0;
-    for (int j = b + lane; j < e; j += 32) {
-      const double a = vals[j];
-      const z_t x = X[(int64_t)indices[j] * ldx];
-      re += a * x.x;
-      im += a * x.y;
-    }
-    re = warp_sum(re);
-    im = warp_sum(im);
-    if (lane == 0) {
-      z_t out = zmul(alpha, zmake(re, im));
-      if (!beta0) out = zfma(out, beta, Y[row * ldy]);
-      Y[row * ldy] = out;
-    }
-  }
-}
-
-// k > 64: column-chunked SpMM.  blockIdx.y = chunk of 64 columns (the slow
-// grid dimension, so all rows of one chunk run before the next): the X slab a
-// chunk touches (rows within the matrix bandwidth x 1 KB) stays in L2 and X is
-// read from HBM about once per chunk instead of once per neighbouring row.
-// One warp per row; lane l owns columns l and l+32 of the chunk.
-constexpr int SPMM_CW = 64;
-
-__global__ void spmm_chunked_kernel(int n_rows, const int32_t* __restrict__ indptr,
-                                    const int32_t* __restrict__ indices, const double* __restrict__ vals,
-                                    int k, const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y,
-                                    int64_t ldy, z_t alpha, z_t beta) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= n_rows) return;
-  const int c0 = blockIdx.y * SPMM_CW + lane, c1 = c0 + 32;
-  const bool v0 = c0 < k, v1 = c1 < k;
-  const int b = __ldg(indptr + row), e = __ldg(indptr + row + 1);
-  z_t a0 = zmake(0.0, 0.0), a1 = zmake(0.0, 0.0);
-  for (int j0 = b; j0 < e; j0 += 32) {
-    double v = 0.0;
-    int col = 0;
-    if (j0 + lane < e) {
-      v = __ldg(vals + j0 + lane);
-      col = __ldg(indices + j0 + lane);
-    }
-    const int cnt = min(32, e - j0);
-#pragma unroll 4
-    for (int q = 0; q < cnt; ++q) {
-      const double a = __shfl_sync(0xffffffffu, v, q);
-      const int cc = __shfl_sync(0xffffffffu, col, q);
-      const z_t* xr = X + (int64_t)cc * ldx;
-      if (v0) { const z_t x = __ldg(xr + c0); a0.x += a * x.x; a0.y += a * x.y; }
-      if (v1) { const z_t x = __ldg(xr + c1); a1.x += a * x.x; a1.y += a * x.y; }
-    }
-  }
-  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
-  if (v0) {
-    z_t out = zmul(alpha, a0);
-    if (!beta0) out = zfma(out, beta, Y[row * ldy + c0]);
-    Y[row * ldy + c0] = out;
-  }
-  if (v1) {
-    z_t out = zmul(alpha, a1);
-    if (!beta0) out = zfma(out, beta, Y[row * ldy + c1]);
-    Y[row * ldy + c1] = out;
-  }
-}
-
-int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
-             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
-  if (n_rows <= 0 || k <= 0) return 0;
-  const int nt = 256;
-  const int64_t warps = n_rows;
-  if (k > SPMM_CW) {
-    const dim3 grid((unsigned)((warps * 32 + nt - 1) / nt), (unsigned)((k + SPMM_CW - 1) / SPMM_CW));
-    spmm_chunked_kernel<<<grid, nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
-    VB_LAUNCHED("spmm_chunked_kernel");
-    return 0;
-  }
-  unsigned grid = (unsigned)((warps * 32 + nt - 1) / nt);
-  if (grid > 148u * 64u) grid = 148u * 64u;
-  if (k == 1)
-    spmv_kernel<<<grid, nt, 0, st>>>(n_rows, indptr, indices, vals, X, ldx, Y, ldy, alpha, beta);
-  else
-    spmm_kernel<<<grid, nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
-  VB_LAUNCHED("spmm_kernel");
-  return 0;
-}
+// csr_spmm (CSR SpMM / SpMV) lives in spmm.cu.
 
 // D += alpha * A (real CSR scattered into a dense complex matrix): the operator
 // K - w^2 M + i w D at an expansion point (mor.py:41-46) for the dense FOM LU.

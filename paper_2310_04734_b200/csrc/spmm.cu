@@ -1,0 +1,402 @@
+// Real-CSR x complex-dense SpMM, Y = alpha A X + beta Y (SURVEY §8a A9 first
+// half; replaces scipy csr_matvecs in `K @ V`, `M @ v`, vibrofem/mor.py:81-85,
+// 117, 162-179).  X, Y complex128 row-major (n x k, row stride ldx / ldy).
+//
+// Three kernels by column count:
+//  * k == 1   SpMV: a warp per row, lanes over the row's nonzeros, fixed-order
+//             warp reduction.
+//  * k <= 16  sub-warp CSR: KP = next_pow2(k) lanes per row, 32/KP rows per
+//             warp; the row's (value, index) pairs are loaded KP at a time,
+//             coalesced, and broadcast inside the sub-warp by shuffle.  One
+//             128-B X piece per nonzero and warp instruction: no idle lanes.
+//  * k > 16   row groups (`vb_csr_row_groups`): up to 8 rows whose column sets
+//             are subsets of one "leader" row's set form a dense 8 x nu block
+//             over the leader's columns (absent slots +0.0); the block times
+//             the gathered X rows runs on the FP64 tensor cores (DMMA) with
+//             the X rows staged through a cp.async ring.  Each X row is read
+//             once per group instead of once per nonzero (hex27 2x2x2 node
+//             blocks: 512 nonzeros over 125 columns = 4.1x less gather
+//             traffic).  Column chunks of 32*CPL are the slow grid dimension
+//             so the X slab of one chunk stays L2-resident.
+#include "common.cuh"
+#include "sweep.cuh"
+#include "mma.cuh"
+
+#include <algorithm>
+#include <vector>
+
+namespace vb {
+
+// ------------------------------------------------------------------ k == 1 --
+__global__ void spmv_kernel(int n_rows, const int32_t* __restrict__ indptr,
+                            const int32_t* __restrict__ indices, const double* __restrict__ vals,
+                            const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y, int64_t ldy,
+                            z_t alpha, z_t beta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+  for (int64_t row = warp; row < n_rows; row += nwarps) {
+    const int b = indptr[row], e = indptr[row + 1];
+    double re = 0.0, im = 0.0;
+    for (int j = b + lane; j < e; j += 32) {
+      const double a = vals[j];
+      const z_t x = X[(int64_t)indices[j] * ldx];
+      re += a * x.x;
+      im += a * x.y;
+    }
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) {
+      z_t out = zmul(alpha, zmake(re, im));
+      if (!beta0) out = zfma(out, beta, Y[row * ldy]);
+      Y[row * ldy] = out;
+    }
+  }
+}
+
+// --------------------------------------------------------------- k <= 16 ---
+template <int KP>
+__global__ void __launch_bounds__(256) spmm_subwarp_kernel(int n_rows, const int32_t* __restrict__ indptr,
+                                                           const int32_t* __restrict__ indices,
+                                                           const double* __restrict__ vals, int k,
+                                                           const z_t* __restrict__ X, int64_t ldx,
+                                                           z_t* __restrict__ Y, int64_t ldy, z_t alpha,
+                                                           z_t beta) {
+  constexpr int RPW = 32 / KP;  // rows per warp
+  const int lane = threadIdx.x & 31, sub = lane / KP, c = lane % KP;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+  const bool cv = c < k;
+  for (int64_t row0 = warp * RPW; row0 < n_rows; row0 += nwarps * RPW) {
+    const int64_t row = row0 + sub;
+    const bool rv = row < n_rows;
+    const int b = rv ? __ldg(indptr + row) : 0;
+    const int len = rv ? __ldg(indptr + row + 1) - b : 0;
+    int mlen = len;  // trip count of the whole warp (shuffles need all lanes)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mlen = max(mlen, __shfl_xor_sync(0xffffffffu, mlen, o));
+    double ar = 0.0, ai = 0.0;
+    for (int j0 = 0; j0 < mlen; j0 += KP) {
+      double v = 0.0;
+      int col = 0;
+      if (j0 + c < len) {
+        v = __ldg(vals + b + j0 + c);
+        col = __ldg(indices + b + j0 + c);
+      }
+      const int cnt = min(KP, mlen - j0);
+#pragma unroll 4
+      for (int q = 0; q < cnt; ++q) {
+        const double a = __shfl_sync(0xffffffffu, v, q, KP);
+        const int cc = __shfl_sync(0xffffffffu, col, q, KP);
+        if (cv && j0 + q < len) {
+          const z_t x = __ldg(X + (int64_t)cc * ldx + c);
+          ar = fma(a, x.x, ar);
+          ai = fma(a, x.y, ai);
+        }
+      }
+    }
+    if (rv && cv) {
+      z_t out = zmul(alpha, zmake(ar, ai));
+      if (!beta0) out = zfma(out, beta, Y[row * ldy + c]);
+      Y[row * ldy + c] = out;
+    }
+  }
+}
+
+// ------------------------------------------------------------- row groups ---
+constexpr int RG = 8;  // rows per group
+
+// Row-group SpMM on the FP64 tensor cores.  One warp per group: the group's
+// rows x leader columns form a dense 8 x nu real block (absent slots +0.0),
+// so Y[8 rows, chunk] = Vals[8, nu] . X[leader columns, chunk] is a real GEMM
+// over the interleaved (re, im) columns of X: DMMA m8n8k4 with A = 8 rows x
+// 4 leader columns of values, B = 4 X rows x 8 real columns, and each lane's
+// (c0, c1) accumulator pair = one complex output (row = lane/4, complex
+// column = 4t + lane%4).  The X rows of the leader's columns and the value
+// rows stream through a per-warp cp.async ring in shared memory (S stages of
+// J leader columns, zero-filled past the row end / past k): the gathers are
+// in flight without holding registers and each X row is read once for all 8
+// member rows.  X stage rows and value rows are padded by 32 B so that the
+// fragment loads of a half-warp (4 rows x 4 consecutive doubles) fall on 4
+// distinct 8-bank ranges (conflict-free).
+template <int CPL, int J, int S>
+struct RgCfg {
+  static constexpr int CW = 32 * CPL;                        // complex columns per chunk
+  static constexpr int RS = 2 * CW + 4;                      // doubles per X stage row (padded)
+  static constexpr int VR = RG + 4;                          // doubles per value row (padded)
+  static constexpr int XS = J * RS;                          // doubles per X stage
+  static constexpr int VS = J * VR;                          // doubles per value stage
+  static constexpr int WARP_BYTES = S * (XS + VS) * 8;       // per warp
+  static constexpr int NT = 2 * CW / 8;                      // 8-wide real n-tiles
+};
+
+constexpr int RG_WARPS = 4;
+
+template <int CPL, int J, int S>
+__global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, const int32_t* __restrict__ g_leader,
+                                                                const int32_t* __restrict__ g_rows,
+                                                                const int32_t* __restrict__ g_uoff,
+                                                                const int32_t* __restrict__ indptr,
+                                                                const int32_t* __restrict__ indices,
+                                                                const double* __restrict__ gvals, int k,
+                                                                const z_t* __restrict__ X, int64_t ldx,
+                                                                z_t* __restrict__ Y, int64_t ldy, z_t alpha,
+                                                                z_t beta) {
+  using C = RgCfg<CPL, J, S>;
+  static_assert(J % 4 == 0 && 32 % J == 0, "stages of whole k4 steps inside one 32-column index block");
+  static_assert(J * RG / 2 <= 32, "value stage copied by one round of 16-B lanes");
+  extern __shared__ __align__(16) unsigned char rg_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int g = blockIdx.x * RG_WARPS + w;
+  if (g >= n_groups) return;
+  double* xs = reinterpret_cast<double*>(rg_smem + (size_t)w * C::WARP_BYTES);
+  double* vs = xs + S * C::XS;
+  const int c0 = blockIdx.y * C::CW;  // first complex column of the chunk
+  bool cv[CPL];
+#pragma unroll
+  for (int t = 0; t < CPL; ++t) cv[t] = c0 + lane + 32 * t < k;
+  const int leader = __ldg(g_leader + g);
+  const int ub = __ldg(indptr + leader), nu = __ldg(indptr + leader + 1) - ub;
+  const double* uv = gvals + (int64_t)__ldg(g_uoff + g) * RG;
+  const int nst = (nu + J - 1) / J;  // stages of J leader columns
+  int colv = 0;                      // leader columns of the current 32-block, lane-parallel
+  auto issue = [&](int st) {
+    const int slot = st % S;
+    const int j0 = st * J;
+    if ((j0 & 31) == 0) colv = j0 + lane < nu ? __ldg(indices + ub + j0 + lane) : 0;
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      const int j = j0 + jj;
+      const int col = __shfl_sync(0xffffffffu, colv, j & 31);
+      const z_t* xr = X + (int64_t)col * ldx + c0 + lane;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t)
+        blk::cp_async16(xs + slot * C::XS + jj * C::RS + 2 * (lane + 32 * t), cv[t] && j < nu ? xr + 32 * t : X,
+                        cv[t] && j < nu);
+    }
+    if (lane < J * RG / 2) {  // J value rows of 8 doubles = J*4 pieces of 16 B
+      const int j = j0 + lane / (RG / 2);
+      blk::cp_async16(vs + slot * C::VS + (lane >> 2) * C::VR + 2 * (lane & 3),
+                      j < nu ? uv + (int64_t)j0 * RG + 2 * lane : gvals, j < nu);
+    }
+    blk::cp_commit();
+  };
+  double acc[C::NT][2];
+#pragma unroll
+  for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < S - 1; ++st) {
+    if (st < nst) issue(st);
+    else blk::cp_commit();
+  }
+  for (int st = 0; st < nst; ++st) {
+    blk::cp_wait<S - 2>();
+    __syncwarp();
+    const double* xsl = xs + (st % S) * C::XS;
+    const double* vsl = vs + (st % S) * C::VS;
+#pragma unroll
+    for (int q = 0; q < J / 4; ++q) {
+      const double a = vsl[(4 * q + tig) * C::VR + gid];  // A[row gid][k tig]
+      const double* xb = xsl + (4 * q + tig) * C::RS + gid;  // B[k tig][n gid]
+#pragma unroll
+      for (int t = 0; t < C::NT; ++t) blk::dmma(acc[t][0], acc[t][1], a, xb[8 * t]);
+    }
+    __syncwarp();
+    if (st + S - 1 < nst) issue(st + S - 1);
+    else blk::cp_commit();
+  }
+  const int row = __ldg(g_rows + (int64_t)g * RG + gid);
+  if (row < 0) return;
+  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+  z_t* yr = Y + (int64_t)row * ldy + c0;
+#pragma unroll
+  for (int t = 0; t < C::NT; ++t) {
+    const int c = 4 * t + tig;  // complex column inside the chunk
+    if (c0 + c >= k) continue;
+    z_t out = zmul(alpha, zmake(acc[t][0], acc[t][1]));
+    if (!beta0) out = zfma(out, beta, yr[c]);
+    yr[c] = out;
+  }
+}
+
+__global__ void rg_gather_values_kernel(int64_t n_slots, const int32_t* __restrict__ vmap,
+                                        const double* __restrict__ vals, double* __restrict__ gvals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_slots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = vmap[i];
+    gvals[i] = p >= 0 ? vals[p] : 0.0;
+  }
+}
+
+// Host-side grouping of a CSR pattern (one-off per pattern, O(nnz) merges).
+// Greedy in row order: an ungrouped row becomes a leader and adopts up to 7
+// ungrouped rows among its own columns whose column sets are subsets of its
+// set (scanned in column order).  On lexicographically numbered hex27 boxes
+// this yields the 2x2x2 node blocks (vertex node as leader).
+int csr_row_groups(int n, const int32_t* indptr, const int32_t* indices, int32_t* g_leader, int32_t* g_rows,
+                   int32_t* g_uoff, uint8_t* masks, int32_t* vmap, int* n_groups, int64_t* n_slots) {
+  std::vector<char> grouped(n, 0);
+  int G = 0;
+  int64_t uoff = 0;
+  for (int r = 0; r < n; ++r) {
+    if (grouped[r]) continue;
+    grouped[r] = 1;
+    const int rb = indptr[r], re = indptr[r + 1];
+    int mem[RG];
+    int nm = 0;
+    mem[nm++] = r;
+    for (int j = rb; j < re && nm < RG; ++j) {
+      const int c = indices[j];
+      if (c < 0 || c >= n || grouped[c]) continue;
+      // subset test: row c's columns inside row r's columns (both sorted)
+      int p = rb;
+      bool sub = true;
+      for (int q = indptr[c]; q < indptr[c + 1]; ++q) {
+        while (p < re && indices[p] < indices[q]) ++p;
+        if (p == re || indices[p] != indices[q]) { sub = false; break; }
+      }
+      if (!sub) continue;
+      grouped[c] = 1;
+      mem[nm++] = c;
+    }
+    if (uoff + (re - rb) > INT32_MAX) return 1;
+    g_leader[G] = r;
+    g_uoff[G] = (int32_t)uoff;
+    for (int i = 0; i < RG; ++i) g_rows[(int64_t)G * RG + i] = i < nm ? mem[i] : -1;
+    for (int j = rb; j < re; ++j) {
+      masks[uoff + (j - rb)] = 0;
+      for (int i = 0; i < RG; ++i) vmap[(uoff + (j - rb)) * RG + i] = -1;
+    }
+    for (int i = 0; i < nm; ++i) {
+      const int rr = mem[i];
+      int p = rb;
+      for (int q = indptr[rr]; q < indptr[rr + 1]; ++q) {
+        while (indices[p] < indices[q]) ++p;  // present by the subset test (leader: itself)
+        masks[uoff + (p - rb)] |= (uint8_t)(1u << i);
+        vmap[(uoff + (p - rb)) * RG + i] = q;
+      }
+    }
+    uoff += re - rb;
+    ++G;
+  }
+  *n_groups = G;
+  *n_slots = uoff;
+  return 0;
+}
+
+int rg_gather_values(int64_t n_union, const int32_t* vmap, const double* vals, double* gvals, cudaStream_t st) {
+  if (n_union <= 0) return 0;
+  const int64_t n = n_union * RG;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  rg_gather_values_kernel<<<grid, 256, 0, st>>>(n, vmap, vals, gvals);
+  VB_LAUNCHED("rg_gather_values_kernel");
+  return 0;
+}
+
+template <int CPL, int J, int S>
+static int rg_launch(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
+                     const int32_t* indptr, const int32_t* indices, const double* gvals, int k, const z_t* X,
+                     int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
+  constexpr int smem = RG_WARPS * RgCfg<CPL, J, S>::WARP_BYTES;
+  static bool attr = false;
+  if (!attr) {
+    VB_CUDA(cudaFuncSetAttribute(rg_spmm_kernel<CPL, J, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const dim3 grid((unsigned)((n_groups + RG_WARPS - 1) / RG_WARPS), (unsigned)((k + 32 * CPL - 1) / (32 * CPL)));
+  rg_spmm_kernel<CPL, J, S><<<grid, 32 * RG_WARPS, smem, st>>>(n_groups, g_leader, g_rows, g_uoff, indptr, indices,
+                                                               gvals, k, X, ldx, Y, ldy, alpha, beta);
+  VB_LAUNCHED("rg_spmm_kernel");
+  return 0;
+}
+
+int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
+            const int32_t* indptr, const int32_t* indices, const uint8_t* /*masks*/, const double* gvals, int k,
+            const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
+  if (n_groups <= 0 || k <= 0) return 0;
+  if (k <= 32)
+    return rg_launch<1, 4, 4>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy,
+                              alpha, beta, st);
+  return rg_launch<2, 4, 4>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy, alpha,
+                            beta, st);
+}
+
+// ------------------------------------------------------------ dispatcher ---
+constexpr int SPMM_CW = 64;
+
+// k > 16 without row groups: one warp per row, lane l owns columns l, l+32 of
+// a 64-column chunk (chunk = slow grid dimension, X slab L2-resident).
+__global__ void spmm_chunked_kernel(int n_rows, const int32_t* __restrict__ indptr,
+                                    const int32_t* __restrict__ indices, const double* __restrict__ vals,
+                                    int k, const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y,
+                                    int64_t ldy, z_t alpha, z_t beta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n_rows) return;
+  const int c0 = blockIdx.y * SPMM_CW + lane, c1 = c0 + 32;
+  const bool v0 = c0 < k, v1 = c1 < k;
+  const int b = __ldg(indptr + row), e = __ldg(indptr + row + 1);
+  z_t a0 = zmake(0.0, 0.0), a1 = zmake(0.0, 0.0);
+  for (int j0 = b; j0 < e; j0 += 32) {
+    double v = 0.0;
+    int col = 0;
+    if (j0 + lane < e) {
+      v = __ldg(vals + j0 + lane);
+      col = __ldg(indices + j0 + lane);
+    }
+    const int cnt = min(32, e - j0);
+#pragma unroll 4
+    for (int q = 0; q < cnt; ++q) {
+      const double a = __shfl_sync(0xffffffffu, v, q);
+      const int cc = __shfl_sync(0xffffffffu, col, q);
+      const z_t* xr = X + (int64_t)cc * ldx;
+      if (v0) { const z_t x = __ldg(xr + c0); a0.x = fma(a, x.x, a0.x); a0.y = fma(a, x.y, a0.y); }
+      if (v1) { const z_t x = __ldg(xr + c1); a1.x = fma(a, x.x, a1.x); a1.y = fma(a, x.y, a1.y); }
+    }
+  }
+  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+  if (v0) {
+    z_t out = zmul(alpha, a0);
+    if (!beta0) out = zfma(out, beta, Y[row * ldy + c0]);
+    Y[row * ldy + c0] = out;
+  }
+  if (v1) {
+    z_t out = zmul(alpha, a1);
+    if (!beta0) out = zfma(out, beta, Y[row * ldy + c1]);
+    Y[row * ldy + c1] = out;
+  }
+}
+
+int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
+             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
+  if (n_rows <= 0 || k <= 0) return 0;
+  const int nt = 256;
+  if (k > 16) {
+    const dim3 grid((unsigned)(((int64_t)n_rows * 32 + nt - 1) / nt), (unsigned)((k + SPMM_CW - 1) / SPMM_CW));
+    spmm_chunked_kernel<<<grid, nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
+    VB_LAUNCHED("spmm_chunked_kernel");
+    return 0;
+  }
+  auto grid_for = [&](int rows_per_warp) {
+    int64_t warps = ((int64_t)n_rows + rows_per_warp - 1) / rows_per_warp;
+    return (unsigned)std::min<int64_t>((warps * 32 + nt - 1) / nt, 148 * 64);
+  };
+  if (k == 1) {
+    spmv_kernel<<<grid_for(1), nt, 0, st>>>(n_rows, indptr, indices, vals, X, ldx, Y, ldy, alpha, beta);
+  } else if (k == 2) {
+    spmm_subwarp_kernel<2><<<grid_for(16), nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
+  } else if (k <= 4) {
+    spmm_subwarp_kernel<4><<<grid_for(8), nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
+  } else if (k <= 8) {
+    spmm_subwarp_kernel<8><<<grid_for(4), nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
+  } else {
+    spmm_subwarp_kernel<16><<<grid_for(2), nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
+  }
+  VB_LAUNCHED("spmm_kernel");
+  return 0;
+}
+
+}  // namespace vb

@@ -60,9 +60,16 @@ int64_t hex27_box_nnz(int nx, int ny, int nz);
 int hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1, int maxnp, int32_t* indptr,
                   int32_t* indices, double* Kv, double* Mv, cudaStream_t st);
 
-// linalg.cu
+// spmm.cu
+int csr_row_groups(int n, const int32_t* indptr, const int32_t* indices, int32_t* g_leader, int32_t* g_rows,
+                   int32_t* g_uoff, uint8_t* masks, int32_t* vmap, int* n_groups, int64_t* n_slots);
+int rg_gather_values(int64_t n_union, const int32_t* vmap, const double* vals, double* gvals, cudaStream_t st);
+int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
+            const int32_t* indptr, const int32_t* indices, const uint8_t* masks, const double* gvals, int k,
+            const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st);
 int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
              const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st);
+// linalg.cu
 int csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
                    z_t alpha, z_t* D, int64_t ldd, cudaStream_t st);
 size_t zgemm_workspace_bytes(char transa, int m, int n, int k);

@@ -24,10 +24,73 @@ def _cols(t: torch.Tensor) -> int:
     return 1 if t.dim() == 1 else t.shape[1]
 
 
-def spmm(A: DeviceCSR, X: torch.Tensor, alpha=1.0, beta=0.0, Y: torch.Tensor | None = None):
+RG_MIN_COLS = 17  # k above this takes the row-group SpMM (below: sub-warp CSR kernels)
+
+
+class RowGroups:
+    """Row-group form of a CSR pattern (vb_csr_row_groups): built once per
+    pattern on the host from the CSR arrays, kept on the device."""
+
+    def __init__(self, n: int, indptr: torch.Tensor, indices: torch.Tensor):
+        import ctypes
+        import numpy as np
+        lib = _lib.load()
+        ip = np.ascontiguousarray(indptr.cpu().numpy(), dtype=np.int32)
+        ix = np.ascontiguousarray(indices.cpu().numpy(), dtype=np.int32)
+        nnz = max(int(ix.size), 1)
+        lead = np.empty(max(n, 1), np.int32)
+        rows = np.empty((max(n, 1), 8), np.int32)
+        uoff = np.empty(max(n, 1), np.int32)
+        masks = np.empty(nnz, np.uint8)
+        vmap = np.empty((nnz, 8), np.int32)
+        G, U = ctypes.c_int(0), ctypes.c_int64(0)
+        hp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _lib.check(lib.vb_csr_row_groups(n, hp(ip), hp(ix), hp(lead), hp(rows), hp(uoff), hp(masks), hp(vmap),
+                                         ctypes.byref(G), ctypes.byref(U)), "vb_csr_row_groups")
+        dev = indptr.device
+        self.n_groups, self.n_union = G.value, U.value
+        g, u = self.n_groups, self.n_union
+        self.leader = torch.from_numpy(lead[:g].copy()).to(dev)
+        self.rows = torch.from_numpy(rows[:g].copy()).to(dev)
+        self.uoff = torch.from_numpy(uoff[:g].copy()).to(dev)
+        self.masks = torch.from_numpy(masks[:u].copy()).to(dev)
+        self.vmap = torch.from_numpy(vmap[:u].copy()).to(dev)
+
+    def values(self, data: torch.Tensor) -> torch.Tensor:
+        lib = _lib.load()
+        gv = torch.empty((self.n_union, 8), dtype=torch.float64, device=data.device)
+        _lib.check(lib.vb_rg_gather_values(self.n_union, _lib.ptr(self.vmap), _lib.ptr(data), _lib.ptr(gv),
+                                           _lib.stream_handle()), "vb_rg_gather_values")
+        return gv
+
+
+def row_groups(A: DeviceCSR) -> RowGroups:
+    """The pattern's row groups, cached on the pattern's indptr tensor (all
+    primitives sharing a pattern share them)."""
+    rg = getattr(A.indptr, "_vb_row_groups", None)
+    if rg is None or rg[0] is not A.indices:
+        rg = (A.indices, RowGroups(A.n, A.indptr, A.indices))
+        A.indptr._vb_row_groups = rg
+    return rg[1]
+
+
+def _rg_values(A: DeviceCSR, rg: RowGroups) -> torch.Tensor:
+    key = (A.data.data_ptr(), A.data._version, id(rg))
+    c = getattr(A.data, "_vb_rg_vals", None)
+    if c is None or c[0] != key:
+        c = (key, rg.values(A.data))
+        A.data._vb_rg_vals = c
+    return c[1]
+
+
+def spmm(A: DeviceCSR, X: torch.Tensor, alpha=1.0, beta=0.0, Y: torch.Tensor | None = None,
+         path: str = "auto"):
     """Y = alpha A X + beta Y (A real CSR, X/Y complex).  Uniform-box primitives
     (A.kron set) with k >= 2 columns take the matrix-free Kronecker apply
-    (vb_kron3_apply; same operator to rounding), everything else the CSR SpMM."""
+    (vb_kron3_apply; same operator to rounding); other matrices with
+    k >= RG_MIN_COLS columns the row-group SpMM (vb_rg_spmm, dense 8-row blocks on
+    the FP64 tensor cores; equal to the CSR kernels to rounding), everything else the CSR SpMM (vb_csr_spmm).
+    path: "auto", or "csr" / "rg" to force a CSR-form kernel."""
     lib = _lib.load()
     k = _cols(X)
     if Y is None:
@@ -36,10 +99,18 @@ def spmm(A: DeviceCSR, X: torch.Tensor, alpha=1.0, beta=0.0, Y: torch.Tensor | N
     ldx = _ld(X) if X.dim() == 2 else 1
     ldy = _ld(Y) if Y.dim() == 2 else 1
     kb = getattr(A, "kron", None)
-    if kb is not None and k >= 2:  # uniform-box primitive: matrix-free Kronecker apply
+    if path == "auto" and kb is not None and k >= 2:  # uniform-box primitive: matrix-free Kronecker apply
         _lib.check(lib.vb_kron3_apply(kb.npx, kb.npy, kb.npz, _lib.ptr(kb.K1), _lib.ptr(kb.M1), kb.maxnp,
                                       kb.stiff, k, _lib.zc(alpha), C_ptr(X), ldx, _lib.zc(beta), C_ptr(Y), ldy,
                                       _lib.stream_handle()), "vb_kron3_apply")
+        return Y
+    if path == "rg" or (path == "auto" and k >= RG_MIN_COLS):
+        rg = row_groups(A)
+        gv = _rg_values(A, rg)
+        _lib.check(lib.vb_rg_spmm(rg.n_groups, _lib.ptr(rg.leader), _lib.ptr(rg.rows), _lib.ptr(rg.uoff),
+                                  _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(rg.masks), _lib.ptr(gv), k,
+                                  C_ptr(X), ldx, C_ptr(Y), ldy, _lib.zc(alpha), _lib.zc(beta),
+                                  _lib.stream_handle()), "vb_rg_spmm")
         return Y
     _lib.check(lib.vb_csr_spmm(A.n, _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(A.data), k,
                                C_ptr(X), ldx, C_ptr(Y), ldy, _lib.zc(alpha), _lib.zc(beta),

@@ -78,13 +78,26 @@ def measure():
     out["box_csr_kernel_ms"] = t
     out["box_csr_GBps"] = alg_box / (t * 1e-3) / 1e9
     out["box_csr_frac_hbm"] = out["box_csr_GBps"] / peak_hbm
-    for k in (32, 400):
+    # CSR SpMM on the general (non-Kronecker) CSR: k = 1 SpMV, k = 8 sub-warp
+    # kernel (cfg3's 8 sources), k = 32 / 400 row-group kernel (+ the plain CSR
+    # warp-per-row kernel it replaces); the row groups are built once per pattern
+    t0 = __import__("time").perf_counter()
+    rg = linalg.row_groups(Kg)
+    out["spmm_row_groups_build_s"] = __import__("time").perf_counter() - t0
+    out["spmm_row_groups"] = rg.n_groups
+    out["spmm_row_group_reuse"] = nnz / rg.n_union
+    peak_fp64 = _lib.probe_fp64_peak()
+    for k in (1, 8, 32, 400):
         X = torch.randn(n, k, dtype=torch.complex128, device=dev)
-        t = timed(lambda: linalg.spmm(Kg, X))
         alg = nnz * 12 + 2 * n * k * 16
-        out[f"spmm_k{k}_ms"] = t
-        out[f"spmm_k{k}_GBps"] = alg / (t * 1e-3) / 1e9
-        out[f"spmm_k{k}_frac_hbm"] = out[f"spmm_k{k}_GBps"] / peak_hbm
+        for tag, path in (("", "auto"), ("_csr", "csr")):
+            if tag and k < 32:
+                continue
+            t = timed(lambda: linalg.spmm(Kg, X, path=path))
+            out[f"spmm{tag}_k{k}_ms"] = t
+            out[f"spmm{tag}_k{k}_GBps"] = alg / (t * 1e-3) / 1e9
+            out[f"spmm{tag}_k{k}_frac_hbm"] = out[f"spmm{tag}_k{k}_GBps"] / peak_hbm
+            out[f"spmm{tag}_k{k}_frac_fp64"] = 4 * nnz * k / (t * 1e-3) / 1e12 / peak_fp64
     # matrix-free Kronecker apply of the same primitive (uniform box): reads X and
     # writes Y once (+ x-y halo); bytes = X + Y (the CSR is not read)
     Kbox, _ = assembly.assemble_helmholtz_box(box, ne)
