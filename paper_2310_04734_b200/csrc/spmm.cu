@@ -3,9 +3,9 @@
 // 117, 162-179).  X, Y complex128 row-major (n x k, row stride ldx / ldy).
 //
 // Three kernels by column count:
-//  * k == 1   SpMV: a warp per row, lanes over the row's nonzeros, fixed-order
-//             warp reduction.
-//  * k <= 16  sub-warp CSR: KP = next_pow2(k) lanes per row, 32/KP rows per
+//  * k <= 2   SpMV-like: 8 lanes per row, 4 loads in flight per lane, both
+//             columns per lane, fixed-order shuffle reduction.
+//  * (k <= 16 sub-warp CSR, used below the row-group threshold or without groups): KP = next_pow2(k) lanes per row, 32/KP rows per
 //             warp; the row's (value, index) pairs are loaded KP at a time,
 //             coalesced, and broadcast inside the sub-warp by shuffle.  One
 //             128-B X piece per nonzero and warp instruction: no idle lanes.
@@ -27,30 +27,74 @@
 
 namespace vb {
 
-// ------------------------------------------------------------------ k == 1 --
-__global__ void spmv_kernel(int n_rows, const int32_t* __restrict__ indptr,
-                            const int32_t* __restrict__ indices, const double* __restrict__ vals,
-                            const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y, int64_t ldy,
-                            z_t alpha, z_t beta) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// ------------------------------------------------------------- k = 1, 2 ---
+// SpMV-like: SW lanes per row (32/SW rows per warp), each lane strides its row
+// by SW with 4 independent (value, index, x) loads in flight and keeps all KC
+// columns of its nonzeros, then a fixed-order shuffle reduction.
+template <int SW, int KC>
+__global__ void __launch_bounds__(256) spmv_kernel(int n_rows, const int32_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ indices,
+                                                   const double* __restrict__ vals, const z_t* __restrict__ X,
+                                                   int64_t ldx, z_t* __restrict__ Y, int64_t ldy, z_t alpha,
+                                                   z_t beta) {
+  constexpr int RPW = 32 / SW;
+  const int lane = threadIdx.x & 31, sl = lane % SW;
+  const int64_t sw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / SW;
+  const int64_t nsw = ((int64_t)gridDim.x * blockDim.x) / SW;
   const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
-  for (int64_t row = warp; row < n_rows; row += nwarps) {
-    const int b = indptr[row], e = indptr[row + 1];
-    double re = 0.0, im = 0.0;
-    for (int j = b + lane; j < e; j += 32) {
-      const double a = vals[j];
-      const z_t x = X[(int64_t)indices[j] * ldx];
-      re += a * x.x;
-      im += a * x.y;
+  const int64_t nr_pad = ((int64_t)n_rows + RPW - 1) / RPW * RPW;  // whole warps stay converged
+  for (int64_t row = sw; row < nr_pad; row += nsw) {
+    const bool rv = row < n_rows;
+    const int b = rv ? __ldg(indptr + row) : 0, e = rv ? __ldg(indptr + row + 1) : 0;
+    double re[KC], im[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) re[c] = im[c] = 0.0;
+    int j = b + sl;
+    for (; j + 3 * SW < e; j += 4 * SW) {
+      double a[4];
+      int ci[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = __ldg(vals + j + u * SW);
+        ci[u] = __ldg(indices + j + u * SW);
+      }
+      z_t x[4][KC];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < KC; ++c) x[u][c] = __ldg(X + (int64_t)ci[u] * ldx + c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          re[c] = fma(a[u], x[u][c].x, re[c]);
+          im[c] = fma(a[u], x[u][c].y, im[c]);
+        }
     }
-    re = warp_sum(re);
-    im = warp_sum(im);
-    if (lane == 0) {
-      z_t out = zmul(alpha, zmake(re, im));
-      if (!beta0) out = zfma(out, beta, Y[row * ldy]);
-      Y[row * ldy] = out;
+    for (; j < e; j += SW) {
+      const double a = __ldg(vals + j);
+      const z_t* xr = X + (int64_t)__ldg(indices + j) * ldx;
+#pragma unroll
+      for (int c = 0; c < KC; ++c) {
+        const z_t x = __ldg(xr + c);
+        re[c] = fma(a, x.x, re[c]);
+        im[c] = fma(a, x.y, im[c]);
+      }
+    }
+#pragma unroll
+    for (int o = SW / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < KC; ++c) {
+        re[c] += __shfl_xor_sync(0xffffffffu, re[c], o);
+        im[c] += __shfl_xor_sync(0xffffffffu, im[c], o);
+      }
+    if (rv && sl == 0) {
+#pragma unroll
+      for (int c = 0; c < KC; ++c) {
+        z_t out = zmul(alpha, zmake(re[c], im[c]));
+        if (!beta0) out = zfma(out, beta, Y[row * ldy + c]);
+        Y[row * ldy + c] = out;
+      }
     }
   }
 }
@@ -121,9 +165,9 @@ constexpr int RG = 8;  // rows per group
 // member rows.  X stage rows and value rows are padded by 32 B so that the
 // fragment loads of a half-warp (4 rows x 4 consecutive doubles) fall on 4
 // distinct 8-bank ranges (conflict-free).
-template <int CPL, int J, int S>
+template <int CW_, int J, int S>
 struct RgCfg {
-  static constexpr int CW = 32 * CPL;                        // complex columns per chunk
+  static constexpr int CW = CW_;                             // complex columns per chunk (8..64)
   static constexpr int RS = 2 * CW + 4;                      // doubles per X stage row (padded)
   static constexpr int VR = RG + 4;                          // doubles per value row (padded)
   static constexpr int XS = J * RS;                          // doubles per X stage
@@ -134,7 +178,7 @@ struct RgCfg {
 
 constexpr int RG_WARPS = 4;
 
-template <int CPL, int J, int S>
+template <int CW, int J, int S>
 __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, const int32_t* __restrict__ g_leader,
                                                                 const int32_t* __restrict__ g_rows,
                                                                 const int32_t* __restrict__ g_uoff,
@@ -144,9 +188,11 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
                                                                 const z_t* __restrict__ X, int64_t ldx,
                                                                 z_t* __restrict__ Y, int64_t ldy, z_t alpha,
                                                                 z_t beta) {
-  using C = RgCfg<CPL, J, S>;
+  using C = RgCfg<CW, J, S>;
   static_assert(J % 4 == 0 && 32 % J == 0, "stages of whole k4 steps inside one 32-column index block");
-  static_assert(J * RG / 2 <= 32, "value stage copied by one round of 16-B lanes");
+  static_assert((J * CW) % 32 == 0 && (J * RG / 2) % 32 == 0 || J * RG / 2 < 32, "copy rounds");
+  constexpr int XP = J * CW / 32;                 // 16-B X pieces per lane per stage
+  constexpr int VP = (J * RG / 2 + 31) / 32;      // 16-B value pieces per lane per stage
   extern __shared__ __align__(16) unsigned char rg_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gid = lane >> 2, tig = lane & 3;
@@ -155,9 +201,6 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
   double* xs = reinterpret_cast<double*>(rg_smem + (size_t)w * C::WARP_BYTES);
   double* vs = xs + S * C::XS;
   const int c0 = blockIdx.y * C::CW;  // first complex column of the chunk
-  bool cv[CPL];
-#pragma unroll
-  for (int t = 0; t < CPL; ++t) cv[t] = c0 + lane + 32 * t < k;
   const int leader = __ldg(g_leader + g);
   const int ub = __ldg(indptr + leader), nu = __ldg(indptr + leader + 1) - ub;
   const double* uv = gvals + (int64_t)__ldg(g_uoff + g) * RG;
@@ -167,20 +210,33 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
     const int slot = st % S;
     const int j0 = st * J;
     if ((j0 & 31) == 0) colv = j0 + lane < nu ? __ldg(indices + ub + j0 + lane) : 0;
+    if constexpr (CW >= 32) {  // one X row per step, CW / 32 pieces per lane
 #pragma unroll
-    for (int jj = 0; jj < J; ++jj) {
-      const int j = j0 + jj;
-      const int col = __shfl_sync(0xffffffffu, colv, j & 31);
-      const z_t* xr = X + (int64_t)col * ldx + c0 + lane;
+      for (int jj = 0; jj < J; ++jj) {
+        const int j = j0 + jj;
+        const int col = __shfl_sync(0xffffffffu, colv, j & 31);
+        const z_t* xr = X + (int64_t)col * ldx + c0 + lane;
 #pragma unroll
-      for (int t = 0; t < CPL; ++t)
-        blk::cp_async16(xs + slot * C::XS + jj * C::RS + 2 * (lane + 32 * t), cv[t] && j < nu ? xr + 32 * t : X,
-                        cv[t] && j < nu);
+        for (int t = 0; t < CW / 32; ++t) {
+          const bool ok = j < nu && c0 + lane + 32 * t < k;
+          blk::cp_async16(xs + slot * C::XS + jj * C::RS + 2 * (lane + 32 * t), ok ? xr + 32 * t : X, ok);
+        }
+      }
+    } else {  // 32 / CW rows per step: piece p = lane + 32 m is row p / CW, column p % CW
+#pragma unroll
+      for (int m = 0; m < XP; ++m) {
+        const int p = lane + 32 * m, jj = p / CW, c = p % CW, j = j0 + jj;
+        const int col = __shfl_sync(0xffffffffu, colv, j & 31);
+        const bool ok = j < nu && c0 + c < k;
+        blk::cp_async16(xs + slot * C::XS + jj * C::RS + 2 * c, ok ? X + (int64_t)col * ldx + c0 + c : X, ok);
+      }
     }
-    if (lane < J * RG / 2) {  // J value rows of 8 doubles = J*4 pieces of 16 B
-      const int j = j0 + lane / (RG / 2);
-      blk::cp_async16(vs + slot * C::VS + (lane >> 2) * C::VR + 2 * (lane & 3),
-                      j < nu ? uv + (int64_t)j0 * RG + 2 * lane : gvals, j < nu);
+#pragma unroll
+    for (int m = 0; m < VP; ++m) {  // J value rows of 8 doubles = J*4 pieces of 16 B
+      const int p = lane + 32 * m, jj = p >> 2, j = j0 + jj;
+      if (jj < J)
+        blk::cp_async16(vs + slot * C::VS + jj * C::VR + 2 * (p & 3),
+                        j < nu ? uv + (int64_t)j0 * RG + 2 * p : gvals, j < nu);
     }
     blk::cp_commit();
   };
@@ -296,19 +352,19 @@ int rg_gather_values(int64_t n_union, const int32_t* vmap, const double* vals, d
   return 0;
 }
 
-template <int CPL, int J, int S>
+template <int CW, int J, int S>
 static int rg_launch(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
                      const int32_t* indptr, const int32_t* indices, const double* gvals, int k, const z_t* X,
                      int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
-  constexpr int smem = RG_WARPS * RgCfg<CPL, J, S>::WARP_BYTES;
+  constexpr int smem = RG_WARPS * RgCfg<CW, J, S>::WARP_BYTES;
   static bool attr = false;
   if (!attr) {
-    VB_CUDA(cudaFuncSetAttribute(rg_spmm_kernel<CPL, J, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    VB_CUDA(cudaFuncSetAttribute(rg_spmm_kernel<CW, J, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  const dim3 grid((unsigned)((n_groups + RG_WARPS - 1) / RG_WARPS), (unsigned)((k + 32 * CPL - 1) / (32 * CPL)));
-  rg_spmm_kernel<CPL, J, S><<<grid, 32 * RG_WARPS, smem, st>>>(n_groups, g_leader, g_rows, g_uoff, indptr, indices,
-                                                               gvals, k, X, ldx, Y, ldy, alpha, beta);
+  const dim3 grid((unsigned)((n_groups + RG_WARPS - 1) / RG_WARPS), (unsigned)((k + CW - 1) / CW));
+  rg_spmm_kernel<CW, J, S><<<grid, 32 * RG_WARPS, smem, st>>>(n_groups, g_leader, g_rows, g_uoff, indptr, indices,
+                                                              gvals, k, X, ldx, Y, ldy, alpha, beta);
   VB_LAUNCHED("rg_spmm_kernel");
   return 0;
 }
@@ -317,11 +373,13 @@ int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const 
             const int32_t* indptr, const int32_t* indices, const uint8_t* /*masks*/, const double* gvals, int k,
             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
   if (n_groups <= 0 || k <= 0) return 0;
-  if (k <= 32)
-    return rg_launch<1, 4, 4>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy,
-                              alpha, beta, st);
-  return rg_launch<2, 4, 4>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy, alpha,
-                            beta, st);
+#define VB_RG(CW, J) \
+  return rg_launch<CW, J, 4>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy, alpha, beta, st)
+  if (k <= 8) VB_RG(8, 16);
+  if (k <= 16) VB_RG(16, 8);
+  if (k <= 32) VB_RG(32, 4);
+  VB_RG(64, 4);
+#undef VB_RG
 }
 
 // ------------------------------------------------------------ dispatcher ---
@@ -385,9 +443,9 @@ int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const do
     return (unsigned)std::min<int64_t>((warps * 32 + nt - 1) / nt, 148 * 64);
   };
   if (k == 1) {
-    spmv_kernel<<<grid_for(1), nt, 0, st>>>(n_rows, indptr, indices, vals, X, ldx, Y, ldy, alpha, beta);
+    spmv_kernel<8, 1><<<grid_for(4), nt, 0, st>>>(n_rows, indptr, indices, vals, X, ldx, Y, ldy, alpha, beta);
   } else if (k == 2) {
-    spmm_subwarp_kernel<2><<<grid_for(16), nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
+    spmv_kernel<8, 2><<<grid_for(4), nt, 0, st>>>(n_rows, indptr, indices, vals, X, ldx, Y, ldy, alpha, beta);
   } else if (k <= 4) {
     spmm_subwarp_kernel<4><<<grid_for(8), nt, 0, st>>>(n_rows, indptr, indices, vals, k, X, ldx, Y, ldy, alpha, beta);
   } else if (k <= 8) {

@@ -24,7 +24,7 @@ def _cols(t: torch.Tensor) -> int:
     return 1 if t.dim() == 1 else t.shape[1]
 
 
-RG_MIN_COLS = 17  # k above this takes the row-group SpMM (below: sub-warp CSR kernels)
+RG_MIN_COLS = 3  # k from here takes the row-group SpMM (below: the SpMV / sub-warp CSR kernels)
 
 
 class RowGroups:

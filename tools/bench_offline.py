@@ -87,11 +87,11 @@ def measure():
     out["spmm_row_groups"] = rg.n_groups
     out["spmm_row_group_reuse"] = nnz / rg.n_union
     peak_fp64 = _lib.probe_fp64_peak()
-    for k in (1, 8, 32, 400):
+    for k in (1, 2, 8, 32, 400):
         X = torch.randn(n, k, dtype=torch.complex128, device=dev)
         alg = nnz * 12 + 2 * n * k * 16
         for tag, path in (("", "auto"), ("_csr", "csr")):
-            if tag and k < 32:
+            if tag and k < 8:
                 continue
             t = timed(lambda: linalg.spmm(Kg, X, path=path))
             out[f"spmm{tag}_k{k}_ms"] = t
