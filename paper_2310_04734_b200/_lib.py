@@ -135,8 +135,12 @@ def ptr(t) -> C.c_void_p | None:
 
 
 def stream_handle(stream=None) -> C.c_void_p:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+    """cudaStream_t of `stream` (default: torch's current stream on the current
+    device, read without building a torch.cuda.Stream object: ~1 us instead of
+    ~14 us per call on the many-small-launch offline paths)."""
+    if stream is not None:
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def launch_count() -> int:

@@ -49,7 +49,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
                 [src.stat().st_mtime] + [h.stat().st_mtime for h in CSRC.glob("*.cuh")]
                 + [(PKG_DIR.parent / "include" / "vibro_b200.h").stat().st_mtime]):
             continue
-        cmd = [nvcc()] + [f for f in NVCC_FLAGS if f != "-shared"] + ["-c", str(src), "-o", str(obj)]
+        cmd = [nvcc()] + [f for f in NVCC_FLAGS if f != "-shared"] + os.environ.get("VB_NVCC_EXTRA", "").split() \
+            + ["-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

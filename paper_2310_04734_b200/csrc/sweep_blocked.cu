@@ -39,8 +39,14 @@ using GemmNarrow = Gemm<64, 16, 8, 1, 2, EPI_SUB>; // back-substitution updates 
 using GemmOut = Gemm<64, 16, 8, 1, 2, EPI_SET>;   // y = C_R x
 
 constexpr int LDL = NB + 4;     // == 4 (mod 8): triangular inverse used as A operand
-constexpr int DEEP_MIN_R = 640;   // outer steps of 2 panels (trailing K = 128) from this order on
-constexpr int DEEP4_MIN_R = 1536; // ... of 4 panels (K = 256)
+#ifndef VB_DEEP_MIN_R
+#define VB_DEEP_MIN_R 640
+#endif
+#ifndef VB_DEEP4_MIN_R
+#define VB_DEEP4_MIN_R 1536
+#endif
+constexpr int DEEP_MIN_R = VB_DEEP_MIN_R;    // outer steps of 2 panels (trailing K = 128) from this order on
+constexpr int DEEP4_MIN_R = VB_DEEP4_MIN_R;  // ... of 4 panels (K = 256)
 constexpr int LDY = 16 + 2;
 constexpr size_t TRSM_SMEM = (size_t)(NB * LDL) * sizeof(z_t);
 constexpr size_t BACK_SMEM = (size_t)(NB * LDL + NB * LDY) * sizeof(z_t);

@@ -16,6 +16,7 @@ CSR primitives) to a relative residual <= 1e-10 (solvers.py:72-73 metric).
 from __future__ import annotations
 
 import math
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import scipy.linalg as sla
@@ -24,6 +25,7 @@ import torch
 from . import _lib, linalg
 
 CDT = torch.complex128
+_POOL = ThreadPoolExecutor(3, thread_name_prefix="vb_fdm_eig")  # the three axes of a factorisation
 GAUSS3 = (np.array([-math.sqrt(0.6), 0.0, math.sqrt(0.6)]), np.array([5 / 9, 8 / 9, 5 / 9]))
 
 
@@ -58,6 +60,7 @@ class BoxFDM:
         self.walls = dict(walls)  # side ('x0', ..., 'z1') -> complex Z
         self.lines = [line_matrices(L, m) for L, m in zip((x1 - x0, y1 - y0, z1 - z0), ne)]
         self.shape = tuple(2 * m + 1 for m in ne)  # (npx, npy, npz)
+        self._chol_inv: dict[int, np.ndarray] = {}
 
     @property
     def n(self) -> int:
@@ -72,6 +75,24 @@ class BoxFDM:
                 i = 0 if side[1] == "0" else A.shape[0] - 1
                 A[i, i] += 1j * w / Z
         return A
+
+    def axis_eig(self, d: int, f: float):
+        """Generalised eigenpairs A_d V = M_d V Lambda with V^T M_d V = I.  M_d
+        is SPD: with M_d = L L^T (cached, frequency independent) this is the
+        standard complex-symmetric problem C W = W Lambda, C = L^-1 A_d L^-T,
+        V = L^-T W (zgeev on C: ~2.5x faster than the QZ of zggev at these
+        sizes).  One BLAS thread: the three axes run concurrently."""
+        from threadpoolctl import threadpool_limits
+        Li = self._chol_inv.get(d)
+        if Li is None:
+            L = np.linalg.cholesky(self.lines[d][1])
+            Li = self._chol_inv[d] = sla.solve_triangular(L, np.eye(L.shape[0]), lower=True)
+        with threadpool_limits(1):
+            C = Li @ self.direction_operator(d, f) @ Li.T
+            lam, W = np.linalg.eig(C)
+            nrm = np.sqrt(np.einsum("ij,ij->j", W, W))  # complex-symmetric normalisation: V^T M V = W^T W
+            V = (Li.T @ W) / nrm
+        return lam, V
 
     def factor(self, f: float, fom=None, device=None, tol: float = 1e-10, max_refine: int = 8):
         return FdmFactor(self, f, fom, device, tol, max_refine)
@@ -90,12 +111,7 @@ class FdmFactor:
         w = 2.0 * math.pi * f
         self.sigma = -w * w / (box.rho * box.c * box.c)
         self.V, self.VT, self.lam = [], [], []
-        for d in range(3):
-            A = box.direction_operator(d, f)
-            M = box.lines[d][1]
-            lam, V = sla.eig(A, M)
-            nrm = np.sqrt(np.einsum("ij,ik,kj->j", V, M, V))  # complex-symmetric normalisation
-            V = V / nrm
+        for lam, V in _POOL.map(lambda d: box.axis_eig(d, f), range(3)):
             self.V.append(torch.as_tensor(np.ascontiguousarray(V), device=self.dev))
             self.VT.append(torch.as_tensor(np.ascontiguousarray(V.T), device=self.dev))
             self.lam.append(torch.as_tensor(lam.astype(complex), device=self.dev))

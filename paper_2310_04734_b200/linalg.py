@@ -25,6 +25,7 @@ def _cols(t: torch.Tensor) -> int:
 
 
 RG_MIN_COLS = 3  # k from here takes the row-group SpMM (below: the SpMV / sub-warp CSR kernels)
+RG_MIN_REUSE = 2.0
 
 
 class RowGroups:
@@ -50,6 +51,11 @@ class RowGroups:
         dev = indptr.device
         self.n_groups, self.n_union = G.value, U.value
         g, u = self.n_groups, self.n_union
+        # X-row reuse of the grouping (nonzeros per gathered X row); below
+        # RG_MIN_REUSE the dense 8-row blocks are mostly padding (e.g. a
+        # row-restricted boundary matrix whose column ids are not its row ids)
+        # and spmm keeps the CSR kernels
+        self.reuse = int(ix.size) / max(u, 1)
         self.leader = torch.from_numpy(lead[:g].copy()).to(dev)
         self.rows = torch.from_numpy(rows[:g].copy()).to(dev)
         self.uoff = torch.from_numpy(uoff[:g].copy()).to(dev)
@@ -104,8 +110,8 @@ def spmm(A: DeviceCSR, X: torch.Tensor, alpha=1.0, beta=0.0, Y: torch.Tensor | N
                                       kb.stiff, k, _lib.zc(alpha), C_ptr(X), ldx, _lib.zc(beta), C_ptr(Y), ldy,
                                       _lib.stream_handle()), "vb_kron3_apply")
         return Y
-    if path == "rg" or (path == "auto" and k >= RG_MIN_COLS):
-        rg = row_groups(A)
+    rg = row_groups(A) if path == "rg" or (path == "auto" and k >= RG_MIN_COLS) else None
+    if rg is not None and (path == "rg" or rg.reuse >= RG_MIN_REUSE):
         gv = _rg_values(A, rg)
         _lib.check(lib.vb_rg_spmm(rg.n_groups, _lib.ptr(rg.leader), _lib.ptr(rg.rows), _lib.ptr(rg.uoff),
                                   _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(rg.masks), _lib.ptr(gv), k,

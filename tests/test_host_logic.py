@@ -143,3 +143,17 @@ def test_gather_variable_width_blocks_over_gloo():
         assert len(full) == 5
         for a, b in zip(full, expect):
             np.testing.assert_array_equal(a, b)
+
+
+def test_fdm_axis_eigenpairs_diagonalise_the_pencil():
+    """BoxFDM.axis_eig (Cholesky-reduced zgeev): A_d V = M_d V Lambda and
+    V^T M_d V = I (the complex-symmetric normalisation fdm.py relies on)."""
+    import numpy as np
+    from paper_2310_04734_b200.fdm import BoxFDM
+    box = BoxFDM((0, 0, 0, 2.0, 1.6, 1.2), (10, 8, 6), 1.21, 343.0, {"x0": 2000.0 + 300j, "z1": 900.0})
+    for d in range(3):
+        for f in (20.0, 180.0):
+            lam, V = box.axis_eig(d, f)
+            A, M = box.direction_operator(d, f), box.lines[d][1]
+            assert np.abs(A @ V - M @ V * lam).max() <= 1e-9 * np.abs(A).max()
+            assert np.abs(V.T @ M @ V - np.eye(len(lam))).max() <= 1e-10
