@@ -172,7 +172,8 @@ int vb_csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const
  * an ungrouped row becomes a group leader and adopts up to 7 ungrouped rows
  * among its columns whose column sets are subsets of its own.  Outputs (sized
  * by the caller for the worst case: n_rows groups, nnz union slots):
- *   g_leader[G], g_rows[G][8] (member rows, -1 padded), g_uoff[G] (offset of
+ *   g_leader[G] (-1: a group of up to 8 EMPTY rows, listed after all others),
+ *   g_rows[G][8] (member rows, -1 padded), g_uoff[G] (offset of
  *   the group's union = the leader's CSR row in the union space),
  *   masks[U] (bit i: member i has that column), vmap[U][8] (CSR position of
  *   (member i, union column j), -1 absent); *n_groups = G, *n_union = U. */

@@ -201,8 +201,9 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
   double* xs = reinterpret_cast<double*>(rg_smem + (size_t)w * C::WARP_BYTES);
   double* vs = xs + S * C::XS;
   const int c0 = blockIdx.y * C::CW;  // first complex column of the chunk
-  const int leader = __ldg(g_leader + g);
-  const int ub = __ldg(indptr + leader), nu = __ldg(indptr + leader + 1) - ub;
+  const int leader = __ldg(g_leader + g);  // -1: a group of empty rows (Y = beta Y)
+  const int ub = leader >= 0 ? __ldg(indptr + leader) : 0;
+  const int nu = leader >= 0 ? __ldg(indptr + leader + 1) - ub : 0;
   const double* uv = gvals + (int64_t)__ldg(g_uoff + g) * RG;
   const int nst = (nu + J - 1) / J;  // stages of J leader columns
   int colv = 0;                      // leader columns of the current 32-block, lane-parallel
@@ -297,16 +298,21 @@ int csr_row_groups(int n, const int32_t* indptr, const int32_t* indices, int32_t
   std::vector<char> grouped(n, 0);
   int G = 0;
   int64_t uoff = 0;
+  std::vector<int> empty;  // empty rows: packed 8 per leaderless group at the end
   for (int r = 0; r < n; ++r) {
     if (grouped[r]) continue;
     grouped[r] = 1;
     const int rb = indptr[r], re = indptr[r + 1];
+    if (rb == re) {
+      empty.push_back(r);
+      continue;
+    }
     int mem[RG];
     int nm = 0;
     mem[nm++] = r;
     for (int j = rb; j < re && nm < RG; ++j) {
       const int c = indices[j];
-      if (c < 0 || c >= n || grouped[c]) continue;
+      if (c < 0 || c >= n || grouped[c] || indptr[c] == indptr[c + 1]) continue;  // empty rows: packed apart
       // subset test: row c's columns inside row r's columns (both sorted)
       int p = rb;
       bool sub = true;
@@ -336,6 +342,12 @@ int csr_row_groups(int n, const int32_t* indptr, const int32_t* indices, int32_t
       }
     }
     uoff += re - rb;
+    ++G;
+  }
+  for (size_t e0 = 0; e0 < empty.size(); e0 += RG) {  // Y rows only scaled by beta
+    g_leader[G] = -1;
+    g_uoff[G] = 0;
+    for (int i = 0; i < RG; ++i) g_rows[(int64_t)G * RG + i] = e0 + i < empty.size() ? empty[e0 + i] : -1;
     ++G;
   }
   *n_groups = G;

@@ -27,6 +27,8 @@ def _emulate(A, rg, X):
     masks, vmap = rg.masks.numpy(), rg.vmap.numpy()
     Y = np.zeros((A.shape[0], X.shape[1]), complex)
     for g in range(rg.n_groups):
+        if lead[g] < 0:       # group of empty rows
+            continue
         b, e = A.indptr[lead[g]], A.indptr[lead[g] + 1]
         for j in range(e - b):
             col, m = A.indices[b + j], masks[uoff[g] + j]
@@ -43,10 +45,16 @@ def _check_structure(A, rg):
     members = rows[rows >= 0]
     assert np.array_equal(np.sort(members), np.arange(n))          # a partition of the rows
     lead, uoff = rg.leader.numpy(), rg.uoff.numpy()
-    assert np.array_equal(rows[:, 0], lead)
+    full = lead >= 0
+    assert np.array_equal(rows[full, 0], lead[full])
+    # leaderless groups hold exactly the empty rows, after all others
+    empty = np.flatnonzero(np.diff(A.indptr) == 0)
+    er = rows[~full]
+    assert np.array_equal(np.sort(er[er >= 0]), empty)
+    assert full[:full.sum()].all()
     masks, vmap = rg.masks.numpy(), rg.vmap.numpy()
     seen = np.zeros(A.nnz, bool)
-    for g in range(rg.n_groups):
+    for g in np.flatnonzero(full):
         lc = A.indices[A.indptr[lead[g]]:A.indptr[lead[g] + 1]]
         for i, r in enumerate(rows[g]):
             if r < 0:
@@ -62,7 +70,7 @@ def _check_structure(A, rg):
             assert (vmap[sl, i][~bits] == -1).all()
             seen[pos] = True
     assert seen.all()
-    assert rg.n_union == sum(A.indptr[l + 1] - A.indptr[l] for l in lead)
+    assert rg.n_union == sum(A.indptr[l + 1] - A.indptr[l] for l in lead[full])
 
 
 def test_row_groups_hex27_box_are_node_blocks():
@@ -115,16 +123,24 @@ def _dev_csr(A, dev):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("k", [2, 3, 5, 8, 11, 16, 17, 32, 33, 64, 100])
-@pytest.mark.parametrize("kind", ["random", "hex27"])
+@pytest.mark.parametrize("kind", ["random", "hex27", "wall"])
 def test_spmm_paths_match_scipy_and_each_other(cuda, k, kind):
     import torch
     from paper_2310_04734_b200 import linalg
     rng = np.random.default_rng(k)
     if kind == "random":
         A = sp.random(700, 700, density=0.03, random_state=k, format="csr")
-    else:
+    elif kind == "hex27":
         A, _ = fe.kron_box((0, 0, 0, 1.2, 0.9, 0.7), 5, 4, 3)
         A = sp.csr_matrix(A)
+        A.sort_indices()
+    else:   # boundary primitive: rows of one wall only (most rows empty)
+        A, _ = fe.kron_box((0, 0, 0, 1.2, 0.9, 0.7), 5, 4, 3)
+        A = sp.csr_matrix(A)
+        keep = np.zeros(A.shape[0])
+        keep[: 11 * 9] = 1.0          # the z = 0 node layer
+        A = sp.csr_matrix(sp.diags(keep) @ A @ sp.diags(keep))
+        A.eliminate_zeros()
         A.sort_indices()
     n = A.shape[0]
     X = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
