@@ -385,10 +385,19 @@ int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const 
             const int32_t* indptr, const int32_t* indices, const uint8_t* /*masks*/, const double* gvals, int k,
             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
   if (n_groups <= 0 || k <= 0) return 0;
+#ifndef VB_RG_S
+#define VB_RG_S 3
+#endif
 #define VB_RG(CW, J) \
-  return rg_launch<CW, J, 4>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy, alpha, beta, st)
-  if (k <= 8) VB_RG(8, 16);
-  if (k <= 16) VB_RG(16, 8);
+  return rg_launch<CW, J, VB_RG_S>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy, alpha, beta, st)
+#ifndef VB_RG_J8
+#define VB_RG_J8 8
+#endif
+#ifndef VB_RG_J16
+#define VB_RG_J16 4
+#endif
+  if (k <= 8) VB_RG(8, VB_RG_J8);
+  if (k <= 16) VB_RG(16, VB_RG_J16);
   if (k <= 32) VB_RG(32, 4);
   VB_RG(64, 4);
 #undef VB_RG
