@@ -16,8 +16,8 @@
 //             the X rows staged through a cp.async ring.  Each X row is read
 //             once per group instead of once per nonzero (hex27 2x2x2 node
 //             blocks: 512 nonzeros over 125 columns = 4.1x less gather
-//             traffic).  Column chunks of 32*CPL are the slow grid dimension
-//             so the X slab of one chunk stays L2-resident.
+//             traffic).  Column chunks are the FAST grid dimension
+//             so a group tile's value rows are read from DRAM once for all chunks.
 #include "common.cuh"
 #include "sweep.cuh"
 #include "mma.cuh"
@@ -177,6 +177,9 @@ struct RgCfg {
 };
 
 constexpr int RG_WARPS = 4;
+#ifndef VB_RG_CHUNK_FAST
+#define VB_RG_CHUNK_FAST 1  // the chunks of a group tile run together: its value rows are read from DRAM once
+#endif
 
 template <int CW, int J, int S>
 __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, const int32_t* __restrict__ g_leader,
@@ -196,11 +199,19 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
   extern __shared__ __align__(16) unsigned char rg_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gid = lane >> 2, tig = lane & 3;
+#if VB_RG_CHUNK_FAST
+  const int g = blockIdx.y * RG_WARPS + w;
+#else
   const int g = blockIdx.x * RG_WARPS + w;
+#endif
   if (g >= n_groups) return;
   double* xs = reinterpret_cast<double*>(rg_smem + (size_t)w * C::WARP_BYTES);
   double* vs = xs + S * C::XS;
+#if VB_RG_CHUNK_FAST
+  const int c0 = blockIdx.x * C::CW;  // first complex column of the chunk
+#else
   const int c0 = blockIdx.y * C::CW;  // first complex column of the chunk
+#endif
   const int leader = __ldg(g_leader + g);  // -1: a group of empty rows (Y = beta Y)
   const int ub = leader >= 0 ? __ldg(indptr + leader) : 0;
   const int nu = leader >= 0 ? __ldg(indptr + leader + 1) - ub : 0;
@@ -374,7 +385,11 @@ static int rg_launch(int n_groups, const int32_t* g_leader, const int32_t* g_row
     VB_CUDA(cudaFuncSetAttribute(rg_spmm_kernel<CW, J, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
+#if VB_RG_CHUNK_FAST
+  const dim3 grid((unsigned)((k + CW - 1) / CW), (unsigned)((n_groups + RG_WARPS - 1) / RG_WARPS));
+#else
   const dim3 grid((unsigned)((n_groups + RG_WARPS - 1) / RG_WARPS), (unsigned)((k + CW - 1) / CW));
+#endif
   rg_spmm_kernel<CW, J, S><<<grid, 32 * RG_WARPS, smem, st>>>(n_groups, g_leader, g_rows, g_uoff, indptr, indices,
                                                               gvals, k, X, ldx, Y, ldy, alpha, beta);
   VB_LAUNCHED("rg_spmm_kernel");
