@@ -23,6 +23,12 @@
 #ifndef VB_SKINNY_3M
 #define VB_SKINNY_3M 0
 #endif
+// GEMM epilogue: results written into the shared-memory C tile and stored by
+// TMA (one bulk tensor store per 8-complex box) instead of scattered 16-byte
+// global stores from every lane.
+#ifndef VB_TMA_STORE_EPI
+#define VB_TMA_STORE_EPI 1
+#endif
 
 namespace vb {
 namespace tma {
@@ -123,6 +129,25 @@ __device__ __forceinline__ void tma_load_3d_w(void* dst, const CUtensorMap* map,
           smem_u32(dst)),
       "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Warp-collective TMA tensor store (shared -> global) + commit of its bulk
+// group; the elected lane owns the group, so completion waits are executed by
+// all lanes (lanes without outstanding groups return at once).
+__device__ __forceinline__ void tma_store_3d_w(const void* src, const CUtensorMap* map, int x, int y, int z) {
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+      " @p cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+      " @p cp.async.bulk.commit_group;\n}\n" ::"l"(map),
+      "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 __device__ __forceinline__ int perm8(int x) { return (x >> 1) | ((x & 1) << 2); }
@@ -522,12 +547,18 @@ struct GemmTma {
               const int cfrag = 2 * ak + v;  // fragment column 0..7
               const int col = wn * 16 + j * 8 + perm8(cfrag);
               if (m0 + row < M && n0 + col < N) {
-                const z_t c = *(const z_t*)(Cs + (col >> 3) * 8192 + swz(row, col & 7));
+                z_t* cp = (z_t*)(Cs + (col >> 3) * 8192 + swz(row, col & 7));
+                const z_t c = *cp;
 #if VB_GEMM_3M
                 const double pr = cr[i][j][v] - c2[i][j][v], pi = ci[i][j][v] - cr[i][j][v] - c2[i][j][v];
-                Cg[(size_t)(cr0 + m0 + row) * ldw + cc0 + n0 + col] = zmake(c.x - pr, c.y - pi);
+                const z_t o = zmake(c.x - pr, c.y - pi);
 #else
-                Cg[(size_t)(cr0 + m0 + row) * ldw + cc0 + n0 + col] = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+                const z_t o = zmake(c.x - cr[i][j][v], c.y - ci[i][j][v]);
+#endif
+#if VB_TMA_STORE_EPI
+                *cp = o;  // out-of-range elements keep their loaded value: the box store rewrites them unchanged
+#else
+                Cg[(size_t)(cr0 + m0 + row) * ldw + cc0 + n0 + col] = o;
 #endif
               }
               cr[i][j][v] = 0.0;
@@ -536,8 +567,24 @@ struct GemmTma {
               c2[i][j][v] = 0.0;
 #endif
             }
+#if VB_TMA_STORE_EPI
+        fence_proxy_async_shared();  // this lane's results -> visible to the TMA store
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->cempty);
+#if VB_TMA_STORE_EPI
+        if (warp < 4) {  // box `warp` of the finished tile back to global, then the next tile's C
+          mbar_wait(&bars->cempty, cempty_ph);
+          cempty_ph ^= 1;
+          tma_store_3d_w(Cs + warp * 8192, &mp->a64, 2 * (cc0 + n0 + 8 * warp), cr0 + m0, cta);
+          if (t + 1 < ntiles) {
+            bulk_wait_read_all();  // the box has left shared memory
+            fence_proxy_async_global();
+            const Cur nx = advance(cc);
+            issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, nx.m * TM, nx.n * TN);
+          }
+        }
+#else
         if (warp < 4 && t + 1 < ntiles) {
           mbar_wait(&bars->cempty, cempty_ph);
           cempty_ph ^= 1;
@@ -545,6 +592,7 @@ struct GemmTma {
           const Cur nx = advance(cc);
           issue_c(warp, mp, Cs, &bars->cfull, cta, cr0, cc0, nx.m * TM, nx.n * TN);
         }
+#endif
         GT_MARK(3);
         kc = 0;
         ++t;
@@ -553,6 +601,12 @@ struct GemmTma {
         ++kc;
       }
     }
+#if VB_TMA_STORE_EPI
+    if (warp < 4) {  // the last tile's stores complete before anyone reads the result
+      bulk_wait_all();
+      fence_proxy_async_global();
+    }
+#endif
     __syncthreads();
     if (tid == 0) {
 #pragma unroll
