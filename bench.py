@@ -148,6 +148,54 @@ def cpu_literal_rate(w, n_freq: int = 20):
     return n_freq / dt, dt, n_freq
 
 
+def cpu_cfg1_pipeline():
+    """SURVEY §8(d) offline CPU baselines: the reference algorithm end to end on
+    cfg1 (oracle restatement: hex27 assembly, scipy splu per expansion point +
+    second-order Krylov, MGS2 _orthonormalise, the literal per-frequency
+    re-projection + zgesv of ReducedModel.output over all 181 frequencies, SPL),
+    stage by stage, on the host cores.  Compare with offline.cfg1_pipeline_s /
+    cfg1_pipeline_fdm_s (the same chain on the GPU)."""
+    from oracle import fe
+    from oracle import mor as omor
+    from paper_2310_04734_b200 import workloads
+    t = {}
+    t0 = time.perf_counter()
+    nodes, elems = fe.structured_hex27(workloads.CFG1_BOX, *workloads.CFG1_NE)
+    Kg, Mn = fe.assemble_helmholtz(nodes, elems, fe.HEX27_IDX)
+    el, loc = fe.hex27_face(workloads.CFG1_NE, "z0")
+    Fz = fe.face_mass_hex27(nodes, elems, el, loc)
+    rho, c = workloads.AIR_RHO, workloads.AIR_C
+    K, M, D = (Kg / rho).astype(complex), (Mn / (rho * c * c)).astype(complex), Fz / workloads.CFG1_Z
+    t["assembly_s"] = time.perf_counter() - t0
+    _, _, src, rec = workloads.cfg1_layout()
+    lay = {"src": src, "rec": rec, "freqs": np.arange(20.0, 200.5, 1.0), "points": workloads.CFG1_POINTS,
+           "moments": workloads.CFG1_MOMENTS}
+    n = K.shape[0]
+    b = np.zeros(n, complex)
+    b[lay["src"]] = 1.0
+    C = np.zeros((len(lay["rec"]), n))
+    C[np.arange(len(lay["rec"])), lay["rec"]] = 1.0
+    fom = omor.Fom(stiffness=lambda f: K, mass=lambda f: M, load=lambda f: b, c_out=C, n=n, damping=lambda f: D)
+    V, tk, to = None, 0.0, 0.0
+    for f0 in lay["points"]:
+        a = time.perf_counter()
+        Q, _ = omor.krylov_block(fom, f0, lay["moments"], second_order=True)
+        bb = time.perf_counter()
+        V = omor.orthonormalise(V, Q)
+        tk += bb - a
+        to += time.perf_counter() - bb
+    t["krylov_splu_s"], t["orthonormalise_s"] = tk, to
+    a = time.perf_counter()
+    for f in lay["freqs"]:
+        omor.mean_spl(omor.reduced_output(fom, V, float(f)))
+    t["sweep_s"] = time.perf_counter() - a
+    t["total_s"] = t["assembly_s"] + tk + to + t["sweep_s"]
+    t["r"] = int(V.shape[1])
+    t["n"] = int(n)
+    t["freqs"] = len(lay["freqs"])
+    return t
+
+
 def cpu_sample_size(w, budget_s: float) -> int:
     """Number of frequencies the CPU port finishes in about budget_s seconds
     (pilot of 8 frequencies after a warm-up call)."""
@@ -409,6 +457,7 @@ def run_ours(args):
         cpu["literal_path"] = {"value": lrate, "unit": UNIT, "sample": f"{ln} random grid frequencies in "
                                f"{ldt:.1f} s", "path": "oracle.mor.reduced_output = ReducedModel.output "
                                "(mor.py:73-98) with dense reduced providers and V = I"}
+        cpu["cfg1_pipeline"] = cpu_cfg1_pipeline()
 
     offline = None
     if ws == 1 and not args.no_offline:
