@@ -193,6 +193,20 @@ int vb_rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, con
                const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha, vb_complex beta,
                void* stream);
 
+/* In-block Gram-Schmidt of a new basis block (vibrofem/mor.py:122-135, the
+ * column loop of _orthonormalise after the block is projected on V), fused
+ * into one cooperative kernel: for each column j of W (n x kb, kb <= 16),
+ * two CGS passes against the kept columns Q[:, :nk], keep iff
+ * refs[j] > 0 and ||w|| > drop_tol * refs[j] (a kept column with
+ * ||w|| < reorth_ratio * refs[j] gets a third pass), Q[:, nk++] = w / ||w||.
+ * W is overwritten with the orthogonalised columns.  kept[kb] (0/1) and
+ * *nk (device) out.  no_drop = 1: keep every column (refs unused); Q may
+ * equal W (in place).  Deterministic fixed-order reductions. */
+size_t vb_block_gs_workspace_bytes(void);
+int vb_block_gs(int n, int kb, vb_complex* W, int64_t ldw, const double* refs, double drop_tol, double reorth_ratio,
+                int no_drop, vb_complex* Q, int64_t ldq, int32_t* kept, int32_t* nk, void* work, size_t work_bytes,
+                void* stream);
+
 /* Y = alpha * Op X + beta * Y for the assembled primitives of a uniform hex27
  * box WITHOUT the CSR: Op = Kx(x)My(x)Mz + Mx(x)Ky(x)Mz + Mx(x)My(x)Kz
  * (stiff = 1, Kgrad) or Mx(x)My(x)Mz (stiff = 0, Mnn), the exact Kronecker

@@ -65,6 +65,9 @@ _SIGS = {
     "vb_rg_spmm": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                              C.c_void_p, C.c_int, _z, C.c_int64, _z, C.c_int64, VbComplex, VbComplex,
                              C.c_void_p]),
+    "vb_block_gs_workspace_bytes": (C.c_size_t, []),
+    "vb_block_gs": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, C.c_double, C.c_double, C.c_int, _z,
+                              C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "vb_kron3_apply": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                  VbComplex, _z, C.c_int64, VbComplex, _z, C.c_int64, C.c_void_p]),
     "vb_csr_axpy_dense": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, VbComplex, _z, C.c_int64,

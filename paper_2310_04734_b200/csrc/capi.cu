@@ -171,6 +171,16 @@ int vb_rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, con
                      (z_t*)Y, ldy, zc(alpha), zc(beta), (cudaStream_t)stream);
 }
 
+size_t vb_block_gs_workspace_bytes(void) { return vb::block_gs_workspace_bytes(); }
+
+int vb_block_gs(int n, int kb, vb_complex* W, int64_t ldw, const double* refs, double drop_tol, double reorth_ratio,
+                int no_drop, vb_complex* Q, int64_t ldq, int32_t* kept, int32_t* nk, void* work, size_t work_bytes,
+                void* stream) {
+  VB_CHECK_ARG(W && Q && kept && nk && (no_drop || refs), "vb_block_gs: null pointer");
+  return vb::block_gs(n, kb, (z_t*)W, ldw, refs, drop_tol, reorth_ratio, no_drop, (z_t*)Q, ldq, kept, nk, work,
+                      work_bytes, (cudaStream_t)stream);
+}
+
 int vb_csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
                       vb_complex alpha, vb_complex* D, int64_t ldd, void* stream) {
   VB_CHECK_ARG(n_rows >= 0 && D, "vb_csr_axpy_dense: bad arguments");

@@ -69,6 +69,10 @@ int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const 
             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st);
 int csr_spmm(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals, int k,
              const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st);
+// blockgs.cu
+size_t block_gs_workspace_bytes();
+int block_gs(int n, int kb, z_t* W, int64_t ldw, const double* refs, double tol, double reorth, int no_drop,
+             z_t* Q, int64_t ldq, int32_t* kept, int32_t* nk, void* work, size_t wb, cudaStream_t st);
 // linalg.cu
 int csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, const double* vals,
                    z_t alpha, z_t* D, int64_t ldd, cudaStream_t st);

@@ -186,3 +186,25 @@ def scale_columns(W: torch.Tensor, scale: torch.Tensor, m: int | None = None):
                                     C_ptr(scale.to(torch.float64).contiguous()), _lib.stream_handle()),
                "vb_scale_columns")
     return W
+
+
+BLOCK_GS_MAX = 16
+
+
+def block_gs(W: torch.Tensor, Q: torch.Tensor, refs: torch.Tensor | None = None, tol: float = 0.0,
+             reorth: float = 0.0, no_drop: bool = False):
+    """Fused in-block Gram-Schmidt (vb_block_gs): the columns of W (n x kb,
+    kb <= 16) orthogonalised twice against the kept ones and kept by the
+    reference drop rule into Q[:, :nk].  Returns (nk, kept flags) — one host
+    read per block."""
+    lib = _lib.load()
+    n, kb = W.shape
+    kept = torch.empty(max(kb, 1), dtype=torch.int32, device=W.device)
+    nk = torch.zeros(1, dtype=torch.int32, device=W.device)
+    wb = lib.vb_block_gs_workspace_bytes()
+    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=W.device)
+    rp = _lib.ptr(refs.contiguous()) if refs is not None else None
+    _lib.check(lib.vb_block_gs(n, kb, C_ptr(W), _ld(W), rp, tol, reorth, int(no_drop), C_ptr(Q), _ld(Q),
+                               _lib.ptr(kept), _lib.ptr(nk), C_ptr(work), wb, _lib.stream_handle()),
+               "vb_block_gs")
+    return int(nk.item()), kept[:kb].cpu().numpy()

@@ -597,8 +597,10 @@ def _orthonormalise(V, block):
         Vd = (V if V.dim() == 2 and V.stride(1) == 1 else V.contiguous()) if V.numel() else None
     else:
         Vd = _as_dev(V, dev) if V.size else None
-    refs = linalg.column_norms(B).cpu().numpy()
+    refs_dev = linalg.column_norms(B)
     W = B.clone()
+    fused = 0 < kb <= linalg.BLOCK_GS_MAX
+    refs = None if fused else refs_dev.cpu().numpy()
 
     def against_V(X):
         for _ in range(2):
@@ -612,15 +614,18 @@ def _orthonormalise(V, block):
         against_V(W)
     Qb = torch.empty((n, max(kb, 1)), dtype=CDT, device=dev)
     nk = 0
-    for j in range(kb):
-        w = W[:, j:j + 1]
-        if nk:
-            w = _cgs2_against(Qb[:, :nk], w)
-        nw = float(linalg.column_norms(w).item())
-        if refs[j] > 0 and nw > ORTH_DROP_TOL * refs[j]:
-            w, nw = _polish((Qb[:, :nk] if nk else None,), w, nw, refs[j])
-            torch.mul(w, 1.0 / nw, out=Qb[:, nk:nk + 1])
-            nk += 1
+    if fused:  # one cooperative kernel for the column loop below (vb_block_gs)
+        nk, _ = linalg.block_gs(W, Qb, refs_dev, ORTH_DROP_TOL, REORTH_RATIO)
+    else:
+        for j in range(kb):
+            w = W[:, j:j + 1]
+            if nk:
+                w = _cgs2_against(Qb[:, :nk], w)
+            nw = float(linalg.column_norms(w).item())
+            if refs[j] > 0 and nw > ORTH_DROP_TOL * refs[j]:
+                w, nw = _polish((Qb[:, :nk] if nk else None,), w, nw, refs[j])
+                torch.mul(w, 1.0 / nw, out=Qb[:, nk:nk + 1])
+                nk += 1
     r = Vd.shape[1] if Vd is not None else 0
     newV = _basis_append_view(Vd, n, nk, dev)
     if nk:
@@ -633,11 +638,14 @@ def _orthonormalise(V, block):
         # block cost.  In place in the basis buffer; norms stay on the device.
         if Vd is not None:
             against_V(Q1)
-            for j in range(nk):
-                w = Q1[:, j:j + 1]
-                if j:
-                    _cgs2_against(Q1[:, :j], w)
-                w.div_(linalg.column_norms(w))
+            if nk <= linalg.BLOCK_GS_MAX:
+                linalg.block_gs(Q1, Q1, no_drop=True)
+            else:
+                for j in range(nk):
+                    w = Q1[:, j:j + 1]
+                    if j:
+                        _cgs2_against(Q1[:, :j], w)
+                    w.div_(linalg.column_norms(w))
     _BASIS_BUFS[newV.data_ptr()] = (r + nk, newV.stride(0), n)
     return newV.cpu().numpy() if is_np else newV
 
