@@ -105,3 +105,37 @@ def test_column_norms_and_scale(cuda):
     np.testing.assert_allclose(nr, np.linalg.norm(W, axis=0), rtol=1e-14)
     linalg.scale_columns(Wd, torch.as_tensor(1 / nr, device=cuda))
     np.testing.assert_allclose(np.linalg.norm(Wd.cpu().numpy(), axis=0), 1.0, rtol=1e-14)
+
+
+@pytest.mark.parametrize("n,kb", [(5000, 10), (37, 16), (100000, 3)])
+def test_block_gs_matches_reference_drop_rule(cuda, n, kb):
+    """vb_block_gs (fused in-block CGS2 + drop rule, mor.py:122-135) against the
+    oracle's MGS2 on a block with an exact duplicate, a near-dependent column
+    (1e-12 residual: dropped) and a weakly dependent one (1e-6: kept)."""
+    import torch
+    from oracle import mor as omor
+    from paper_2310_04734_b200 import linalg, mor
+    rng = np.random.default_rng(n + kb)
+    B = _c(rng, n, kb)
+    if kb >= 3:
+        B[:, 1] = B[:, 0]
+        B[:, 2] = B[:, 0] + 1e-12 * _c(rng, n)
+    if kb >= 5:
+        B[:, 4] = B[:, 3] + 1e-6 * _c(rng, n)
+    Wd = torch.as_tensor(B, device=cuda).clone()
+    Qd = torch.empty((n, kb), dtype=torch.complex128, device=cuda)
+    refs = linalg.column_norms(torch.as_tensor(B, device=cuda))
+    nk, kept = linalg.block_gs(Wd, Qd, refs, mor.ORTH_DROP_TOL, mor.REORTH_RATIO)
+    Qo = omor.orthonormalise(None, B)
+    assert nk == Qo.shape[1]
+    Q = Qd[:, :nk].cpu().numpy()
+    assert np.abs(Q.conj().T @ Q - np.eye(nk)).max() <= 1e-12
+    # same span as the reference's basis
+    assert np.abs(Qo - Q @ (Q.conj().T @ Qo)).max() <= 1e-8
+    if kb >= 3:
+        assert list(kept[:3]) == [1, 0, 0]
+    # no_drop, in place: re-orthonormalise an orthonormal-ish block
+    P = torch.as_tensor(Q + 1e-9 * _c(rng, n, nk), device=cuda)
+    linalg.block_gs(P, P, no_drop=True)
+    Pn = P.cpu().numpy()
+    assert np.abs(Pn.conj().T @ Pn - np.eye(nk)).max() <= 1e-12
