@@ -427,7 +427,7 @@ class ReducedModel:
         bR = self._br([f])
         bR = bR[0] if bR.dim() == 3 else bR
         bR = bR.cpu().numpy()
-        vec = np.ndim(self.fom.load(f)) == 1
+        vec = _vec_load(self.fom, f)
         return AR.cpu().numpy(), (bR[:, 0] if vec else bR)
 
     def sweep(self, freqs, want_x: bool = False, rayleigh=None):
@@ -501,11 +501,25 @@ class ReducedModel:
         return lo <= f <= hi
 
 
+def _vec_load(fom, f) -> bool:
+    """Whether the model's load is a single vector (the reference's 1-D load);
+    evaluated once per model — the load's shape does not depend on f, and a
+    provider call can be expensive (a plane wave evaluated on the host)."""
+    v = getattr(fom, "_vec_load_cache", None)
+    if v is None:
+        v = bool(np.ndim(fom.load(f)) == 1)
+        try:
+            fom._vec_load_cache = v
+        except AttributeError:
+            pass
+    return v
+
+
 def _shape_output(y, fom, f):
     """(n_out, s) -> the reference's output(x) shape: scalar for a 1-D c_out and a
     single RHS, else the ndarray c_out @ x."""
     scalar_c = np.ndim(fom.c_out) == 1
-    vec_load = np.ndim(fom.load(f)) == 1
+    vec_load = _vec_load(fom, f)
     if scalar_c:
         y = y[0]
     if vec_load:

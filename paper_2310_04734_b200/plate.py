@@ -134,6 +134,7 @@ class PlaneWaveLoad:
         self.xg = torch.as_tensor(np.array(xg) - xyz[:, 0].min(), device=dev)
         self.c0, self.theta, self.n = c0, theta, n_total
         self.G_host = G
+        self.xg_host = self.xg.cpu().numpy()
 
     def phases(self, freqs) -> torch.Tensor:
         k = 2.0 * math.pi * torch.as_tensor(np.asarray(freqs, float), device=self.xg.device) / self.c0 \
@@ -149,7 +150,7 @@ class PlaneWaveLoad:
 
     def host(self, f: float) -> np.ndarray:
         k = 2.0 * math.pi * f / self.c0 * math.sin(self.theta)
-        return self.G_host @ np.exp(-1j * k * self.xg.cpu().numpy())
+        return self.G_host @ np.exp(-1j * k * self.xg_host)
 
 
 def eta_cfg2(f, f0: float = 20.0, f1: float = 500.0) -> float:
