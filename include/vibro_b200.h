@@ -253,6 +253,12 @@ size_t vb_zgetrf_aux_bytes(int n);
 int vb_zgetrf(int n, vb_complex* A, int64_t lda, int32_t* ipiv, int32_t* info, void* aux,
               size_t aux_bytes, void* work, size_t work_bytes, void* stream);
 
+/* Calling host thread only: launch vb_zgetrf / vb_zgetrs on at most n CTAs
+ * (0 = one per SM, the default), so that independent factorisations and
+ * solves issued from several host threads on their own streams run
+ * concurrently (e.g. the expansion points of one Krylov basis). */
+void vb_set_lu_max_ctas(int n);
+
 /* X = A^-1 B from vb_zgetrf factors (1 <= nrhs <= 16; B may alias X).
  * Replaces SuperLU `lu.solve` (vibrofem/mor.py:49, 156, 166, 175). */
 size_t vb_zgetrs_workspace_bytes(int n, int nrhs);

@@ -220,6 +220,8 @@ int vb_zgetrf(int n, vb_complex* A, int64_t lda, int32_t* ipiv, int32_t* info, v
   return vb::zgetrf(n, (z_t*)A, lda, ipiv, info, aux, aux_bytes, work, work_bytes, (cudaStream_t)stream);
 }
 
+void vb_set_lu_max_ctas(int n) { vb::set_lu_max_ctas(n); }
+
 size_t vb_zgetrs_workspace_bytes(int n, int nrhs) { return (size_t)n * nrhs * sizeof(vb_complex); }
 
 int vb_zgetrs(int n, int nrhs, const vb_complex* LU, int64_t lda, const void* aux, const vb_complex* B,

@@ -16,6 +16,7 @@
 // The diagonal-block inverses L_kk^-1, U_kk^-1 and the final row permutation are
 // kept for the blocked triangular solves of vb_zgetrs.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "mma.cuh"
@@ -445,6 +446,12 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
 
 constexpr size_t SOLVE_SMEM = (size_t)(NB * (NB + 1) + NB * MAXRHS) * sizeof(z_t);
 
+// Per host thread: at most this many CTAs for the whole-GPU factor/solve
+// kernels (0 = all SMs).  Independent factorisations / solves driven from
+// several host threads on their own streams then share the GPU: the solves
+// are latency-bound (1.26 ms at n = 3,565 on 148 CTAs, 1.29 ms on 64).
+static thread_local int t_max_ctas = 0;
+
 static int coop_grid(const void* kern, size_t smem, int* grid) {
   int dev = 0, nsm = 0, per = 0, coop = 0;
   VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -463,10 +470,13 @@ static int coop_grid(const void* kern, size_t smem, int* grid) {
     return 2;
   }
   *grid = nsm;  // one CTA per SM
+  if (t_max_ctas > 0 && t_max_ctas < *grid) *grid = t_max_ctas;  // a share of the GPU (concurrent solves)
   return 0;
 }
 
 }  // namespace lu
+
+void set_lu_max_ctas(int n) { lu::t_max_ctas = n > 0 ? n : 0; }
 
 int lu_debug_cycles(unsigned long long* out, int reset) {
   VB_CUDA(cudaMemcpyFromSymbol(out, lu::g_lu_cycles, 4 * sizeof(unsigned long long)));

@@ -112,8 +112,11 @@ def krylov_basis_sharded(fom, points, moments: int, second_order: bool = False):
     lo, hi = shard_range(len(points), rank, ws)
     mine = []
     n_load = None
-    for f in points[lo:hi]:
-        blocks = mor.krylov_blocks_mimo_dev(fom, f, moments, second_order=second_order)
+    local = points[lo:hi]
+    per_point = (mor.krylov_blocks_concurrent(fom, local, moments, second_order, mimo=True)
+                 if mor._lu_factored(fom) else
+                 [mor.krylov_blocks_mimo_dev(fom, f, moments, second_order=second_order) for f in local])
+    for blocks in per_point:
         n_load = len(blocks)
         mine += [Q for Q, _ in blocks]
     if n_load is None:  # a rank without points still needs the per-point block count

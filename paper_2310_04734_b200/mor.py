@@ -772,6 +772,72 @@ def krylov_blocks_mimo_dev(fom: FullOrderModel, f_j: float, m: int, second_order
     return [(Qs[j][:, :cnt[j]].contiguous(), not alive[j]) for j in range(s)]
 
 
+def krylov_blocks_concurrent(fom: FullOrderModel, points, m: int, second_order: bool = False,
+                             mimo: bool = False, workers: int | None = None):
+    """The Krylov blocks of several expansion points at once: each point's
+    factorisation and moment recurrence (krylov_block_dev, or
+    krylov_blocks_mimo_dev with `mimo`) runs on its own CUDA stream from its
+    own host thread, with the whole-GPU LU kernels capped at a share of the
+    SMs (vb_set_lu_max_ctas) so that the points' latency-bound factor / solve
+    kernels overlap.  Returns the per-point results in point order — the same
+    blocks as the sequential loop (the kernels do not depend on the CTA
+    count), ready for _orthonormalise in point order (mor.py:337-352 builds a
+    window basis from its points one after the other)."""
+    pts = [float(f) for f in points]
+    nw = min(len(pts), workers or len(pts))
+    run = (lambda f: krylov_blocks_mimo_dev(fom, f, m, second_order)) if mimo else \
+        (lambda f: krylov_block_dev(fom, f, m, second_order))
+    if nw <= 1:
+        return [run(f) for f in pts]
+    from concurrent.futures import ThreadPoolExecutor
+    dev = _device()
+    lib = _lib.load()
+    cap = max(16, torch.cuda.get_device_properties(dev).multi_processor_count // nw)
+    caller = torch.cuda.current_stream(dev)
+
+    def work(f):
+        torch.cuda.set_device(dev)
+        st = torch.cuda.Stream(device=dev)
+        st.wait_stream(caller)  # model data produced on the caller's stream
+        lib.vb_set_lu_max_ctas(cap)
+        try:
+            with torch.cuda.stream(st):
+                out = run(f)
+            st.synchronize()
+        finally:
+            lib.vb_set_lu_max_ctas(0)
+        return out
+
+    with ThreadPoolExecutor(nw, thread_name_prefix="vb_krylov") as ex:
+        return list(ex.map(work, pts))
+
+
+def _lu_factored(fom: FullOrderModel) -> bool:
+    """True when fom.factor goes through the dense GPU LU (directly or on a
+    Schur complement) — the latency-bound factor / solve kernels that gain
+    from concurrent expansion points; the box FDM solver's transforms are
+    throughput-bound GEMMs (and its host eigensolves already use 3 threads)."""
+    return not (fom.fdm is not None and (fom.prefer_fdm or fom.n > DENSE_MAX_N))
+
+
+def krylov_basis(fom: FullOrderModel, points, m: int, second_order: bool = False, mimo: bool = False,
+                 concurrent: bool | None = None):
+    """V of one window: the Krylov blocks of `points` (concurrently for the
+    LU-factored models when `concurrent` is None), appended with
+    _orthonormalise in point order (mor.py:337-352 / tests/test_mor.py:55-107
+    usage).  Returns (V, breakdown flags per point (per source with mimo))."""
+    if concurrent is None:
+        concurrent = _lu_factored(fom)
+    res = krylov_blocks_concurrent(fom, points, m, second_order, mimo) if concurrent else \
+        [(krylov_blocks_mimo_dev if mimo else krylov_block_dev)(fom, f, m, second_order) for f in points]
+    V, flags = None, []
+    for r in res:
+        for Q, br in (r if mimo else [r]):
+            V = _orthonormalise(V, Q)
+            flags.append(br)
+    return V, flags
+
+
 # ------------------------------------------------------ certification ----
 def relative_error(y_full, y_rom):
     """Pointwise relative error and its maximum (mor.py:194-208)."""
