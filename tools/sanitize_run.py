@@ -33,5 +33,32 @@ x = lu.solve(fom.load_dev(77.0))
 Kb, Mb = assembly.assemble_helmholtz_box((0, 0, 0, 1, 1, 1), (3, 2, 2))
 fom2, lay2 = workloads.cfg2_model(box=(0, 0, 0, 0.8, 0.6, 0.5), ne=(4, 3, 3), n_rec=4)
 y = fom2.output(fom2.solve(123.0))
+# CSR SpMV / sub-warp / row-group SpMM (incl. a boundary matrix with empty rows)
+import scipy.sparse as sp  # noqa: E402
+
+from oracle import fe  # noqa: E402
+
+A, _ = fe.kron_box((0, 0, 0, 1.2, 0.9, 0.7), 3, 2, 2)
+A = sp.csr_matrix(A)
+keep = np.zeros(A.shape[0])
+keep[:20] = 1.0
+for M in (A, sp.csr_matrix(sp.diags(keep) @ A @ sp.diags(keep))):
+    M.eliminate_zeros()
+    M.sort_indices()
+    Ad = assembly.DeviceCSR(M.shape[0], torch.as_tensor(M.indptr.astype(np.int32), device=dev),
+                            torch.as_tensor(M.indices.astype(np.int32), device=dev), torch.as_tensor(M.data, device=dev))
+    for k in (1, 2, 5, 8, 13, 33, 70):
+        X = torch.randn(M.shape[0], k, dtype=torch.complex128, device=dev)
+        for path in ("csr", "rg"):
+            linalg.spmm(Ad, X, 1.0 - 0.5j, 0.0, None, path=path)
+# fused in-block Gram-Schmidt (drops + no_drop in place)
+B = torch.randn(500, 7, dtype=torch.complex128, device=dev)
+B[:, 3] = B[:, 1]
+Qb = torch.empty_like(B)
+nk, _ = linalg.block_gs(B.clone(), Qb, linalg.column_norms(B), 1e-10, 1e-4)
+linalg.block_gs(Qb[:, :nk].contiguous(), Qb[:, :nk].contiguous(), no_drop=True)
+# concurrent expansion points (streams + thread-local LU CTA cap)
+fom1, lay1 = workloads.cfg1_model(box=(0, 0, 0, 1.0, 0.8, 0.6), ne=(3, 3, 2), n_rec=4)
+V1, _ = mor.krylov_basis(fom1, [40.0, 90.0, 150.0], 3, second_order=True, concurrent=True)
 torch.cuda.synchronize()
-print("sanitize run ok", V.shape, float(np.abs(y).max()))
+print("sanitize run ok", V.shape, V1.shape, float(np.abs(y).max()))
