@@ -390,7 +390,9 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
       if (e < nb * s) {
         yb[e] = yv[q];
         const int i = k0 + e / s;
-        if (i >= lo && i < hi) S.X[(int64_t)i * S.ldx + e % s] = yv[q];
+        // y goes to tmp, not back into X: other CTAs may still be loading
+        // this block's b from X (no barrier between their load and this store)
+        if (i >= lo && i < hi) S.tmp[(int64_t)i * s + e % s] = yv[q];
       }
     }
     __syncthreads();
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
   for (int kb = nblk - 1; kb >= 0; --kb) {
     const int k0 = kb * NB, nb = min(NB, n - k0);
     for (int e = tid; e < NB * NB; e += NT) Ti[(e / NB) * (NB + 1) + e % NB] = __ldcg(S.Uinv + (int64_t)kb * NB * NB + e);
-    for (int e = tid; e < nb * s; e += NT) yb[e] = __ldcg(S.X + (int64_t)(k0 + e / s) * S.ldx + e % s);
+    for (int e = tid; e < nb * s; e += NT) yb[e] = __ldcg(S.tmp + (int64_t)(k0 + e / s) * s + e % s);
     __syncthreads();
     z_t yv[(NB * MAXRHS + NT - 1) / NT];
 #pragma unroll
@@ -433,12 +435,13 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
       }
     }
     __syncthreads();
+    // own rows above the block (still y - updates, in tmp): y_i -= U[i, k0:kend] x_kb
     for (int64_t e = tid; e < (int64_t)max(0, min(hi, k0) - lo) * s; e += NT) {
       const int i = lo + (int)(e / s), r = (int)(e % s);
-      z_t acc = S.X[(int64_t)i * S.ldx + r];
+      z_t acc = S.tmp[(int64_t)i * s + r];
       const z_t* Urow = S.LU + (int64_t)i * S.lda + k0;
       for (int k = 0; k < nb; ++k) acc = zfms(acc, Urow[k], yb[k * s + r]);
-      S.X[(int64_t)i * S.ldx + r] = acc;
+      S.tmp[(int64_t)i * s + r] = acc;
     }
     grid.sync();
   }
