@@ -341,6 +341,67 @@ struct SolveParams {
   z_t* tmp;       // n x nrhs scratch for the permuted RHS when B aliases X
 };
 
+// T[i, :] -= M[i, k0 : k0+nb] yb for rows i in [i0, i0 + nrows) (T row stride
+// ldt): KS threads per (row, rhs) item split k mod KS with their loads in
+// flight in batches of 16, then a fixed-order shuffle reduction — instead of
+// one thread per item walking a 64-long chain of dependent-latency loads.
+template <int KS>
+__device__ __forceinline__ void rows_update_ks(const SolveParams& S, z_t* T, int64_t ldt, int i0, int nrows, int k0,
+                                               int nb, const z_t* yb) {
+  const int s = S.nrhs, tid = threadIdx.x, kq = tid % KS;
+  const int nitems = nrows * s;
+  for (int base = 0; base < nitems; base += NT / KS) {
+    const int e = base + tid / KS;
+    const bool valid = e < nitems;
+    const int i = i0 + (valid ? e / s : 0), r = valid ? e % s : 0;
+    const z_t* Mrow = S.LU + (int64_t)i * S.lda + k0;
+    constexpr int NM = 64 / KS, CH = NM < 16 ? NM : 16;
+    z_t acc = zmake(0.0, 0.0);
+#pragma unroll
+    for (int m0 = 0; m0 < NM; m0 += CH) {
+      z_t l[CH];
+#pragma unroll
+      for (int m = 0; m < CH; ++m) {
+        const int k = kq + KS * (m0 + m);
+        l[m] = (valid && k < nb) ? Mrow[k] : zmake(0.0, 0.0);
+      }
+#pragma unroll
+      for (int m = 0; m < CH; ++m) {
+        const int k = kq + KS * (m0 + m);
+        if (k < nb) acc = zfma(acc, l[m], yb[k * s + r]);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < KS; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (valid && kq == 0) {
+      z_t* tp = T + (int64_t)i * ldt + r;
+      *tp = zsub(*tp, acc);
+    }
+  }
+}
+
+__device__ __forceinline__ void rows_update(const SolveParams& S, z_t* T, int64_t ldt, int i0, int nrows, int k0,
+                                            int nb, const z_t* yb) {
+  if (nrows <= 0) return;
+  // the split depends on the RHS count only, so the summation order (and the
+  // result) does not depend on the grid size (vb_set_lu_max_ctas)
+  const int s = S.nrhs;
+  if (s == 1) rows_update_ks<8>(S, T, ldt, i0, nrows, k0, nb, yb);
+  else if (s == 2) rows_update_ks<4>(S, T, ldt, i0, nrows, k0, nb, yb);
+  else if (s <= 4) rows_update_ks<2>(S, T, ldt, i0, nrows, k0, nb, yb);
+  else
+    for (int64_t e = threadIdx.x; e < (int64_t)nrows * s; e += NT) {  // many items: one thread each
+      const int i = i0 + (int)(e / s), r = (int)(e % s);
+      z_t acc = T[(int64_t)i * ldt + r];
+      const z_t* Mrow = S.LU + (int64_t)i * S.lda + k0;
+      for (int k = 0; k < nb; ++k) acc = zfms(acc, Mrow[k], yb[k * s + r]);
+      T[(int64_t)i * ldt + r] = acc;
+    }
+}
+
 constexpr int MAXRHS = 16;
 
 __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
@@ -397,13 +458,7 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
     }
     __syncthreads();
     // own rows below the block: b_i -= L[i, k0:kend] y_kb
-    for (int64_t e = tid; e < (int64_t)max(0, hi - max(lo, kend)) * s; e += NT) {
-      const int i = max(lo, kend) + (int)(e / s), r = (int)(e % s);
-      z_t acc = S.X[(int64_t)i * S.ldx + r];
-      const z_t* Lrow = S.LU + (int64_t)i * S.lda + k0;
-      for (int k = 0; k < nb; ++k) acc = zfms(acc, Lrow[k], yb[k * s + r]);
-      S.X[(int64_t)i * S.ldx + r] = acc;
-    }
+    rows_update(S, S.X, S.ldx, max(lo, kend), hi - max(lo, kend), k0, nb, yb);
     grid.sync();
   }
   // backward: U x = y
@@ -436,13 +491,7 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
     }
     __syncthreads();
     // own rows above the block (still y - updates, in tmp): y_i -= U[i, k0:kend] x_kb
-    for (int64_t e = tid; e < (int64_t)max(0, min(hi, k0) - lo) * s; e += NT) {
-      const int i = lo + (int)(e / s), r = (int)(e % s);
-      z_t acc = S.tmp[(int64_t)i * s + r];
-      const z_t* Urow = S.LU + (int64_t)i * S.lda + k0;
-      for (int k = 0; k < nb; ++k) acc = zfms(acc, Urow[k], yb[k * s + r]);
-      S.tmp[(int64_t)i * s + r] = acc;
-    }
+    rows_update(S, S.tmp, s, lo, min(hi, k0) - lo, k0, nb, yb);
     grid.sync();
   }
 }
