@@ -248,8 +248,10 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(const __grid_constant__ L
         for (int j = k0; j < kend; ++j) {
           const int p = __ldcg(P.ipiv + j);
           if (p != j) {
-            const z_t t = A[(int64_t)j * lda + col];
-            A[(int64_t)j * lda + col] = A[(int64_t)p * lda + col];
+            // L2 reads (__ldcg): rows written by other CTAs earlier in this
+            // kernel must never come from a stale line in this SM's L1
+            const z_t t = __ldcg(A + (int64_t)j * lda + col);
+            A[(int64_t)j * lda + col] = __ldcg(A + (int64_t)p * lda + col);
             A[(int64_t)p * lda + col] = t;
           }
         }
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(const __grid_constant__ L
           const int cs = kend + st * TRS_N, ncol = min(TRS_N, n - cs);
           for (int e = tid; e < NB * TRS_N; e += NT) {
             const int i = e / TRS_N, jx = e - i * TRS_N;
-            Bs[i * LDS_B + jx] = (i < nb && jx < ncol) ? A[(int64_t)(k0 + i) * lda + cs + jx] : zmake(0.0, 0.0);
+            Bs[i * LDS_B + jx] = (i < nb && jx < ncol) ? __ldcg(A + (int64_t)(k0 + i) * lda + cs + jx) : zmake(0.0, 0.0);
           }
           __syncthreads();
           double cr[2][2][2], ci[2][2][2];
@@ -376,9 +378,9 @@ __device__ __forceinline__ void rows_update_ks(const SolveParams& S, z_t* T, int
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
     }
-    if (valid && kq == 0) {
+    if (valid && kq == 0) {  // T rows may have been written by another CTA (X = P B): read from L2
       z_t* tp = T + (int64_t)i * ldt + r;
-      *tp = zsub(*tp, acc);
+      *tp = zsub(__ldcg(tp), acc);
     }
   }
 }
@@ -395,7 +397,7 @@ __device__ __forceinline__ void rows_update(const SolveParams& S, z_t* T, int64_
   else
     for (int64_t e = threadIdx.x; e < (int64_t)nrows * s; e += NT) {  // many items: one thread each
       const int i = i0 + (int)(e / s), r = (int)(e % s);
-      z_t acc = T[(int64_t)i * ldt + r];
+      z_t acc = __ldcg(T + (int64_t)i * ldt + r);
       const z_t* Mrow = S.LU + (int64_t)i * S.lda + k0;
       for (int k = 0; k < nb; ++k) acc = zfms(acc, Mrow[k], yb[k * s + r]);
       T[(int64_t)i * ldt + r] = acc;
