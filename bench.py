@@ -251,50 +251,57 @@ def offline_measurements(w):
     spec.loader.exec_module(mod)
     out = mod.measure()
     from paper_2310_04734_b200 import mor, workloads
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    fom, lay = workloads.cfg1_model()
-    V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"], second_order=True)
-    rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 200.0))
-    res = mor.rom_sweep([rom], list(lay["freqs"]))
-    torch.cuda.synchronize()
-    out["cfg1_pipeline_s"] = time.perf_counter() - t0
-    out["cfg1_r"] = int(V.shape[1])
+
+    def cfg1(fdm):
+        fom, lay = workloads.cfg1_model(fdm=fdm)
+        V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"], second_order=True)
+        rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 200.0))
+        mor.rom_sweep([rom], list(lay["freqs"]))
+        return fom, V
+
+    def cfg2():
+        fom, lay = workloads.cfg2_model()
+        V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"])
+        rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 500.0))
+        mor.rom_sweep([rom], list(lay["freqs"]))
+        return fom, V
+
+    def cfg3():
+        fom, lay = workloads.cfg3_model()
+        V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"], second_order=True, mimo=True)
+        rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 300.0))
+        mor.rom_sweep([rom], list(lay["freqs"]))
+        return fom, V
+
+    def timed_twice(fn):
+        """(first run, warm run) wall clock incl. host orchestration; the warm
+        run is the reported number (first runs include one-off module loading,
+        thread-pool and allocator warm-up)."""
+        ts = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return ts, res
+
+    (t1, t1w), (_, V) = timed_twice(lambda: cfg1(False))
+    out["cfg1_pipeline_s"], out["cfg1_pipeline_first_s"], out["cfg1_r"] = t1w, t1, int(V.shape[1])
     out["cfg1_note"] = ("GPU assembly + 4 dense LUs (n=4641, the 4 expansion points concurrent on their own "
-                        "streams) + 2nd-order Krylov + CGS2 + projection + "
-                        "181-frequency sweep + SPL, wall clock incl. host orchestration")
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    fom, lay = workloads.cfg1_model(fdm=True)
-    V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"], second_order=True)
-    rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 200.0))
-    res = mor.rom_sweep([rom], list(lay["freqs"]))
-    torch.cuda.synchronize()
-    out["cfg1_pipeline_fdm_s"] = time.perf_counter() - t0
-    out["cfg1_fdm_r"] = int(V.shape[1])
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    fom, lay = workloads.cfg2_model()
-    V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"])
-    rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 500.0))
-    mor.rom_sweep([rom], list(lay["freqs"]))
-    torch.cuda.synchronize()
-    out["cfg2_pipeline_s"] = time.perf_counter() - t0
-    out["cfg2_n"] = int(fom.n)
-    out["cfg2_r"] = int(V.shape[1])
+                        "streams) + 2nd-order Krylov + CGS2 + projection + 181-frequency sweep + SPL, wall clock "
+                        "incl. host orchestration (warm run; *_first_s = first run in the process)")
+    (t1, t1w), (_, V) = timed_twice(lambda: cfg1(True))
+    out["cfg1_pipeline_fdm_s"], out["cfg1_pipeline_fdm_first_s"], out["cfg1_fdm_r"] = t1w, t1, int(V.shape[1])
+    (t2, t2w), (fom, V) = timed_twice(cfg2)
+    out["cfg2_pipeline_s"], out["cfg2_pipeline_first_s"] = t2w, t2
+    out["cfg2_n"], out["cfg2_r"] = int(fom.n), int(V.shape[1])
     out["cfg2_note"] = ("GPU plate+cavity assembly (n=20890) + 6 Schur-complement (plate) / fast-diagonalisation "
-                        "(cavity) factorisations with refinement (expansion points concurrent) + Krylov + CGS2 + projection + batched plane-wave "
-                        "RHS + 961-frequency sweep + SPL")
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    fom, lay = workloads.cfg3_model()
-    V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"], second_order=True, mimo=True)
-    rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 300.0))
-    mor.rom_sweep([rom], list(lay["freqs"]))
-    torch.cuda.synchronize()
-    out["cfg3_pipeline_s"] = time.perf_counter() - t0
-    out["cfg3_n"] = int(fom.n)
-    out["cfg3_r"] = int(V.shape[1])
+                        "(cavity) factorisations with refinement (expansion points concurrent) + Krylov + CGS2 + "
+                        "projection + batched plane-wave RHS + 961-frequency sweep + SPL")
+    (t3, t3w), (fom, V) = timed_twice(cfg3)
+    out["cfg3_pipeline_s"], out["cfg3_pipeline_first_s"] = t3w, t3
+    out["cfg3_n"], out["cfg3_r"] = int(fom.n), int(V.shape[1])
     out["cfg3_note"] = ("GPU box assembly (n=376431) + fast-diagonalisation FOM solves at 5 points x 10 "
                         "second-order moments x 8 sources + block CGS2 + Kronecker-apply projection + "
                         "1121-frequency sweep (8 RHS) + SPL")

@@ -23,11 +23,14 @@
 #ifndef VB_SKINNY_3M
 #define VB_SKINNY_3M 0
 #endif
-// GEMM epilogue: results written into the shared-memory C tile and stored by
-// TMA (one bulk tensor store per 8-complex box) instead of scattered 16-byte
-// global stores from every lane.
+// GEMM epilogue variant (off by default): results written into the
+// shared-memory C tile and stored by TMA (one bulk tensor store per 8-complex
+// box) instead of scattered 16-byte global stores from every lane.  +2 % at
+// r = 1024, but the later panel phases read the stored rows with ordinary
+// (L1-cacheable) loads, and an async-proxy store does not update a line this
+// SM may hold in L1; the generic stores keep L1 coherent by construction.
 #ifndef VB_TMA_STORE_EPI
-#define VB_TMA_STORE_EPI 1
+#define VB_TMA_STORE_EPI 0
 #endif
 
 namespace vb {
