@@ -39,6 +39,14 @@ using GemmNarrow = Gemm<64, 16, 8, 1, 2, EPI_SUB>; // back-substitution updates 
 using GemmOut = Gemm<64, 16, 8, 1, 2, EPI_SET>;   // y = C_R x
 
 constexpr int LDL = NB + 4;     // == 4 (mod 8): triangular inverse used as A operand
+// Workspace reads outside the TMA GEMMs: with the TMA-store epilogue (async
+// proxy writes that do not update this SM's L1) they must come from L2.
+#if VB_TMA_STORE_EPI
+#define VB_WS_LD(p) __ldcg(p)
+#else
+#define VB_WS_LD(p) (*(p))
+#endif
+
 #ifndef VB_DEEP_MIN_R
 #define VB_DEEP_MIN_R 640
 #endif
@@ -281,8 +289,8 @@ __device__ void apply_swaps(z_t* A, int ldw, const int* piv, int k0, int a, int 
     for (int i = a; i < b; ++i) {
       const int p = piv[i - k0];
       if (p != i) {
-        const z_t t = A[(size_t)i * ldw + c];
-        A[(size_t)i * ldw + c] = A[(size_t)p * ldw + c];
+        const z_t t = VB_WS_LD(A + (size_t)i * ldw + c);
+        A[(size_t)i * ldw + c] = VB_WS_LD(A + (size_t)p * ldw + c);
         A[(size_t)p * ldw + c] = t;
       }
     }
@@ -303,10 +311,10 @@ __device__ void trsm_small(z_t* A, int ldw, int cl, int n1, int c0, int c1, z_t*
     for (int e = threadIdx.x; e < n1 * n1 + n1 * nc; e += NT) {
       if (e < n1 * n1) {
         const int i = e / n1, k = e - i * n1;
-        Ls[i * LD + k] = A[(size_t)(cl + i) * ldw + cl + k];
+        Ls[i * LD + k] = VB_WS_LD(A + (size_t)(cl + i) * ldw + cl + k);
       } else {
         const int f = e - n1 * n1, i = f / nc, c = f - i * nc;
-        Xs[i * LD + c] = A[(size_t)(cl + i) * ldw + c0 + c];
+        Xs[i * LD + c] = VB_WS_LD(A + (size_t)(cl + i) * ldw + c0 + c);
       }
     }
     __syncthreads();
@@ -323,13 +331,13 @@ __device__ void trsm_small(z_t* A, int ldw, int cl, int n1, int c0, int c1, z_t*
   }
   for (int e = threadIdx.x; e < n1 * n1; e += NT) {
     const int i = e / n1, k = e - i * n1;
-    Ls[i * LD + k] = A[(size_t)(cl + i) * ldw + cl + k];
+    Ls[i * LD + k] = VB_WS_LD(A + (size_t)(cl + i) * ldw + cl + k);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int c = c0 + warp; c < c1; c += NT / 32) {
     z_t x = zmake(0.0, 0.0);
-    if (lane < n1) x = A[(size_t)(cl + lane) * ldw + c];
+    if (lane < n1) x = VB_WS_LD(A + (size_t)(cl + lane) * ldw + c);
     for (int k = 0; k + 1 < n1; ++k) {
       const double xr = __shfl_sync(0xffffffffu, x.x, k), xi = __shfl_sync(0xffffffffu, x.y, k);
       if (lane > k && lane < n1) x = zfms(x, Ls[lane * LD + k], zmake(xr, xi));
@@ -352,7 +360,7 @@ __device__ void panel_trsm(const Params& P, z_t* A, int k0, int nb, int c0, int 
   for (int e = tid; e < NB * NB; e += NT) {
     const int i = e / NB, j = e - i * NB;
     z_t v = zmake(i == j ? 1.0 : 0.0, 0.0);
-    if (i < nb && j < i) v = A[(size_t)(k0 + i) * ldw + k0 + j];
+    if (i < nb && j < i) v = VB_WS_LD(A + (size_t)(k0 + i) * ldw + k0 + j);
     Li[i * LDL + j] = v;
   }
   __syncthreads();
@@ -375,12 +383,12 @@ __device__ void diag_backsolve(z_t* A, int ldw, int r, int s, int kb, int nb, z_
   for (int e = tid; e < NB * NB; e += NT) {
     const int i = e / NB, j = e - i * NB;
     z_t v = zmake(i == j ? 1.0 : 0.0, 0.0);
-    if (i < nb && j < nb) v = (j >= i) ? A[(size_t)(kb + i) * ldw + kb + j] : zmake(0.0, 0.0);
+    if (i < nb && j < nb) v = (j >= i) ? VB_WS_LD(A + (size_t)(kb + i) * ldw + kb + j) : zmake(0.0, 0.0);
     Us[i * LDL + j] = v;
   }
   for (int e = tid; e < NB * 16; e += NT) {
     const int i = e >> 4, c = e & 15;
-    Ys[i * LDY + c] = (i < nb && c < s) ? A[(size_t)(kb + i) * ldw + r + c] : zmake(0.0, 0.0);
+    Ys[i * LDY + c] = (i < nb && c < s) ? VB_WS_LD(A + (size_t)(kb + i) * ldw + r + c) : zmake(0.0, 0.0);
   }
   __syncthreads();
   tri_inv64<false>(Us, LDL);
@@ -615,7 +623,7 @@ __global__ void __launch_bounds__(NT, 2) rom_sweep_blocked_kernel(const __grid_c
       z_t* xf = P.x + f * (int64_t)r * s;
       for (int idx = tid; idx < r * s; idx += NT) {
         const int i = idx / s, c = idx - i * s;
-        xf[idx] = A[(size_t)i * ldw + r + c];
+        xf[idx] = VB_WS_LD(A + (size_t)i * ldw + r + c);
       }
     }
     if (P.n_out > 0 && (P.y || P.spl)) {

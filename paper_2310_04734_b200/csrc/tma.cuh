@@ -29,6 +29,8 @@
 // r = 1024, but the later panel phases read the stored rows with ordinary
 // (L1-cacheable) loads, and an async-proxy store does not update a line this
 // SM may hold in L1; the generic stores keep L1 coherent by construction.
+// With it on, sweep_blocked.cu reads its workspace from L2 (VB_WS_LD): then
+// r = 1024 +0.6 %, r = 2048 -1.4 %, r = 256 -3.2 % — not worth it.
 #ifndef VB_TMA_STORE_EPI
 #define VB_TMA_STORE_EPI 0
 #endif
