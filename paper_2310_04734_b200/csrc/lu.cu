@@ -404,6 +404,29 @@ __device__ __forceinline__ void rows_update(const SolveParams& S, z_t* T, int64_
     }
 }
 
+// One right-hand side: y = T yb for the diagonal block with 4 lanes per row
+// (k split mod 4, fixed-order shuffle reduction); true on the lane that holds
+// row tid/4's value.
+template <bool LOWER>
+__device__ __forceinline__ bool diag_mult_s1(const z_t* Ti, const z_t* yb, int nb, z_t& out) {
+  const int i = threadIdx.x >> 2, kq = threadIdx.x & 3;
+  z_t acc = zmake(0.0, 0.0);
+  if (i < nb) {
+#pragma unroll
+    for (int m = 0; m < NB / 4; ++m) {
+      const int k = kq + 4 * m;
+      if (k < nb && (LOWER ? k <= i : k >= i)) acc = zfma(acc, Ti[i * (NB + 1) + k], yb[k]);
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  out = acc;
+  return kq == 0 && i < nb;
+}
+
 constexpr int MAXRHS = 16;
 
 __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
@@ -433,29 +456,40 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
     for (int e = tid; e < NB * NB; e += NT) Ti[(e / NB) * (NB + 1) + e % NB] = __ldcg(S.Linv + (int64_t)kb * NB * NB + e);
     for (int e = tid; e < nb * s; e += NT) yb[e] = __ldcg(S.X + (int64_t)(k0 + e / s) * S.ldx + e % s);
     __syncthreads();
-    // y_kb = Linv * b_kb (every CTA redundantly; the owner writes it back)
-    z_t yv[(NB * MAXRHS + NT - 1) / NT];
-#pragma unroll
-    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
-      const int e = tid + q * NT;
-      yv[q] = zmake(0.0, 0.0);
-      if (e < nb * s) {
-        const int i = e / s, r = e - i * s;
-        z_t acc = zmake(0.0, 0.0);
-        for (int k = 0; k <= i; ++k) acc = zfma(acc, Ti[i * (NB + 1) + k], yb[k * s + r]);
-        yv[q] = acc;
+    // y_kb = Linv * b_kb (every CTA redundantly; the owner writes it back).
+    // y goes to tmp, not back into X: other CTAs may still be loading this
+    // block's b from X (no barrier between their load and this store).
+    if (s == 1) {
+      z_t v;
+      const bool mine = diag_mult_s1<true>(Ti, yb, nb, v);
+      __syncthreads();
+      if (mine) {
+        const int i = tid >> 2;
+        yb[i] = v;
+        if (k0 + i >= lo && k0 + i < hi) S.tmp[k0 + i] = v;
       }
-    }
-    __syncthreads();
+    } else {
+      z_t yv[(NB * MAXRHS + NT - 1) / NT];
 #pragma unroll
-    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
-      const int e = tid + q * NT;
-      if (e < nb * s) {
-        yb[e] = yv[q];
-        const int i = k0 + e / s;
-        // y goes to tmp, not back into X: other CTAs may still be loading
-        // this block's b from X (no barrier between their load and this store)
-        if (i >= lo && i < hi) S.tmp[(int64_t)i * s + e % s] = yv[q];
+      for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+        const int e = tid + q * NT;
+        yv[q] = zmake(0.0, 0.0);
+        if (e < nb * s) {
+          const int i = e / s, r = e - i * s;
+          z_t acc = zmake(0.0, 0.0);
+          for (int k = 0; k <= i; ++k) acc = zfma(acc, Ti[i * (NB + 1) + k], yb[k * s + r]);
+          yv[q] = acc;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+        const int e = tid + q * NT;
+        if (e < nb * s) {
+          yb[e] = yv[q];
+          const int i = k0 + e / s;
+          if (i >= lo && i < hi) S.tmp[(int64_t)i * s + e % s] = yv[q];
+        }
       }
     }
     __syncthreads();
@@ -469,26 +503,37 @@ __global__ void __launch_bounds__(NT, 1) zgetrs_kernel(SolveParams S) {
     for (int e = tid; e < NB * NB; e += NT) Ti[(e / NB) * (NB + 1) + e % NB] = __ldcg(S.Uinv + (int64_t)kb * NB * NB + e);
     for (int e = tid; e < nb * s; e += NT) yb[e] = __ldcg(S.tmp + (int64_t)(k0 + e / s) * s + e % s);
     __syncthreads();
-    z_t yv[(NB * MAXRHS + NT - 1) / NT];
-#pragma unroll
-    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
-      const int e = tid + q * NT;
-      yv[q] = zmake(0.0, 0.0);
-      if (e < nb * s) {
-        const int i = e / s, r = e - i * s;
-        z_t acc = zmake(0.0, 0.0);
-        for (int k = i; k < nb; ++k) acc = zfma(acc, Ti[i * (NB + 1) + k], yb[k * s + r]);
-        yv[q] = acc;
+    if (s == 1) {
+      z_t v;
+      const bool mine = diag_mult_s1<false>(Ti, yb, nb, v);
+      __syncthreads();
+      if (mine) {
+        const int i = tid >> 2;
+        yb[i] = v;
+        if (k0 + i >= lo && k0 + i < hi) S.X[(int64_t)(k0 + i) * S.ldx] = v;
       }
-    }
-    __syncthreads();
+    } else {
+      z_t yv[(NB * MAXRHS + NT - 1) / NT];
 #pragma unroll
-    for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
-      const int e = tid + q * NT;
-      if (e < nb * s) {
-        yb[e] = yv[q];
-        const int i = k0 + e / s;
-        if (i >= lo && i < hi) S.X[(int64_t)i * S.ldx + e % s] = yv[q];
+      for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+        const int e = tid + q * NT;
+        yv[q] = zmake(0.0, 0.0);
+        if (e < nb * s) {
+          const int i = e / s, r = e - i * s;
+          z_t acc = zmake(0.0, 0.0);
+          for (int k = i; k < nb; ++k) acc = zfma(acc, Ti[i * (NB + 1) + k], yb[k * s + r]);
+          yv[q] = acc;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < (NB * MAXRHS + NT - 1) / NT; ++q) {
+        const int e = tid + q * NT;
+        if (e < nb * s) {
+          yb[e] = yv[q];
+          const int i = k0 + e / s;
+          if (i >= lo && i < hi) S.X[(int64_t)i * S.ldx + e % s] = yv[q];
+        }
       }
     }
     __syncthreads();
