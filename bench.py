@@ -204,6 +204,77 @@ def cpu_sample_size(w, budget_s: float) -> int:
     return int(max(4, min(len(w.freqs), rate * budget_s)))
 
 
+def bench_config(r: int, s: int, n_out: int, nprim: int, B: int, ws: int) -> dict:
+    """The workload both arms report (identical dict, so the driver can pair them)."""
+    return {"workload": f"cfg5_r{r}", "r": r, "rhs": s, "n_out": n_out, "n_prim": nprim,
+            "freqs_per_step_per_rank": B, "grid": "linspace(1,1000,100000), rank-disjoint slices",
+            "l2": "flushed between timed steps (512 MiB write)",
+            "parallelism": f"frequency-sharded x{ws}"}
+
+
+def default_batch(args) -> int:
+    """16 frequencies per SM per rank (148 SMs on B200 when no GPU is visible)."""
+    if args.batch:
+        return args.batch
+    nsm = 148
+    try:
+        import torch
+        if torch.cuda.is_available():
+            nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        pass
+    return 16 * nsm
+
+
+def parity_sample(w, freqs_timed: np.ndarray, n: int = 64, n_res: int = 16, seed: int = 17) -> np.ndarray:
+    """Indices into freqs_timed to check against the oracle: the n_res timed
+    frequencies nearest the workload's undamped eigenfrequencies (where the
+    LU pivots hardest) plus seeded random others, n in total."""
+    from paper_2310_04734_b200 import workloads
+    ef = workloads.cfg5_eigenfrequencies(w)
+    order = np.argsort(freqs_timed)
+    fs = freqs_timed[order]
+    lo, hi = fs[0], fs[-1]
+    ef = ef[(ef >= lo) & (ef <= hi)]
+    pick = []
+    if ef.size:
+        pos = np.clip(np.searchsorted(fs, ef), 1, len(fs) - 1)
+        near = np.where(np.abs(fs[pos - 1] - ef) <= np.abs(fs[pos] - ef), pos - 1, pos)
+        dist = np.abs(fs[near] - ef)
+        for j in near[np.argsort(dist)]:
+            if order[j] not in pick:
+                pick.append(int(order[j]))
+            if len(pick) >= n_res:
+                break
+    rng = np.random.default_rng(seed)
+    rest = np.setdiff1d(np.arange(len(freqs_timed)), pick)
+    extra = rng.choice(rest, min(len(rest), n - len(pick)), replace=False)
+    return np.array(sorted(pick + [int(i) for i in extra]), dtype=np.int64)
+
+
+def parity_check(w, freqs, y, spl, n_res_probe: int = 16) -> dict:
+    """Compare GPU outputs y (F, n_out, s) / spl (F, s) at `freqs` with the oracle
+    (oracle.mor.affine_sweep = mor.py:73-102 restated, LAPACK zgesv): the
+    reference's pointwise relative_error (mor.py:194-208) and |dSPL|."""
+    from oracle import mor as omor
+    y_ref, spl_ref = omor.affine_sweep(w.prims, w.alpha(freqs), w.b, w.c_r)
+    pt = max(omor.relative_error(y_ref[i].ravel(), y[i].ravel())[1] for i in range(len(freqs)))
+    nw = max(float(np.linalg.norm(y_ref[i] - y[i]) / np.linalg.norm(y_ref[i])) for i in range(len(freqs)))
+    return {"n": int(len(freqs)), "n_near_resonance": int(n_res_probe),
+            "max_tf_rel_err": float(pt), "max_tf_rel_err_normwise": nw,
+            "max_dspl_db": float(np.abs(spl - spl_ref).max()),
+            "tol": {"tf_rel": 1e-8, "dspl_db": 0.01},
+            "pass": bool(pt <= 1e-8 and np.abs(spl - spl_ref).max() <= 0.01),
+            "oracle": "oracle.mor.affine_sweep (numpy.linalg.solve = LAPACK zgesv per frequency)"}
+
+
+def probe_peak(n: int = 5) -> tuple[float, list]:
+    """FP64 DMMA peak: median of n live probes (one figure for every fraction)."""
+    from paper_2310_04734_b200 import _lib
+    vals = [_lib.probe_fp64_peak() for _ in range(n)]
+    return float(np.median(vals)), vals
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port; the reference is
     pure Python and cannot travel to the GPU box) on the host cores."""
@@ -212,6 +283,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     w = workloads.cfg5(r=args.r)
+    B = default_batch(args)
     n_per_step = cpu_sample_size(w, args.cpu_step_s)
     rng = np.random.default_rng(11)
     times, count = [], 0
@@ -228,19 +300,18 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128",
         "data": "synthetic (seeded cfg5)",
-        "config": {"workload": f"cfg5_r{args.r}", "r": args.r, "rhs": w.b.shape[1],
-                   "n_out": w.c_r.shape[0], "freqs_per_step": n_per_step,
-                   "grid": "linspace(1,1000,100000) (seeded random sample per step)"},
+        "config": bench_config(args.r, w.b.shape[1], w.c_r.shape[0], w.prims.shape[0], B, ws),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{n_per_step} random grid frequencies per step, numpy.linalg.solve "
-                                   f"(LAPACK zgesv) per frequency, BLAS threads={cores}"},
+                         "sample": f"bounded sample of each {B}-frequency step: {n_per_step} seeded random "
+                                   f"grid frequencies per step, numpy.linalg.solve (LAPACK zgesv) per "
+                                   f"frequency, BLAS threads={cores}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def offline_measurements(w):
+def offline_measurements(w, peak_fp64=None):
     """Secondary numbers (not the headline): the other stages of the MOR chain at
     BASELINE sizes, CUDA-event timed — cfg3 assembly / SpMM / projection / FDM
     solve (tools/bench_offline.py) and the cfg1 pipeline end to end."""
@@ -249,7 +320,7 @@ def offline_measurements(w):
     spec = importlib.util.spec_from_file_location("bench_offline", ROOT / "tools" / "bench_offline.py")
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
-    out = mod.measure()
+    out = mod.measure(peak_fp64)
     from paper_2310_04734_b200 import mor, workloads
 
     def cfg1(fdm):
@@ -308,72 +379,141 @@ def offline_measurements(w):
     return out
 
 
-def run_ours(args):
+def sweep_timed(w, B, steps, warmup, dev, flush, rank=0, ws=1, keep=False, gather=None):
+    """Device-resident sweep of `steps` timed batches of B frequencies (after
+    `warmup` untimed ones): returns (step ms list, kernel ms list, kept outputs).
+    Each step's frequencies are a rank-disjoint slice of the 100k grid; L2 is
+    flushed before every timed step (outside the events)."""
     import torch
-    from paper_2310_04734_b200 import _lib, dist as vdist, sweep, workloads
-
-    rank, ws, local = vdist.init()
-    _lib.require_cuda()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    lib = _lib.load()
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-
-    w = workloads.cfg5(r=args.r)
-    r, s, n_out, nprim = w.r, w.b.shape[1], w.c_r.shape[0], w.prims.shape[0]
-    B = args.batch or 16 * nsm
+    from paper_2310_04734_b200 import sweep
     nF = len(w.freqs)
     freqs_dev = torch.from_numpy(w.freqs).to(dev)
-
-    def step_freqs(step):
-        # rank-disjoint slices walking the 100k grid (weak scaling)
-        start = ((step * ws + rank) * B) % nF
-        idx = (torch.arange(B, device=dev) + start) % nF
-        return freqs_dev[idx]
-
     rs = sweep.ReducedSweep(w.prims, w.b, w.c_r, kinds=w.kinds, device=dev)
-    flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
-    path = lib.vb_rom_sweep_path(r, nprim, s, n_out)
     stream = torch.cuda.current_stream(dev)
 
+    def idx_of(step):
+        start = ((step * ws + rank) * B) % nF
+        return (np.arange(B) + start) % nF
+
     def one_step(step, ev=None):
-        f = step_freqs(step)
+        f = freqs_dev[torch.from_numpy(idx_of(step)).to(dev)]
         alpha = rs.alpha(f)
         if ev is not None:
             ev[0].record(stream)
         out = sweep.rom_sweep_affine(rs.P, alpha, rs.b, rs.c, want_y=True, want_spl=True)
         if ev is not None:
             ev[1].record(stream)
-        if ws > 1:
-            vdist.gather_rows(out.spl, B * ws, ws)
+        if gather is not None:
+            gather(out)
         return out
 
-    for i in range(args.warmup):
+    for i in range(warmup):
         one_step(i)
     torch.cuda.synchronize()
     sweep.raise_if_singular(one_step(0).info)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    kept = []
+    from paper_2310_04734_b200 import dist as vdist
+    vdist.barrier()
+    torch.cuda.synchronize()
+    from paper_2310_04734_b200 import _lib
+    n0 = _lib.launch_count()
+    for i in range(steps):
+        flush.zero_()
+        e = evs[i]
+        e[0].record(stream)
+        out = one_step(warmup + i, ev=(e[2], e[3]))
+        e[1].record(stream)
+        if keep:
+            kept.append((idx_of(warmup + i), out))
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - n0
+    vdist.barrier()
+    step_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    kern_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    for _, o in kept:
+        sweep.raise_if_singular(o.info)
+    sweep_timed.launches = launches
+    return step_ms, kern_ms, kept
+
+
+def parity_of_kept(w, kept, n=64):
+    """Parity of >= n of the frequencies the timed steps produced (bench's own
+    outputs), n_res of them next to the eigenfrequencies."""
+    idx = np.concatenate([i for i, _ in kept])
+    freqs = w.freqs[idx]
+    pick = parity_sample(w, freqs, n=n)
+    # outputs of the picked rows (step, row within step)
+    B = len(kept[0][0])
+    ys = np.stack([kept[p // B][1].y[p % B].cpu().numpy() for p in pick])
+    spls = np.stack([kept[p // B][1].spl[p % B].cpu().numpy() for p in pick])
+    res = parity_check(w, freqs[pick], ys, spls)
+    res["freq_range_hz"] = [float(freqs.min()), float(freqs.max())]
+    return res
+
+
+def per_order(args, dev, flush, peak, nsm):
+    """The other cfg5 orders (BASELINE configs[4]: r in {256, 1024, 2048}) on
+    the same kernel: throughput, roofline fraction and parity of 64 of their
+    own timed frequencies (16 next to resonances)."""
+    from paper_2310_04734_b200 import _lib, workloads
+    out = {}
+    for r in args.orders:
+        if r == args.r:
+            continue
+        w = workloads.cfg5(r=r)
+        B = 16 * nsm
+        steps = 8 if r <= 512 else 3
+        step_ms, kern_ms, kept = sweep_timed(w, B, steps, 2, dev, flush, keep=True)
+        fl = flops_per_freq(r, w.prims.shape[0], w.b.shape[1], w.c_r.shape[0])
+        kavg = sum(kern_ms) / len(kern_ms)
+        ach = fl * B / (kavg * 1e-3) / 1e12
+        out[f"r{r}"] = {"value": B * steps / (sum(step_ms) * 1e-3), "unit": UNIT, "freqs_per_step": B,
+                        "steps": steps, "kernel_ms": kavg, "achieved_TFLOPs": ach, "frac": ach / peak,
+                        "path": "blocked" if _lib.load().vb_rom_sweep_path(r, 3, 16, 50) == 1 else "shared-memory",
+                        "parity": parity_of_kept(w, kept)}
+        del kept
+    return out
+
+
+def run_ours(args):
+    import torch
+    from paper_2310_04734_b200 import _lib, dist as vdist, sweep, workloads
+
+    rank, ws, local = vdist.init()
+    _lib.require_cuda()
+    if torch.cuda.device_count() < ws:
+        raise SystemExit(f"bench.py: {ws} ranks but only {torch.cuda.device_count()} visible GPUs")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak, peak_probes = probe_peak() if rank == 0 else (None, None)
+
+    w = workloads.cfg5(r=args.r)
+    r, s, n_out, nprim = w.r, w.b.shape[1], w.c_r.shape[0], w.prims.shape[0]
+    B = args.batch or 16 * nsm
+    nF = len(w.freqs)
+    flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
+    path = lib.vb_rom_sweep_path(r, nprim, s, n_out)
+    gather = (lambda out: vdist.gather_rows(out.spl, B * ws, ws)) if ws > 1 else None
 
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    vdist.barrier()
-    torch.cuda.synchronize()
     n0 = _lib.launch_count()
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        e = evs[i]
-        e[0].record(stream)
-        one_step(args.warmup + i, ev=(e[2], e[3]))
-        e[1].record(stream)
-    torch.cuda.synchronize()
-    vdist.barrier()
-    launches = _lib.launch_count() - n0
+    persist = sweep.persist_primitives_in_l2() if args.l2_persist else None
+    if persist:
+        persist.__enter__()
+    try:
+        step_ms, kern_ms, kept = sweep_timed(w, B, args.steps, args.warmup, dev, flush, rank, ws,
+                                             keep=(rank == 0 and not args.no_parity), gather=gather)
+    finally:
+        if persist:
+            persist.__exit__(None, None, None)
+    launches = _lib.launch_count() - n0  # warm-up + timed
+    launches_timed = sweep_timed.launches
     clocks = sampler.stop() if sampler else None
-    step_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    kern_ms = [e[2].elapsed_time(e[3]) for e in evs]
     total_ms = vdist.max_over_ranks(sum(step_ms), dev)
     kern_avg_ms = vdist.max_over_ranks(sum(kern_ms) / len(kern_ms), dev)
     value = ws * B * args.steps / (total_ms * 1e-3)
@@ -387,6 +527,7 @@ def run_ours(args):
         f_h = torch.from_numpy(w.freqs).pin_memory()
         y_h = torch.empty((B, n_out, s), dtype=torch.complex128).pin_memory()
         spl_h = torch.empty((B, s), dtype=torch.float64).pin_memory()
+        stream = torch.cuda.current_stream(dev)
 
         def e2e_step(step):
             start = ((step * ws + rank) * B) % nF
@@ -421,8 +562,11 @@ def run_ours(args):
 
     if rank != 0:
         return 0
+    # ---- parity of the headline's own outputs ----
+    parity = parity_of_kept(w, kept) if kept else None
+    del kept
+
     # ---- roofline of the dominant kernel ----
-    peak = _lib.probe_fp64_peak()
     fl = flops_per_freq(r, nprim, s, n_out)
     achieved = fl * B / (kern_avg_ms * 1e-3) / 1e12
     traffic = None
@@ -436,9 +580,17 @@ def run_ours(args):
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": "rom_sweep_blocked_kernel" if path == 1 else "rom_sweep_small_kernel",
                 "peak_source": "FP64 DMMA (mma.sync.m8n8k4.f64) throughput measured live by "
-                               "vb_probe_fp64_peak on this GPU (MEASURED_PEAKS.json has no FP64)",
+                               "vb_probe_fp64_peak on this GPU, median of 5 probes "
+                               "(MEASURED_PEAKS.json has no FP64)",
+                "peak_probes": peak_probes,
                 "flops_per_freq": fl, "freqs_per_launch": B,
                 "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu)"}
+
+    orders = None
+    if ws == 1 and not args.no_per_order:
+        orders = per_order(args, dev, flush, peak, nsm)
+        orders[f"r{r}"] = {"value": value, "frac": achieved / peak, "kernel_ms": kern_avg_ms,
+                           "note": "headline (this line's value / roofline / parity)"}
 
     cpu = None
     if ws == 1 and not args.no_cpu:
@@ -457,24 +609,45 @@ def run_ours(args):
 
     offline = None
     if ws == 1 and not args.no_offline:
-        offline = offline_measurements(w)
+        offline = offline_measurements(w, peak)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
         "data": "synthetic (seeded cfg5: K_r, D_r, M_r, 16 RHS, 50 outputs)",
-        "config": {"workload": f"cfg5_r{r}", "r": r, "rhs": s, "n_out": n_out, "n_prim": nprim,
-                   "freqs_per_step_per_rank": B,
-                   "grid": "linspace(1,1000,100000), rank-disjoint slices",
-                   "sweep_path": "blocked" if path == 1 else "shared-memory",
-                   "l2": "flushed between timed steps (512 MiB write)",
-                   "parallelism": f"frequency-sharded x{ws}"},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "config": bench_config(r, s, n_out, nprim, B, ws),
+        "method": {"sweep_path": "blocked" if path == 1 else "shared-memory",
+                   "l2_persistence": bool(args.l2_persist),
+                   "timing": "CUDA events on the launching stream, L2 flushed before each timed step, "
+                             "max over ranks"},
+        "roofline": roofline, "parity": parity, "per_order": orders, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(launches_timed), "gpu_launches_incl_warmup": int(launches),
         "clocks": clocks, "offline": offline,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def spawn_ranks(args, argv) -> int | None:
+    """`python bench.py --gpus N` without a torchrun environment: re-launch
+    this script under torch.distributed.run with N ranks on this node (one
+    process per GPU) and return its exit code.  Under torchrun, WORLD_SIZE
+    must equal --gpus."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None:
+        if int(ws_env) != args.gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + list(argv)
+    return subprocess.call(cmd)
 
 
 def main(argv=None):
@@ -490,7 +663,15 @@ def main(argv=None):
     ap.add_argument("--no-offline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--cpu-step-s", type=float, default=4.0)
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-per-order", action="store_true")
+    ap.add_argument("--orders", type=int, nargs="*", default=[256, 1024, 2048])
+    ap.add_argument("--l2-persist", type=int, default=1, help="pin the primitives in L2 during the sweep")
+    argv = sys.argv[1:] if argv is None else argv
     args = ap.parse_args(argv)
+    rc = spawn_ranks(args, argv)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -300,6 +300,19 @@ int vb_column_norms(int n, int m, const vb_complex* W, int64_t ldw, double* norm
 /* W[:, j] *= scale[j] (scale: device float64[m]). */
 int vb_scale_columns(int n, int m, vb_complex* W, int64_t ldw, const double* scale, void* stream);
 
+/* Batched classical Gram-Schmidt pass of k side-by-side Arnoldi processes
+ * (GPU GMRES, gmres.py; replaces the MGS loop of solvers.py:236-239 in the
+ * reference's gmres, solvers.py:191-264).  Column c's basis is V[:, c, 0:j]
+ * with element (row, c, i) at V[row * ldr + c * ldc + i]; W is n x k
+ * row-major (ldw).  vb_batched_dots: H[c * j + i] = sum_row conj(V[row,c,i])
+ * W[row,c] (per-CTA partials reduced in a fixed order: deterministic);
+ * vb_batched_update: W[row,c] -= sum_i V[row,c,i] H[c * j + i]. */
+size_t vb_batched_dots_workspace_bytes(int k, int j);
+int vb_batched_dots(int64_t n, int k, int j, const vb_complex* V, int64_t ldr, int64_t ldc, const vb_complex* W,
+                    int64_t ldw, vb_complex* H, void* work, size_t work_bytes, void* stream);
+int vb_batched_update(int64_t n, int k, int j, const vb_complex* V, int64_t ldr, int64_t ldc, const vb_complex* H,
+                      vb_complex* W, int64_t ldw, void* stream);
+
 /* Measured FP64 tensor-pipe (DMMA, mma.sync.m8n8k4.f64) throughput of this
  * device in TFLOP/s, written to *tflops_host; synchronous (~10 ms).  Used as
  * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */
@@ -314,10 +327,16 @@ int vb_probe_fp64_peak(double* tflops_host, void* stream);
  * TRSM / GEMM phases (CTA 0). */
 int vb_debug_phase_cycles(unsigned long long* cycles_host, int reset);
 
-/* Give back the L2 set-aside that vb_rom_sweep reserves for the reduced
- * primitives (persisting-access window): resets persisting lines and the
- * device's persisting-L2 limit to 0, so later bandwidth-bound work gets the
- * whole L2.  The next blocked sweep launch re-reserves it. */
+/* Opt-in L2 persistence for the blocked reduced sweep (default off): while
+ * enabled, each vb_rom_sweep launch on the blocked path raises the device's
+ * persisting-L2 limit to the primitives' size and marks them persisting
+ * (access-policy window), so the per-frequency workspace streaming does not
+ * evict them.  Device-wide state: pair with vb_release_l2_persistence. */
+void vb_set_l2_persistence(int enable);
+
+/* Give back the L2 set-aside reserved while persistence was enabled: resets
+ * persisting lines and restores the persisting-L2 limit the device had
+ * before the first raise. */
 int vb_release_l2_persistence(void);
 
 /* Number of this library's kernel launches since load (process-wide counter,

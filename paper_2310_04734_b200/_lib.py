@@ -32,6 +32,7 @@ _SIGS = {
     "vb_last_error": (C.c_char_p, []),
     "vb_launch_count": (C.c_int64, []),
     "vb_release_l2_persistence": (C.c_int, []),
+    "vb_set_l2_persistence": (None, [C.c_int]),
     "vb_debug_phase_cycles": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
     "vb_rom_sweep_path": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "vb_set_sweep_path_override": (None, [C.c_int]),
@@ -78,6 +79,11 @@ _SIGS = {
     "vb_column_norms_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "vb_column_norms": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t,
                                   C.c_void_p]),
+    "vb_batched_dots_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "vb_batched_dots": (C.c_int, [C.c_int64, C.c_int, C.c_int, _z, C.c_int64, C.c_int64, _z, C.c_int64, _z,
+                                  C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vb_batched_update": (C.c_int, [C.c_int64, C.c_int, C.c_int, _z, C.c_int64, C.c_int64, _z, _z, C.c_int64,
+                                    C.c_void_p]),
     "vb_scale_columns": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p]),
     "vb_zgetrf_workspace_bytes": (C.c_size_t, [C.c_int]),
     "vb_zgetrf_aux_bytes": (C.c_size_t, [C.c_int]),

@@ -204,6 +204,20 @@ def assemble_face_mass(xyz, face_conn, device=None) -> DeviceCSR:
     return pat.gather(face_mass(xyz_d, f_d))
 
 
+def assemble_weighted_face_mass(xyz, face_conn, weights, device=None) -> DeviceCSR:
+    """sum_e w_e int_{Gamma_e} N N^T dGamma over the given 9-node faces (real
+    per-element weights, e.g. 1 / Z_e of an impedance wall whose impedance
+    varies per element): element matrices scaled before the deterministic
+    element-order gather, so the CSR pattern is the unweighted face mass's."""
+    dev = torch.device(device or "cuda")
+    xyz_d = torch.as_tensor(np.ascontiguousarray(xyz, dtype=np.float64), device=dev)
+    f_d = torch.as_tensor(np.ascontiguousarray(face_conn, dtype=np.int32), device=dev)
+    pat = pattern_from_elements(xyz.shape[0], f_d)
+    Fe = face_mass(xyz_d, f_d)
+    w = torch.as_tensor(np.asarray(weights, dtype=np.float64), device=dev).view(-1, *([1] * (Fe.dim() - 1)))
+    return pat.gather((Fe * w).contiguous())
+
+
 def box_band_tables(box, ne):
     """[3][maxnp][5] band entries of the assembled 1D quadratic stiffness / mass
     along x, y, z (host; a few KB)."""

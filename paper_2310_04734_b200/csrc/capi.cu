@@ -40,12 +40,9 @@ const char* vb_last_error(void) { return vb::g_last_error.c_str(); }
 
 int64_t vb_launch_count(void) { return vb::g_launches.load(); }
 
-int vb_release_l2_persistence(void) {
-  VB_CUDA(cudaFree(nullptr));  // make sure the primary context exists
-  VB_CUDA(cudaCtxResetPersistingL2Cache());
-  VB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
-  return 0;
-}
+int vb_release_l2_persistence(void) { return vb::sweep_release_l2_persistence(); }
+
+void vb_set_l2_persistence(int enable) { vb::sweep_set_l2_persistence(enable); }
 
 int vb_rom_sweep_path(int r, int nprim, int s, int n_out) { return vb::sweep_path(r, nprim, s, n_out); }
 
@@ -209,6 +206,21 @@ int vb_column_norms(int n, int m, const vb_complex* W, int64_t ldw, double* norm
 int vb_scale_columns(int n, int m, vb_complex* W, int64_t ldw, const double* scale, void* stream) {
   VB_CHECK_ARG(n >= 0 && m >= 0, "vb_scale_columns: bad sizes");
   return vb::scale_columns(n, m, (z_t*)W, ldw, scale, (cudaStream_t)stream);
+}
+
+size_t vb_batched_dots_workspace_bytes(int k, int j) { return vb::batched_dots_workspace_bytes(k, j); }
+
+int vb_batched_dots(int64_t n, int k, int j, const vb_complex* V, int64_t ldr, int64_t ldc, const vb_complex* W,
+                    int64_t ldw, vb_complex* H, void* work, size_t work_bytes, void* stream) {
+  VB_CHECK_ARG(n >= 0 && k >= 0 && j >= 0 && (k * j == 0 || (V && W && H)), "vb_batched_dots: bad arguments");
+  return vb::batched_dots(n, k, j, (const z_t*)V, ldr, ldc, (const z_t*)W, ldw, (z_t*)H, work, work_bytes,
+                          (cudaStream_t)stream);
+}
+
+int vb_batched_update(int64_t n, int k, int j, const vb_complex* V, int64_t ldr, int64_t ldc, const vb_complex* H,
+                      vb_complex* W, int64_t ldw, void* stream) {
+  VB_CHECK_ARG(n >= 0 && k >= 0 && j >= 0 && (k * j == 0 || (V && W && H)), "vb_batched_update: bad arguments");
+  return vb::batched_update(n, k, j, (const z_t*)V, ldr, ldc, (const z_t*)H, (z_t*)W, ldw, (cudaStream_t)stream);
 }
 
 size_t vb_zgetrf_workspace_bytes(int n) { return vb::zgetrf_workspace_bytes(n); }

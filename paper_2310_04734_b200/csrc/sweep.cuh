@@ -17,6 +17,8 @@ int sweep_small_launch(int r, int nprim, int s, int n_out, int64_t F, const z_t*
 
 int sweep_path(int r, int nprim, int s, int n_out);
 void sweep_set_override(int path);
+void sweep_set_l2_persistence(int enable);
+int sweep_release_l2_persistence();
 size_t sweep_workspace_bytes(int r, int nprim, int s, int n_out, int64_t F);
 int sweep_run(int r, int nprim, int s, int n_out, int64_t F, const z_t* prims, const z_t* alpha,
               const z_t* b, int64_t b_stride_f, const z_t* c_r, z_t* y, double* spl, z_t* x,
@@ -79,6 +81,11 @@ int csr_axpy_dense(int n_rows, const int32_t* indptr, const int32_t* indices, co
 size_t zgemm_workspace_bytes(char transa, int m, int n, int k);
 int zgemm(char transa, int m, int n, int k, z_t alpha, const z_t* A, int64_t lda, const z_t* B,
           int64_t ldb, z_t beta, z_t* C, int64_t ldc, void* work, size_t work_bytes, cudaStream_t st);
+size_t batched_dots_workspace_bytes(int k, int j);
+int batched_dots(int64_t n, int k, int j, const z_t* V, int64_t ldr, int64_t ldc, const z_t* W, int64_t ldw, z_t* H,
+                 void* work, size_t work_bytes, cudaStream_t st);
+int batched_update(int64_t n, int k, int j, const z_t* V, int64_t ldr, int64_t ldc, const z_t* H, z_t* W,
+                   int64_t ldw, cudaStream_t st);
 size_t column_norms_workspace_bytes(int n, int m);
 int column_norms(int n, int m, const z_t* W, int64_t ldw, double* out, void* work, size_t wb,
                  cudaStream_t st);

@@ -677,6 +677,25 @@ static size_t cta_stride(int r, int s, int n_out) {
 
 }  // namespace blk
 
+// Opt-in (vb_set_l2_persistence): reserving persisting L2 is device-wide state
+// that outlives the call, so it is only done while the caller asked for it and
+// vb_release_l2_persistence() restores the limit the process had before.
+static int g_l2_persist = 0;
+static size_t g_l2_prev_limit = 0;
+static int g_l2_raised = 0;
+
+void sweep_set_l2_persistence(int enable) { g_l2_persist = enable ? 1 : 0; }
+
+int sweep_release_l2_persistence() {
+  VB_CUDA(cudaFree(nullptr));  // make sure the primary context exists
+  VB_CUDA(cudaCtxResetPersistingL2Cache());
+  if (g_l2_raised) {
+    VB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_prev_limit));
+    g_l2_raised = 0;
+  }
+  return 0;
+}
+
 static int blocked_grid(int64_t F) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -772,12 +791,18 @@ int sweep_blocked_launch(int r, int nprim, int s, int n_out, int64_t F, const z_
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
   const size_t pbytes = (size_t)nprim * r * r * sizeof(z_t);
-  if (max_persist > 0 && max_window > 0) {
+  if (g_l2_persist && max_persist > 0 && max_window > 0) {
     const size_t win = pbytes < (size_t)max_window ? pbytes : (size_t)max_window;
     const size_t lim = win < (size_t)max_persist ? win : (size_t)max_persist;
     size_t cur = 0;
     cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-    if (cur < lim) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+    if (cur < lim) {
+      if (!g_l2_raised) {
+        g_l2_prev_limit = cur;
+        g_l2_raised = 1;
+      }
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+    }
     attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
     attr[0].val.accessPolicyWindow.base_ptr = (void*)prims;
     attr[0].val.accessPolicyWindow.num_bytes = win;

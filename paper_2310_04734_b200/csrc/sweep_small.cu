@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(NT) rom_sweep_small_kernel(
         }
         warp_argmax(v, pi);
         if (lane == 0) {
-          if (v == 0.0) {  // exactly singular column: LAPACK sets info and skips
+          if (!(v > 0.0)) {  // zero (or NaN) pivot column: LAPACK sets info and skips
             if (s_info == 0) s_info = k + 1;
             s_piv = -1;
           } else {
@@ -70,7 +70,10 @@ __global__ void __launch_bounds__(NT) rom_sweep_small_kernel(
       }
       __syncthreads();
       const int p = s_piv;
-      if (p < 0) continue;  // uniform across the block
+      if (p < 0) {  // uniform across the block; the barrier keeps warp 0 from
+        __syncthreads();  // publishing step k+1's pivot before every warp read p
+        continue;
+      }
       const z_t pv = As[p * ld + k];
       const z_t pinv = zrecip(pv);
       // phase A: multipliers (read column k through the swap) and swap cols > k

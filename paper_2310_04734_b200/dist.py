@@ -39,6 +39,22 @@ def shard_range(n: int, rank: int, world_size: int) -> tuple[int, int]:
     return lo, hi
 
 
+def _host_staged() -> bool:
+    """gloo has no CUDA all-gather: device tensors travel through host copies
+    (the CPU tests and the world-2-on-one-GPU tests use gloo; NCCL moves device
+    memory directly)."""
+    return dist.is_initialized() and dist.get_backend() == "gloo"
+
+
+def _all_gather_into(out: torch.Tensor, inp: torch.Tensor):
+    if inp.is_cuda and _host_staged():
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(o, inp.cpu())
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp)
+
+
 def gather_rows(local: torch.Tensor, n_total: int, world_size: int) -> torch.Tensor:
     """Concatenate per-rank row blocks (shard_range layout) on every rank.
 
@@ -53,7 +69,7 @@ def gather_rows(local: torch.Tensor, n_total: int, world_size: int) -> torch.Ten
     pad[: local.shape[0]] = local
     out = torch.empty((world_size * width,) + tuple(local.shape[1:]), dtype=local.dtype,
                       device=local.device)
-    dist.all_gather_into_tensor(out, pad)
+    _all_gather_into(out, pad)
     parts = [out[r * width: r * width + (hi - lo)] for r, (lo, hi) in enumerate(sizes)]
     return torch.cat(parts, dim=0)
 
@@ -61,7 +77,7 @@ def gather_rows(local: torch.Tensor, n_total: int, world_size: int) -> torch.Ten
 def max_over_ranks(x: float, device=None) -> float:
     if not (dist.is_available() and dist.is_initialized()):
         return x
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device=None if _host_staged() else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -89,9 +105,9 @@ def gather_blocks(local: list, counts: list[int], n_rows: int, max_cols: int, dt
         widths[i] = b2.shape[1]
     real = torch.view_as_real(buf) if buf.is_complex() else buf
     out = torch.empty((ws * cmax,) + tuple(real.shape[1:]), dtype=real.dtype, device=device)
-    dist.all_gather_into_tensor(out, real.contiguous())
+    _all_gather_into(out, real.contiguous())
     wout = torch.empty(ws * cmax, dtype=torch.int64, device=device)
-    dist.all_gather_into_tensor(wout, widths)
+    _all_gather_into(wout, widths)
     full = torch.view_as_complex(out) if buf.is_complex() else out
     wl = wout.cpu().tolist()
     return [full[q * cmax + i, :, : wl[q * cmax + i]] for q in range(ws) for i in range(counts[q])]
@@ -142,11 +158,16 @@ def sweep_sharded(rs, freqs: torch.Tensor, want_y: bool = False):
     s, n_out = int(rs.b.shape[-1]), int(rs.c.shape[0])
     if hi > lo:
         out = rs.sweep_device(freqs[lo:hi], want_y=want_y)
-        raise_if_singular(out.info)
-        spl_l, y_l = out.spl, out.y
+        spl_l, y_l, info_l = out.spl, out.y, out.info
     else:  # more ranks than frequencies
         spl_l = torch.empty((0, s), dtype=torch.float64, device=rs.device)
         y_l = torch.empty((0, n_out, s), dtype=torch.complex128, device=rs.device) if want_y else None
+        info_l = torch.empty((0,), dtype=torch.int32, device=rs.device)
+    # gather first, then every rank checks the same full info vector: a zero
+    # pivot on one rank raises LinAlgError on all of them (no rank is left
+    # waiting in a collective the failing rank never reaches)
+    info = gather_rows(info_l, F, ws)
     spl = gather_rows(spl_l, F, ws)
     y = gather_rows(y_l, F, ws) if want_y else None
+    raise_if_singular(info)
     return spl, y

@@ -90,6 +90,43 @@ def _to_dense_dev(M, device) -> torch.Tensor:
     return torch.as_tensor(np.asarray(M), device=device).to(CDT).contiguous()
 
 
+_PROVIDER_CACHE: dict = {}
+
+
+def _provider_on_device(M, device):
+    """A provider's matrix on the device, uploaded once per matrix object:
+    scipy sparse -> real CSR primitives (real / imaginary parts on one
+    pattern, model_operator.device_csr_terms), dense -> a dense tensor.
+    Providers that return the same object every call (the reference tests'
+    `lambda f: K`) hit the cache."""
+    key = (id(M), str(device))
+    hit = _PROVIDER_CACHE.get(key)
+    if hit is not None and hit[0] is M:
+        return hit[1]
+    if sp.issparse(M):
+        from .model_operator import device_csr_terms
+        val = ("csr", device_csr_terms(M, device))
+    else:
+        val = ("dense", _to_dense_dev(M, device))
+    if len(_PROVIDER_CACHE) > 32:
+        _PROVIDER_CACHE.pop(next(iter(_PROVIDER_CACHE)))
+    _PROVIDER_CACHE[key] = (M, val)
+    return val
+
+
+def _provider_matmul(M, X: torch.Tensor, scale: complex = 1.0) -> torch.Tensor:
+    """scale * M X on the device for a provider matrix M (sparse stays sparse)."""
+    kind, v = _provider_on_device(M, X.device)
+    X2 = X.view(-1, 1) if X.dim() == 1 else X
+    if kind == "dense":
+        out = linalg.zgemm("N", v, X2, scale, 0.0)
+    else:
+        out = torch.zeros((v[0][0].n, X2.shape[1]), dtype=CDT, device=X.device)
+        for P, fac in v:
+            linalg.spmm(P, X2, scale * fac, 1.0, out)
+    return out.view(-1) if X.dim() == 1 else out
+
+
 # ----------------------------------------------------------- FOM / ROM ----
 @dataclass
 class FullOrderModel:
@@ -107,6 +144,7 @@ class FullOrderModel:
     fdm: object = None            # fdm.BoxFDM for structured boxes (cfg3-size solves)
     prefer_fdm: bool = False
     schur: object = None  # schur.CoupledBoxSchur: structure + box cavity (cfg2)
+    iterative: object = None  # gmres.BoxGmres: preconditioned GMRES (per-element wall impedances)
 
     def c_out_adjoint_dev(self, device) -> torch.Tensor:
         """C^H (n x n_out, complex) on the device, uploaded once per c_out and
@@ -182,6 +220,8 @@ class FullOrderModel:
         """GPU factorisation of A(f): dense LU (n <= DENSE_MAX_N), the
         fast-diagonalisation solver of a structured box (any n), or a Schur
         complement on a structure coupled to a box cavity (schur.py)."""
+        if self.iterative is not None:
+            return self.iterative.factor(f, self)
         if self.fdm is not None and (self.prefer_fdm or self.n > DENSE_MAX_N):
             return self.fdm.factor(f, self)
         if self.schur is not None:  # Schur complement on the structure, FDM cavity
@@ -210,9 +250,7 @@ class FullOrderModel:
         """out = scale * Op(f) X + beta out with Op in {'K','M','D'} (device SpMM)."""
         if self.affine is None:
             prov = {"K": self.stiffness, "M": self.mass, "D": self.damping}[which]
-            Md = _to_dense_dev(prov(f), X.device)
-            r = linalg.zgemm("N", Md, X.view(-1, 1) if X.dim() == 1 else X, scale, 0.0)
-            r = r.view(-1) if X.dim() == 1 else r
+            r = _provider_matmul(prov(f), X, scale)
             if out is None:
                 return r
             out.mul_(beta).add_(r)
@@ -413,14 +451,11 @@ class ReducedModel:
                 MR = sum(P[i] * kinds[i][1].at(f) for i in range(len(kinds)) if kinds[i][0] == "M")
                 AR = AR + 1j * w * (a * MR + b * KR)
         else:
-            K = _to_dense_dev(self.fom.stiffness(f), Vd.device)
-            M = _to_dense_dev(self.fom.mass(f), Vd.device)
-            KR = linalg.zgemm("C", Vd, linalg.zgemm("N", K, Vd))
-            MR = linalg.zgemm("C", Vd, linalg.zgemm("N", M, Vd))
+            KR = linalg.zgemm("C", Vd, _provider_matmul(self.fom.stiffness(f), Vd))
+            MR = linalg.zgemm("C", Vd, _provider_matmul(self.fom.mass(f), Vd))
             AR = KR - w * w * MR
             if self.fom.damping is not None:
-                D = _to_dense_dev(self.fom.damping(f), Vd.device)
-                AR = AR + 1j * w * linalg.zgemm("C", Vd, linalg.zgemm("N", D, Vd))
+                AR = AR + 1j * w * linalg.zgemm("C", Vd, _provider_matmul(self.fom.damping(f), Vd))
             if rayleigh is not None:
                 a, b = rayleigh
                 AR = AR + 1j * w * (a * MR + b * KR)
@@ -532,8 +567,14 @@ def project(fom: FullOrderModel, V, f: float):
     if V.shape[0] != fom.n:
         raise ValueError("basis row count does not match model dimension")
     Vd = _as_dev(V)
-    A = fom.operator_dense(f, Vd.device)
-    AR = linalg.zgemm("C", Vd, linalg.zgemm("N", A, Vd))
+    if fom.affine is not None:
+        # sum_k alpha_k(f) V^H P_k V: sparse products, never an n x n matrix
+        return ReducedModel(fom=fom, V=Vd, window=(f, f)).reduced_system(f)
+    w = 2.0 * math.pi * f
+    AR = linalg.zgemm("C", Vd, _provider_matmul(fom.stiffness(f), Vd))
+    AR = AR - w * w * linalg.zgemm("C", Vd, _provider_matmul(fom.mass(f), Vd))
+    if fom.damping is not None:
+        AR = AR + 1j * w * linalg.zgemm("C", Vd, _provider_matmul(fom.damping(f), Vd))
     bR = linalg.zgemm("C", Vd, fom.load_dev(f, Vd.device)).cpu().numpy()
     return AR.cpu().numpy(), (bR[:, 0] if np.ndim(fom.load(f)) == 1 else bR)
 
@@ -817,6 +858,8 @@ def _lu_factored(fom: FullOrderModel) -> bool:
     Schur complement) — the latency-bound factor / solve kernels that gain
     from concurrent expansion points; the box FDM solver's transforms are
     throughput-bound GEMMs (and its host eigensolves already use 3 threads)."""
+    if fom.iterative is not None:
+        return False
     return not (fom.fdm is not None and (fom.prefer_fdm or fom.n > DENSE_MAX_N))
 
 
@@ -1025,12 +1068,25 @@ def rom_sweep(roms: list, grid, time_against_fom: bool = False) -> RomSweepResul
     return res
 
 
+def _is_model_operator(op) -> bool:
+    """Duck test for the reference's ModelOperator (assembly.py:221-287)."""
+    return all(hasattr(op, a) for a in ("config", "primitives", "couplings", "block_map", "kinds", "load"))
+
+
 def fom_from_operator(op, output_dof: int) -> FullOrderModel:
-    """Full-order model over an assembled operator with one output dof (mor.py:397-402)."""
+    """Full-order model over an assembled operator with one output dof
+    (mor.py:397-402).  A reference ModelOperator is read as data into the
+    device-side affine operator (model_operator.affine_from_operator: CSR
+    primitives on the GPU, per-frequency scalars from the reference's own
+    functions); its K/M/load stay the host providers of the reference API."""
     n = sum(size for _, size in op.block_map.values())
     c = np.zeros(n)
     c[output_dof] = 1.0
     aff = getattr(op, "affine", None)
+    if aff is None and _is_model_operator(op):
+        from .model_operator import affine_from_operator
+        aff = affine_from_operator(op)
+        return FullOrderModel(stiffness=op.K, mass=op.M, load=op.load, c_out=c, n=n, affine=aff)
     if aff is not None:
         return FullOrderModel(c_out=c, n=n, affine=aff)
     return FullOrderModel(stiffness=op.K, mass=op.M, load=op.load, c_out=c, n=n)

@@ -94,12 +94,39 @@ def rom_sweep_affine(prims: torch.Tensor, alpha: torch.Tensor, b: torch.Tensor, 
             info=torch.empty((F,), dtype=torch.int32, device=dev))
     wbytes = lib.vb_rom_sweep_workspace_bytes(r, K, s, n_out, F)
     work = torch.empty((max(wbytes, 1),), dtype=torch.uint8, device=dev)
+    side = stream is not None and stream != torch.cuda.current_stream(dev)
+    if side:
+        # inputs, outputs and workspace come from the current stream: order the
+        # launch after them, and keep the caching allocator from recycling any
+        # of them before the side stream is done with them
+        stream.wait_stream(torch.cuda.current_stream(dev))
     rc = lib.vb_rom_sweep(r, K, s, n_out, F, _lib.ptr(prims), _lib.ptr(alpha), _lib.ptr(b), bstride,
                           _lib.ptr(c_r) if n_out else None, _lib.ptr(out.y), _lib.ptr(out.spl),
                           _lib.ptr(out.x), _lib.ptr(out.info), _lib.ptr(work), wbytes,
                           _lib.stream_handle(stream))
     _lib.check(rc, "vb_rom_sweep")
+    if side:
+        for t in (work, prims, alpha, b, c_r, out.y, out.spl, out.x, out.info):
+            if t is not None:
+                t.record_stream(stream)
     return out
+
+
+class persist_primitives_in_l2:
+    """Context manager: blocked sweeps launched inside it pin their reduced
+    primitives in L2 (persisting access-policy window); on exit the persisting
+    lines are reset and the device's persisting-L2 limit is restored."""
+
+    def __enter__(self):
+        _lib.load().vb_set_l2_persistence(1)
+        return self
+
+    def __exit__(self, *exc):
+        lib = _lib.load()
+        lib.vb_set_l2_persistence(0)
+        torch.cuda.synchronize()
+        _lib.check(lib.vb_release_l2_persistence(), "vb_release_l2_persistence")
+        return False
 
 
 MAX_RHS_BLOCKED = 16  # right-hand sides per launch on the blocked path
@@ -184,11 +211,14 @@ class ReducedSweep:
         out = self.sweep_device(f)
         y = torch.empty(out.y.shape, dtype=out.y.dtype, pin_memory=True)
         spl = torch.empty(out.spl.shape, dtype=out.spl.dtype, pin_memory=True)
-        y.copy_(out.y, non_blocking=True)
-        spl.copy_(out.spl, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
+        st = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):  # the kernel's stream: copy after it, then wait for it
+            y.copy_(out.y, non_blocking=True)
+            spl.copy_(out.spl, non_blocking=True)
+            info = out.info.to("cpu", non_blocking=True)
+        st.synchronize()
         if check_singular:
-            raise_if_singular(out.info)
+            raise_if_singular(info)
         return y.numpy(), spl.numpy()
 
 

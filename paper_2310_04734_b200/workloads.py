@@ -75,6 +75,18 @@ def cfg5(r: int = 1024, n_freq: int = CFG5_NFREQ, s: int = CFG5_RHS, n_out: int 
                            b=B, c_r=C, freqs=freqs, seed=seed)
 
 
+def cfg5_eigenfrequencies(w: ReducedWorkload) -> np.ndarray:
+    """Undamped eigenfrequencies (Hz) of a cfg5 workload: K_h x = w^2 M x with
+    K_h = K_r / (1 + i eta) Hermitian PD (host, scipy eigh).  The frequencies
+    next to these are where the reduced LU pivots hardest (parity probes)."""
+    import scipy.linalg as sla
+    Kh = w.prims[0] / (1 + 1j * CFG5_ETA)
+    Kh = 0.5 * (Kh + Kh.conj().T)
+    M = w.prims[2]
+    lam = sla.eigh(Kh, 0.5 * (M + M.conj().T), eigvals_only=True)
+    return np.sqrt(np.maximum(lam, 0.0)) / (2.0 * math.pi)
+
+
 # ---------------------------------------------------------------- cfg1 -----
 CFG1_BOX = (0.0, 0.0, 0.0, 2.0, 1.6, 1.2)
 CFG1_NE = (10, 8, 6)
@@ -142,7 +154,7 @@ CFG3_NSRC = 8
 
 
 def cfg3_model(seed: int = 3, box=CFG3_BOX, ne=CFG3_NE, n_src: int = CFG3_NSRC, n_rec: int = CFG1_NREC,
-               device=None):
+               device=None, per_element_z: bool = False):
     """cfg3 (BASELINE configs[2]): 6 x 3 x 2.5 m air box, 60 x 30 x 25 hex27
     (n = 376,431, nnz = 23,300,121), three absorbing walls with seeded
     Z_w = rho c U[2, 10] (real, one value per wall — keeps the FDM solver
@@ -164,17 +176,35 @@ def cfg3_model(seed: int = 3, box=CFG3_BOX, ne=CFG3_NE, n_src: int = CFG3_NSRC, 
     Kg, Mn = assembly.assemble_helmholtz_box(box, ne, device)
     n = xyz.shape[0]
     D_terms = []
-    for w, Z in Zs.items():
-        F = assembly.assemble_face_mass(xyz, assembly.hex27_box_face(ne, w, conn), device)
-        D_terms.append(AffineTerm(F, 1.0 / Z))
+    iterative, Ze = None, {}
+    if per_element_z:
+        # seeded Z_e = rho c U[2, 10] per wall face element (separate stream, so
+        # sources / receivers stay those of the per-wall model); the walls enter
+        # as D_w = sum_e F_e / Z_e and the full-order solver becomes GMRES
+        # preconditioned by the box FDM with per-wall harmonic-mean impedances
+        from .fdm import BoxFDM
+        from .gmres import BoxGmres
+        rz = np.random.default_rng(seed + 1000)
+        zmean = {}
+        for w in CFG3_WALLS:
+            fc = assembly.hex27_box_face(ne, w, conn)
+            Ze[w] = AIR_RHO * AIR_C * rz.uniform(2.0, 10.0, len(fc))
+            D_terms.append(AffineTerm(assembly.assemble_weighted_face_mass(xyz, fc, 1.0 / Ze[w], device), 1.0))
+            zmean[w] = 1.0 / float(np.mean(1.0 / Ze[w]))
+        iterative = BoxGmres(BoxFDM(box, ne, AIR_RHO, AIR_C, zmean))
+    else:
+        for w, Z in Zs.items():
+            F = assembly.assemble_face_mass(xyz, assembly.hex27_box_face(ne, w, conn), device)
+            D_terms.append(AffineTerm(F, 1.0 / Z))
     b = torch.zeros((n, n_src), dtype=torch.complex128, device=Kg.data.device)
     b[torch.as_tensor(src, device=b.device), torch.arange(n_src, device=b.device)] = 1.0
     C = np.zeros((n_rec, n))
     C[np.arange(n_rec), rec] = 1.0
     aff = AffineOperator(K=[AffineTerm(Kg, 1.0 / AIR_RHO)],
                          M=[AffineTerm(Mn, 1.0 / (AIR_RHO * AIR_C * AIR_C))], D=D_terms, load=b)
-    fom = FullOrderModel(c_out=C, n=n, affine=aff, fdm=BoxFDM(box, ne, AIR_RHO, AIR_C, Zs))
-    return fom, {"xyz": xyz, "conn": conn, "src": src, "rec": rec, "walls": Zs, "Kg": Kg, "Mn": Mn,
+    fom = FullOrderModel(c_out=C, n=n, affine=aff, fdm=None if per_element_z else BoxFDM(box, ne, AIR_RHO, AIR_C, Zs),
+                         iterative=iterative)
+    return fom, {"xyz": xyz, "conn": conn, "src": src, "rec": rec, "walls": Zs, "Kg": Kg, "Mn": Mn, "Z_e": Ze,
                  "freqs": np.arange(20.0, 300.0 + 1e-9, 0.25), "points": CFG3_POINTS,
                  "moments": CFG3_MOMENTS}
 

@@ -205,12 +205,77 @@ def gold_spl():
     np.savez_compressed(HERE / "spl.npz", p=p, **vals)
 
 
+def oscillator_chain(n=120, damping=0.02):
+    """tests/test_mor.py:40-52 (reference test fixture): spring-mass chain with
+    structural damping, forced at one end, observed at the other."""
+    main = 2.0 * np.ones(n)
+    off = -np.ones(n - 1)
+    K = sp.diags([off, main, off], [-1, 0, 1], format="csc") * 1e6 * (1 + 1j * damping)
+    M = sp.identity(n, format="csc") * 1.0
+    b = np.zeros(n)
+    b[0] = 1.0
+    c = np.zeros(n)
+    c[-1] = 1.0
+    return rmor.FullOrderModel(stiffness=lambda f: K, mass=lambda f: M, load=lambda f: b, c_out=c, n=n)
+
+
+class Settings:
+    """MorSettings duck type (config.py:172-184; tests/test_mor.py:17-23)."""
+
+    def __init__(self, tol=1e-2, max_points=20, moments_per_point=4, candidate_stride=4, windows="auto"):
+        self.tol, self.max_points, self.moments_per_point = tol, max_points, moments_per_point
+        self.candidate_stride, self.windows = candidate_stride, windows
+
+
+GREEDY_CASES = {
+    # name: (model, grid, settings kwargs, band or window, entry)
+    "chain_tol1e-3": ("chain", (10.0, 120.0, 56), dict(tol=1e-3, max_points=15, candidate_stride=3), "greedy"),
+    "chain_tol1e-4_budget10": ("chain", (10.0, 120.0, 56), dict(tol=1e-4, max_points=10, candidate_stride=3),
+                               "greedy"),
+    "chain_tol_inf": ("chain", (10.0, 60.0, 26), dict(tol=math.inf), "greedy"),
+    "chain_two_windows": ("chain", (10.0, 120.0, 56),
+                          dict(tol=1e-3, max_points=15, candidate_stride=3, windows=[(10.0, 60.0), (60.0, 120.0)]),
+                          "local"),
+    "chain_auto_bisect": ("chain", (10.0, 200.0, 96), dict(tol=1e-7, max_points=3, moments_per_point=2,
+                                                           candidate_stride=3), "local"),
+    "frozen_tol1e-6": ("frozen", (10.0, 100.0, 46), dict(tol=1e-6, max_points=8, moments_per_point=3,
+                                                          candidate_stride=2), "greedy"),
+}
+
+
+def gold_greedy():
+    """Reference greedy_expand / build_local_roms (mor.py:224-353) decisions:
+    expansion points, r, error logs, converged/stalled/budget flags,
+    auto-bisected windows, and the rom_sweep FRF of the result."""
+    out = {"cases": np.array(list(GREEDY_CASES))}
+    for name, (model, (g0, g1, ng), kw, entry) in GREEDY_CASES.items():
+        fom = oscillator_chain() if model == "chain" else frozen_fom(n=200)[0]
+        grid = list(np.linspace(g0, g1, ng))
+        st = Settings(**kw)
+        if entry == "greedy":
+            roms = [rmor.greedy_expand(fom, grid, st, (g0, g1))]
+        else:
+            roms = rmor.build_local_roms(fom, grid, st, (g0, g1))
+        out[f"{name}__n_windows"] = np.array(len(roms))
+        for k, r in enumerate(roms):
+            out[f"{name}__window{k}"] = np.array(r.window)
+            out[f"{name}__points{k}"] = np.array(r.expansion_points)
+            out[f"{name}__r{k}"] = np.array(r.r)
+            out[f"{name}__errlog{k}"] = np.array(r.error_log)
+            out[f"{name}__flags{k}"] = np.array([r.converged, r.stalled, r.budget_exhausted])
+        sw = rmor.rom_sweep(roms, grid)
+        out[f"{name}__frf"] = np.array(sw.frf)
+        out[f"{name}__window_index"] = np.array(sw.window_index)
+    np.savez_compressed(HERE / "greedy_ref.npz", **out)
+
+
+ALL = {"frozen": gold_frozen, "assembly_2d": gold_assembly_2d, "box_mor": gold_box_mor,
+       "reduced_dense": gold_reduced_dense, "spl": gold_spl, "artifacts": gold_artifacts,
+       "greedy": gold_greedy}
+
+
 if __name__ == "__main__":
-    gold_frozen()
-    gold_assembly_2d()
-    gold_box_mor()
-    gold_reduced_dense()
-    gold_spl()
-    gold_artifacts()
+    for name in (sys.argv[1:] or list(ALL)):
+        ALL[name]()
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -122,3 +122,25 @@ def test_kron_apply_equals_csr_spmm(cuda, ne, k):
         y1 = linalg.spmm(A, X[:, :1].contiguous())
         r1 = linalg.spmm(A.with_data(A.data), X[:, :1].contiguous())
         assert torch.equal(y1, r1)
+
+
+def test_cfg3_full_size_pattern_bit_exact(cuda):
+    """cfg3 at its BASELINE size (60 x 30 x 25 hex27, n = 376,431, nnz =
+    23,300,121): both the general element sort/gather builder and the box
+    fast path give indptr/indices bit-identical to the independent Kronecker
+    pattern (oracle/fe.kron_pattern) = scipy's coo -> csr -> sum_duplicates
+    structure of assembly.py:166-173."""
+    import torch
+    from paper_2310_04734_b200 import assembly, workloads
+    ne = workloads.CFG3_NE
+    R = fe.kron_pattern(*ne)
+    n, nnz = fe.hex27_pattern_counts(*ne)
+    assert R.shape == (n, n) and R.nnz == nnz == 23_300_121
+    Kb, _ = assembly.assemble_helmholtz_box(workloads.CFG3_BOX, ne)
+    np.testing.assert_array_equal(Kb.indptr.cpu().numpy(), R.indptr)
+    np.testing.assert_array_equal(Kb.indices.cpu().numpy(), R.indices)
+    del Kb
+    xyz, conn = assembly.hex27_box(workloads.CFG3_BOX, *ne)
+    pat = assembly.pattern_from_elements(n, torch.as_tensor(conn, device=cuda))
+    np.testing.assert_array_equal(pat.indptr.cpu().numpy(), R.indptr)
+    np.testing.assert_array_equal(pat.indices.cpu().numpy(), R.indices)

@@ -108,17 +108,21 @@ def test_cfg3_mor_chain(cuda):
     G = V[:, :64].conj().T @ V[:, :64]
     assert torch.abs(G - torch.eye(64, dtype=G.dtype, device=G.device)).max().item() <= 1e-10
     rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 300.0))
-    grid = list(lay["freqs"][::40])
+    grid = list(lay["freqs"])  # the full 1,121-point grid
     y, spl, _, info = rom.sweep(grid)
     assert int(info.abs().sum()) == 0
     P, kinds, br = rom._projected()
     alpha = rom._alpha(np.array(grid), kinds)
-    yo, splo = omor.affine_sweep(P.cpu().numpy(), alpha[::7], br.cpu().numpy(), rom._cR.cpu().numpy())
-    yg = y.cpu().numpy()[::7]
+    yo, splo = omor.affine_sweep(P.cpu().numpy(), alpha, br.cpu().numpy(), rom._cR.cpu().numpy())
+    yg = y.cpu().numpy()
+    worst = 0.0
     for i in range(len(yo)):
         _, e, _, _ = omor.relative_error(yo[i].ravel(), yg[i].ravel())
-        assert e <= 1e-8
-    np.testing.assert_allclose(spl.cpu().numpy()[::7], splo, atol=0.01)
+        worst = max(worst, e)
+    assert worst <= 1e-8, worst
+    np.testing.assert_allclose(spl.cpu().numpy(), splo, atol=0.01)
+    grid = grid[::40]
+    y = y[::40]
     # ROM approximation vs the full-order model at sampled frequencies
     C = np.atleast_2d(fom.c_out)
     worst = 0.0

@@ -47,6 +47,23 @@ def test_cfg2_primitives_match_oracle(cuda):
         np.testing.assert_allclose(lay["load"].at(f).cpu().numpy()[:, 0], prims["load"](f), rtol=0, atol=1e-14)
 
 
+def test_cfg2_full_size_primitives_match_oracle(cuda):
+    """BASELINE cfg2 size (16 x 12 plate, 16 x 12 x 10 cavity, n = 20,890): all
+    six primitives' CSR indptr/indices bit-identical to the oracle's
+    coo -> csr -> sum_duplicates of the same triplets, values to rounding."""
+    from paper_2310_04734_b200 import workloads
+    fom, lay = workloads.cfg2_model(use_schur=False)
+    P = workloads.CFG2_PLATE
+    prims = shell.cfg2_primitives(workloads.CFG2_BOX, workloads.CFG2_NE, P["E"], P["nu"], P["rho"], P["t"],
+                                  workloads.AIR_RHO, workloads.AIR_C, workloads.CFG2_THETA)
+    assert fom.n == prims["n"] == 20_890
+    for name in ("Kg", "Mn", "Kp", "Mp", "Fsf", "Ffs"):
+        G, R = lay[name].to_scipy(), prims[name]
+        np.testing.assert_array_equal(G.indptr, R.indptr, err_msg=name)
+        np.testing.assert_array_equal(G.indices, R.indices, err_msg=name)
+        np.testing.assert_allclose(G.data, R.data, rtol=0, atol=1e-12 * np.abs(R.data).max(), err_msg=name)
+
+
 def test_cfg2_small_chain_matches_oracle(cuda):
     """Stage-by-stage parity on identical inputs (the coupled operator has
     cond ~ 2e12, so an unconverged ROM's output is rounding-sensitive to the

@@ -158,18 +158,99 @@ def test_blocked_pivoting_and_singular(cuda, force_blocked):
     assert out.info.cpu().tolist() == [r, r]
 
 
-@pytest.mark.parametrize("r,nf", [(1024, 6), (2048, 2)])
-def test_cfg5_full_size_sample(cuda, r, nf):
-    """BASELINE cfg5 at its full reduced orders: a seeded sample of the 100k grid
-    against the oracle (numpy zgesv), TF <= 1e-8 and |dSPL| <= 0.01 dB."""
+def _resonance_probes(w, n_res: int = 16, n_total: int = 64, seed: int = 0) -> np.ndarray:
+    """n_res grid frequencies right next to the workload's undamped
+    eigenfrequencies (the 100k grid point nearest each of n_res eigenfrequencies
+    spread over the band, and its neighbour) plus seeded random grid points."""
+    from paper_2310_04734_b200 import workloads
+    ef = workloads.cfg5_eigenfrequencies(w)
+    ef = ef[(ef > w.freqs[0]) & (ef < w.freqs[-1])]
+    pick = ef[np.linspace(0, len(ef) - 1, n_res // 2).astype(int)]
+    idx = np.clip(np.searchsorted(w.freqs, pick), 1, len(w.freqs) - 1)
+    res = np.unique(np.concatenate([idx - 1, idx]))
+    rng = np.random.default_rng(seed)
+    rest = rng.choice(np.setdiff1d(np.arange(len(w.freqs)), res), n_total - len(res), replace=False)
+    return np.sort(np.concatenate([res, rest]))
+
+
+@pytest.mark.parametrize("r", [256, 1024, 2048])
+def test_cfg5_full_size_64_frequencies(cuda, r):
+    """BASELINE cfg5 at its full reduced orders (the bench's headline kernel):
+    64 frequencies of the 100k grid, 16 of them straddling undamped
+    eigenfrequencies, against the oracle (numpy zgesv): TF <= 1e-8 pointwise
+    (mor.py:194-208) and |dSPL| <= 0.01 dB."""
     from paper_2310_04734_b200 import workloads
     w = workloads.cfg5(r=r, n_freq=100_000)
-    idx = np.random.default_rng(r).choice(100_000, nf, replace=False)
-    f = w.freqs[np.sort(idx)]
+    f = w.freqs[_resonance_probes(w, seed=r)]
     alpha = w.alpha(f)
     y_ref, spl_ref = omor.affine_sweep(w.prims, alpha, w.b, w.c_r)
     out = _run(cuda, w.prims, alpha, w.b, w.c_r)
+    assert int(out.info.abs().sum()) == 0
     _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+
+
+@pytest.mark.parametrize("r", [700, 1001, 1537, 1601])
+@pytest.mark.parametrize("s", [1, 3])
+def test_blocked_partial_outer_steps(cuda, force_blocked, r, s):
+    """Orders whose last outer step is partial: fewer panels than the 2-panel
+    (r >= 640) / 4-panel (r >= 1536) step holds, a last panel narrower than 64
+    and GEMM depths that are not multiples of 8 (greedy ROMs have any r)."""
+    rng = np.random.default_rng(r + 10 * s)
+    K, F, n_out = 3, 5, 20
+    X = rng.standard_normal((r, r)) + 1j * rng.standard_normal((r, r))
+    prims = np.stack([X @ X.conj().T / r + np.eye(r),
+                      0.1 * (rng.standard_normal((r, r)) + 1j * rng.standard_normal((r, r))),
+                      np.eye(r) + 0j])
+    alpha = np.stack([np.ones(F), 1j * rng.uniform(0.5, 2, F), -rng.uniform(0.5, 3, F) + 0j], 1)
+    b = rng.standard_normal((r, s)) + 1j * rng.standard_normal((r, s))
+    c_r = rng.standard_normal((n_out, r)) + 1j * rng.standard_normal((n_out, r))
+    y_ref, spl_ref = omor.affine_sweep(prims, alpha, b, c_r)
+    out = _run(cuda, prims, alpha, b, c_r, want_x=True)
+    assert int(out.info.abs().sum()) == 0
+    _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
+    x_ref = np.stack([np.linalg.solve(np.tensordot(alpha[i], prims, 1), b) for i in range(F)])
+    rel = np.abs(out.x.cpu().numpy() - x_ref).max() / np.abs(x_ref).max()
+    assert rel <= 1e-9, rel
+
+
+@pytest.mark.parametrize("force", [0, 1])
+def test_nan_column_sets_info_without_fault(cuda, force):
+    """A NaN pivot column is reported like a zero pivot (info = k + 1, as
+    LAPACK's izamax never selects it) instead of indexing shared memory with an
+    invalid row; the other frequencies of the launch are unaffected."""
+    import torch
+    from paper_2310_04734_b200 import _lib
+    r = 40
+    rng = np.random.default_rng(3)
+    P = (rng.standard_normal((1, r, r)) + 1j * rng.standard_normal((1, r, r))) + 8 * np.eye(r)
+    alpha = np.ones((3, 1), complex)
+    alpha[1, 0] = np.nan
+    b = rng.standard_normal((r, 1)) + 0j
+    c_r = np.eye(r, dtype=complex)
+    _lib.load().vb_set_sweep_path_override(force)
+    try:
+        out = _run(cuda, P, alpha, b, c_r)
+    finally:
+        _lib.load().vb_set_sweep_path_override(-1)
+    torch.cuda.synchronize()
+    info = out.info.cpu().tolist()
+    assert info[0] == 0 and info[2] == 0 and info[1] >= 1
+    y_ref, spl_ref = omor.affine_sweep(P, alpha[[0]], b, c_r)
+    _check(out.y[:1].cpu().numpy(), out.spl[:1].cpu().numpy(), y_ref, spl_ref)
+
+
+def test_sweep_on_side_stream_matches_current_stream(cuda):
+    """ReducedSweep(stream=s): the launch is ordered after the inputs produced
+    on the current stream and the results equal the default-stream sweep."""
+    import torch
+    from paper_2310_04734_b200 import sweep, workloads
+    w = workloads.cfg5(r=256, n_freq=300)
+    side = torch.cuda.Stream()
+    rs1 = sweep.ReducedSweep(w.prims, w.b, w.c_r, kinds=w.kinds)
+    rs2 = sweep.ReducedSweep(w.prims, w.b, w.c_r, kinds=w.kinds, stream=side)
+    y1, s1 = rs1.sweep(w.freqs)
+    y2, s2 = rs2.sweep(w.freqs)
+    assert np.array_equal(y1, y2) and np.array_equal(s1, s2)
 
 
 def test_cfg5_r1024_residuals_and_determinism(cuda):

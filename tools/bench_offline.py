@@ -27,7 +27,7 @@ def timed(fn, reps=3):
     return best
 
 
-def measure():
+def measure(peak_fp64=None):
     # a preceding blocked sweep leaves part of L2 set aside for its primitives
     _lib.check(_lib.load().vb_release_l2_persistence(), "vb_release_l2_persistence")
     dev = torch.device("cuda")
@@ -86,7 +86,8 @@ def measure():
     out["spmm_row_groups_build_s"] = __import__("time").perf_counter() - t0
     out["spmm_row_groups"] = rg.n_groups
     out["spmm_row_group_reuse"] = nnz / rg.n_union
-    peak_fp64 = _lib.probe_fp64_peak()
+    if peak_fp64 is None:
+        peak_fp64 = _lib.probe_fp64_peak()
     for k in (1, 2, 8, 32, 400):
         X = torch.randn(n, k, dtype=torch.complex128, device=dev)
         alg = nnz * 12 + 2 * n * k * 16
@@ -114,7 +115,7 @@ def measure():
     t = timed(lambda: linalg.zgemm("C", V, W))
     out["proj_zgemm_ms"] = t
     out["proj_zgemm_TFLOPs"] = 8 * n * 400 * 400 / (t * 1e-3) / 1e12
-    out["peak_fp64_TFLOPs"] = _lib.probe_fp64_peak()
+    out["peak_fp64_TFLOPs"] = peak_fp64
     out["proj_zgemm_frac"] = out["proj_zgemm_TFLOPs"] / out["peak_fp64_TFLOPs"]
     fom, lay = workloads.cfg3_model()
     fd = fom.factor(104.0)

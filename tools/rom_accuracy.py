@@ -1,0 +1,69 @@
+"""ROM accuracy at the reference's certification tolerance (tests/test_acceptance.py:
+272-305: eps_max <= tol = 1e-2 on frequencies disjoint from the candidate /
+expansion set): for cfg1, cfg2 and cfg3 build the window basis, sweep, and
+compare the ROM outputs with GPU full-order solves (residual <= 1e-10) on a
+disjoint grid (every `stride`-th grid frequency, expansion points excluded).
+Prints one JSON object per config."""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np
+import torch
+
+
+def eps_disjoint(fom, V, freqs, window, points, stride):
+    from paper_2310_04734_b200 import mor
+    rom = mor.ReducedModel(fom=fom, V=V, window=window)
+    ver = [f for f in freqs[::stride] if f not in set(points)]
+    y, _, _, info = rom.sweep(ver)
+    yr = y.cpu().numpy()
+    C = np.atleast_2d(fom.c_out)
+    worst, wf = 0.0, None
+    for i, f in enumerate(ver):
+        X = fom.factor(f).solve(fom.load_dev(f)).cpu().numpy()
+        yf = C @ X
+        _, e, _, _ = mor.relative_error(yf.ravel(), yr[i].ravel())
+        if e > worst:
+            worst, wf = e, f
+    return worst, wf, len(ver)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", nargs="*", default=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--stride", type=int, default=7)
+    ap.add_argument("--points", type=str, default="")
+    ap.add_argument("--moments", type=int, default=0)
+    a = ap.parse_args()
+    from paper_2310_04734_b200 import mor, workloads
+    for cfg in a.configs:
+        t0 = time.perf_counter()
+        if cfg == "cfg1":
+            fom, lay = workloads.cfg1_model(fdm=True)
+            kw = dict(second_order=True)
+            win = (20.0, 200.0)
+        elif cfg == "cfg2":
+            fom, lay = workloads.cfg2_model()
+            kw = {}
+            win = (20.0, 500.0)
+        else:
+            fom, lay = workloads.cfg3_model()
+            kw = dict(second_order=True, mimo=True)
+            win = (20.0, 300.0)
+        pts = [float(p) for p in a.points.split(",")] if a.points else list(lay["points"])
+        m = a.moments or lay["moments"]
+        V, _ = mor.krylov_basis(fom, pts, m, **kw)
+        torch.cuda.synchronize()
+        tb = time.perf_counter() - t0
+        e, wf, nv = eps_disjoint(fom, V, list(lay["freqs"]), win, pts, a.stride)
+        print(json.dumps({"config": cfg, "r": int(V.shape[1]), "points": pts, "moments": m, "eps_max": e,
+                          "at_hz": wf, "n_verify": nv, "build_s": tb}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
