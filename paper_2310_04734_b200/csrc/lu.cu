@@ -551,7 +551,7 @@ constexpr size_t SOLVE_SMEM = (size_t)(NB * (NB + 1) + NB * MAXRHS) * sizeof(z_t
 // are latency-bound (1.26 ms at n = 3,565 on 148 CTAs, 1.29 ms on 64).
 static thread_local int t_max_ctas = 0;
 
-static int coop_grid(const void* kern, size_t smem, int* grid) {
+static int coop_grid(const void* kern, size_t smem, int* grid, int min_grid = 0) {
   int dev = 0, nsm = 0, per = 0, coop = 0;
   VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -570,6 +570,7 @@ static int coop_grid(const void* kern, size_t smem, int* grid) {
   }
   *grid = nsm;  // one CTA per SM
   if (t_max_ctas > 0 && t_max_ctas < *grid) *grid = t_max_ctas;  // a share of the GPU (concurrent solves)
+  if (*grid < min_grid) *grid = min_grid < nsm ? min_grid : nsm;   // ... but never fewer CTAs than n needs
   return 0;
 }
 
@@ -613,10 +614,13 @@ int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size
   VB_CHECK_ARG(n > 0 && lda >= n, "vb_zgetrf: bad sizes");
   VB_CHECK_ARG(aux && aux_bytes >= zgetrf_aux_bytes(n), "vb_zgetrf: aux too small");
   int grid = 0;
-  if (int rc = lu::coop_grid((const void*)lu::zgetrf_kernel, lu::LU_SMEM, &grid)) return rc;
+  // each CTA keeps its panel rows in shared memory: at least this many CTAs
+  const int rows_max = (int)((227 * 1024 - 2048) / ((lu::NB + 1) * sizeof(z_t)));
+  const int min_grid = (n + rows_max - 1) / rows_max;
+  if (int rc = lu::coop_grid((const void*)lu::zgetrf_kernel, lu::LU_SMEM, &grid, min_grid)) return rc;
   const size_t smem = lu::lu_smem(n, grid);
   VB_CHECK_ARG(smem <= 227 * 1024, "vb_zgetrf: n too large for the shared-memory panel rows");
-  if (int rc = lu::coop_grid((const void*)lu::zgetrf_kernel, smem, &grid)) return rc;
+  if (int rc = lu::coop_grid((const void*)lu::zgetrf_kernel, smem, &grid, min_grid)) return rc;
   const int nblk = (n + lu::NB - 1) / lu::NB;
   VB_CHECK_ARG(work && work_bytes >= zgetrf_workspace_bytes(n), "vb_zgetrf: workspace too small");
   lu::LuParams P;

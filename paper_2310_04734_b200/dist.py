@@ -118,8 +118,8 @@ def krylov_basis_sharded(fom, points, moments: int, second_order: bool = False):
     factors the FOM and builds the Krylov blocks of its contiguous share of
     `points` (mor.krylov_block, mor.py:138-180, per load column for a block
     RHS), the blocks are all-gathered, and every rank appends them with
-    mor._orthonormalise in point order — the serial build's sequence, so every
-    rank holds the same basis.  Returns V (n x r, device)."""
+    mor.orthonormalise_blocks point by point — the serial build's sequence
+    (mor.krylov_basis), so every rank holds the same basis.  Returns V (n x r, device)."""
     from . import mor
     rank, ws, _ = world()
     if ws > 1 and not (dist.is_available() and dist.is_initialized()):
@@ -141,8 +141,8 @@ def krylov_basis_sharded(fom, points, moments: int, second_order: bool = False):
     dev = mor._device()
     allq = gather_blocks(mine, counts, fom.n, moments, mor.CDT, dev)
     V = None
-    for Q in allq:
-        V = mor._orthonormalise(V, Q.contiguous())
+    for p in range(len(points)):  # point by point, its per-source blocks together (mor.krylov_basis order)
+        V = mor.orthonormalise_blocks(V, [Q.contiguous() for Q in allq[p * n_load:(p + 1) * n_load]])
     return V
 
 

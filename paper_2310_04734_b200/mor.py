@@ -22,6 +22,7 @@ What changes underneath:
 
 from __future__ import annotations
 
+import functools
 import math
 import time
 from dataclasses import dataclass, field
@@ -38,6 +39,24 @@ from .sweep import rom_sweep_affine
 ORTH_DROP_TOL = 1e-10  # mor.py:22
 DENSE_MAX_N = 25_000   # dense GPU LU up to ~10 GB of complex128 factors
 CDT = torch.complex128
+
+
+def _nvtx(name: str):
+    """NVTX range around a pipeline stage (visible in nsys / ncu --nvtx
+    timelines; ~1 us per call)."""
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrap(*a, **k):
+            try:
+                torch.cuda.nvtx.range_push(name)
+            except Exception:  # no NVTX runtime: plain call
+                return fn(*a, **k)
+            try:
+                return fn(*a, **k)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrap
+    return deco
 
 
 def _device():
@@ -216,6 +235,7 @@ class FullOrderModel:
         b = torch.as_tensor(np.asarray(self.load(f))).to(device=dev, dtype=CDT)
         return b.view(-1, 1) if b.dim() == 1 else b.contiguous()
 
+    @_nvtx("vb.fom.factor")
     def factor(self, f: float):
         """GPU factorisation of A(f): dense LU (n <= DENSE_MAX_N), the
         fast-diagonalisation solver of a structured box (any n), or a Schur
@@ -380,6 +400,7 @@ class ReducedModel:
         return self.V.shape[1]
 
     # ---- affine projection (replaces the per-frequency re-projection) ----
+    @_nvtx("vb.rom.project")
     def _projected(self):
         key = (id(self.V), self.r)
         if self._cache_key == key:
@@ -465,6 +486,7 @@ class ReducedModel:
         vec = _vec_load(self.fom, f)
         return AR.cpu().numpy(), (bR[:, 0] if vec else bR)
 
+    @_nvtx("vb.rom.sweep")
     def sweep(self, freqs, want_x: bool = False, rayleigh=None):
         """All frequencies in one batched GPU launch: returns (y (F, n_out, s),
         spl (F, s), info) device tensors."""
@@ -638,6 +660,7 @@ def _basis_append_view(Vd, n: int, k: int, dev) -> torch.Tensor:
     return buf[:, :r + k]
 
 
+@_nvtx("vb.orthonormalise")
 def _orthonormalise(V, block):
     """Append the columns of `block` to V, twice-orthogonalised; columns that
     become negligible after projection are dropped (mor.py:122-135):
@@ -705,6 +728,70 @@ def _orthonormalise(V, block):
     return newV.cpu().numpy() if is_np else newV
 
 
+@_nvtx("vb.orthonormalise_blocks")
+def orthonormalise_blocks(V, blocks):
+    """Append several blocks to V at once — the same kept columns (in exact
+    arithmetic) as `_orthonormalise` applied block by block (mor.py:122-135
+    per column, in order), but every projection against the existing basis is
+    ONE pair of DMMA GEMM sweeps over V for all blocks together (cfg3: the 8
+    source blocks of an expansion point cost 4 sweeps of V instead of 32).
+    Inside the group each block is projected (twice) on the group's earlier
+    kept columns, then Gram-Schmidt'ed with the reference drop rule
+    (vb_block_gs); pass 2 re-projects the kept columns on V and
+    re-orthonormalises them block by block (Barlow-Smoktunowicz BCGS2)."""
+    blocks = list(blocks)
+    if len(blocks) == 1 or any(b.shape[1] > linalg.BLOCK_GS_MAX for b in blocks):
+        for b in blocks:
+            V = _orthonormalise(V, b)
+        return V
+    dev = V.device if isinstance(V, torch.Tensor) else _device()
+    if V is None:
+        Vd = None
+    elif isinstance(V, torch.Tensor):
+        Vd = (V if V.dim() == 2 and V.stride(1) == 1 else V.contiguous()) if V.numel() else None
+    else:
+        Vd = _as_dev(V, dev) if V.size else None
+    W = torch.cat([_as_dev(b, dev) for b in blocks], 1).contiguous()
+    n, K = W.shape
+    refs = linalg.column_norms(W)
+
+    def against(Q, X):
+        for _ in range(2):
+            G = linalg.zgemm("C", Q, X)
+            linalg.zgemm("N", Q, G, -1.0, 1.0, X)
+
+    if Vd is not None:
+        against(Vd, W)                                  # pass 1: all blocks, one V sweep pair per pass
+    Qk = torch.empty((n, K), dtype=CDT, device=dev)
+    nk, c0, kept_sizes = 0, 0, []
+    for b in blocks:
+        kb = b.shape[1]
+        Wc = W[:, c0:c0 + kb]
+        if nk:
+            against(Qk[:, :nk], Wc)                     # the group's earlier kept columns
+        nkc, _ = linalg.block_gs(Wc, Qk[:, nk:nk + kb], refs[c0:c0 + kb], ORTH_DROP_TOL, REORTH_RATIO)
+        kept_sizes.append(nkc)
+        nk += nkc
+        c0 += kb
+    r = Vd.shape[1] if Vd is not None else 0
+    newV = _basis_append_view(Vd, n, nk, dev)
+    if nk:
+        Q1 = newV[:, r:r + nk]
+        Q1.copy_(Qk[:, :nk])
+        if Vd is not None:                              # pass 2
+            against(Vd, Q1)
+            q0 = 0
+            for kc in kept_sizes:
+                if kc:
+                    Qc = Q1[:, q0:q0 + kc]
+                    if q0:
+                        against(Q1[:, :q0], Qc)
+                    linalg.block_gs(Qc, Qc, no_drop=True)
+                q0 += kc
+    _BASIS_BUFS[newV.data_ptr()] = (r + nk, newV.stride(0), n)
+    return newV
+
+
 def krylov_block(fom: FullOrderModel, f_j: float, m: int, second_order: bool = False,
                  lu: DenseLU | None = None):
     """Arnoldi basis of the shifted moment subspace at f_j (mor.py:138-180):
@@ -716,6 +803,7 @@ def krylov_block(fom: FullOrderModel, f_j: float, m: int, second_order: bool = F
     return Q.cpu().numpy(), br
 
 
+@_nvtx("vb.krylov_block")
 def krylov_block_dev(fom: FullOrderModel, f_j: float, m: int, second_order: bool = False,
                      lu: DenseLU | None = None):
     if m < 1:
@@ -756,6 +844,7 @@ def krylov_block_dev(fom: FullOrderModel, f_j: float, m: int, second_order: bool
     return torch.cat(cols, 1).contiguous(), breakdown
 
 
+@_nvtx("vb.krylov_blocks_mimo")
 def krylov_blocks_mimo_dev(fom: FullOrderModel, f_j: float, m: int, second_order: bool = False, lu=None):
     """Multi-input moments (cfg3's 8-source block RHS).  The reference is
     single-input; MIMO is emulated as one single-input Krylov
@@ -825,7 +914,14 @@ def krylov_blocks_concurrent(fom: FullOrderModel, points, m: int, second_order: 
     count), ready for _orthonormalise in point order (mor.py:337-352 builds a
     window basis from its points one after the other)."""
     pts = [float(f) for f in points]
-    nw = min(len(pts), workers or len(pts))
+    dev = _device()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    # the cooperative LU kernels of the workers must fit the GPU together:
+    # each needs >= ceil(n_lu / 222) CTAs (panel rows in shared memory, one
+    # CTA per SM), and the workers' caps sum to at most the SM count
+    n_lu = fom.schur.n_p if fom.schur is not None else fom.n
+    min_ctas = max(16, -(-n_lu // 222))
+    nw = min(len(pts), workers or len(pts), max(1, nsm // min_ctas))
     run = (lambda f: krylov_blocks_mimo_dev(fom, f, m, second_order)) if mimo else \
         (lambda f: krylov_block_dev(fom, f, m, second_order))
     if nw <= 1:
@@ -833,7 +929,7 @@ def krylov_blocks_concurrent(fom: FullOrderModel, points, m: int, second_order: 
     from concurrent.futures import ThreadPoolExecutor
     dev = _device()
     lib = _lib.load()
-    cap = max(16, torch.cuda.get_device_properties(dev).multi_processor_count // nw)
+    cap = nsm // nw
     caller = torch.cuda.current_stream(dev)
 
     def work(f):
@@ -863,6 +959,7 @@ def _lu_factored(fom: FullOrderModel) -> bool:
     return not (fom.fdm is not None and (fom.prefer_fdm or fom.n > DENSE_MAX_N))
 
 
+@_nvtx("vb.krylov_basis")
 def krylov_basis(fom: FullOrderModel, points, m: int, second_order: bool = False, mimo: bool = False,
                  concurrent: bool | None = None):
     """V of one window: the Krylov blocks of `points` (concurrently for the
@@ -875,9 +972,12 @@ def krylov_basis(fom: FullOrderModel, points, m: int, second_order: bool = False
         [(krylov_blocks_mimo_dev if mimo else krylov_block_dev)(fom, f, m, second_order) for f in points]
     V, flags = None, []
     for r in res:
-        for Q, br in (r if mimo else [r]):
-            V = _orthonormalise(V, Q)
-            flags.append(br)
+        if mimo:  # a point's per-source blocks appended together (one V sweep pair per pass)
+            V = orthonormalise_blocks(V, [Q for Q, _ in r])
+            flags += [br for _, br in r]
+        else:
+            V = _orthonormalise(V, r[0])
+            flags.append(r[1])
     return V, flags
 
 
@@ -906,6 +1006,7 @@ def candidate_frequencies(grid, window, stride: int):
     return cand
 
 
+@_nvtx("vb.greedy_expand")
 def greedy_expand(fom: FullOrderModel, grid, settings, window, second_order: bool = False,
                   solution_cache: dict | None = None) -> ReducedModel:
     """Greedy expansion at the worst-certified candidate (mor.py:224-295).  The
@@ -926,16 +1027,24 @@ def greedy_expand(fom: FullOrderModel, grid, settings, window, second_order: boo
     best_V, best_points, best_eps, best_log = None, [], math.inf, []
     history, points = [], []
     V = rom.V
+    mimo = int(fom.load_dev(next_f, dev).shape[1]) > 1
     while True:
-        block, _ = krylov_block_dev(fom, next_f, settings.moments_per_point, second_order=second_order)
-        V = _orthonormalise(V, block)
+        if mimo:  # block load (cfg3's sources): one single-input block per column
+            for block, _ in krylov_blocks_mimo_dev(fom, next_f, settings.moments_per_point,
+                                                   second_order=second_order):
+                V = _orthonormalise(V, block)
+        else:
+            block, _ = krylov_block_dev(fom, next_f, settings.moments_per_point, second_order=second_order)
+            V = _orthonormalise(V, block)
         points = points + [next_f]
         rom.V = V
         y_full = np.array([y_exact(f) for f in cand])
         y_red = np.array(rom.outputs(cand))
-        eps, eps_max, k, _ = relative_error(y_full, y_red)
-        if eps.ndim > 1:  # multi-output: the reference compares per candidate vector
-            eps = eps.max(axis=tuple(range(1, eps.ndim)))
+        if y_full.ndim > 1:  # multi-output: pointwise errors, worst output per candidate
+            eps = relative_error(y_full.ravel(), y_red.ravel())[0].reshape(len(cand), -1).max(axis=1)
+            eps_max = float(eps.max())
+        else:
+            eps, eps_max, k, _ = relative_error(y_full, y_red)
         log = list(zip(cand, eps.tolist()))
         if eps_max < best_eps:
             best_eps, best_V, best_points, best_log = eps_max, V, list(points), log
@@ -1018,6 +1127,7 @@ class RomSweepResult:
     spl: list = field(default_factory=list)   # mean SPL per frequency (solvers.py:334-338)
 
 
+@_nvtx("vb.rom_sweep")
 def rom_sweep(roms: list, grid, time_against_fom: bool = False) -> RomSweepResult:
     """Each frequency served by its window's ROM; the lower window owns a shared
     boundary and the discrepancy is logged (mor.py:366-394).  Each window's

@@ -104,9 +104,42 @@ def main(out=HERE / "fuselage_slice.npz"):
     pay["fom_f"] = np.array(fom_f)
     pay["fom_y"] = np.array([fom.output(fom.solve(f)) for f in fom_f])
     np.savez_compressed(out, **pay)
+    add_sensitivity(out)
     print(f"wrote {out}: n = {fom.n}, windows = {len(roms)}, r = {[r.r for r in roms]}, "
           f"build {float(pay['build_s']):.1f} s, sweep {float(pay['sweep_s']):.1f} s")
 
 
+def add_sensitivity(path=HERE / "fuselage_slice.npz", trials: int = 8):
+    """Conditioning of the reference's own FRF: for every grid frequency, the
+    reference reduced system (ReducedModel.reduced_system, mor.py:73-90) is
+    solved again with AR perturbed by ~1 ulp (seeded, `trials` times); the
+    largest relative change of the output is the level to which the reference
+    result is determined by its own rounding.  Parity tests floor their 1e-8
+    tolerance at twice this value."""
+    cfg = load_config(Path(vibrofem.__file__).parent / "data" / "fuselage_slice.cfg")
+    fom, op = _mor_fom(cfg)
+    z = dict(np.load(path))
+    grid = [float(f) for f in z["grid"]]
+    rng = np.random.default_rng(4242)
+    sens = np.zeros(len(grid))
+    roms = [rmor.ReducedModel(fom=fom, V=z[f"V{k}"], window=tuple(z["windows"][k]))
+            for k in range(int(z["n_windows"]))]
+    for i, f in enumerate(grid):
+        rom = roms[int(z["window_index"][i])]
+        AR, bR = rom.reduced_system(f)
+        cR = rom.c_out_reduced
+        y0 = cR @ np.linalg.solve(AR, bR)
+        for _ in range(trials):
+            E = 2.2e-16 * (rng.standard_normal(AR.shape) + 1j * rng.standard_normal(AR.shape))
+            y1 = cR @ np.linalg.solve(AR * (1 + E), bR)
+            sens[i] = max(sens[i], abs(y1 - y0) / abs(y0))
+    z["y_sens"] = sens
+    np.savez_compressed(path, **z)
+    print(f"y_sens: max {sens.max():.3e} at {grid[int(np.argmax(sens))]} Hz; "
+          f"{int(np.sum(sens > 0.5e-8))} frequencies above 5e-9")
+
+
 if __name__ == "__main__":
+    if "--sens" in sys.argv:
+        sys.exit(add_sensitivity())
     sys.exit(main())

@@ -92,19 +92,16 @@ def test_fdm_cfg3_scale_residual(cuda):
 
 
 def test_cfg3_mor_chain(cuda):
-    """MIMO Krylov (5 points x 10 moments x 8 sources) -> CGS2 union -> r <= 400
-    projection -> batched sweep; GPU sweep == oracle zgesv sweep on the same
-    reduced operator (TF <= 1e-8), ROM vs FDM full-order solves at sampled
-    frequencies."""
+    """MIMO Krylov (10 points x 5 moments x 8 sources) -> block CGS2 union ->
+    r = 400 projection -> batched sweep over all 1,121 frequencies; GPU sweep ==
+    oracle zgesv sweep on the same reduced operator (TF <= 1e-8), and the ROM
+    certified against FDM full-order solves at the reference tolerance."""
     import torch
     from paper_2310_04734_b200 import mor, workloads
     fom, lay = workloads.cfg3_model()
-    V = None
-    for f0 in lay["points"]:
-        for Q, _ in mor.krylov_blocks_mimo_dev(fom, f0, lay["moments"], second_order=True):
-            V = mor._orthonormalise(V, Q)
+    V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"], second_order=True, mimo=True)
     r = V.shape[1]
-    assert 300 <= r <= 400
+    assert r == 400
     G = V[:, :64].conj().T @ V[:, :64]
     assert torch.abs(G - torch.eye(64, dtype=G.dtype, device=G.device)).max().item() <= 1e-10
     rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 300.0))
@@ -121,18 +118,18 @@ def test_cfg3_mor_chain(cuda):
         worst = max(worst, e)
     assert worst <= 1e-8, worst
     np.testing.assert_allclose(spl.cpu().numpy(), splo, atol=0.01)
-    grid = grid[::40]
-    y = y[::40]
-    # ROM approximation vs the full-order model at sampled frequencies
+    # certification at the reference tolerance (tests/test_acceptance.py:
+    # 272-305, eps_max <= 1e-2) on every 7th grid frequency (disjoint from the
+    # expansion points), pointwise over all 50 receivers x 8 sources
     C = np.atleast_2d(fom.c_out)
     worst = 0.0
-    for i in (3, 10, 17):
+    ver = [i for i in range(0, len(grid), 7) if grid[i] not in lay["points"]]
+    for i in ver:
         f = grid[i]
         X = fom.factor(f).solve(fom.load_dev(f)).cpu().numpy()
-        yf = C @ X
-        _, e, _, _ = omor.relative_error(yf.ravel(), yg[0].ravel() if False else y.cpu().numpy()[i].ravel())
+        _, e, _, _ = omor.relative_error((C @ X).ravel(), yg[i].ravel())
         worst = max(worst, e)
-    assert worst <= 5e-2, worst
+    assert len(ver) >= 150 and worst <= 1e-2, worst
 
 
 def test_sharded_krylov_basis_world1_matches_serial(cuda):
@@ -144,8 +141,5 @@ def test_sharded_krylov_basis_world1_matches_serial(cuda):
     fom, _ = _small_box(cuda)
     pts = (80.0, 190.0, 300.0)
     V1 = vdist.krylov_basis_sharded(fom, pts, 4, second_order=True)
-    V2 = None
-    for f0 in pts:
-        for Q, _ in mor.krylov_blocks_mimo_dev(fom, f0, 4, second_order=True):
-            V2 = mor._orthonormalise(V2, Q)
+    V2, _ = mor.krylov_basis(fom, pts, 4, second_order=True, mimo=True)
     assert V1.shape == V2.shape and torch.equal(V1, V2)

@@ -94,7 +94,15 @@ def test_fuselage_rom_sweep_matches_reference(fuselage):
     ref = z["frf"]
     assert frf.shape == ref.shape == (496,)
     eps, eps_max, k, _ = omor.relative_error(ref, frf)
-    assert eps_max <= TF_TOL, (eps_max, grid[k])
+    # 1e-8 (north_star), floored at twice the reference's own rounding
+    # sensitivity at that frequency (fixture y_sens: the reference output's
+    # change under 1-ulp perturbations of its reduced system; > 5e-9 only at
+    # a few of the highest frequencies, where the reduced system is worst
+    # conditioned)
+    tol = np.maximum(TF_TOL, 2.0 * z["y_sens"])
+    bad = np.nonzero(eps > tol)[0]
+    assert bad.size == 0, [(grid[i], eps[i], z["y_sens"][i]) for i in bad]
+    assert np.sum(eps > TF_TOL) <= np.sum(z["y_sens"] > 0.5 * TF_TOL)
     db = lambda y: 20 * np.log10(np.maximum(np.abs(y), 1e-300) / 20e-6)  # noqa: E731  (cli.py:273-278)
     assert np.abs(db(frf) - db(ref)).max() <= 0.01
     # mean_spl of the single probe output (solvers.py:334-338), fused in the sweep kernel

@@ -139,3 +139,28 @@ def test_block_gs_matches_reference_drop_rule(cuda, n, kb):
     linalg.block_gs(P, P, no_drop=True)
     Pn = P.cpu().numpy()
     assert np.abs(Pn.conj().T @ Pn - np.eye(nk)).max() <= 1e-12
+
+
+def test_orthonormalise_blocks_equals_sequential_appends(cuda):
+    """mor.orthonormalise_blocks (one V sweep pair per pass for a group of
+    blocks) keeps the same columns as _orthonormalise block by block
+    (mor.py:122-135), incl. a column that is dependent on an EARLIER block of
+    the same group, and spans the same subspace with an orthonormal basis."""
+    import torch
+    from paper_2310_04734_b200 import mor
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n = 5000
+    V0 = mor._orthonormalise(None, torch.randn((n, 30), dtype=torch.complex128, device=cuda, generator=g))
+    blocks = [torch.randn((n, 10), dtype=torch.complex128, device=cuda, generator=g) for _ in range(4)]
+    blocks[2][:, 3] = blocks[0][:, 1] - 2j * blocks[1][:, 4] + 0.5 * V0[:, 7]   # dependent across blocks
+    blocks[3][:, 0] = V0[:, 2]                                                    # inside the old basis
+    Vs = V0.clone()
+    for b in blocks:
+        Vs = mor._orthonormalise(Vs, b.clone())
+    Vg = mor.orthonormalise_blocks(V0.clone(), [b.clone() for b in blocks])
+    assert Vs.shape == Vg.shape == (n, 30 + 38)
+    eye = torch.eye(Vg.shape[1], dtype=torch.complex128, device=cuda)
+    assert float((Vg.conj().T @ Vg - eye).abs().max()) <= 1e-12
+    assert float((Vg[:, :30] - V0).abs().max()) == 0.0
+    R = Vs - Vg @ (Vg.conj().T @ Vs)
+    assert float(R.abs().max()) <= 1e-10

@@ -128,7 +128,7 @@ def test_clamped_plate_fundamental(cuda):
 
 def test_cfg2_full_size_fom_and_rom(cuda):
     """n = 20,890 coupled non-symmetric system: GPU dense LU residual <= 1e-10
-    (host check), and a 6 x 10 ROM against full-order solves."""
+    (host check), and the r = 60 ROM certified against full-order solves."""
     import torch
     from paper_2310_04734_b200 import mor, workloads
     fom, lay = workloads.cfg2_model()
@@ -140,21 +140,22 @@ def test_cfg2_full_size_fom_and_rom(cuda):
     A = fom.operator(f)
     bh = lay["load"].host(f)
     assert np.linalg.norm(A @ x - bh) / np.linalg.norm(bh) <= 1e-10
-    V = None
-    for f0 in lay["points"]:
-        Q, _ = mor.krylov_block_dev(fom, f0, lay["moments"])
-        V = mor._orthonormalise(V, Q)
+    V, _ = mor.krylov_basis(fom, lay["points"], lay["moments"])
     assert V.shape[1] == 60
     rom = mor.ReducedModel(fom=fom, V=V, window=(20.0, 500.0))
     grid = list(lay["freqs"])
     res = mor.rom_sweep([rom], grid)
     assert len(res.spl) == 961
+    # certification at the reference tolerance on a grid disjoint from the
+    # expansion points (tests/test_acceptance.py:272-305: eps_max <= 1e-2),
+    # pointwise over all 50 receivers (mor.py:194-208)
+    ver = [i for i in range(0, len(grid), 9) if grid[i] not in lay["points"]]
     worst = 0.0
-    for i in (50, 400, 900):
+    for i in ver:
         yf = fom.output(fom.solve(grid[i]))
         _, e, _, _ = mor.relative_error(yf, res.frf[i])
         worst = max(worst, e)
-    assert worst <= 5e-2, worst
+    assert len(ver) >= 100 and worst <= 1e-2, worst
 
 
 def test_cfg2_schur_solver_matches_dense_lu(cuda):
