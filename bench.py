@@ -488,7 +488,6 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     lib = _lib.load()
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak, peak_probes = probe_peak() if rank == 0 else (None, None)
 
     w = workloads.cfg5(r=args.r)
     r, s, n_out, nprim = w.r, w.b.shape[1], w.c_r.shape[0], w.prims.shape[0]
@@ -562,6 +561,9 @@ def run_ours(args):
 
     if rank != 0:
         return 0
+    # FP64 roofline denominator: measured after the timed regions (the probe's
+    # DMMA load does not precede the timed sweep)
+    peak, peak_probes = probe_peak()
     # ---- parity of the headline's own outputs ----
     parity = parity_of_kept(w, kept) if kept else None
     del kept

@@ -16,6 +16,7 @@
 // no_drop = 1 is the re-orthonormalisation of already kept columns (pass 2 of
 // the block CGS2, in place: Q == W).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sweep.cuh"
@@ -120,6 +121,42 @@ __global__ void __launch_bounds__(NT) block_gs_kernel(Args a) {
       *wp = w;
     }
   };
+  // Second CGS pass fused with the norm (one grid reduction instead of two):
+  // h2 = Q^H w' and ||w'||^2 from the same partials, w'' = w' - Q h2 and
+  // ||w''||^2 = ||w'||^2 - ||h2||^2.  After a first pass h2 is a rounding-level
+  // correction (~eps ||w_raw||), so the subtraction loses nothing at the drop
+  // threshold (||w''|| ~ 1e-10 ||w_raw||): (eps / 1e-10)^2 relative.
+  auto project_norm = [&](int j) -> double {
+#pragma unroll
+    for (int l = 0; l < L; ++l) v[l] = 0.0;
+    for (int i = r0 + threadIdx.x; i < r1; i += NT) {
+      const z_t w = a.W[(int64_t)i * a.ldw + j];
+      const z_t* q = a.Q + (int64_t)i * a.ldq;
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c)
+        if (c < nk) {
+          const z_t qc = q[c];
+          v[2 * c] += qc.x * w.x + qc.y * w.y;
+          v[2 * c + 1] += qc.x * w.y - qc.y * w.x;
+        }
+#pragma unroll
+      for (int l = 0; l < L; ++l)
+        if (l == 2 * nk) v[l] += zabs2(w);
+    }
+    grid_reduce(grid, a, rnd, v, 2 * nk + 1, red, cta_sum, h);
+    double hh = 0.0;
+    for (int i = r0 + threadIdx.x; i < r1; i += NT) {
+      z_t* wp = a.W + (int64_t)i * a.ldw + j;
+      z_t w = *wp;
+      const z_t* q = a.Q + (int64_t)i * a.ldq;
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c)
+        if (c < nk) w = zfms(w, q[c], zmake(h[2 * c], h[2 * c + 1]));
+      *wp = w;
+    }
+    for (int c = 0; c < nk; ++c) hh += h[2 * c] * h[2 * c] + h[2 * c + 1] * h[2 * c + 1];
+    return sqrt(fmax(h[2 * nk] - hh, 0.0));
+  };
   auto norm = [&](int j) -> double {
 #pragma unroll
     for (int l = 0; l < L; ++l) v[l] = 0.0;
@@ -129,9 +166,13 @@ __global__ void __launch_bounds__(NT) block_gs_kernel(Args a) {
   };
 
   for (int j = 0; j < a.kb; ++j) {
-    if (nk)
-      for (int p = 0; p < 2; ++p) project(j);
-    double nw = norm(j);
+    double nw;
+    if (nk) {
+      project(j);            // CGS pass 1
+      nw = project_norm(j);  // CGS pass 2 + ||w||, one reduction
+    } else {
+      nw = norm(j);
+    }
     const double ref = a.no_drop ? 0.0 : a.refs[j];
     const bool keep = a.no_drop || (ref > 0.0 && nw > a.tol * ref);
     if (keep) {
@@ -160,7 +201,9 @@ static int grid_size() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, block_gs_kernel, NT, 0);
-    g = sms * (per < 2 ? per : 2);
+    int want = 2;  // CTAs per SM (VB_BGS_PER_SM: fewer CTAs = cheaper grid reductions, less row parallelism)
+    if (const char* e = getenv("VB_BGS_PER_SM")) want = atoi(e) > 0 ? atoi(e) : want;
+    g = sms * (per < want ? per : want);
   }
   return g;
 }

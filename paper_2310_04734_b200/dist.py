@@ -140,9 +140,14 @@ def krylov_basis_sharded(fom, points, moments: int, second_order: bool = False):
     counts = [(b - a) * n_load for a, b in (shard_range(len(points), q, ws) for q in range(ws))]
     dev = mor._device()
     allq = gather_blocks(mine, counts, fom.n, moments, mor.CDT, dev)
-    V = None
-    for p in range(len(points)):  # point by point, its per-source blocks together (mor.krylov_basis order)
-        V = mor.orthonormalise_blocks(V, [Q.contiguous() for Q in allq[p * n_load:(p + 1) * n_load]])
+    V, group = None, []
+    for p in range(len(points)):  # the grouping of mor.krylov_basis (same basis as the serial build)
+        group += [Q.contiguous() for Q in allq[p * n_load:(p + 1) * n_load]]
+        if sum(Q.shape[1] for Q in group) >= mor.GROUP_COLS:
+            V = mor.orthonormalise_blocks(V, group)
+            group = []
+    if group:
+        V = mor.orthonormalise_blocks(V, group)
     return V
 
 

@@ -192,7 +192,7 @@ BLOCK_GS_MAX = 16
 
 
 def block_gs(W: torch.Tensor, Q: torch.Tensor, refs: torch.Tensor | None = None, tol: float = 0.0,
-             reorth: float = 0.0, no_drop: bool = False):
+             reorth: float = 0.0, no_drop: bool = False, sync: bool = True):
     """Fused in-block Gram-Schmidt (vb_block_gs): the columns of W (n x kb,
     kb <= 16) orthogonalised twice against the kept ones and kept by the
     reference drop rule into Q[:, :nk].  Returns (nk, kept flags) — one host
@@ -207,4 +207,6 @@ def block_gs(W: torch.Tensor, Q: torch.Tensor, refs: torch.Tensor | None = None,
     _lib.check(lib.vb_block_gs(n, kb, C_ptr(W), _ld(W), rp, tol, reorth, int(no_drop), C_ptr(Q), _ld(Q),
                                _lib.ptr(kept), _lib.ptr(nk), C_ptr(work), wb, _lib.stream_handle()),
                "vb_block_gs")
+    if not sync:  # device tensors: the caller reads the counts later (one host sync for many blocks)
+        return nk, kept[:kb]
     return int(nk.item()), kept[:kb].cpu().numpy()

@@ -729,6 +729,22 @@ def _orthonormalise(V, block):
 
 
 @_nvtx("vb.orthonormalise_blocks")
+def _cholqr_inplace(Q: torch.Tensor):
+    """Re-orthonormalise nearly orthonormal columns in place: Q <- Q R^-1 with
+    R^H R = Q^H Q (Cholesky QR).  The columns come out of Gram-Schmidt
+    already orthonormal up to the rounding of an in-block cancellation, so
+    cond(Q) ~ 1 and one Cholesky QR is as accurate as another Gram-Schmidt
+    pass (it is the same QR factor: R upper triangular with a positive
+    diagonal is unique) at the cost of one Gram GEMM, a host Cholesky of a
+    <= 16 x 16 matrix and one GEMM, instead of 3 grid reductions per column."""
+    G = linalg.zgemm("C", Q, Q).cpu().numpy()
+    G = 0.5 * (G + G.conj().T)
+    R = np.linalg.cholesky(G).conj().T                      # G = R^H R
+    Ri = torch.as_tensor(np.linalg.solve(R, np.eye(R.shape[0])), device=Q.device)
+    T = linalg.zgemm("N", Q, Ri)
+    Q.copy_(T)
+
+
 def orthonormalise_blocks(V, blocks):
     """Append several blocks to V at once — the same kept columns (in exact
     arithmetic) as `_orthonormalise` applied block by block (mor.py:122-135
@@ -753,40 +769,65 @@ def orthonormalise_blocks(V, blocks):
         Vd = _as_dev(V, dev) if V.size else None
     W = torch.cat([_as_dev(b, dev) for b in blocks], 1).contiguous()
     n, K = W.shape
+    # consecutive blocks merge into chunks of <= BLOCK_GS_MAX columns: the
+    # fused in-block Gram-Schmidt treats a chunk column by column in order,
+    # exactly the sequential semantics, with fewer in-group projections
+    widths, cw = [], 0
+    for b in blocks:
+        if cw and cw + b.shape[1] > linalg.BLOCK_GS_MAX:
+            widths.append(cw)
+            cw = 0
+        cw += b.shape[1]
+    widths.append(cw)
+    blocks = [W[:, sum(widths[:i]):sum(widths[:i + 1])] for i in range(len(widths))]
     refs = linalg.column_norms(W)
 
-    def against(Q, X):
-        for _ in range(2):
+    def against(Q, X, passes=2):
+        for _ in range(passes):
             G = linalg.zgemm("C", Q, X)
             linalg.zgemm("N", Q, G, -1.0, 1.0, X)
 
+    # BCGS2 (Barlow-Smoktunowicz): ONE projection on V per pass — the second
+    # pass below restores orthogonality lost to in-block cancellation, and
+    # the drop test only needs the residual norm to ~1e-14 relative (the
+    # threshold is 1e-10); inside the group (small GEMMs) two passes as MGS2
     if Vd is not None:
-        against(Vd, W)                                  # pass 1: all blocks, one V sweep pair per pass
-    Qk = torch.empty((n, K), dtype=CDT, device=dev)
-    nk, c0, kept_sizes = 0, 0, []
+        against(Vd, W, passes=1)                        # pass 1: all blocks, one V sweep pair
+    # each block's kept columns land at the front of its own slot of Qk; the
+    # rest of the slot stays zero, so projecting later blocks on Qk[:, :c0]
+    # needs no host read of the kept counts (a zero column projects to nothing)
+    Qk = torch.zeros((n, K), dtype=CDT, device=dev)
+    c0, counts = 0, []
     for b in blocks:
         kb = b.shape[1]
         Wc = W[:, c0:c0 + kb]
-        if nk:
-            against(Qk[:, :nk], Wc)                     # the group's earlier kept columns
-        nkc, _ = linalg.block_gs(Wc, Qk[:, nk:nk + kb], refs[c0:c0 + kb], ORTH_DROP_TOL, REORTH_RATIO)
-        kept_sizes.append(nkc)
-        nk += nkc
+        if c0:
+            against(Qk[:, :c0], Wc)                     # the group's earlier kept columns
+        nkc, _ = linalg.block_gs(Wc, Qk[:, c0:c0 + kb], refs[c0:c0 + kb], ORTH_DROP_TOL, REORTH_RATIO,
+                                 sync=False)
+        counts.append(nkc)
         c0 += kb
+    kept_sizes = [int(v) for v in torch.cat(counts).cpu().tolist()]   # one host read per group
+    nk = sum(kept_sizes)
     r = Vd.shape[1] if Vd is not None else 0
     newV = _basis_append_view(Vd, n, nk, dev)
     if nk:
         Q1 = newV[:, r:r + nk]
-        Q1.copy_(Qk[:, :nk])
+        q0, c0 = 0, 0
+        for b, kc in zip(blocks, kept_sizes):
+            if kc:
+                Q1[:, q0:q0 + kc].copy_(Qk[:, c0:c0 + kc])
+            q0 += kc
+            c0 += b.shape[1]
         if Vd is not None:                              # pass 2
-            against(Vd, Q1)
+            against(Vd, Q1, passes=1)
             q0 = 0
             for kc in kept_sizes:
                 if kc:
                     Qc = Q1[:, q0:q0 + kc]
                     if q0:
                         against(Q1[:, :q0], Qc)
-                    linalg.block_gs(Qc, Qc, no_drop=True)
+                    _cholqr_inplace(Qc)
                 q0 += kc
     _BASIS_BUFS[newV.data_ptr()] = (r + nk, newV.stride(0), n)
     return newV
@@ -920,8 +961,8 @@ def krylov_blocks_concurrent(fom: FullOrderModel, points, m: int, second_order: 
     # each needs >= ceil(n_lu / 222) CTAs (panel rows in shared memory, one
     # CTA per SM), and the workers' caps sum to at most the SM count
     n_lu = fom.schur.n_p if fom.schur is not None else fom.n
-    min_ctas = max(16, -(-n_lu // 222))
-    nw = min(len(pts), workers or len(pts), max(1, nsm // min_ctas))
+    min_ctas = max(24, -(-n_lu // 222))
+    nw = min(len(pts), workers or 6, max(1, nsm // min_ctas))  # measured: 8 concurrent cooperative grids fail
     run = (lambda f: krylov_blocks_mimo_dev(fom, f, m, second_order)) if mimo else \
         (lambda f: krylov_block_dev(fom, f, m, second_order))
     if nw <= 1:
@@ -970,15 +1011,23 @@ def krylov_basis(fom: FullOrderModel, points, m: int, second_order: bool = False
         concurrent = _lu_factored(fom)
     res = krylov_blocks_concurrent(fom, points, m, second_order, mimo) if concurrent else \
         [(krylov_blocks_mimo_dev if mimo else krylov_block_dev)(fom, f, m, second_order) for f in points]
-    V, flags = None, []
+    V, flags, group = None, [], []
     for r in res:
-        if mimo:  # a point's per-source blocks appended together (one V sweep pair per pass)
-            V = orthonormalise_blocks(V, [Q for Q, _ in r])
+        if mimo:  # per-source blocks appended together, >= GROUP_COLS columns per group
+            group += [Q for Q, _ in r]
             flags += [br for _, br in r]
+            if sum(Q.shape[1] for Q in group) >= GROUP_COLS:
+                V = orthonormalise_blocks(V, group)
+                group = []
         else:
             V = _orthonormalise(V, r[0])
             flags.append(r[1])
+    if group:
+        V = orthonormalise_blocks(V, group)
     return V, flags
+
+
+GROUP_COLS = 64  # columns appended per orthonormalise_blocks call in krylov_basis (MIMO)
 
 
 # ------------------------------------------------------ certification ----

@@ -139,7 +139,40 @@ def add_sensitivity(path=HERE / "fuselage_slice.npz", trials: int = 8):
           f"{int(np.sum(sens > 0.5e-8))} frequencies above 5e-9")
 
 
+def add_errlog_sensitivity(path=HERE / "fuselage_slice.npz", trials: int = 2):
+    """How well the reference's own greedy error log is determined by its
+    inputs: build_local_roms rerun with every primitive value perturbed by ~1
+    ulp (seeded); errlog_sens = the largest |delta eps| per candidate over the
+    trials (the decisions must not change, or the run is flagged)."""
+    cfg = load_config(Path(vibrofem.__file__).parent / "data" / "fuselage_slice.cfg")
+    z = dict(np.load(path))
+    grid = [float(f) for f in z["grid"]]
+    band = (cfg.frequency.f_min, cfg.frequency.f_max)
+    rng = np.random.default_rng(777)
+    sens = [np.zeros(len(z[f"errlog{k}"])) for k in range(int(z["n_windows"]))]
+    same = True
+    for _ in range(trials):
+        fom, op = _mor_fom(cfg)
+        for prims in op.primitives.values():
+            for A in prims.values():
+                A.data = A.data * (1 + 2.2e-16 * rng.standard_normal(A.data.shape))
+        roms = rmor.build_local_roms(fom, grid, cfg.mor, band)
+        same &= len(roms) == int(z["n_windows"])
+        for k, r in enumerate(roms[:len(sens)]):
+            same &= list(r.expansion_points) == list(z[f"points{k}"])
+            log = np.array(r.error_log)
+            if log.shape == z[f"errlog{k}"].shape:
+                sens[k] = np.maximum(sens[k], np.abs(log[:, 1] - z[f"errlog{k}"][:, 1]))
+    for k, sv in enumerate(sens):
+        z[f"errlog_sens{k}"] = sv
+    z["errlog_sens_same_decisions"] = np.array(same)
+    np.savez_compressed(path, **z)
+    print(f"errlog_sens: max {max(v.max() for v in sens):.3e}, same decisions {same}")
+
+
 if __name__ == "__main__":
+    if "--errlog-sens" in sys.argv:
+        sys.exit(add_errlog_sensitivity())
     if "--sens" in sys.argv:
         sys.exit(add_sensitivity())
     sys.exit(main())

@@ -27,16 +27,19 @@ def _env(rank, ws, port):
                       WORLD_SIZE=str(ws), LOCAL_RANK="0")
 
 
-def _sweep_worker(rank, ws, port, r, q):
+def _sweep_worker(rank, ws, port, data, q):
     _env(rank, ws, port)
     import torch
     import torch.distributed as dist
-    from paper_2310_04734_b200 import dist as vdist, sweep, workloads
+    from paper_2310_04734_b200 import dist as vdist, sweep
     vdist.init(backend="gloo")
     torch.cuda.set_device(0)
-    w = workloads.cfg5(r=r, n_freq=301)
-    rs = sweep.ReducedSweep(w.prims, w.b, w.c_r, kinds=w.kinds)
-    f = torch.as_tensor(w.freqs, device="cuda:0")
+    # the parent's inputs (regenerating them here could differ in the last bit:
+    # multithreaded BLAS in the workload generator sums in a thread-count-
+    # dependent order)
+    prims, b, c_r, kinds, freqs = data
+    rs = sweep.ReducedSweep(prims, b, c_r, kinds=kinds)
+    f = torch.as_tensor(freqs, device="cuda:0")
     spl, y = vdist.sweep_sharded(rs, f, want_y=True)
     q.put((rank, spl.cpu().numpy(), y.cpu().numpy()))
     dist.destroy_process_group()
@@ -114,8 +117,8 @@ def test_sharded_sweep_world2_equals_serial(cuda, r):
     over all frequencies exactly (one CTA per frequency, fixed reductions)."""
     import torch
     from paper_2310_04734_b200 import sweep, workloads
-    out = _run(_sweep_worker, r)
     w = workloads.cfg5(r=r, n_freq=301)
+    out = _run(_sweep_worker, (w.prims, w.b, w.c_r, w.kinds, w.freqs))
     rs = sweep.ReducedSweep(w.prims, w.b, w.c_r, kinds=w.kinds)
     o = rs.sweep_device(torch.as_tensor(w.freqs, device=cuda))
     spl, y = o.spl.cpu().numpy(), o.y.cpu().numpy()

@@ -160,3 +160,52 @@ def test_fuselage_reduced_system_matches_literal_projection(fuselage):
         AR, bR = rom.reduced_system(f)
         assert np.abs(AR - AR_ref).max() <= 1e-10 * np.abs(AR_ref).max()
         assert np.abs(bR - V.conj().T @ load(f)).max() <= 1e-12 * np.abs(bR).max()
+
+
+class _MorSettings:
+    """fuselage_slice.cfg `mor:` block (config.py:172-184 MorSettings)."""
+    tol, max_points, moments_per_point, candidate_stride, windows = 1e-2, 20, 4, 4, "auto"
+
+
+def test_fuselage_build_local_roms_matches_reference(fuselage):
+    """The whole offline phase on the reference's benchmark through the drop-in:
+    build_local_roms (mor.py:322-353: greedy expansion, auto windows) takes the
+    reference's decisions — same windows, expansion points in order, r, flags
+    and candidate error log — with every FOM solve a GPU LU and every
+    candidate ROM evaluation batched (reference: 183.6 s on 8 cores)."""
+    import time
+    import torch
+    from paper_2310_04734_b200 import mor
+    z, fom, _ = fuselage
+    grid = [float(f) for f in z["grid"]]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    roms = mor.build_local_roms(fom, grid, _MorSettings(), (grid[0], grid[-1]))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    print(f"GPU build_local_roms on the reference benchmark: {dt:.2f} s "
+          f"(reference {float(z['build_s']):.1f} s)")
+    assert len(roms) == int(z["n_windows"])
+    for k, r in enumerate(roms):
+        assert tuple(r.window) == tuple(z["windows"][k])
+        assert [float(p) for p in r.expansion_points] == [float(p) for p in z[f"points{k}"]]
+        assert r.r == z[f"V{k}"].shape[1]
+        assert [r.converged, r.stalled, r.budget_exhausted] == list(z[f"flags{k}"])
+        log, ref = np.array(r.error_log), z[f"errlog{k}"]
+        np.testing.assert_array_equal(log[:, 0], ref[:, 0])
+        # eps = |y_full - y_rom| / |y_full| is the ROM's own truncation error;
+        # the late Krylov columns of a window are nearly dependent moment
+        # vectors, determined by the data only to ~1e-7 (DESIGN §4.5), so two
+        # correct builds (splu + MGS2 vs GPU LU + CGS2) give ROMs whose errors
+        # agree to a fraction of eps (measured <= 22 %), not to rounding.  The
+        # reference is itself this sensitive: rebuilt with its primitives
+        # perturbed by 1 ulp it changes its error log by up to 2.9e-3 and
+        # even its expansion points (fixture errlog_sens0,
+        # errlog_sens_same_decisions = False).  The decisions above are what
+        # the candidate errors drive, and they are identical; the sweep with
+        # the reference's OWN bases matches to 1e-8
+        # (test_fuselage_rom_sweep_matches_reference).
+        assert not bool(z["errlog_sens_same_decisions"])
+        d = np.abs(log[:, 1] - ref[:, 1])
+        bad = d > 5e-8 + 0.3 * np.abs(ref[:, 1])
+        assert not bad.any(), list(zip(ref[bad, 0], ref[bad, 1], d[bad]))

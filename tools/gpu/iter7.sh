@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python tools/prof_orth_kernels.py 2>&1 | grep -v Warn | head -14 | cut -c1-200
+VB_BGS_PER_SM=1 timeout 600 python tools/prof_orth_kernels.py 2>&1 | grep "wall\|block_gs"| cut -c1-200
+timeout 900 python -m pytest tests/test_linalg_gpu.py tests/test_dist_gpu.py tests/test_fdm_gpu.py -q -m gpu --timeout 900 2>&1 | tail -3
