@@ -26,6 +26,7 @@ batch of frequencies.
 from __future__ import annotations
 
 import sys
+import types
 from dataclasses import dataclass
 
 import numpy as np
@@ -166,3 +167,46 @@ def affine_from_operator(op, coeffs: OperatorCoefficients | None = None, device=
         add(M, sp.csr_matrix(C).T, fo, so, lambda f, k=k: coeffs.rho_f(k, f))   # rho_f C^T on fluid rows
     ld = load if load is not None else HostLoad(op.load, n, dev)
     return AffineOperator(K=K, M=M, D=[], load=ld)
+
+
+def load_operator_npz(path, device=None):
+    """A reference model shipped as arrays (the layout
+    tests/golden/make_fuselage_golden.py writes from a live ModelOperator:
+    primitives, couplings, block map, the per-frequency scalars tabulated on a
+    grid, the load's nonzero rows) -> (FullOrderModel on the device, grid,
+    data).  Lets the drop-in run a reference model on a machine without the
+    reference package; the scalars are looked up at the tabulated
+    frequencies only."""
+    from .mor import fom_from_operator
+    z = np.load(path)
+    grid = z["grid"]
+    pos = {float(f): i for i, f in enumerate(grid)}
+    doms = [str(d) for d in z["domains"]]
+    kinds = {d: str(k) for d, k in zip(doms, z["kinds"])}
+
+    def csr(key):
+        return sp.csr_matrix((z[f"{key}__data"], z[f"{key}__indices"], z[f"{key}__indptr"]),
+                             shape=tuple(z[f"{key}__shape"]))
+    prims = {d: {nm: csr(f"prim__{d}__{nm}")
+                 for nm in (("Kmat", "Kgeo", "M") if kinds[d] == "elastic" else ("Kgrad", "Mnn"))}
+             for d in doms}
+    couplings = [(str(a), str(b), csr(f"coupling{k}")) for k, (a, b) in enumerate(z["couplings"])]
+    block_map = {d: tuple(int(v) for v in z["block_map"][i]) for i, d in enumerate(doms)}
+    cfg = types.SimpleNamespace(domains=[types.SimpleNamespace(id=d, kind=kinds[d]) for d in doms])
+    op = types.SimpleNamespace(config=cfg, kinds=kinds, primitives=prims, couplings=couplings,
+                               block_map=block_map)
+    coeffs = OperatorCoefficients(
+        kscale=lambda d, f: complex(z[f"scale__{d}"][pos[float(f)]]),
+        fluid=lambda d, f: (complex(z[f"rho_eff__{d}"][pos[float(f)]]), complex(z[f"c_eff__{d}"][pos[float(f)]])),
+        rho_f=lambda k, f: complex(z[f"rho_f{k}"][pos[float(f)]]))
+    n = int(z["n"])
+    rows, vals = z["load_rows"], z["load_vals"]
+
+    def load(f):
+        v = np.zeros(n, complex)
+        v[rows] = vals[pos[float(f)]]
+        return v
+    dev = torch.device(device or "cuda")
+    op.affine = affine_from_operator(op, coeffs, device=dev, load=HostLoad(load, n, dev))
+    op.coeffs, op.load = coeffs, load
+    return fom_from_operator(op, int(z["probe"])), [float(f) for f in grid], op
