@@ -193,6 +193,12 @@ int vb_rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, con
                const vb_complex* X, int64_t ldx, vb_complex* Y, int64_t ldy, vb_complex alpha, vb_complex beta,
                void* stream);
 
+/* Row-group SpMM kernel choice (default 0 = by column count): 1 forces the
+ * FP64-tensor-core (DMMA) form over the padded dense 8-row blocks, 2 the
+ * padding-free CUDA-core form (per-slot 8-bit membership masks).  Process-
+ * wide; also read from the VB_RG_MODE environment variable at first use. */
+void vb_set_rg_spmm_mode(int mode);
+
 /* In-block Gram-Schmidt of a new basis block (vibrofem/mor.py:122-135, the
  * column loop of _orthonormalise after the block is projected on V), fused
  * into one cooperative kernel: for each column j of W (n x kb, kb <= 16),

@@ -36,6 +36,7 @@ _SIGS = {
     "vb_debug_phase_cycles": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
     "vb_rom_sweep_path": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "vb_set_sweep_path_override": (None, [C.c_int]),
+    "vb_set_rg_spmm_mode": (None, [C.c_int]),
     "vb_probe_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.c_void_p]),
     "vb_rom_sweep_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64]),
     "vb_csr_pattern_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),

@@ -48,6 +48,8 @@ int vb_rom_sweep_path(int r, int nprim, int s, int n_out) { return vb::sweep_pat
 
 void vb_set_sweep_path_override(int path) { vb::sweep_set_override(path); }
 
+void vb_set_rg_spmm_mode(int mode) { vb::set_rg_mode(mode); }
+
 int vb_probe_fp64_peak(double* tflops_host, void* stream) {
   VB_CHECK_ARG(tflops_host != nullptr, "vb_probe_fp64_peak: null output");
   return vb::probe_fp64_peak(tflops_host, (cudaStream_t)stream);

@@ -23,6 +23,7 @@
 #include "mma.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace vb {
@@ -151,6 +152,10 @@ __global__ void __launch_bounds__(256) spmm_subwarp_kernel(int n_rows, const int
 
 // ------------------------------------------------------------- row groups ---
 constexpr int RG = 8;  // rows per group
+#ifndef VB_RG_CC_MIN_K
+#define VB_RG_CC_MIN_K 1000000  // set after measuring (tools/bench_offline.py, VB_RG_MODE)
+#endif
+constexpr int RG_CC_MIN_K = VB_RG_CC_MIN_K;
 
 // Row-group SpMM on the FP64 tensor cores.  One warp per group: the group's
 // rows x leader columns form a dense 8 x nu real block (absent slots +0.0),
@@ -290,6 +295,103 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
   }
 }
 
+// Row-group SpMM on the CUDA cores (FP64 FMA pipe), padding-free: the DMMA
+// kernel above multiplies the whole dense 8 x nu block (on hex27 only 512 of
+// its 1,000 slots are nonzero), so it is bound by the FP64 pipe on padding.
+// Here each lane owns one complex column of a CW-wide chunk and keeps the 8
+// member rows' accumulators in registers; for every union column j of the
+// group the X element is loaded ONCE and fused into exactly the member rows
+// present at j (the group's 8-bit mask: the same for all lanes of the
+// sub-warp, so the branches do not diverge).  Per nonzero: 2 DFMA; per union
+// slot: one 16-byte X load per lane plus uniform (broadcast) loads of the
+// slot's column id, mask and 8 values.  G = 32 / CW groups per warp.
+template <int CW>
+__global__ void __launch_bounds__(256) rg_cc_kernel(int n_groups, const int32_t* __restrict__ g_leader,
+                                                    const int32_t* __restrict__ g_rows,
+                                                    const int32_t* __restrict__ g_uoff,
+                                                    const int32_t* __restrict__ indptr,
+                                                    const int32_t* __restrict__ indices,
+                                                    const uint8_t* __restrict__ masks,
+                                                    const double* __restrict__ gvals, int k,
+                                                    const z_t* __restrict__ X, int64_t ldx, z_t* __restrict__ Y,
+                                                    int64_t ldy, z_t alpha, z_t beta) {
+  constexpr int G = 32 / CW;
+  const int lane = threadIdx.x & 31, sub = lane / CW, c = lane % CW;
+  const int64_t g = ((int64_t)blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G + sub;
+  const int col = blockIdx.x * CW + c;
+  const bool cv = col < k;
+  if (g >= n_groups) return;
+  const int leader = __ldg(g_leader + g);
+  const int ub = leader >= 0 ? __ldg(indptr + leader) : 0;
+  const int nu = leader >= 0 ? __ldg(indptr + leader + 1) - ub : 0;
+  const int64_t uo = __ldg(g_uoff + g);
+  const int32_t* cols = indices + ub;
+  const uint8_t* mk = masks + uo;
+  const double2* vv = reinterpret_cast<const double2*>(gvals + uo * RG);
+  double ar[RG], ai[RG];
+#pragma unroll
+  for (int i = 0; i < RG; ++i) ar[i] = ai[i] = 0.0;
+  const z_t* Xc = X + (cv ? col : 0);
+  constexpr int U = 4;  // union slots in flight
+  int j = 0;
+  for (; j + U <= nu; j += U) {
+    z_t x[U];
+    unsigned m[U];
+    double2 v[U][RG / 2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x[u] = cv ? __ldg(Xc + (int64_t)__ldg(cols + j + u) * ldx) : zmake(0.0, 0.0);
+      m[u] = __ldg(mk + j + u);
+#pragma unroll
+      for (int h = 0; h < RG / 2; ++h) v[u][h] = __ldg(vv + (int64_t)(j + u) * (RG / 2) + h);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < RG; ++i)
+        if ((m[u] >> i) & 1u) {
+          const double a = (i & 1) ? v[u][i >> 1].y : v[u][i >> 1].x;
+          ar[i] = fma(a, x[u].x, ar[i]);
+          ai[i] = fma(a, x[u].y, ai[i]);
+        }
+  }
+  for (; j < nu; ++j) {
+    const z_t x = cv ? __ldg(Xc + (int64_t)__ldg(cols + j) * ldx) : zmake(0.0, 0.0);
+    const unsigned m = __ldg(mk + j);
+#pragma unroll
+    for (int i = 0; i < RG; ++i)
+      if ((m >> i) & 1u) {
+        const double a = __ldg(gvals + (uo + j) * RG + i);
+        ar[i] = fma(a, x.x, ar[i]);
+        ai[i] = fma(a, x.y, ai[i]);
+      }
+  }
+  if (!cv) return;
+  const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+#pragma unroll
+  for (int i = 0; i < RG; ++i) {
+    const int row = __ldg(g_rows + g * RG + i);
+    if (row < 0) continue;
+    z_t out = zmul(alpha, zmake(ar[i], ai[i]));
+    if (!beta0) out = zfma(out, beta, Y[(int64_t)row * ldy + col]);
+    Y[(int64_t)row * ldy + col] = out;
+  }
+}
+
+template <int CW>
+static int rg_cc_launch(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
+                        const int32_t* indptr, const int32_t* indices, const uint8_t* masks, const double* gvals,
+                        int k, const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta,
+                        cudaStream_t st) {
+  constexpr int G = 32 / CW, WARPS = 8;
+  const int64_t warps = ((int64_t)n_groups + G - 1) / G;
+  const dim3 grid((unsigned)((k + CW - 1) / CW), (unsigned)((warps + WARPS - 1) / WARPS));
+  rg_cc_kernel<CW><<<grid, 32 * WARPS, 0, st>>>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals,
+                                                k, X, ldx, Y, ldy, alpha, beta);
+  VB_LAUNCHED("rg_cc_kernel");
+  return 0;
+}
+
 __global__ void rg_gather_values_kernel(int64_t n_slots, const int32_t* __restrict__ vmap,
                                         const double* __restrict__ vals, double* __restrict__ gvals) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_slots;
@@ -396,10 +498,31 @@ static int rg_launch(int n_groups, const int32_t* g_leader, const int32_t* g_row
   return 0;
 }
 
+static int g_rg_mode = -1;  // 0 auto, 1 tensor-core (DMMA) groups, 2 CUDA-core groups
+
+void set_rg_mode(int m) { g_rg_mode = m; }
+
+static int rg_mode() {
+  if (g_rg_mode < 0) {
+    const char* e = getenv("VB_RG_MODE");
+    g_rg_mode = e ? atoi(e) : 0;
+  }
+  return g_rg_mode;
+}
+
 int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
-            const int32_t* indptr, const int32_t* indices, const uint8_t* /*masks*/, const double* gvals, int k,
+            const int32_t* indptr, const int32_t* indices, const uint8_t* masks, const double* gvals, int k,
             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
   if (n_groups <= 0 || k <= 0) return 0;
+  const int mode = rg_mode();
+  if (masks && (mode == 2 || (mode == 0 && k >= RG_CC_MIN_K))) {
+    if (k <= 8) return rg_cc_launch<8>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals, k, X, ldx,
+                                       Y, ldy, alpha, beta, st);
+    if (k <= 16) return rg_cc_launch<16>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals, k, X,
+                                         ldx, Y, ldy, alpha, beta, st);
+    return rg_cc_launch<32>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals, k, X, ldx, Y, ldy,
+                            alpha, beta, st);
+  }
 #ifndef VB_RG_S
 #define VB_RG_S 3
 #endif

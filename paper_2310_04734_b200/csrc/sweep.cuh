@@ -17,6 +17,7 @@ int sweep_small_launch(int r, int nprim, int s, int n_out, int64_t F, const z_t*
 
 int sweep_path(int r, int nprim, int s, int n_out);
 void sweep_set_override(int path);
+void set_rg_mode(int mode);
 void sweep_set_l2_persistence(int enable);
 int sweep_release_l2_persistence();
 size_t sweep_workspace_bytes(int r, int nprim, int s, int n_out, int64_t F);

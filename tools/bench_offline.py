@@ -91,10 +91,12 @@ def measure(peak_fp64=None):
     for k in (1, 2, 8, 32, 400):
         X = torch.randn(n, k, dtype=torch.complex128, device=dev)
         alg = nnz * 12 + 2 * n * k * 16
-        for tag, path in (("", "auto"), ("_csr", "csr")):
+        for tag, path, mode in (("", "auto", 0), ("_csr", "csr", 0), ("_rgtc", "rg", 1), ("_rgcc", "rg", 2)):
             if tag and k < 8:
                 continue
+            lib.vb_set_rg_spmm_mode(mode)
             t = timed(lambda: linalg.spmm(Kg, X, path=path))
+            lib.vb_set_rg_spmm_mode(0)
             out[f"spmm{tag}_k{k}_ms"] = t
             out[f"spmm{tag}_k{k}_GBps"] = alg / (t * 1e-3) / 1e9
             out[f"spmm{tag}_k{k}_frac_hbm"] = out[f"spmm{tag}_k{k}_GBps"] / peak_hbm
