@@ -344,24 +344,24 @@ def offline_measurements(w, peak_fp64=None):
         mor.rom_sweep([rom], list(lay["freqs"]))
         return fom, V
 
-    def timed_twice(fn):
-        """(first run, warm run) wall clock incl. host orchestration; the warm
-        run is the reported number (first runs include one-off module loading,
-        thread-pool and allocator warm-up)."""
+    def timed_twice(fn, reps: int = 5):
+        """(first run, median of the next `reps` runs) wall clock incl. host
+        orchestration; the median is the reported number (first runs include
+        one-off module loading, thread-pool and allocator warm-up)."""
         ts = []
-        for _ in range(2):
+        for _ in range(1 + reps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res = fn()
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
-        return ts, res
+        return (ts[0], float(np.median(ts[1:]))), res
 
     (t1, t1w), (_, V) = timed_twice(lambda: cfg1(False))
     out["cfg1_pipeline_s"], out["cfg1_pipeline_first_s"], out["cfg1_r"] = t1w, t1, int(V.shape[1])
     out["cfg1_note"] = ("GPU assembly + 4 dense LUs (n=4641, the 4 expansion points concurrent on their own "
                         "streams) + 2nd-order Krylov + CGS2 + projection + 181-frequency sweep + SPL, wall clock "
-                        "incl. host orchestration (warm run; *_first_s = first run in the process)")
+                        "incl. host orchestration (median of 5 warm runs; *_first_s = first run in the process)")
     (t1, t1w), (_, V) = timed_twice(lambda: cfg1(True))
     out["cfg1_pipeline_fdm_s"], out["cfg1_pipeline_fdm_first_s"], out["cfg1_fdm_r"] = t1w, t1, int(V.shape[1])
     (t2, t2w), (fom, V) = timed_twice(cfg2)

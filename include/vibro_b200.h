@@ -265,6 +265,13 @@ int vb_zgetrf(int n, vb_complex* A, int64_t lda, int32_t* ipiv, int32_t* info, v
  * concurrently (e.g. the expansion points of one Krylov basis). */
 void vb_set_lu_max_ctas(int n);
 
+/* Whole-GPU LU variant (default 1, also env VB_LU_LOOKAHEAD at first use):
+ * 1 = look-ahead kernel (a group of panel CTAs factors panel k+1 while the
+ * other CTAs run the trailing update of panel k) where the order and grid
+ * allow it, 0 = one grid barrier per panel column for all CTAs.  Same pivots
+ * and results either way. */
+void vb_set_lu_lookahead(int on);
+
 /* X = A^-1 B from vb_zgetrf factors (1 <= nrhs <= 16; B may alias X).
  * Replaces SuperLU `lu.solve` (vibrofem/mor.py:49, 156, 166, 175). */
 size_t vb_zgetrs_workspace_bytes(int n, int nrhs);

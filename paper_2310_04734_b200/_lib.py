@@ -91,6 +91,7 @@ _SIGS = {
     "vb_zgetrf": (C.c_int, [C.c_int, _z, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                             C.c_void_p, C.c_size_t, C.c_void_p]),
     "vb_set_lu_max_ctas": (None, [C.c_int]),
+    "vb_set_lu_lookahead": (None, [C.c_int]),
     "vb_zgetrs_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "vb_zgetrs": (C.c_int, [C.c_int, C.c_int, _z, C.c_int64, C.c_void_p, _z, C.c_int64, _z, C.c_int64,
                             C.c_void_p, C.c_size_t, C.c_void_p]),

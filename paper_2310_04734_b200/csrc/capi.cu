@@ -236,6 +236,8 @@ int vb_zgetrf(int n, vb_complex* A, int64_t lda, int32_t* ipiv, int32_t* info, v
 
 void vb_set_lu_max_ctas(int n) { vb::set_lu_max_ctas(n); }
 
+void vb_set_lu_lookahead(int on) { vb::set_lu_lookahead(on); }
+
 size_t vb_zgetrs_workspace_bytes(int n, int nrhs) { return (size_t)n * nrhs * sizeof(vb_complex); }
 
 int vb_zgetrs(int n, int nrhs, const vb_complex* LU, int64_t lda, const void* aux, const vb_complex* B,

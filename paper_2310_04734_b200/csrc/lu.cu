@@ -82,6 +82,8 @@ struct __align__(64) LuParams {
   z_t* rowj;      // [2][NB]
   z_t* Linv;      // [nblk][NB][NB]
   z_t* Uinv;      // [nblk][NB][NB]
+  int npan;       // look-ahead kernel: CTAs [0, npan) factor the panels
+  unsigned* bar;  // look-ahead kernel: the panel CTAs' barrier counter (zeroed before launch)
 };
 
 __device__ __forceinline__ void row_range(int n, int& lo, int& hi) {
@@ -313,6 +315,258 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(const __grid_constant__ L
     LU_MARK(3);
   }
   // final permutation from the interchange sequence (LAPACK ipiv semantics)
+  if (c == 0) {
+    for (int i = tid; i < n; i += NT) P.perm[i] = i;
+    __syncthreads();
+    if (tid == 0)
+      for (int j = 0; j < n; ++j) {
+        const int p = P.ipiv[j];
+        if (p != j) {
+          const int t = P.perm[j];
+          P.perm[j] = P.perm[p];
+          P.perm[p] = t;
+        }
+      }
+  }
+}
+
+// ------------------------------------------------- look-ahead variant ---
+// The same right-looking LU, but the next panel's factorisation (a chain of
+// 64 pivot steps, latency-bound) overlaps the current trailing update
+// (throughput-bound DMMA GEMM): CTAs [0, npan) are PANEL CTAs, the rest GEMM
+// CTAs.  Per panel k:
+//   all CTAs    : interchanges of panel k on the other columns, U12 = L11^-1 A12,
+//                 then the update of panel k+1's 64 columns only (look-ahead);
+//   panel CTAs  : factor panel k+1 (its rows [k0', n) re-split over the panel
+//                 CTAs, held in shared memory; one barrier among the panel
+//                 CTAs per column instead of a grid barrier);
+//   GEMM CTAs   : meanwhile A22 -= L21 U12 on the columns right of panel k+1.
+// Panel k+1 only touches its own 64 columns and the GEMM only the columns to
+// their right, both reading the finished L21 / U12 of panel k; the row
+// interchanges of panel k+1 reach the other columns after the grid barrier,
+// as in LAPACK.  Same pivots (izamax order, lowest row on ties) and the same
+// arithmetic per element as zgetrf_kernel.
+
+// Barrier among the npan panel CTAs: monotone counter in global memory.
+__device__ __forceinline__ void panel_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+// Factor panel [k0, k0 + nb) by the npan panel CTAs (pc = this CTA's index).
+__device__ void la_factor_panel(const LuParams& P, int k0, int nb, int pc, unsigned& epoch, z_t* Ps, z_t* s_prow,
+                                z_t* s_rowj, double* rv, int* ri, int& s_piv, int& s_idx, double& s_val) {
+  const int n = P.n, np = P.npan, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t lda = P.lda;
+  z_t* A = P.A;
+  const int kend = k0 + nb;
+  const int rpc = (n - k0 + np - 1) / np;
+  const int plo = k0 + pc * rpc, phi = min(n, plo + rpc), pn = max(0, phi - plo);
+  constexpr int LP = NB + 1;
+  for (int e = tid; e < pn * nb; e += NT) {
+    const int i = e / nb, t = e - i * nb;
+    Ps[i * LP + t] = __ldcg(A + (int64_t)(plo + i) * lda + k0 + t);
+  }
+  __syncthreads();
+  for (int j = k0; j < kend; ++j) {
+    const int buf = j & 1, jj = j - k0;
+    double v = -1.0;
+    int pi = 0x7fffffff;
+    for (int i = max(plo, j) + tid; i < phi; i += NT) {
+      const double a = zabs1(Ps[(i - plo) * LP + jj]);
+      if (a > v) { v = a; pi = i; }
+    }
+    warp_argmax(v, pi);
+    if (lane == 0) { rv[warp] = v; ri[warp] = pi; }
+    __syncthreads();
+    if (warp == 0) {
+      v = lane < NT / 32 ? rv[lane] : -1.0;
+      pi = lane < NT / 32 ? ri[lane] : 0x7fffffff;
+      warp_argmax(v, pi);
+      if (lane == 0) { s_val = v; s_idx = pi; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      P.pval[buf * np + pc] = s_val;
+      P.pidx[buf * np + pc] = s_idx;
+    }
+    if (s_val >= 0.0)
+      for (int t = tid; t < nb; t += NT) P.prow[((int64_t)buf * np + pc) * NB + t] = Ps[(s_idx - plo) * LP + t];
+    if (j >= plo && j < phi)
+      for (int t = tid; t < nb; t += NT) P.rowj[buf * NB + t] = Ps[(j - plo) * LP + t];
+    panel_barrier(P.bar, ++epoch * (unsigned)np);
+    if (warp == 0) {
+      double bv = -1.0;
+      int bi = 0x7fffffff, bc = 0;
+      for (int q = lane; q < np; q += 32) {
+        const double pv = __ldcg(P.pval + buf * np + q);
+        const int px = __ldcg(P.pidx + buf * np + q);
+        if (pv > bv || (pv == bv && px < bi)) { bv = pv; bi = px; bc = q; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; bc = oc; }
+      }
+      if (lane == 0) {
+        s_val = bv;
+        s_piv = bv > 0.0 ? bi : -1;
+        s_idx = bc;
+      }
+    }
+    __syncthreads();
+    const int p = s_piv;
+    if (p < 0) {  // exactly singular column (LAPACK: INFO = j+1, no interchange)
+      if (pc == 0 && tid == 0) {
+        if (*P.info == 0) *P.info = j + 1;
+        P.ipiv[j] = j;
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int t = tid; t < nb; t += NT) {
+      s_prow[t] = __ldcg(P.prow + ((int64_t)buf * np + s_idx) * NB + t);
+      s_rowj[t] = __ldcg(P.rowj + buf * NB + t);
+    }
+    if (pc == 0 && tid == 0) P.ipiv[j] = p;
+    __syncthreads();
+    const z_t pinv = zrecip(s_prow[jj]);
+    if (p != j && j >= plo && j < phi)
+      for (int t = tid; t < nb; t += NT) Ps[(j - plo) * LP + t] = s_prow[t];
+    const int r0 = max(plo, j + 1);
+    const int nrows = phi - r0, ncols = nb - jj - 1;
+    if (nrows > 0) {
+      for (int i = r0 + tid; i < phi; i += NT) {
+        const z_t aij = (i == p) ? s_rowj[jj] : Ps[(i - plo) * LP + jj];
+        Ps[(i - plo) * LP + jj] = zmul(aij, pinv);
+      }
+      if (p != j && p >= r0 && p < phi)
+        for (int t = tid; t < nb; t += NT)
+          if (t != jj) Ps[(p - plo) * LP + t] = s_rowj[t];
+      __syncthreads();
+      if (ncols > 0)
+        for (int e = tid; e < nrows * ncols; e += NT) {
+          const int ii = e / ncols, t = jj + 1 + (e - ii * ncols);
+          z_t* row = Ps + (r0 - plo + ii) * LP;
+          row[t] = zfms(row[t], row[jj], s_prow[t]);
+        }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < pn * nb; e += NT) {
+    const int i = e / nb, t = e - i * nb;
+    A[(int64_t)(plo + i) * lda + k0 + t] = Ps[i * LP + t];
+  }
+  __threadfence();
+}
+
+__global__ void __launch_bounds__(NT, 1) zgetrf_la_kernel(const __grid_constant__ LuParams P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(1024) char smem_raw[];
+  double2* smem = (double2*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ GemmT::Bars bars;
+  __shared__ z_t s_prow[NB];
+  __shared__ z_t s_rowj[NB];
+  __shared__ double rv[NT / 32];
+  __shared__ int ri[NT / 32];
+  __shared__ int s_piv, s_idx;
+  __shared__ double s_val;
+  const int n = P.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, c = blockIdx.x, np = P.npan;
+  const bool pan = c < np;
+  const int64_t lda = P.lda;
+  z_t* A = P.A;
+  unsigned epoch = 0;
+  if (c == 0 && tid == 0) *P.info = 0;
+  grid.sync();
+  if (pan) la_factor_panel(P, 0, min(NB, n), c, epoch, smem, s_prow, s_rowj, rv, ri, s_piv, s_idx, s_val);
+  for (int k0 = 0; k0 < n; k0 += NB) {
+    const int nb = min(NB, n - k0), kend = k0 + nb;
+    grid.sync();  // panel k factored and written back; the previous trailing update done
+    // ------------------------------------------------------------ swaps
+    {
+      const int64_t ncol = (int64_t)n - nb;
+      for (int64_t q = (int64_t)c * NT + tid; q < ncol; q += (int64_t)G * NT) {
+        const int col = q < k0 ? (int)q : (int)(q + nb);
+        for (int j = k0; j < kend; ++j) {
+          const int p = __ldcg(P.ipiv + j);
+          if (p != j) {
+            const z_t t = __ldcg(A + (int64_t)j * lda + col);
+            A[(int64_t)j * lda + col] = __ldcg(A + (int64_t)p * lda + col);
+            A[(int64_t)p * lda + col] = t;
+          }
+        }
+      }
+    }
+    grid.sync();
+    // ------------------------------------------------------------ TRSM
+    {
+      z_t* Li = smem;
+      z_t* Bs = smem + NB * LDL;
+      const int nblk = k0 / NB;
+      const int nstrips = (n - kend + TRS_N - 1) / TRS_N;
+      if (nstrips > c || c == 0) {
+        load_diag_block<true>(A, lda, k0, nb, Li);
+        if (c == 0)
+          for (int e = tid; e < NB * NB; e += NT) P.Linv[(int64_t)nblk * NB * NB + e] = Li[(e / NB) * LDL + e % NB];
+        const int wm = warp >> 1, wn = warp & 1;
+        for (int st = c; st < nstrips; st += G) {
+          const int cs = kend + st * TRS_N, ncol = min(TRS_N, n - cs);
+          for (int e = tid; e < NB * TRS_N; e += NT) {
+            const int i = e / TRS_N, jx = e - i * TRS_N;
+            Bs[i * LDS_B + jx] = (i < nb && jx < ncol) ? __ldcg(A + (int64_t)(k0 + i) * lda + cs + jx) : zmake(0.0, 0.0);
+          }
+          __syncthreads();
+          double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+          blk::warp_cmma<2, 2, false>(cr, ci, Li + (wm * 16) * LDL, LDL, Bs + wn * 16, LDS_B, (nb + 3) >> 2);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+              for (int vv = 0; vv < 2; ++vv) {
+                const int row = wm * 16 + a * 8 + (lane >> 2);
+                const int col = wn * 16 + b * 8 + 2 * (lane & 3) + vv;
+                if (row < nb && col < ncol) A[(int64_t)(k0 + row) * lda + cs + col] = zmake(cr[a][b][vv], ci[a][b][vv]);
+              }
+          __syncthreads();
+        }
+      }
+      if (c == (G > 1 ? 1 : 0)) {
+        __syncthreads();
+        load_diag_block<false>(A, lda, k0, nb, Li);
+        for (int e = tid; e < NB * NB; e += NT) P.Uinv[(int64_t)nblk * NB * NB + e] = Li[(e / NB) * LDL + e % NB];
+      }
+    }
+    grid.sync();
+    if (kend >= n) break;
+    // ------------------------------------------------ look-ahead update
+    const int nbn = min(NB, n - kend);
+    GemmT::run(&P.maps, A, lda, kend, k0, k0, kend, n - kend, nbn, nb, (char*)smem, &bars, c, G);
+    grid.sync();
+    // ------------------------- panel k+1 (panel CTAs) || A22 update (GEMM CTAs)
+    if (pan) {
+      la_factor_panel(P, kend, nbn, c, epoch, smem, s_prow, s_rowj, rv, ri, s_piv, s_idx, s_val);
+    } else if (kend + nbn < n) {
+      GemmT::run(&P.maps, A, lda, kend, k0, k0, kend + nbn, n - kend, n - kend - nbn, nb, (char*)smem, &bars,
+                 c - np, G - np);
+    }
+  }
+  grid.sync();
   if (c == 0) {
     for (int i = tid; i < n; i += NT) P.perm[i] = i;
     __syncthreads();
@@ -598,7 +852,7 @@ size_t zgetrf_workspace_bytes(int n) {
   b += 2 * (size_t)grid * lu::NB * sizeof(z_t);
   b += 2 * (size_t)lu::NB * sizeof(z_t);
   b += 2 * (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
-  return b + 1024;
+  return b + 1024 + 256;  // + the look-ahead kernel's panel barrier counter
 }
 
 // Factor data kept for the solves: Linv/Uinv of the diagonal blocks and the
@@ -609,10 +863,72 @@ size_t zgetrf_aux_bytes(int n) {
   return 2 * (size_t)nblk * lu::NB * lu::NB * sizeof(z_t) + (size_t)n * sizeof(int) + 256;
 }
 
+static int zgetrf_la(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size_t aux_bytes, void* work,
+                     size_t work_bytes, cudaStream_t st, int np) {
+  const size_t prow_bytes = (size_t)((n + np - 1) / np) * (lu::NB + 1) * sizeof(z_t) + 1024;
+  const size_t smem = prow_bytes > lu::LU_SMEM ? prow_bytes : lu::LU_SMEM;
+  VB_CHECK_ARG(smem <= 227 * 1024, "vb_zgetrf: n too large for the look-ahead panel rows");
+  int grid = 0;
+  if (int rc = lu::coop_grid((const void*)lu::zgetrf_la_kernel, smem, &grid)) return rc;
+  VB_CHECK_ARG(np < grid, "vb_zgetrf: too few CTAs for the look-ahead split");
+  const int nblk = (n + lu::NB - 1) / lu::NB;
+  VB_CHECK_ARG(work && work_bytes >= zgetrf_workspace_bytes(n), "vb_zgetrf: workspace too small");
+  lu::LuParams P;
+  P.n = n; P.A = A; P.lda = lda; P.ipiv = ipiv; P.info = info_dev; P.npan = np;
+  char* w = (char*)work;
+  P.pval = (double*)w; w += 2 * (size_t)grid * sizeof(double);
+  P.pidx = (int*)w; w += 2 * (size_t)grid * sizeof(int);
+  w = (char*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  P.prow = (z_t*)w; w += 2 * (size_t)grid * lu::NB * sizeof(z_t);
+  P.rowj = (z_t*)w; w += 2 * (size_t)lu::NB * sizeof(z_t);
+  w = (char*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  P.bar = (unsigned*)w;
+  VB_CUDA(cudaMemsetAsync(P.bar, 0, sizeof(unsigned), st));
+  char* x = (char*)aux;
+  P.Linv = (z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
+  P.Uinv = (z_t*)x; x += (size_t)nblk * lu::NB * lu::NB * sizeof(z_t);
+  P.perm = (int*)x;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * lda, (cuuint64_t)n, 1};
+    const cuuint64_t strides[2] = {(cuuint64_t)lda * 16, (cuuint64_t)lda * 16 * n};
+    const cuuint32_t box64[3] = {16, 64, 1}, box8[3] = {16, 8, 1}, es[3] = {1, 1, 1};
+    if (int rc = tma_encode_map(&P.maps.a64, A, dims, strides, box64, es)) return rc;
+    if (int rc = tma_encode_map(&P.maps.b8, A, dims, strides, box8, es)) return rc;
+  }
+  void* args[] = {&P};
+  VB_CUDA(cudaLaunchCooperativeKernel((const void*)lu::zgetrf_la_kernel, grid, lu::NT, args, smem, st));
+  VB_LAUNCHED("zgetrf_la_kernel");
+  return 0;
+}
+
+static int g_lu_lookahead = -1;  // -1: VB_LU_LOOKAHEAD env (default on), 0 off, 1 on
+void set_lu_lookahead(int on) { g_lu_lookahead = on; }
+
+// Panel CTAs of the look-ahead kernel for order n (0: use the plain kernel):
+// the panel rows [k0, n) split over them must fit shared memory, and they
+// must leave most of the grid to the trailing update.
+static int la_panel_ctas(int n, int grid) {
+  if (g_lu_lookahead < 0) {
+    const char* e = getenv("VB_LU_LOOKAHEAD");
+    g_lu_lookahead = e ? atoi(e) : 1;
+  }
+  if (!g_lu_lookahead || grid < 48) return 0;
+  const int rows_max = 200;
+  int np = (n + rows_max - 1) / rows_max;
+  if (np < 16) np = 16;
+  return np <= grid / 3 ? np : 0;
+}
+
 int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size_t aux_bytes, void* work,
            size_t work_bytes, cudaStream_t st) {
   VB_CHECK_ARG(n > 0 && lda >= n, "vb_zgetrf: bad sizes");
   VB_CHECK_ARG(aux && aux_bytes >= zgetrf_aux_bytes(n), "vb_zgetrf: aux too small");
+  {
+    int gfull = 0;
+    if (int rc = lu::coop_grid((const void*)lu::zgetrf_la_kernel, lu::LU_SMEM, &gfull)) return rc;
+    const int np = la_panel_ctas(n, gfull);
+    if (np > 0) return zgetrf_la(n, A, lda, ipiv, info_dev, aux, aux_bytes, work, work_bytes, st, np);
+  }
   int grid = 0;
   // each CTA keeps its panel rows in shared memory: at least this many CTAs
   const int rows_max = (int)((227 * 1024 - 2048) / ((lu::NB + 1) * sizeof(z_t)));

@@ -99,6 +99,7 @@ size_t zgetrf_aux_bytes(int n);
 int zgetrf(int n, z_t* A, int64_t lda, int* ipiv, int* info_dev, void* aux, size_t aux_bytes, void* work,
            size_t work_bytes, cudaStream_t st);
 void set_lu_max_ctas(int n);
+void set_lu_lookahead(int on);
 int zgetrs(int n, int nrhs, const z_t* LU, int64_t lda, const void* aux, const z_t* B, int64_t ldb,
            z_t* X, int64_t ldx, void* work, size_t work_bytes, cudaStream_t st);
 

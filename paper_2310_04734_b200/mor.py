@@ -1009,8 +1009,28 @@ def krylov_basis(fom: FullOrderModel, points, m: int, second_order: bool = False
     usage).  Returns (V, breakdown flags per point (per source with mimo))."""
     if concurrent is None:
         concurrent = _lu_factored(fom)
-    res = krylov_blocks_concurrent(fom, points, m, second_order, mimo) if concurrent else \
-        [(krylov_blocks_mimo_dev if mimo else krylov_block_dev)(fom, f, m, second_order) for f in points]
+    if concurrent:
+        res = krylov_blocks_concurrent(fom, points, m, second_order, mimo)
+    else:
+        # FDM-type factorisations are host eigen-decompositions of the 1-D
+        # pencils + uploads: prepared on a host thread one point ahead, so the
+        # host work of point p+1 overlaps the GPU moment solves of point p
+        from concurrent.futures import ThreadPoolExecutor
+        run = krylov_blocks_mimo_dev if mimo else krylov_block_dev
+        dev = _device()
+        pts = list(points)
+        if _lu_factored(fom):  # dense LU factors are GBs: no look-ahead
+            res = [run(fom, f, m, second_order) for f in pts]
+        else:
+            with ThreadPoolExecutor(1, thread_name_prefix="vb_factor") as ex:
+                def prep(f):
+                    torch.cuda.set_device(dev)
+                    return fom.factor(f)
+                res, nxt = [], ex.submit(prep, pts[0]) if pts else None
+                for i, f in enumerate(pts):
+                    lu = nxt.result()
+                    nxt = ex.submit(prep, pts[i + 1]) if i + 1 < len(pts) else None
+                    res.append(run(fom, f, m, second_order, lu=lu))
     V, flags, group = None, [], []
     for r in res:
         if mimo:  # per-source blocks appended together, >= GROUP_COLS columns per group

@@ -60,5 +60,13 @@ linalg.block_gs(Qb[:, :nk].contiguous(), Qb[:, :nk].contiguous(), no_drop=True)
 # concurrent expansion points (streams + thread-local LU CTA cap)
 fom1, lay1 = workloads.cfg1_model(box=(0, 0, 0, 1.0, 0.8, 0.6), ne=(3, 3, 2), n_rec=4)
 V1, _ = mor.krylov_basis(fom1, [40.0, 90.0, 150.0], 3, second_order=True, concurrent=True)
+# round 2: GPU GMRES (batched CGS kernels) on a per-element-impedance box,
+# grouped appends (chunked block GS + Cholesky QR), CUDA-core row groups
+fom3, lay3 = workloads.cfg3_model(box=(0, 0, 0, 1.0, 0.8, 0.6), ne=(4, 3, 3), n_src=2, n_rec=5, per_element_z=True)
+xg = fom3.factor(140.0).solve(fom3.load_dev(140.0))
+V3, _ = mor.krylov_basis(fom3, [60.0, 200.0], 3, second_order=True, mimo=True)
+lib.vb_set_rg_spmm_mode(2)
+linalg.spmm(Ad, torch.randn(Ad.n, 40, dtype=torch.complex128, device=dev), 1.0, 0.0, None, path="rg")
+lib.vb_set_rg_spmm_mode(0)
 torch.cuda.synchronize()
-print("sanitize run ok", V.shape, V1.shape, float(np.abs(y).max()))
+print("sanitize run ok", V.shape, V1.shape, V3.shape, float(np.abs(y).max()))
