@@ -493,23 +493,11 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_la_kernel(const __grid_constant_
   for (int k0 = 0; k0 < n; k0 += NB) {
     const int nb = min(NB, n - k0), kend = k0 + nb;
     grid.sync();  // panel k factored and written back; the previous trailing update done
-    // ------------------------------------------------------------ swaps
-    {
-      const int64_t ncol = (int64_t)n - nb;
-      for (int64_t q = (int64_t)c * NT + tid; q < ncol; q += (int64_t)G * NT) {
-        const int col = q < k0 ? (int)q : (int)(q + nb);
-        for (int j = k0; j < kend; ++j) {
-          const int p = __ldcg(P.ipiv + j);
-          if (p != j) {
-            const z_t t = __ldcg(A + (int64_t)j * lda + col);
-            A[(int64_t)j * lda + col] = __ldcg(A + (int64_t)p * lda + col);
-            A[(int64_t)p * lda + col] = t;
-          }
-        }
-      }
-    }
-    grid.sync();
-    // ------------------------------------------------------------ TRSM
+    // ------------------------------------------------ swaps + TRSM
+    // each U12 strip applies panel k's interchanges to its own columns first
+    // (whole column: rows j in the panel and their pivot rows below), so no
+    // separate swap phase and grid barrier; the columns left of the panel
+    // (finished L factors) are swapped off the critical path by the GEMM CTAs
     {
       z_t* Li = smem;
       z_t* Bs = smem + NB * LDL;
@@ -522,6 +510,16 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_la_kernel(const __grid_constant_
         const int wm = warp >> 1, wn = warp & 1;
         for (int st = c; st < nstrips; st += G) {
           const int cs = kend + st * TRS_N, ncol = min(TRS_N, n - cs);
+          for (int col = cs + tid; col < cs + ncol; col += NT)
+            for (int j = k0; j < kend; ++j) {
+              const int p = __ldcg(P.ipiv + j);
+              if (p != j) {
+                const z_t t = __ldcg(A + (int64_t)j * lda + col);
+                A[(int64_t)j * lda + col] = __ldcg(A + (int64_t)p * lda + col);
+                A[(int64_t)p * lda + col] = t;
+              }
+            }
+          __syncthreads();
           for (int e = tid; e < NB * TRS_N; e += NT) {
             const int i = e / TRS_N, jx = e - i * TRS_N;
             Bs[i * LDS_B + jx] = (i < nb && jx < ncol) ? __ldcg(A + (int64_t)(k0 + i) * lda + cs + jx) : zmake(0.0, 0.0);
@@ -553,7 +551,18 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_la_kernel(const __grid_constant_
       }
     }
     grid.sync();
-    if (kend >= n) break;
+    if (kend >= n) {  // last panel: its interchanges on the L columns left of it, by everyone
+      for (int64_t col = (int64_t)c * NT + tid; col < k0; col += (int64_t)G * NT)
+        for (int j = k0; j < kend; ++j) {
+          const int p = __ldcg(P.ipiv + j);
+          if (p != j) {
+            const z_t t = __ldcg(A + (int64_t)j * lda + col);
+            A[(int64_t)j * lda + col] = __ldcg(A + (int64_t)p * lda + col);
+            A[(int64_t)p * lda + col] = t;
+          }
+        }
+      break;
+    }
     // ------------------------------------------------ look-ahead update
     const int nbn = min(NB, n - kend);
     GemmT::run(&P.maps, A, lda, kend, k0, k0, kend, n - kend, nbn, nb, (char*)smem, &bars, c, G);
@@ -561,9 +570,20 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_la_kernel(const __grid_constant_
     // ------------------------- panel k+1 (panel CTAs) || A22 update (GEMM CTAs)
     if (pan) {
       la_factor_panel(P, kend, nbn, c, epoch, smem, s_prow, s_rowj, rv, ri, s_piv, s_idx, s_val);
-    } else if (kend + nbn < n) {
-      GemmT::run(&P.maps, A, lda, kend, k0, k0, kend + nbn, n - kend, n - kend - nbn, nb, (char*)smem, &bars,
-                 c - np, G - np);
+    } else {
+      if (kend + nbn < n)
+        GemmT::run(&P.maps, A, lda, kend, k0, k0, kend + nbn, n - kend, n - kend - nbn, nb, (char*)smem, &bars,
+                   c - np, G - np);
+      // panel k's interchanges on the finished L columns [0, k0)
+      for (int64_t col = (int64_t)(c - np) * NT + tid; col < k0; col += (int64_t)(G - np) * NT)
+        for (int j = k0; j < kend; ++j) {
+          const int p = __ldcg(P.ipiv + j);
+          if (p != j) {
+            const z_t t = __ldcg(A + (int64_t)j * lda + col);
+            A[(int64_t)j * lda + col] = __ldcg(A + (int64_t)p * lda + col);
+            A[(int64_t)p * lda + col] = t;
+          }
+        }
     }
   }
   grid.sync();
