@@ -275,9 +275,25 @@ def probe_peak(n: int = 5) -> tuple[float, list]:
     return float(np.median(vals)), vals
 
 
+def all_host_threads():
+    """BLAS thread pool opened to every host core (torchrun exports
+    OMP_NUM_THREADS=1 to its ranks; the CPU baseline uses the whole host)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
+    except Exception:  # no threadpoolctl: keep the defaults
+        import contextlib
+        return contextlib.nullcontext()
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port; the reference is
     pure Python and cannot travel to the GPU box) on the host cores."""
+    with all_host_threads():
+        return _run_reference(args)
+
+
+def _run_reference(args):
     from paper_2310_04734_b200 import dist as vdist, workloads
     rank, ws, _ = vdist.world()
     if rank != 0:
@@ -626,6 +642,8 @@ def run_ours(args):
 
     cpu = None
     if ws == 1 and not args.no_cpu:
+        _threads = all_host_threads()
+        _threads.__enter__()
         n = cpu_sample_size(w, args.cpu_budget_s)
         rng = np.random.default_rng(12)
         idx = np.sort(rng.choice(nF, n, replace=False))
@@ -638,6 +656,7 @@ def run_ours(args):
                                f"{ldt:.1f} s", "path": "oracle.mor.reduced_output = ReducedModel.output "
                                "(mor.py:73-98) with dense reduced providers and V = I"}
         cpu["cfg1_pipeline"] = cpu_cfg1_pipeline()
+        _threads.__exit__(None, None, None)
 
     offline = None
     if ws == 1 and not args.no_offline:

@@ -901,8 +901,13 @@ def krylov_blocks_mimo_dev(fom: FullOrderModel, f_j: float, m: int, second_order
     nv = linalg.column_norms(Vb).cpu().numpy()
     if np.any(nv == 0):
         raise ValueError("zero load at expansion point")
-    # per-source bases grow in place in (n x m) buffers; cnt[j] columns kept
-    Qs = [torch.empty((Vb.shape[0], m), dtype=CDT, device=Vb.device) for _ in range(s)]
+    # per-source bases grow in place: source j's basis is Qall[:, j, :cnt[j]]
+    # (zero beyond), so the per-source Gram-Schmidt of ALL sources is one
+    # batched pass (vb_batched_dots / vb_batched_update) instead of 4 GEMM
+    # launches per source
+    from .gmres import batched_dots, batched_update
+    Qall = torch.zeros((Vb.shape[0], s, m), dtype=CDT, device=Vb.device)
+    Qs = [Qall[:, j, :] for j in range(s)]
     for j in range(s):
         torch.mul(Vb[:, j:j + 1], 1.0 / nv[j], out=Qs[j][:, 0:1])
     cnt = [1] * s
@@ -924,13 +929,17 @@ def krylov_blocks_mimo_dev(fom: FullOrderModel, f_j: float, m: int, second_order
                 prev[j] = Qs[j][:, cnt[j] - 1:cnt[j]]
         else:
             rhs = fom.apply("M", f_j, cur)
-        W = lu.solve(rhs)
+        W = lu.solve(rhs).contiguous()
         W.neg_()
         refs = linalg.column_norms(W).cpu().numpy()
-        # two CGS sweeps per source against its own basis (all sources queued),
-        # then ONE norm read for the drop decisions of the whole moment
-        for q, j in enumerate(act):
-            _cgs2_against(Qs[j][:, :cnt[j]], W[:, q:q + 1])
+        # two CGS sweeps per source against its own basis, then ONE norm read
+        # for the drop decisions of the whole moment
+        if len(act) == s and len(set(cnt)) == 1:   # all sources alive: batched
+            for _ in range(2):
+                batched_update(Qall, cnt[0], batched_dots(Qall, cnt[0], W), W)
+        else:
+            for q, j in enumerate(act):
+                _cgs2_against(Qs[j][:, :cnt[j]], W[:, q:q + 1])
         nws = linalg.column_norms(W).cpu().numpy()
         for q, j in enumerate(act):
             nw = float(nws[q])
