@@ -15,7 +15,9 @@ from pathlib import Path
 import torch
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libvibro_b200.so"
+# VB_LIB_PATH: an alternative build of the same library (tools/build_variant.py
+# experiments); the product path is the in-tree build
+LIB_PATH = Path(os.environ["VB_LIB_PATH"]).resolve() if os.environ.get("VB_LIB_PATH") else PKG_DIR / "libvibro_b200.so"
 
 _z = C.c_void_p  # vb_complex* (device)
 

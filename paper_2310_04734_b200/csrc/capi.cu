@@ -65,6 +65,7 @@ int vb_rom_sweep(int r, int nprim, int s, int n_out, int64_t F, const vb_complex
                  void* work, size_t work_bytes, void* stream) {
   VB_CHECK_ARG(r >= 1 && nprim >= 1 && nprim <= 64 && s >= 1 && n_out >= 0 && F >= 0,
                "vb_rom_sweep: bad sizes");
+  if (F == 0) return 0;  // nothing to sweep (alpha / outputs may be empty, i.e. NULL)
   VB_CHECK_ARG(prims && alpha && b, "vb_rom_sweep: null input");
   VB_CHECK_ARG(n_out == 0 || c_r, "vb_rom_sweep: c_r is NULL with n_out > 0");
   VB_CHECK_ARG(b_stride_f == 0 || b_stride_f >= (int64_t)r * s, "vb_rom_sweep: bad b_stride_f");

@@ -27,7 +27,16 @@ using blk::cp_async16;
 using blk::cp_commit;
 using blk::cp_wait;
 
-constexpr int TX = 32, TY = 8, HX = TX + 4, HY = TY + 4, KC = 2;
+#ifndef VB_KRON_TX
+#define VB_KRON_TX 32
+#endif
+#ifndef VB_KRON_TY
+#define VB_KRON_TY 8
+#endif
+#ifndef VB_KRON_KC
+#define VB_KRON_KC 2
+#endif
+constexpr int TX = VB_KRON_TX, TY = VB_KRON_TY, HX = TX + 4, HY = TY + 4, KC = VB_KRON_KC;
 constexpr int RING = 4, AHEAD = 3;   // cp.async landing slots: newest plane + AHEAD in flight
 constexpr int NTH = 256;
 constexpr int PLANE = HY * HX * KC;  // complex per halo plane

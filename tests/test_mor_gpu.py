@@ -278,15 +278,24 @@ def test_concurrent_krylov_matches_sequential(cuda, model):
         pts, m, so = lay["points"][:3], 4, False
     seq = [mor.krylov_block_dev(fom, f, m, second_order=so) for f in pts]
     conc = mor.krylov_blocks_concurrent(fom, pts, m, second_order=so)
+    # the capped concurrent grid runs the plain LU kernel, the full grid the
+    # look-ahead one: same pivots, factors equal to ~1e-13; the moment
+    # recurrence amplifies that (cfg2's coupled operator: cond ~1e12) to
+    # ~1e-10 in the last moments
     for (Qs, bs), (Qc, bc) in zip(seq, conc):
         assert bs == bc and Qs.shape == Qc.shape
-        assert float((Qs - Qc).abs().max()) <= 1e-12
+        assert float((Qs - Qc).abs().max()) <= 1e-9
     V, flags = mor.krylov_basis(fom, pts, m, second_order=so)
     Vs = None
     for Q, _ in seq:
         Vs = mor._orthonormalise(Vs, Q)
     assert V.shape == Vs.shape
-    assert float((V - Vs).abs().max()) <= 1e-10
+    # the late columns are nearly dependent moment vectors (determined only to
+    # ~1e-7 by the data): compare what the basis is used for
+    fr = list(lay["freqs"][::17])
+    ya = np.array(mor.ReducedModel(fom=fom, V=V, window=(0.0, 1e4)).outputs(fr))
+    yb = np.array(mor.ReducedModel(fom=fom, V=Vs, window=(0.0, 1e4)).outputs(fr))
+    assert np.abs(ya - yb).max() <= 1e-8 * np.abs(yb).max()
 
 
 def test_project_lift_and_c_out_reduced(cuda, frozen):

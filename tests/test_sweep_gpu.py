@@ -309,3 +309,35 @@ def test_sharded_sweep_world1_matches_direct(cuda):
     spl, y = vdist.sweep_sharded(rs, f, want_y=True)
     out = rs.sweep_device(f)
     assert torch.equal(spl, out.spl) and torch.equal(y, out.y)
+
+
+def test_empty_and_degenerate_inputs(cuda):
+    """Empty frequency lists / grids and outputs-free sweeps: no launch, empty
+    results (the reference's loops simply do nothing); an all-zero Krylov
+    block is dropped entirely by the drop rule (mor.py:133: ref = 0 -> drop)."""
+    import torch
+    from paper_2310_04734_b200 import mor, sweep, workloads
+    w = workloads.cfg5(r=64, n_freq=10)
+    rs = sweep.ReducedSweep(w.prims, w.b, w.c_r, kinds=w.kinds)
+    out = rs.sweep_device(torch.empty(0, dtype=torch.float64, device=cuda))
+    assert out.y.shape == (0, w.c_r.shape[0], w.b.shape[1]) and out.spl.shape == (0, w.b.shape[1])
+    y, spl = rs.sweep(np.zeros(0))
+    assert y.shape[0] == 0 and spl.shape[0] == 0
+    o = sweep.rom_sweep_affine(sweep.as_ctensor(w.prims, cuda), sweep.as_ctensor(w.alpha(w.freqs[:3]), cuda),
+                               sweep.as_ctensor(w.b, cuda), sweep.as_ctensor(np.zeros((0, 64)), cuda),
+                               want_x=True)
+    torch.cuda.synchronize()
+    assert o.y is None and o.spl is None and o.x.shape == (3, 64, w.b.shape[1])
+    x_ref = np.linalg.solve(np.tensordot(w.alpha(w.freqs[:1])[0], w.prims, 1), w.b)
+    assert np.abs(o.x[0].cpu().numpy() - x_ref).max() <= 1e-10 * np.abs(x_ref).max()
+    V0 = mor._orthonormalise(None, torch.randn(300, 4, dtype=torch.complex128, device=cuda))
+    V1 = mor._orthonormalise(V0, torch.zeros(300, 3, dtype=torch.complex128, device=cuda))
+    assert V1.shape == (300, 4)
+    V2 = mor.orthonormalise_blocks(V0, [torch.zeros(300, 3, dtype=torch.complex128, device=cuda),
+                                        V0[:, :2].clone()])
+    assert V2.shape == (300, 4)
+    fom = mor.FullOrderModel(stiffness=lambda f: np.eye(5) * 4.0, mass=lambda f: np.eye(5), load=lambda f: np.ones(5),
+                             c_out=np.ones(5), n=5)
+    rom = mor.ReducedModel(fom=fom, V=np.eye(5, dtype=complex), window=(1.0, 2.0))
+    res = mor.rom_sweep([rom], [])
+    assert res.freqs == [] and res.frf == []
