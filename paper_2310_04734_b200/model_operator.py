@@ -178,7 +178,8 @@ def load_operator_npz(path, device=None):
     reference package; the scalars are looked up at the tabulated
     frequencies only."""
     from .mor import fom_from_operator
-    z = np.load(path)
+    with np.load(path) as zf:   # materialised: the coefficient callables run on several host threads
+        z = {k: zf[k] for k in zf.files}
     grid = z["grid"]
     pos = {float(f): i for i, f in enumerate(grid)}
     doms = [str(d) for d in z["domains"]]

@@ -999,6 +999,45 @@ def krylov_blocks_concurrent(fom: FullOrderModel, points, m: int, second_order: 
         return list(ex.map(work, pts))
 
 
+def fom_outputs_concurrent(fom: FullOrderModel, freqs, workers: int | None = None) -> list:
+    """[fom.output(fom.solve(f)) for f in freqs] (mor.py:239-242: the greedy's
+    exact candidate outputs, one factorisation per frequency) with the
+    factorisations running concurrently on their own streams / host threads,
+    the whole-GPU LU kernels capped at a share of the SMs — their panel steps
+    are latency chains that overlap across frequencies.  Only for dense-LU
+    models (FDM / iterative models keep the sequential loop)."""
+    fr = [float(f) for f in freqs]
+    if len(fr) <= 1 or not _lu_factored(fom):
+        return [fom.output(fom.solve(f)) for f in fr]
+    from concurrent.futures import ThreadPoolExecutor
+    dev = _device()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    n_lu = fom.schur.n_p if fom.schur is not None else fom.n
+    min_ctas = max(24, -(-n_lu // 222))
+    nw = min(len(fr), workers or 6, max(1, nsm // min_ctas))
+    if nw <= 1:
+        return [fom.output(fom.solve(f)) for f in fr]
+    lib = _lib.load()
+    cap = nsm // nw
+    caller = torch.cuda.current_stream(dev)
+
+    def work(f):
+        torch.cuda.set_device(dev)
+        st = torch.cuda.Stream(device=dev)
+        st.wait_stream(caller)
+        lib.vb_set_lu_max_ctas(cap)
+        try:
+            with torch.cuda.stream(st):
+                y = fom.output(fom.solve(f))
+            st.synchronize()
+        finally:
+            lib.vb_set_lu_max_ctas(0)
+        return y
+
+    with ThreadPoolExecutor(nw, thread_name_prefix="vb_fom") as ex:
+        return list(ex.map(work, fr))
+
+
 def _lu_factored(fom: FullOrderModel) -> bool:
     """True when fom.factor goes through the dense GPU LU (directly or on a
     Schur complement) — the latency-bound factor / solve kernels that gain
@@ -1116,6 +1155,10 @@ def greedy_expand(fom: FullOrderModel, grid, settings, window, second_order: boo
             V = _orthonormalise(V, block)
         points = points + [next_f]
         rom.V = V
+        missing = [f for f in cand if f not in cache]
+        if missing:  # all uncached candidates at once (concurrent factorisations)
+            for f, y in zip(missing, fom_outputs_concurrent(fom, missing)):
+                cache[f] = y
         y_full = np.array([y_exact(f) for f in cand])
         y_red = np.array(rom.outputs(cand))
         if y_full.ndim > 1:  # multi-output: pointwise errors, worst output per candidate

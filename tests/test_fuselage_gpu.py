@@ -68,7 +68,7 @@ def _emb(A, r0, c0, n):
 def fuselage(golden_dir, cuda):
     from paper_2310_04734_b200 import mor
     from paper_2310_04734_b200.model_operator import load_operator_npz
-    z = np.load(golden_dir / "fuselage_slice.npz")
+    z = dict(np.load(golden_dir / "fuselage_slice.npz"))
     fom, _, _ = load_operator_npz(golden_dir / "fuselage_slice.npz", cuda)
     roms = []
     for k in range(int(z["n_windows"])):

@@ -96,7 +96,7 @@ def test_gmres_additive_schwarz_on_reference_benchmark(cuda, golden_dir, overlap
     from paper_2310_04734_b200.model_operator import load_operator_npz
     from paper_2310_04734_b200.schwarz import AdditiveSchwarz, SchwarzGmres
     fom, grid, op = load_operator_npz(golden_dir / "fuselage_slice.npz", cuda)
-    z = np.load(golden_dir / "fuselage_slice.npz")
+    z = dict(np.load(golden_dir / "fuselage_slice.npz"))
     sets = [np.arange(o, o + s) for o, s in op.block_map.values()]
     fom.iterative = SchwarzGmres(AdditiveSchwarz(fom, sets, overlap=overlap, variant=variant))
     for f, yr in list(zip(z["fom_f"], z["fom_y"]))[:: 1 if overlap == 1 and variant == "restricted" else 2]:

@@ -290,12 +290,12 @@ def test_concurrent_krylov_matches_sequential(cuda, model):
     for Q, _ in seq:
         Vs = mor._orthonormalise(Vs, Q)
     assert V.shape == Vs.shape
-    # the late columns are nearly dependent moment vectors (determined only to
-    # ~1e-7 by the data): compare what the basis is used for
-    fr = list(lay["freqs"][::17])
-    ya = np.array(mor.ReducedModel(fom=fom, V=V, window=(0.0, 1e4)).outputs(fr))
-    yb = np.array(mor.ReducedModel(fom=fom, V=Vs, window=(0.0, 1e4)).outputs(fr))
-    assert np.abs(ya - yb).max() <= 1e-8 * np.abs(yb).max()
+    # the late columns are nearly dependent moment vectors, determined only to
+    # ~1e-7 by the data: the two bases span the same subspace
+    # to that level (outputs of an unconverged r = 12 ROM near its own
+    # resonances are too sensitive to compare)
+    R = Vs - V @ (V.conj().T @ Vs)
+    assert float(R.abs().max()) <= 1e-6, float(R.abs().max())
 
 
 def test_project_lift_and_c_out_reduced(cuda, frozen):
