@@ -62,6 +62,24 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Device-side index checks (build variant -DVB_DEBUG_CHECKS, tools/build_variant.py):
+// compute-sanitizer is unavailable on the GPU pool, so the debug build traps
+// on an out-of-range pivot / column index instead of corrupting memory.
+#ifdef VB_DEBUG_CHECKS
+#define VB_DCHECK(cond)                                                                   \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("VB_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,     \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define VB_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 void set_error(const std::string& msg);
 int check_cuda(cudaError_t e, const char* where);
 int check_launch(const char* where);

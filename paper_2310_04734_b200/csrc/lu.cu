@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(NT, 1) zgetrf_kernel(const __grid_constant__ L
         s_prow[t] = __ldcg(P.prow + ((int64_t)buf * G + s_idx) * NB + t);
         s_rowj[t] = __ldcg(P.rowj + buf * NB + t);
       }
+      VB_DCHECK(p >= j && p < n && s_idx >= 0 && s_idx < G);
       if (c == 0 && tid == 0) P.ipiv[j] = p;
       __syncthreads();
       const z_t pinv = zrecip(s_prow[jj]);
@@ -438,6 +439,7 @@ __device__ void la_factor_panel(const LuParams& P, int k0, int nb, int pc, unsig
       s_prow[t] = __ldcg(P.prow + ((int64_t)buf * np + s_idx) * NB + t);
       s_rowj[t] = __ldcg(P.rowj + buf * NB + t);
     }
+    VB_DCHECK(p >= j && p < n && s_idx >= 0 && s_idx < np);
     if (pc == 0 && tid == 0) P.ipiv[j] = p;
     __syncthreads();
     const z_t pinv = zrecip(s_prow[jj]);

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int n_rows, const int32_t* __
     }
     for (; j < e; j += SW) {
       const double a = __ldg(vals + j);
+      VB_DCHECK(__ldg(indices + j) >= 0);  // (row-compacted CSRs: columns may exceed n_rows)
       const z_t* xr = X + (int64_t)__ldg(indices + j) * ldx;
 #pragma unroll
       for (int c = 0; c < KC; ++c) {
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(256) spmm_subwarp_kernel(int n_rows, const int
       if (j0 + c < len) {
         v = __ldg(vals + b + j0 + c);
         col = __ldg(indices + b + j0 + c);
+        VB_DCHECK(col >= 0);
       }
       const int cnt = min(KP, mlen - j0);
 #pragma unroll 4

@@ -217,6 +217,7 @@ __device__ void inner_panel_w(const Params& P, z_t* A, int k0, int j0, int wc, z
     const bool zero = !(best.v > 0.0);
     const int p = zero ? jj : (best.key >> 16);
     const int b = best.key & 0xffff;
+    VB_DCHECK(zero || (p >= jj && p < H && b >= 0 && b < H));
     if (tid == 0) {
       if (zero && *s_info == 0) *s_info = j0 + jj + 1;  // LAPACK INFO: no interchange, no scaling
       piv[j0 - k0 + jj] = j0 + p;

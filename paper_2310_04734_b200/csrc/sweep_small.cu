@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(NT) rom_sweep_small_kernel(
         __syncthreads();  // publishing step k+1's pivot before every warp read p
         continue;
       }
+      VB_DCHECK(p >= k && p < r);
       const z_t pv = As[p * ld + k];
       const z_t pinv = zrecip(pv);
       // phase A: multipliers (read column k through the swap) and swap cols > k
