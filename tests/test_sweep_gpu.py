@@ -173,7 +173,7 @@ def _resonance_probes(w, n_res: int = 16, n_total: int = 64, seed: int = 0) -> n
     return np.sort(np.concatenate([res, rest]))
 
 
-@pytest.mark.parametrize("r", [256, 1024, 2048])
+@pytest.mark.parametrize("r", [256, 400, 1024, 1536, 2048])
 def test_cfg5_full_size_64_frequencies(cuda, r):
     """BASELINE cfg5 at its full reduced orders (the bench's headline kernel):
     64 frequencies of the 100k grid, 16 of them straddling undamped
