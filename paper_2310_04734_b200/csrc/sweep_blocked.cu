@@ -48,12 +48,12 @@ constexpr int LDL = NB + 4;     // == 4 (mod 8): triangular inverse used as A op
 #endif
 
 #ifndef VB_DEEP_MIN_R
-#define VB_DEEP_MIN_R 640
+#define VB_DEEP_MIN_R 384
 #endif
 #ifndef VB_DEEP4_MIN_R
 #define VB_DEEP4_MIN_R 1536
 #endif
-constexpr int DEEP_MIN_R = VB_DEEP_MIN_R;    // outer steps of 2 panels (trailing K = 128) from this order on
+constexpr int DEEP_MIN_R = VB_DEEP_MIN_R;    // outer steps of 2 panels (trailing K = 128) from this order on (r = 400: +3 %, tools/sweep_rates.py)
 constexpr int DEEP4_MIN_R = VB_DEEP4_MIN_R;  // ... of 4 panels (K = 256)
 constexpr int LDY = 16 + 2;
 constexpr size_t TRSM_SMEM = (size_t)(NB * LDL) * sizeof(z_t);
