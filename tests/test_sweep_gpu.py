@@ -189,7 +189,7 @@ def test_cfg5_full_size_64_frequencies(cuda, r):
     _check(out.y.cpu().numpy(), out.spl.cpu().numpy(), y_ref, spl_ref)
 
 
-@pytest.mark.parametrize("r", [700, 1001, 1537, 1601])
+@pytest.mark.parametrize("r", [401, 450, 700, 1001, 1537, 1601])
 @pytest.mark.parametrize("s", [1, 3])
 def test_blocked_partial_outer_steps(cuda, force_blocked, r, s):
     """Orders whose last outer step is partial: fewer panels than the 2-panel
