@@ -154,6 +154,9 @@ __global__ void __launch_bounds__(256) spmm_subwarp_kernel(int n_rows, const int
 
 // ------------------------------------------------------------- row groups ---
 constexpr int RG = 8;  // rows per group
+#ifndef VB_RG_S
+#define VB_RG_S 3  // cp.async ring stages of the row-group kernels
+#endif
 #ifndef VB_RG_CC_MIN_K
 #define VB_RG_CC_MIN_K 1000000  // set after measuring (tools/bench_offline.py, VB_RG_MODE)
 #endif
@@ -188,7 +191,11 @@ constexpr int RG_WARPS = 4;
 #define VB_RG_CHUNK_FAST 1  // the chunks of a group tile run together: its value rows are read from DRAM once
 #endif
 
-template <int CW, int J, int S>
+// CC = true: the same staging, but the products on the CUDA cores without the
+// padding (see rg_cc below): lane <-> complex column, the 8 member rows'
+// accumulators in registers, each staged X element fused into exactly the
+// rows present at that slot (its 8-bit mask, uniform over the warp).
+template <int CW, int J, int S, bool CC = false>
 __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, const int32_t* __restrict__ g_leader,
                                                                 const int32_t* __restrict__ g_rows,
                                                                 const int32_t* __restrict__ g_uoff,
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
                                                                 const double* __restrict__ gvals, int k,
                                                                 const z_t* __restrict__ X, int64_t ldx,
                                                                 z_t* __restrict__ Y, int64_t ldy, z_t alpha,
-                                                                z_t beta) {
+                                                                z_t beta, const uint8_t* __restrict__ masks = nullptr) {
   using C = RgCfg<CW, J, S>;
   static_assert(J % 4 == 0 && 32 % J == 0, "stages of whole k4 steps inside one 32-column index block");
   static_assert((J * CW) % 32 == 0 && (J * RG / 2) % 32 == 0 || J * RG / 2 < 32, "copy rounds");
@@ -259,9 +266,19 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
     }
     blk::cp_commit();
   };
-  double acc[C::NT][2];
+  constexpr int NACC = CC ? 1 : C::NT;
+  double acc[NACC][2];
 #pragma unroll
-  for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  for (int t = 0; t < NACC; ++t) acc[t][0] = acc[t][1] = 0.0;
+  constexpr int CPL = CC ? C::CW / 32 : 1;  // complex columns per lane (CUDA-core form)
+  double ar[CPL][RG], ai[CPL][RG];
+  if constexpr (CC) {
+#pragma unroll
+    for (int t = 0; t < CPL; ++t)
+#pragma unroll
+      for (int i = 0; i < RG; ++i) ar[t][i] = ai[t][i] = 0.0;
+  }
+  const uint8_t* mk = CC ? masks + __ldg(g_uoff + g) : nullptr;
 #pragma unroll
   for (int st = 0; st < S - 1; ++st) {
     if (st < nst) issue(st);
@@ -272,16 +289,57 @@ __global__ void __launch_bounds__(32 * RG_WARPS) rg_spmm_kernel(int n_groups, co
     __syncwarp();
     const double* xsl = xs + (st % S) * C::XS;
     const double* vsl = vs + (st % S) * C::VS;
+    if constexpr (!CC) {
 #pragma unroll
-    for (int q = 0; q < J / 4; ++q) {
-      const double a = vsl[(4 * q + tig) * C::VR + gid];  // A[row gid][k tig]
-      const double* xb = xsl + (4 * q + tig) * C::RS + gid;  // B[k tig][n gid]
+      for (int q = 0; q < J / 4; ++q) {
+        const double a = vsl[(4 * q + tig) * C::VR + gid];  // A[row gid][k tig]
+        const double* xb = xsl + (4 * q + tig) * C::RS + gid;  // B[k tig][n gid]
 #pragma unroll
-      for (int t = 0; t < C::NT; ++t) blk::dmma(acc[t][0], acc[t][1], a, xb[8 * t]);
+        for (int t = 0; t < C::NT; ++t) blk::dmma(acc[t][0], acc[t][1], a, xb[8 * t]);
+      }
+    } else {
+      const int jb = st * J;
+#pragma unroll
+      for (int q = 0; q < J; ++q) {
+        const unsigned m = jb + q < nu ? __ldg(mk + jb + q) : 0u;  // uniform: one broadcast load
+        const double2* vq = reinterpret_cast<const double2*>(vsl + q * C::VR);
+        double2 v[RG / 2];
+#pragma unroll
+        for (int h = 0; h < RG / 2; ++h) v[h] = vq[h];
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) {
+          const double2 x = *reinterpret_cast<const double2*>(xsl + q * C::RS + 2 * (lane + 32 * t));
+#pragma unroll
+          for (int i = 0; i < RG; ++i)
+            if ((m >> i) & 1u) {
+              const double a = (i & 1) ? v[i >> 1].y : v[i >> 1].x;
+              ar[t][i] = fma(a, x.x, ar[t][i]);
+              ai[t][i] = fma(a, x.y, ai[t][i]);
+            }
+        }
+      }
     }
     __syncwarp();
     if (st + S - 1 < nst) issue(st + S - 1);
     else blk::cp_commit();
+  }
+  if constexpr (CC) {
+    const bool beta0 = beta.x == 0.0 && beta.y == 0.0;
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      const int row = __ldg(g_rows + (int64_t)g * RG + i);
+      if (row < 0) continue;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const int c = c0 + lane + 32 * t;
+        if (c >= k) continue;
+        z_t* yp = Y + (int64_t)row * ldy + c;
+        z_t out = zmul(alpha, zmake(ar[t][i], ai[t][i]));
+        if (!beta0) out = zfma(out, beta, *yp);
+        *yp = out;
+      }
+    }
+    return;
   }
   const int row = __ldg(g_rows + (int64_t)g * RG + gid);
   if (row < 0) return;
@@ -479,14 +537,15 @@ int rg_gather_values(int64_t n_union, const int32_t* vmap, const double* vals, d
   return 0;
 }
 
-template <int CW, int J, int S>
+template <int CW, int J, int S, bool CC = false>
 static int rg_launch(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const int32_t* g_uoff,
                      const int32_t* indptr, const int32_t* indices, const double* gvals, int k, const z_t* X,
-                     int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
+                     int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st,
+                     const uint8_t* masks = nullptr) {
   constexpr int smem = RG_WARPS * RgCfg<CW, J, S>::WARP_BYTES;
   static bool attr = false;
   if (!attr) {
-    VB_CUDA(cudaFuncSetAttribute(rg_spmm_kernel<CW, J, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    VB_CUDA(cudaFuncSetAttribute(rg_spmm_kernel<CW, J, S, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
 #if VB_RG_CHUNK_FAST
@@ -494,8 +553,9 @@ static int rg_launch(int n_groups, const int32_t* g_leader, const int32_t* g_row
 #else
   const dim3 grid((unsigned)((n_groups + RG_WARPS - 1) / RG_WARPS), (unsigned)((k + CW - 1) / CW));
 #endif
-  rg_spmm_kernel<CW, J, S><<<grid, 32 * RG_WARPS, smem, st>>>(n_groups, g_leader, g_rows, g_uoff, indptr, indices,
-                                                              gvals, k, X, ldx, Y, ldy, alpha, beta);
+  rg_spmm_kernel<CW, J, S, CC><<<grid, 32 * RG_WARPS, smem, st>>>(n_groups, g_leader, g_rows, g_uoff, indptr,
+                                                                  indices, gvals, k, X, ldx, Y, ldy, alpha, beta,
+                                                                  masks);
   VB_LAUNCHED("rg_spmm_kernel");
   return 0;
 }
@@ -517,7 +577,13 @@ int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const 
             const z_t* X, int64_t ldx, z_t* Y, int64_t ldy, z_t alpha, z_t beta, cudaStream_t st) {
   if (n_groups <= 0 || k <= 0) return 0;
   const int mode = rg_mode();
-  if (masks && (mode == 2 || (mode == 0 && k >= RG_CC_MIN_K))) {
+  if (masks && k > 16 && (mode == 2 || (mode == 0 && k >= RG_CC_MIN_K))) {  // staged CUDA-core groups
+    if (k <= 32) return rg_launch<32, 4, VB_RG_S, true>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals,
+                                                        k, X, ldx, Y, ldy, alpha, beta, st, masks);
+    return rg_launch<64, 4, VB_RG_S, true>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx,
+                                           Y, ldy, alpha, beta, st, masks);
+  }
+  if (masks && mode == 3) {  // direct-gather CUDA-core groups (no staging)
     if (k <= 8) return rg_cc_launch<8>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals, k, X, ldx,
                                        Y, ldy, alpha, beta, st);
     if (k <= 16) return rg_cc_launch<16>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals, k, X,
@@ -525,9 +591,6 @@ int rg_spmm(int n_groups, const int32_t* g_leader, const int32_t* g_rows, const 
     return rg_cc_launch<32>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, masks, gvals, k, X, ldx, Y, ldy,
                             alpha, beta, st);
   }
-#ifndef VB_RG_S
-#define VB_RG_S 3
-#endif
 #define VB_RG(CW, J) \
   return rg_launch<CW, J, VB_RG_S>(n_groups, g_leader, g_rows, g_uoff, indptr, indices, gvals, k, X, ldx, Y, ldy, alpha, beta, st)
 #ifndef VB_RG_J8

@@ -151,7 +151,7 @@ def test_spmm_paths_match_scipy_and_each_other(cuda, k, kind):
     outs = {}
     from paper_2310_04734_b200 import _lib
     lib = _lib.load()
-    for path, mode in (("csr", 0), ("rg", 1), ("rg", 2)):   # mode: DMMA groups / CUDA-core groups
+    for path, mode in (("csr", 0), ("rg", 1), ("rg", 2), ("rg", 3)):   # DMMA / staged CUDA-core / direct CUDA-core
         lib.vb_set_rg_spmm_mode(mode)
         try:
             Yd = torch.as_tensor(Y0, device=cuda).clone()
@@ -162,6 +162,7 @@ def test_spmm_paths_match_scipy_and_each_other(cuda, k, kind):
         np.testing.assert_allclose(outs[(path, mode)], alpha * (A @ X) + beta * Y0, rtol=1e-13, atol=1e-12)
     np.testing.assert_allclose(outs[("rg", 1)], outs[("csr", 0)], rtol=1e-14, atol=1e-13)
     np.testing.assert_allclose(outs[("rg", 2)], outs[("csr", 0)], rtol=1e-14, atol=1e-13)
+    np.testing.assert_allclose(outs[("rg", 3)], outs[("csr", 0)], rtol=1e-14, atol=1e-13)
     # strided views (ldx, ldy > k) through the auto path
     Xw = torch.zeros((n, k + 3), dtype=torch.complex128, device=cuda)
     Xw[:, :k] = Xd

@@ -91,7 +91,8 @@ def measure(peak_fp64=None):
     for k in (1, 2, 8, 32, 400):
         X = torch.randn(n, k, dtype=torch.complex128, device=dev)
         alg = nnz * 12 + 2 * n * k * 16
-        for tag, path, mode in (("", "auto", 0), ("_csr", "csr", 0), ("_rgtc", "rg", 1), ("_rgcc", "rg", 2)):
+        for tag, path, mode in (("", "auto", 0), ("_csr", "csr", 0), ("_rgtc", "rg", 1), ("_rgcc", "rg", 2),
+                                ("_rgcc_direct", "rg", 3)):
             if tag and k < 8:
                 continue
             lib.vb_set_rg_spmm_mode(mode)
