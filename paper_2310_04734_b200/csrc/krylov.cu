@@ -18,24 +18,40 @@ namespace vb {
 
 constexpr int KR_NT = 256;
 
-// partial[cta][c * j + i] over the CTA's row range
+// partial[cta][c * j + i] over the CTA's row range.  The k * j (column, basis
+// vector) pairs are few (8 x 1..60), so the CTA's threads split into
+// 256 / pairs row slots per pair: every thread streams a strided share of the
+// rows (enough loads in flight to cover HBM latency), then the slots are
+// summed in a fixed order in shared memory (deterministic).
 __global__ void __launch_bounds__(KR_NT) batched_dots_partial(int64_t n, int k, int j, const z_t* __restrict__ V,
                                                               int64_t ldr, int64_t ldc, const z_t* __restrict__ W,
                                                               int64_t ldw, z_t* __restrict__ part, int64_t rows_per) {
+  __shared__ z_t red[KR_NT];
   const int64_t r0 = (int64_t)blockIdx.x * rows_per;
   const int64_t r1 = min(n, r0 + rows_per);
   const int pairs = k * j;
-  for (int p = threadIdx.x; p < pairs; p += KR_NT) {
-    const int c = p / j, i = p - c * j;
-    z_t acc0 = zmake(0.0, 0.0), acc1 = zmake(0.0, 0.0);
-    int64_t row = r0;
-    for (; row + 1 < r1; row += 2) {  // two independent accumulators
-      acc0 = zfma(acc0, zmake(V[row * ldr + c * ldc + i].x, -V[row * ldr + c * ldc + i].y), W[row * ldw + c]);
-      const int64_t q = row + 1;
-      acc1 = zfma(acc1, zmake(V[q * ldr + c * ldc + i].x, -V[q * ldr + c * ldc + i].y), W[q * ldw + c]);
+  for (int pbase = 0; pbase < pairs; pbase += KR_NT) {
+    const int np = min(KR_NT, pairs - pbase);
+    const int nslot = KR_NT / np;           // row slots per pair
+    const int p = pbase + threadIdx.x % np, slot = threadIdx.x / np;
+    z_t acc = zmake(0.0, 0.0);
+    if (slot < nslot) {
+      const int c = p / j, i = p - c * j;
+      const z_t* vp = V + c * ldc + i;
+      const z_t* wp = W + c;
+      for (int64_t row = r0 + slot; row < r1; row += nslot) {
+        const z_t v = vp[row * ldr];
+        acc = zfma(acc, zmake(v.x, -v.y), wp[row * ldw]);
+      }
     }
-    if (row < r1) acc0 = zfma(acc0, zmake(V[row * ldr + c * ldc + i].x, -V[row * ldr + c * ldc + i].y), W[row * ldw + c]);
-    part[(int64_t)blockIdx.x * pairs + p] = zadd(acc0, acc1);
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < np) {
+      z_t s = zmake(0.0, 0.0);
+      for (int q = 0; q < nslot; ++q) s = zadd(s, red[q * np + threadIdx.x]);  // fixed order
+      part[(int64_t)blockIdx.x * pairs + pbase + threadIdx.x] = s;
+    }
+    __syncthreads();
   }
 }
 
