@@ -36,7 +36,10 @@ using blk::NT;
 // Trailing update: the large-tile TMA + mbarrier DMMA GEMM (csrc/tma_big.cuh,
 // 128 x 64 tiles, one CTA per SM) over a 2-D tensor map of the matrix, tiles
 // spread over the CTAs.
-using GemmT = tma::GemmBig<3>;
+#ifndef VB_LU_STAGES
+#define VB_LU_STAGES 3
+#endif
+using GemmT = tma::GemmBig<VB_LU_STAGES>;
 
 // Profiling aid (-DVB_PHASE_TIMING): CTA 0's SM cycles in panel / swaps /
 // TRSM / GEMM (each phase ends at a grid barrier), vb_debug_phase_cycles 32..35.
