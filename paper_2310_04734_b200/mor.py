@@ -195,8 +195,14 @@ class FullOrderModel:
                     self.load = a.load.host
                 elif callable(a.load):
                     self.load = lambda f, a=a: np.asarray(a.load(f))
-                else:
-                    self.load = lambda f, b=np.asarray(torch.as_tensor(a.load).cpu()): b
+                else:  # host copy of the constant device load made on first use only
+                    cache = {}
+
+                    def load(f, a=a, cache=cache):
+                        if "b" not in cache:
+                            cache["b"] = np.asarray(torch.as_tensor(a.load).cpu())
+                        return cache["b"]
+                    self.load = load
             if not self.n:
                 self.n = a.n
 
@@ -564,7 +570,11 @@ def _vec_load(fom, f) -> bool:
     provider call can be expensive (a plane wave evaluated on the host)."""
     v = getattr(fom, "_vec_load_cache", None)
     if v is None:
-        v = bool(np.ndim(fom.load(f)) == 1)
+        aff = fom.affine
+        if aff is not None and aff.constant_load and isinstance(aff.load, torch.Tensor):
+            v = aff.load.dim() == 1          # no host copy of a device load
+        else:
+            v = bool(np.ndim(fom.load(f)) == 1)
         try:
             fom._vec_load_cache = v
         except AttributeError:
