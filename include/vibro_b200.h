@@ -156,6 +156,25 @@ int vb_hex27_box_csr(int nx, int ny, int nz, const double* K1, const double* M1,
 int vb_quad9_face_mass(int n_faces, const double* xyz, const int32_t* face_conn, double* Fe,
                        void* stream);
 
+/* cfg4 synthetic fuselage (BASELINE configs[3]; no reference element, SURVEY
+ * §8c tier 2 — checked against oracle/fuselage.py):
+ * the Helmholtz integrals of vb_hex27_helmholtz_elements with the chain rule
+ * dN = dshape inv(J)^T instead of the reference's dshape inv(J)
+ * (vibrofem/assembly.py:88; equal for diagonal J, the fuselage's mapped
+ * cylindrical elements have non-diagonal J). */
+int vb_hex27_helmholtz_elements_chain(int n_elem, const double* xyz, const int32_t* conn, double* Ke,
+                                      double* Me, int32_t* bad_elem_host, void* stream);
+
+/* Flat 9-node facet shells (skin, lining, floor, frame webs, stringers) in
+ * global node DoFs (u_x, u_y, u_z, th_x, th_y, th_z): membrane = the
+ * reference's plane-stress element (vibrofem/assembly.py:31-67), Reissner-
+ * Mindlin bending + 2x2 shear, Hughes-Brezzi drilling term (drill * G t),
+ * rotated from the facet frame.  mat [n_elem] indexes props [n_mat][4] =
+ * (E, nu, rho, t) (device); Ke, Me [n_elem][54][54] out. */
+int vb_facet_shell_elements(int n_elem, const double* xyz, const int32_t* conn, const int32_t* mat,
+                            const double* props, double drill, double* Ke, double* Me, int32_t* bad_elem_host,
+                            void* stream);
+
 /* ------------------------------------------------------------------------
  * Offline-phase linear algebra
  * ---------------------------------------------------------------------- */

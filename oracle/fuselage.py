@@ -1,0 +1,167 @@
+"""Oracle restatement of the cfg4 synthetic-fuselage element primitives
+(BASELINE configs[3]; SURVEY §8c tier 2 / §8d "cfg4: stretch") — TEST
+INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The reference has no shell or curved-solid element, so this is a
+restatement in the reference's conventions, pinned by analytic properties in
+the tests (rigid-body null spaces, symmetry, patch/rotation invariance) and
+used as the checker of the GPU element kernels and of the assembled CSR:
+
+  * fluids (cabin air, equivalent-fluid insulation): the Helmholtz integrals of
+    assembly.py:77-91 on 27-node hexahedra, but with the chain rule
+    dN/dx = dshape inv(J)^T (the reference's dshape inv(J) — see DESIGN §3
+    "Known reference quirk" — equals it only for diagonal J; the fuselage's
+    cylindrical mapping has non-diagonal J everywhere);
+  * shells (skin, lining, floor, frames, stringers): flat 9-node facets,
+    membrane + Reissner–Mindlin bending/shear exactly as oracle/shell.py's
+    plate (the reference's plane-stress element assembly.py:31-67 for the
+    membrane), with the chain rule above, a Hughes–Brezzi drilling term
+    gamma int (theta_3 - (v,x - u,y)/2)^2 dA (gamma = drill * G t) and the
+    node rotation from the facet frame to global (u, v, w, theta_x, theta_y,
+    theta_z);
+  * equivalent fluid: Delany–Bazley characteristic impedance and wavenumber
+    mapped to (rho_eff, c_eff) and used like the reference's JCA fluid
+    (assembly.py:242-257: K = Kgrad / rho_eff, M = Mnn / (rho_eff c_eff^2);
+    coupling M term rho_eff C^T, assembly.py:199-207, 290-294), in the
+    reference's e^{+i w t} convention (materials.py:112-167).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import fe
+
+NDOF = 6  # u_x, u_y, u_z, theta_x, theta_y, theta_z (global)
+
+
+def helmholtz_element_chain(idx: np.ndarray, coords: np.ndarray):
+    """assembly.py:77-91 with the chain rule dN = dshape inv(J)^T."""
+    pts, wts = fe.gauss_nd(coords.shape[1])
+    nn = idx.shape[0]
+    Kg = np.zeros((nn, nn))
+    Mn = np.zeros((nn, nn))
+    for xi, w in zip(pts, wts):
+        dS = fe.dshape_nd(idx, xi)
+        J = dS.T @ coords
+        det = np.linalg.det(J)
+        if det <= 0:
+            raise ValueError("non-positive Jacobian in Helmholtz element")
+        dN = dS @ np.linalg.inv(J).T
+        N = fe.shape_nd(idx, xi)
+        Kg += w * det * (dN @ dN.T)
+        Mn += w * det * np.outer(N, N)
+    return Kg, Mn
+
+
+def facet_frame(X3: np.ndarray):
+    """Rows e1, e2, e3 of the facet frame: e1 along the local xi edge (node 0 ->
+    node 2), e3 the normal of the corner plane, e2 = e3 x e1."""
+    e1 = X3[2] - X3[0]
+    e1 = e1 / np.linalg.norm(e1)
+    n = np.cross(X3[2] - X3[0], X3[6] - X3[0])
+    e3 = n / np.linalg.norm(n)
+    e2 = np.cross(e3, e1)
+    return np.array([e1, e2, e3])
+
+
+def facet_local_matrices(E, nu, rho, t, X2, drill=1e-3):
+    """54 x 54 local (u, v, w, bx, by, t3) per node: the plate of oracle/shell.py
+    (bx, by with u = z bx, v = z by; 3x3 rule, 2x2 shear rule) with the chain
+    rule, plus the drilling term and rotary inertia rho t^3/12 on t3."""
+    idx = fe.QUAD9_LEX_IDX
+    nd = 6
+    Dm = E * t / (1 - nu * nu) * np.array([[1, nu, 0], [nu, 1, 0], [0, 0, 0.5 * (1 - nu)]])
+    Db = E * t ** 3 / (12 * (1 - nu * nu)) * np.array([[1, nu, 0], [nu, 1, 0], [0, 0, 0.5 * (1 - nu)]])
+    G = E / (2 * (1 + nu))
+    Gs = 5.0 / 6.0 * G * t
+    gam = drill * G * t
+    K = np.zeros((54, 54))
+    M = np.zeros((54, 54))
+    u, v, w, bx, by, t3 = (np.arange(9) * nd + k for k in range(6))
+    for order, part in ((3, "full"), (2, "shear")):
+        pts, wts = fe.gauss_nd(2, order)
+        for xi, wq in zip(pts, wts):
+            dS = fe.dshape_nd(idx, xi)
+            J = dS.T @ X2
+            det = np.linalg.det(J)
+            if det <= 0:
+                raise ValueError("non-positive Jacobian in shell element")
+            dN = dS @ np.linalg.inv(J).T
+            N = fe.shape_nd(idx, xi)
+            if part == "full":
+                Bm = np.zeros((3, 54))
+                Bm[0, u] = dN[:, 0]
+                Bm[1, v] = dN[:, 1]
+                Bm[2, u] = dN[:, 1]
+                Bm[2, v] = dN[:, 0]
+                Bb = np.zeros((3, 54))
+                Bb[0, bx] = dN[:, 0]
+                Bb[1, by] = dN[:, 1]
+                Bb[2, bx] = dN[:, 1]
+                Bb[2, by] = dN[:, 0]
+                Bd = np.zeros(54)
+                Bd[t3] = N
+                Bd[v] = -0.5 * dN[:, 0]
+                Bd[u] = 0.5 * dN[:, 1]
+                K += wq * det * (Bm.T @ Dm @ Bm + Bb.T @ Db @ Bb + gam * np.outer(Bd, Bd))
+                nn = np.outer(N, N)
+                for comp, mass in ((u, rho * t), (v, rho * t), (w, rho * t), (bx, rho * t ** 3 / 12),
+                                   (by, rho * t ** 3 / 12), (t3, rho * t ** 3 / 12)):
+                    M[np.ix_(comp, comp)] += wq * det * mass * nn
+            else:
+                Bs = np.zeros((2, 54))
+                Bs[0, w] = dN[:, 0]
+                Bs[0, bx] = N
+                Bs[1, w] = dN[:, 1]
+                Bs[1, by] = N
+                K += wq * det * Gs * (Bs.T @ Bs)
+    return K, M
+
+
+def node_rotation(R: np.ndarray) -> np.ndarray:
+    """6 x 6 map global (u_x,u_y,u_z,th_x,th_y,th_z) -> local (u1,u2,u3,bx,by,t3):
+    u_loc = R u, th_loc = R th, bx = th_2, by = -th_1, t3 = th_3."""
+    T = np.zeros((6, 6))
+    T[:3, :3] = R
+    T[3, 3:] = R[1]
+    T[4, 3:] = -R[0]
+    T[5, 3:] = R[2]
+    return T
+
+
+def facet_shell_element(E, nu, rho, t, X3, drill=1e-3):
+    """(K, M) 54 x 54 in the global node DoFs of one flat 9-node facet whose
+    nodes X3 (9, 3) may lie slightly off the corner plane (projected)."""
+    R = facet_frame(X3)
+    X2 = (X3 - X3[0]) @ R[:2].T
+    Kl, Ml = facet_local_matrices(E, nu, rho, t, X2, drill)
+    T = np.kron(np.eye(9), node_rotation(R))
+    return T.T @ Kl @ T, T.T @ Ml @ T
+
+
+def delany_bazley(f, sigma, rho0=1.21, c0=343.0):
+    """(rho_eff, c_eff) of a Delany–Bazley equivalent fluid at f (e^{+i w t}:
+    Zc = rho0 c0 (1 + 0.0571 X^-0.754 - 0.087i X^-0.732),
+    kc = w/c0 (1 + 0.0978 X^-0.700 - 0.189i X^-0.595), X = rho0 f / sigma;
+    rho_eff = Zc kc / w, c_eff = w / kc)."""
+    w = 2.0 * math.pi * f
+    X = rho0 * f / sigma
+    Zc = rho0 * c0 * (1 + 0.0571 * X ** -0.754 - 0.087j * X ** -0.732)
+    kc = w / c0 * (1 + 0.0978 * X ** -0.700 - 0.189j * X ** -0.595)
+    return Zc * kc / w, w / kc
+
+
+def rigid_body_modes(xyz: np.ndarray) -> np.ndarray:
+    """(6 n, 6) global rigid-body displacement fields of shell nodes xyz."""
+    n = xyz.shape[0]
+    Rm = np.zeros((n * 6, 6))
+    for i in range(3):
+        Rm[i::6, i] = 1.0
+    for a in range(3):  # rotation about axis a: u = e_a x x, theta = e_a
+        ea = np.eye(3)[a]
+        Rm[np.arange(n)[:, None] * 6 + np.arange(3), 3 + a] = np.cross(ea, xyz)
+        Rm[np.arange(n) * 6 + 3 + a, 3 + a] = 1.0
+    return Rm

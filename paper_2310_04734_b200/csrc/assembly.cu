@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(EL_NT, 2) hex27_helmholtz_kernel(int n_elem, c
                                                                 const int32_t* __restrict__ conn,
                                                                 double* __restrict__ Ke,
                                                                 double* __restrict__ Me,
-                                                                int* __restrict__ bad) {
+                                                                int* __restrict__ bad, int chain) {
   extern __shared__ double el_smem[];
   double* sdN = el_smem;               // [27 g][27 i][3 a] reference gradients
   double* sN = sdN + 2187;             // [28 g][32 i] shape values, zero padded
@@ -205,6 +205,11 @@ __global__ void __launch_bounds__(EL_NT, 2) hex27_helmholtz_kernel(int n_elem, c
       iJ[6] = (J[3] * J[7] - J[4] * J[6]) * id;
       iJ[7] = (J[1] * J[6] - J[0] * J[7]) * id;
       iJ[8] = (J[0] * J[4] - J[1] * J[3]) * id;
+      if (chain) {  // chain rule dN inv(J)^T (cfg4 curved elements): store inv(J) transposed
+        double tmp = iJ[1]; iJ[1] = iJ[3]; iJ[3] = tmp;
+        tmp = iJ[2]; iJ[2] = iJ[6]; iJ[6] = tmp;
+        tmp = iJ[5]; iJ[5] = iJ[7]; iJ[7] = tmp;
+      }
       w.wdet[g] = __ldg(&c_hexW[g]) * det;
     } else if (lane == 27) {
       w.wdet[27] = 0.0;
@@ -455,6 +460,169 @@ int rm_plate_elements(int n_elem, const double* xyz, const int32_t* conn, double
   return 0;
 }
 
+// ------------------------------------------------------ facet shells (cfg4) ---
+// Flat 9-node facet shell with global node DoFs (u_x, u_y, u_z, th_x, th_y, th_z):
+// the plate above in the facet frame (e1 = node 0 -> 2, e3 = corner-plane normal,
+// e2 = e3 x e1; nodes projected onto that plane), with the chain rule
+// dN = dshape inv(J)^T (annular frame webs have non-diagonal J), a Hughes-Brezzi
+// drilling term gamma int (t3 - (v,x - u,y)/2)^2 dA (gamma = drill G t) and rotary
+// inertia rho t^3/12 on t3, rotated to global per node block:
+// u_loc = R u, bx = R[1].th, by = -R[0].th, t3 = R[2].th (oracle/fuselage.py).
+// One CTA per element; the local 54 x 54 matrix is staged in shared memory and
+// each thread forms global entries from the 3 x 3 non-zero rotation sub-blocks.
+constexpr int FS_NT = 128;
+
+__device__ __forceinline__ void quad9_geom_chain(const double (*X)[2], const double* dN_ref, double* dNx,
+                                                 double* wdet, double w, int* bad, int e) {
+  double J[2][2] = {{0, 0}, {0, 0}};
+  for (int i = 0; i < 9; ++i)
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) J[a][b] += dN_ref[i * 2 + a] * X[i][b];
+  const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  if (!(det > 0.0)) atomicMin(bad, e);
+  const double id = 1.0 / det;
+  const double iJ[2][2] = {{J[1][1] * id, -J[0][1] * id}, {-J[1][0] * id, J[0][0] * id}};
+  for (int i = 0; i < 9; ++i)
+    for (int b = 0; b < 2; ++b) dNx[i * 2 + b] = dN_ref[i * 2] * iJ[b][0] + dN_ref[i * 2 + 1] * iJ[b][1];
+  *wdet = w * det;
+}
+
+__global__ void __launch_bounds__(FS_NT) facet_shell_kernel(int n_elem, const double* __restrict__ xyz,
+                                                            const int32_t* __restrict__ conn,
+                                                            const int32_t* __restrict__ mat,
+                                                            const double* __restrict__ props, double drill,
+                                                            double* __restrict__ Ke, double* __restrict__ Me,
+                                                            int* __restrict__ bad) {
+  __shared__ double X3[9][3], X[9][2], R[3][3], T[6][6];
+  __shared__ double dF[9][18], wF[9], NF[9][9];
+  __shared__ double dR[4][18], wR[4], NR[4][9];
+  __shared__ double Ls[54 * 54];
+  const int tid = threadIdx.x;
+  for (int e = blockIdx.x; e < n_elem; e += gridDim.x) {
+    const int m = mat[e];
+    const double E = props[m * 4 + 0], nu = props[m * 4 + 1], rho = props[m * 4 + 2], t = props[m * 4 + 3];
+    const double cm = E * t / (1.0 - nu * nu), cb = E * t * t * t / (12.0 * (1.0 - nu * nu));
+    const double G = E / (2.0 * (1.0 + nu));
+    const double gs = 5.0 / 6.0 * G * t, gam = drill * G * t;
+    const double mt = rho * t, mr = rho * t * t * t / 12.0;
+    if (tid < 27) X3[tid / 3][tid % 3] = xyz[(size_t)conn[(size_t)e * 9 + tid / 3] * 3 + tid % 3];
+    __syncthreads();
+    if (tid == 0) {
+      double e1[3], v2[3], e3[3];
+      for (int b = 0; b < 3; ++b) { e1[b] = X3[2][b] - X3[0][b]; v2[b] = X3[6][b] - X3[0][b]; }
+      e3[0] = e1[1] * v2[2] - e1[2] * v2[1];
+      e3[1] = e1[2] * v2[0] - e1[0] * v2[2];
+      e3[2] = e1[0] * v2[1] - e1[1] * v2[0];
+      const double n1 = 1.0 / sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+      const double n3 = 1.0 / sqrt(e3[0] * e3[0] + e3[1] * e3[1] + e3[2] * e3[2]);
+      for (int b = 0; b < 3; ++b) { R[0][b] = e1[b] * n1; R[2][b] = e3[b] * n3; }
+      R[1][0] = R[2][1] * R[0][2] - R[2][2] * R[0][1];
+      R[1][1] = R[2][2] * R[0][0] - R[2][0] * R[0][2];
+      R[1][2] = R[2][0] * R[0][1] - R[2][1] * R[0][0];
+    }
+    __syncthreads();
+    if (tid < 18) {
+      const int i = tid / 2, a = tid % 2;
+      X[i][a] = (X3[i][0] - X3[0][0]) * R[a][0] + (X3[i][1] - X3[0][1]) * R[a][1] + (X3[i][2] - X3[0][2]) * R[a][2];
+    } else if (tid >= 32 && tid < 68) {
+      const int q = tid - 32, p = q / 6, j = q % 6;
+      double v = 0.0;
+      if (p < 3 && j < 3) v = R[p][j];
+      else if (p == 3 && j >= 3) v = R[1][j - 3];
+      else if (p == 4 && j >= 3) v = -R[0][j - 3];
+      else if (p == 5 && j >= 3) v = R[2][j - 3];
+      T[p][j] = v;
+    }
+    __syncthreads();
+    if (tid < 9) {
+      quad9_geom_chain(X, &c_qdN[tid * 18], dF[tid], &wF[tid], c_qW[tid], bad, e);
+      for (int i = 0; i < 9; ++i) NF[tid][i] = c_qN[tid * 9 + i];
+    } else if (tid >= 32 && tid < 36) {
+      const int g = tid - 32;
+      quad9_geom_chain(X, &c_rdN[g * 18], dR[g], &wR[g], c_rW[g], bad, e);
+      for (int i = 0; i < 9; ++i) NR[g][i] = c_rN[g * 9 + i];
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      // local 54 x 54 (pass 0: stiffness, pass 1: mass)
+      for (int q = tid; q < 2916; q += FS_NT) {
+        const int A = q / 54, B = q - A * 54;
+        const int a = A / 6, pa = A - a * 6, b = B / 6, pb = B - b * 6;
+        double v = 0.0;
+        if (pass == 0) {
+          const bool mem = pa < 2 && pb < 2, ben = (pa == 3 || pa == 4) && (pb == 3 || pb == 4);
+          if (mem || ben) {
+            const int ta = mem ? pa : pa - 3, tb = mem ? pb : pb - 3;
+            const double c = mem ? cm : cb;
+            for (int g = 0; g < 9; ++g) {
+              const double ax = dF[g][a * 2], ay = dF[g][a * 2 + 1], bx = dF[g][b * 2], by = dF[g][b * 2 + 1];
+              double s;
+              if (ta == 0 && tb == 0) s = ax * bx + 0.5 * (1.0 - nu) * ay * by;
+              else if (ta == 1 && tb == 1) s = ay * by + 0.5 * (1.0 - nu) * ax * bx;
+              else if (ta == 0) s = nu * ax * by + 0.5 * (1.0 - nu) * ay * bx;
+              else s = nu * ay * bx + 0.5 * (1.0 - nu) * ax * by;
+              v += wF[g] * c * s;
+            }
+          }
+          if (pa >= 2 && pa <= 4 && pb >= 2 && pb <= 4) {  // transverse shear, reduced rule
+            for (int g = 0; g < 4; ++g) {
+              double sa0, sa1, sb0, sb1;
+              if (pa == 2) { sa0 = dR[g][a * 2]; sa1 = dR[g][a * 2 + 1]; }
+              else if (pa == 3) { sa0 = NR[g][a]; sa1 = 0.0; }
+              else { sa0 = 0.0; sa1 = NR[g][a]; }
+              if (pb == 2) { sb0 = dR[g][b * 2]; sb1 = dR[g][b * 2 + 1]; }
+              else if (pb == 3) { sb0 = NR[g][b]; sb1 = 0.0; }
+              else { sb0 = 0.0; sb1 = NR[g][b]; }
+              v += wR[g] * gs * (sa0 * sb0 + sa1 * sb1);
+            }
+          }
+          const bool da = pa == 0 || pa == 1 || pa == 5, db = pb == 0 || pb == 1 || pb == 5;
+          if (da && db) {  // drilling: Bd = [u: +N,y / 2, v: -N,x / 2, t3: N]
+            for (int g = 0; g < 9; ++g) {
+              const double sa = pa == 0 ? 0.5 * dF[g][a * 2 + 1] : (pa == 1 ? -0.5 * dF[g][a * 2] : NF[g][a]);
+              const double sb = pb == 0 ? 0.5 * dF[g][b * 2 + 1] : (pb == 1 ? -0.5 * dF[g][b * 2] : NF[g][b]);
+              v += wF[g] * gam * sa * sb;
+            }
+          }
+        } else if (pa == pb) {
+          const double mc = pa >= 3 ? mr : mt;
+          for (int g = 0; g < 9; ++g) v += wF[g] * mc * NF[g][a] * NF[g][b];
+        }
+        Ls[q] = v;
+      }
+      __syncthreads();
+      double* out = (pass == 0 ? Ke : Me) + (size_t)e * 2916;
+      for (int q = tid; q < 2916; q += FS_NT) {
+        const int A = q / 54, B = q - A * 54;
+        const int a = A / 6, i = A - a * 6, b = B / 6, j = B - b * 6;
+        const int p0 = i < 3 ? 0 : 3, q0 = j < 3 ? 0 : 3;
+        double v = 0.0;
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+            v += T[p0 + p][i] * Ls[(a * 6 + p0 + p) * 54 + b * 6 + q0 + r] * T[q0 + r][j];
+        out[q] = v;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+int facet_shell_elements(int n_elem, const double* xyz, const int32_t* conn, const int32_t* mat,
+                         const double* props, double drill, double* Ke, double* Me, int32_t* bad_elem_host,
+                         cudaStream_t stream) {
+  if (int rc = init_tables()) return rc;
+  if (int rc = bad_flag_reset(stream)) return rc;
+  if (n_elem > 0) {
+    const int grid = n_elem < 148 * 16 ? n_elem : 148 * 16;
+    facet_shell_kernel<<<grid, FS_NT, 0, stream>>>(n_elem, xyz, conn, mat, props, drill, Ke, Me, bad_flag_dev());
+    VB_LAUNCHED("facet_shell_kernel");
+  }
+  if (int rc = bad_flag_read(stream, bad_elem_host)) return rc;
+  return 0;
+}
+
 // ------------------------------------------------------------ pattern ---
 // Triplet t = e*nr*nc + a*nc + b of element e has row rdofs[e][a] and column
 // cdofs[e][b] (assembly.py:166-167: rows = repeat(dofs), cols = tile(dofs));
@@ -651,7 +819,7 @@ int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const doub
 }
 
 int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* Ke, double* Me,
-                    int32_t* bad_elem_host, cudaStream_t stream) {
+                    int32_t* bad_elem_host, cudaStream_t stream, int chain) {
   if (int rc = init_tables()) return rc;
   if (int rc = bad_flag_reset(stream)) return rc;
   int dev = 0, nsm = 148;
@@ -661,7 +829,7 @@ int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* 
   const int grid = need < nsm * 2 ? need : nsm * 2;
   if (grid > 0) {
     VB_CUDA(cudaFuncSetAttribute(hex27_helmholtz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EL_SMEM));
-    hex27_helmholtz_kernel<<<grid, EL_NT, EL_SMEM, stream>>>(n_elem, xyz, conn, Ke, Me, bad_flag_dev());
+    hex27_helmholtz_kernel<<<grid, EL_NT, EL_SMEM, stream>>>(n_elem, xyz, conn, Ke, Me, bad_flag_dev(), chain);
     VB_LAUNCHED("hex27_helmholtz_kernel");
   }
   if (int rc = bad_flag_read(stream, bad_elem_host)) return rc;

@@ -129,6 +129,22 @@ int vb_hex27_helmholtz_elements(int n_elem, const double* xyz, const int32_t* co
   return vb::hex27_helmholtz(n_elem, xyz, conn, Ke, Me, bad_elem_host, (cudaStream_t)stream);
 }
 
+int vb_hex27_helmholtz_elements_chain(int n_elem, const double* xyz, const int32_t* conn, double* Ke,
+                                      double* Me, int32_t* bad_elem_host, void* stream) {
+  VB_CHECK_ARG(n_elem >= 0 && xyz && conn && Ke && Me && bad_elem_host,
+               "vb_hex27_helmholtz_elements_chain: bad arguments");
+  return vb::hex27_helmholtz(n_elem, xyz, conn, Ke, Me, bad_elem_host, (cudaStream_t)stream, 1);
+}
+
+int vb_facet_shell_elements(int n_elem, const double* xyz, const int32_t* conn, const int32_t* mat,
+                            const double* props, double drill, double* Ke, double* Me, int32_t* bad_elem_host,
+                            void* stream) {
+  VB_CHECK_ARG(n_elem >= 0 && xyz && conn && mat && props && Ke && Me && bad_elem_host && drill >= 0.0,
+               "vb_facet_shell_elements: bad arguments");
+  return vb::facet_shell_elements(n_elem, xyz, conn, mat, props, drill, Ke, Me, bad_elem_host,
+                                  (cudaStream_t)stream);
+}
+
 int vb_quad9_face_mass(int n_faces, const double* xyz, const int32_t* face_conn, double* Fe,
                        void* stream) {
   VB_CHECK_ARG(n_faces >= 0 && xyz && face_conn && Fe, "vb_quad9_face_mass: bad arguments");

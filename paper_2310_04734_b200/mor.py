@@ -164,6 +164,7 @@ class FullOrderModel:
     prefer_fdm: bool = False
     schur: object = None  # schur.CoupledBoxSchur: structure + box cavity (cfg2)
     iterative: object = None  # gmres.BoxGmres: preconditioned GMRES (per-element wall impedances)
+    planes: object = None  # planes.PlaneBlockSolver: block elimination over node planes (cfg4 fuselage)
 
     def c_out_adjoint_dev(self, device) -> torch.Tensor:
         """C^H (n x n_out, complex) on the device, uploaded once per c_out and
@@ -252,6 +253,8 @@ class FullOrderModel:
             return self.fdm.factor(f, self)
         if self.schur is not None:  # Schur complement on the structure, FDM cavity
             return RefinedSolver(self.schur.factor(f), self, f)
+        if self.planes is not None:  # z-extruded plane-major model (cfg4)
+            return RefinedSolver(self.planes.factor(f), self, f)
         if self.n > DENSE_MAX_N:
             raise RuntimeError(f"n = {self.n} exceeds the dense GPU LU limit ({DENSE_MAX_N}); "
                                "attach a BoxFDM solver (FullOrderModel.fdm)")

@@ -95,3 +95,56 @@ class DenseLU:
                                  _lib.ptr(X), X.stride(0) if X.dim() == 2 else 1, _lib.ptr(work), wb,
                                  _lib.stream_handle(self.stream)), "vb_zgetrs")
         return X.view(-1) if vec else X
+
+
+LU_NB = 64  # diagonal block size of vb_zgetrf's aux inverses (csrc/lu.cu)
+
+
+def _lu_aux_views(lu: DenseLU):
+    """(Linv, Uinv, perm) views of vb_zgetrf's aux block: per 64-row diagonal
+    block the inverse of the unit-lower / upper factor (masked to its
+    triangle) and the final row permutation."""
+    cached = getattr(lu, "_aux_views", None)
+    if cached is not None:
+        return cached
+    n, nb = lu.n, LU_NB
+    nblk = (n + nb - 1) // nb
+    zb = nblk * nb * nb * 16
+    inv = lu.aux[:2 * zb].view(CDT).view(2, nblk, nb, nb)
+    Linv = torch.tril(inv[0])
+    Uinv = torch.triu(inv[1])
+    perm = lu.aux[2 * zb:2 * zb + 4 * n].view(torch.int32).long()
+    lu._aux_views = (Linv, Uinv, perm)
+    return lu._aux_views
+
+
+def lu_solve_many(lu: DenseLU, B: torch.Tensor) -> torch.Tensor:
+    """X = A^-1 B for any number of right-hand sides from vb_zgetrf factors:
+    block forward / backward substitution over the factor's 64-row diagonal
+    blocks, each step two DMMA GEMMs (vb_zgemm) — the diagonal-block inverse
+    times the block rows, then a rank-64 update of the rows still to solve."""
+    from . import linalg
+    if lu.info != 0:
+        raise RuntimeError("Factor is exactly singular")
+    n, nb = lu.n, LU_NB
+    Linv, Uinv, perm = _lu_aux_views(lu)
+    Y = B.to(CDT).index_select(0, perm).contiguous()
+    s = Y.shape[1]
+    T = torch.empty((nb, s), dtype=CDT, device=Y.device)
+    nblk = (n + nb - 1) // nb
+    A = lu.A
+    for kb in range(nblk):
+        k0 = kb * nb
+        w = min(nb, n - k0)
+        linalg.zgemm("N", Linv[kb, :w, :w], Y[k0:k0 + w], C=T[:w])
+        Y[k0:k0 + w].copy_(T[:w])
+        if k0 + w < n:
+            linalg.zgemm("N", A[k0 + w:, k0:k0 + w], T[:w], -1.0, 1.0, C=Y[k0 + w:])
+    for kb in range(nblk - 1, -1, -1):
+        k0 = kb * nb
+        w = min(nb, n - k0)
+        linalg.zgemm("N", Uinv[kb, :w, :w], Y[k0:k0 + w], C=T[:w])
+        Y[k0:k0 + w].copy_(T[:w])
+        if k0 > 0:
+            linalg.zgemm("N", A[:k0, k0:k0 + w], T[:w], -1.0, 1.0, C=Y[:k0])
+    return Y
