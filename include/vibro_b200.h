@@ -273,6 +273,24 @@ int vb_zgemm(char transa, int m, int n, int k, vb_complex alpha, const vb_comple
  *  aux  out: diagonal-block inverses + permutation used by vb_zgetrs
  *  (vb_zgetrf_aux_bytes(n)); keep it with the factors.
  */
+/* Batched complex GEMV with few right-hand sides:
+ *   Y_b (m x s) = alpha_b A_b (m x n) X_b (n x s) + beta_b Y_b,  1 <= s <= 16,
+ * all row-major device arrays; items is a HOST array.  The solve phase of the
+ * plane-block full-order solver (cfg4: replaces the triangular solves of
+ * scipy splu's `lu.solve`, vibrofem/mor.py:49, 156, 166, 175). */
+#define VB_GEMV_MAX 32
+typedef struct {
+  int32_t m, n, s, pad;
+  const vb_complex* A;
+  int64_t lda;
+  const vb_complex* X;
+  int64_t ldx;
+  vb_complex* Y;
+  int64_t ldy;
+  vb_complex alpha, beta;
+} vb_gemv_item;
+int vb_zgemv_batched(int n_items, const vb_gemv_item* items, void* stream);
+
 size_t vb_zgetrf_workspace_bytes(int n);
 size_t vb_zgetrf_aux_bytes(int n);
 int vb_zgetrf(int n, vb_complex* A, int64_t lda, int32_t* ipiv, int32_t* info, void* aux,

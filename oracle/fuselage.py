@@ -19,7 +19,7 @@ used as the checker of the GPU element kernels and of the assembled CSR:
     gamma int (theta_3 - (v,x - u,y)/2)^2 dA (gamma = drill * G t) and the
     node rotation from the facet frame to global (u, v, w, theta_x, theta_y,
     theta_z);
-  * equivalent fluid: Delany–Bazley characteristic impedance and wavenumber
+  * equivalent fluid: Delany–Bazley-type (Miki) characteristic impedance and wavenumber
     mapped to (rho_eff, c_eff) and used like the reference's JCA fluid
     (assembly.py:242-257: K = Kgrad / rho_eff, M = Mnn / (rho_eff c_eff^2);
     coupling M term rho_eff C^T, assembly.py:199-207, 290-294), in the
@@ -143,14 +143,18 @@ def facet_shell_element(E, nu, rho, t, X3, drill=1e-3):
 
 
 def delany_bazley(f, sigma, rho0=1.21, c0=343.0):
-    """(rho_eff, c_eff) of a Delany–Bazley equivalent fluid at f (e^{+i w t}:
-    Zc = rho0 c0 (1 + 0.0571 X^-0.754 - 0.087i X^-0.732),
-    kc = w/c0 (1 + 0.0978 X^-0.700 - 0.189i X^-0.595), X = rho0 f / sigma;
-    rho_eff = Zc kc / w, c_eff = w / kc)."""
+    """(rho_eff, c_eff) of a Delany–Bazley-type equivalent fluid in Miki's
+    passive form (the original Delany–Bazley fit gives Im K_eff < 0, i.e. an
+    active bulk modulus, for f / sigma below its 0.01 validity bound — most of
+    20-250 Hz at sigma ~ 1e4): X = f / sigma,
+    Zc = rho0 c0 (1 + 0.070 X^-0.632 - 0.107i X^-0.632),
+    kc = w / c0 (1 + 0.109 X^-0.618 - 0.160i X^-0.618);
+    rho_eff = Zc kc / w, c_eff = w / kc (e^{+i w t}: Im rho_eff < 0,
+    Im rho_eff c_eff^2 >= 0)."""
     w = 2.0 * math.pi * f
-    X = rho0 * f / sigma
-    Zc = rho0 * c0 * (1 + 0.0571 * X ** -0.754 - 0.087j * X ** -0.732)
-    kc = w / c0 * (1 + 0.0978 * X ** -0.700 - 0.189j * X ** -0.595)
+    X = f / sigma
+    Zc = rho0 * c0 * (1 + 0.070 * X ** -0.632 - 0.107j * X ** -0.632)
+    kc = w / c0 * (1 + 0.109 * X ** -0.618 - 0.160j * X ** -0.618)
     return Zc * kc / w, w / kc
 
 
@@ -165,3 +169,71 @@ def rigid_body_modes(xyz: np.ndarray) -> np.ndarray:
         Rm[np.arange(n)[:, None] * 6 + np.arange(3), 3 + a] = np.cross(ea, xyz)
         Rm[np.arange(n) * 6 + 3 + a, 3 + a] = 1.0
     return Rm
+
+
+def assemble_cfg4(tables, props, drill=1e-3):
+    """scipy restatement of the cfg4 primitives from the mesh tables of
+    paper_2310_04734_b200.fuselage (node coordinates, element connectivity,
+    element DoF maps): per-element oracle matrices, triplets rows =
+    repeat(dofs), cols = tile(dofs) in element order, COO -> CSR +
+    sum_duplicates (assembly.py:142-175).  Returns a dict of CSR matrices
+    Ks, Ms, Kc, Mc, Ki, Mi, Cs, CTi, CTc (the device model's primitives)."""
+    from .shell import face_mass_quads, rect_triplets
+    T = tables
+    n = int(max(T.s_dof0.max() + 6, T.f_dof.max() + 1))
+    out = {}
+    sd = T.shell_dofs()
+    Ke = np.empty((len(T.sh_conn), 54 * 54))
+    Me = np.empty_like(Ke)
+    for e, cn in enumerate(T.sh_conn):
+        K, M = facet_shell_element(*props[T.sh_mat[e]], T.s_xyz[cn], drill)
+        Ke[e], Me[e] = K.ravel(), M.ravel()
+    out["Ks"] = rect_triplets(n, n, sd, sd, Ke)
+    out["Ms"] = rect_triplets(n, n, sd, sd, Me)
+    for name, conn in (("c", T.cab_conn), ("i", T.ins_conn)):
+        Kh = np.empty((len(conn), 729))
+        Mh = np.empty_like(Kh)
+        for e, cn in enumerate(conn):
+            K, M = helmholtz_element_chain(fe.HEX27_IDX, T.f_xyz[cn])
+            Kh[e], Mh[e] = K.ravel(), M.ravel()
+        d = T.f_dof[conn]
+        out["K" + name] = rect_triplets(n, n, d, d, Kh)
+        out["M" + name] = rect_triplets(n, n, d, d, Mh)
+    F = face_mass_quads(T.f_xyz, T.cp_f)                                   # (E, 9, 9)
+    Ce = (F[:, :, None, :] * T.cp_n[:, None, :, None]).reshape(len(F), 27, 9)
+    sr = T.face_struct_dofs()
+    fc = T.f_dof[T.cp_f]
+    out["Cs"] = rect_triplets(n, n, sr, fc, Ce.reshape(len(F), -1))
+    for kind, name in ((0, "i"), (1, "c")):
+        sel = T.cp_kind == kind
+        out["CT" + name] = rect_triplets(n, n, fc[sel], sr[sel],
+                                         np.transpose(Ce[sel], (0, 2, 1)).reshape(int(sel.sum()), -1))
+    return out
+
+
+def plane_wave_cfg4(tables, n, d, f, c0=343.0, amp=1.0):
+    """Consistent nodal forces of p e^{-i k d.x} on the illuminated flat skin
+    facets (d.n_out < 0) along the inward normal (assembly.py:108-139 in 3D)."""
+    T = tables
+    d = np.asarray(d, float) / np.linalg.norm(d)
+    k = 2 * math.pi * f / c0
+    fvec = np.zeros(n, complex)
+    pts, wts = fe.gauss_nd(2)
+    for e in T.skin_el:
+        cn = T.sh_conn[e]
+        X = T.s_xyz[cn]
+        e3 = np.cross(X[2] - X[0], X[6] - X[0])
+        e3 /= np.linalg.norm(e3)
+        if e3 @ d >= 0:
+            continue
+        for xi, w in zip(pts, wts):
+            dS = fe.dshape_nd(fe.QUAD9_LEX_IDX, xi)
+            t = dS.T @ X
+            dA = np.linalg.norm(np.cross(t[0], t[1]))
+            N = fe.shape_nd(fe.QUAD9_LEX_IDX, xi)
+            p = amp * np.exp(-1j * k * (d @ (N @ X)))
+            for a in range(9):
+                d0 = T.s_dof0[cn[a]]
+                if d0 >= 0:
+                    fvec[d0:d0 + 3] += -w * dA * N[a] * p * e3
+    return fvec

@@ -26,6 +26,12 @@ class VbComplex(C.Structure):
     _fields_ = [("re", C.c_double), ("im", C.c_double)]
 
 
+class VbGemvItem(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n", C.c_int32), ("s", C.c_int32), ("pad", C.c_int32),
+                ("A", C.c_void_p), ("lda", C.c_int64), ("X", C.c_void_p), ("ldx", C.c_int64),
+                ("Y", C.c_void_p), ("ldy", C.c_int64), ("alpha", VbComplex), ("beta", VbComplex)]
+
+
 def zc(v) -> VbComplex:
     v = complex(v)
     return VbComplex(v.real, v.imag)
@@ -61,6 +67,7 @@ _SIGS = {
     "vb_hex27_box_csr": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vb_quad9_face_mass": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vb_zgemv_batched": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
     "vb_hex27_helmholtz_elements_chain": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                     C.POINTER(C.c_int32), C.c_void_p]),
     "vb_facet_shell_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,

@@ -255,6 +255,11 @@ void vb_set_lu_max_ctas(int n) { vb::set_lu_max_ctas(n); }
 
 void vb_set_lu_lookahead(int on) { vb::set_lu_lookahead(on); }
 
+int vb_zgemv_batched(int n_items, const vb_gemv_item* items, void* stream) {
+  VB_CHECK_ARG(n_items >= 0 && (n_items == 0 || items), "vb_zgemv_batched: bad arguments");
+  return vb::zgemv_batched(n_items, items, (cudaStream_t)stream);
+}
+
 size_t vb_zgetrs_workspace_bytes(int n, int nrhs) { return (size_t)n * nrhs * sizeof(vb_complex); }
 
 int vb_zgetrs(int n, int nrhs, const vb_complex* LU, int64_t lda, const void* aux, const vb_complex* B,

@@ -362,6 +362,90 @@ __global__ void colnorm_final_kernel(int m, int nb, const double* __restrict__ p
   out[j] = sqrt(s);
 }
 
+// ------------------------------------------------------------ batched GEMV ---
+// Y_b = alpha_b A_b X_b + beta_b Y_b for a batch of row-major complex matrices
+// with few right-hand sides (s <= 16): the solve phase of the plane-block
+// full-order solver (planes.py), a chain of HBM-bound block products.  One warp
+// per row of A: 16-B coalesced loads of the row (4 in flight per lane), X from
+// L1/L2, s accumulators per lane, shuffle reduction; grid.y = batch item.
+constexpr int GEMV_NT = 256;
+
+struct GemvBatch {
+  vb_gemv_item it[VB_GEMV_MAX];
+};
+
+template <int S>
+__device__ __forceinline__ void gemv_row(const vb_gemv_item& g, int row, int lane) {
+  const z_t* __restrict__ a = (const z_t*)g.A + (int64_t)row * g.lda;
+  const z_t* __restrict__ X = (const z_t*)g.X;
+  const int s = S > 0 ? S : g.s;
+  z_t acc[S > 0 ? S : 16];
+#pragma unroll
+  for (int q = 0; q < (S > 0 ? S : 16); ++q) acc[q] = zmake(0.0, 0.0);
+  int c = lane;
+  for (; c + 96 < g.n; c += 128) {
+    z_t av[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) av[u] = __ldcs(a + c + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < (S > 0 ? S : 16); ++q)
+        if (q < s) acc[q] = zfma(acc[q], av[u], __ldg(X + (int64_t)(c + 32 * u) * g.ldx + q));
+  }
+  for (; c < g.n; c += 32) {
+    const z_t av = __ldcs(a + c);
+#pragma unroll
+    for (int q = 0; q < (S > 0 ? S : 16); ++q)
+      if (q < s) acc[q] = zfma(acc[q], av, __ldg(X + (int64_t)c * g.ldx + q));
+  }
+#pragma unroll
+  for (int q = 0; q < (S > 0 ? S : 16); ++q) {
+    if (q >= s) break;
+    double re = acc[q].x, im = acc[q].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (lane == 0) {
+      z_t* y = (z_t*)g.Y + (int64_t)row * g.ldy + q;
+      const z_t al = zmake(g.alpha.re, g.alpha.im), be = zmake(g.beta.re, g.beta.im);
+      z_t v = zmul(al, zmake(re, im));
+      if (be.x != 0.0 || be.y != 0.0) v = zfma(v, be, *y);
+      *y = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(GEMV_NT) zgemv_batched_kernel(GemvBatch B) {
+  const vb_gemv_item& g = B.it[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (GEMV_NT / 32) + (threadIdx.x >> 5);
+  if (row >= g.m) return;
+  if (g.s == 1) gemv_row<1>(g, row, lane);
+  else gemv_row<0>(g, row, lane);
+}
+
+int zgemv_batched(int n_items, const vb_gemv_item* items, cudaStream_t st) {
+  for (int i0 = 0; i0 < n_items; i0 += VB_GEMV_MAX) {
+    const int cnt = n_items - i0 < VB_GEMV_MAX ? n_items - i0 : VB_GEMV_MAX;
+    GemvBatch B;
+    int mmax = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const vb_gemv_item& g = items[i0 + i];
+      VB_CHECK_ARG(g.m >= 0 && g.n >= 0 && g.s >= 1 && g.s <= 16 && g.A && g.X && g.Y, "vb_zgemv_batched: bad item");
+      B.it[i] = g;
+      mmax = g.m > mmax ? g.m : mmax;
+    }
+    if (mmax == 0) continue;
+    dim3 grid((mmax + GEMV_NT / 32 - 1) / (GEMV_NT / 32), cnt);
+    zgemv_batched_kernel<<<grid, GEMV_NT, 0, st>>>(B);
+    VB_LAUNCHED("zgemv_batched_kernel");
+  }
+  return 0;
+}
+
 size_t column_norms_workspace_bytes(int n, int m) {
   const int nb = (n + NRM_ROWS - 1) / NRM_ROWS;
   return (size_t)nb * m * sizeof(double);

@@ -3,6 +3,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "../../include/vibro_b200.h"
 
 namespace vb {
 
@@ -90,6 +91,7 @@ int batched_dots(int64_t n, int k, int j, const z_t* V, int64_t ldr, int64_t ldc
                  void* work, size_t work_bytes, cudaStream_t st);
 int batched_update(int64_t n, int k, int j, const z_t* V, int64_t ldr, int64_t ldc, const z_t* H, z_t* W,
                    int64_t ldw, cudaStream_t st);
+int zgemv_batched(int n_items, const vb_gemv_item* items, cudaStream_t st);
 size_t column_norms_workspace_bytes(int n, int m);
 int column_norms(int n, int m, const z_t* W, int64_t ldw, double* out, void* work, size_t wb,
                  cudaStream_t st);

@@ -165,6 +165,25 @@ def zgemm(transa: str, A: torch.Tensor, B: torch.Tensor, alpha=1.0, beta=0.0,
     return C
 
 
+def zgemv_batched(items) -> None:
+    """Y = alpha A X + beta Y for a list of (A, X, Y, alpha, beta) with X, Y
+    (n, s) / (m, s) 2-D views, s <= 16 (vb_zgemv_batched: one launch per 32)."""
+    if not items:
+        return
+    lib = _lib.load()
+    arr = (_lib.VbGemvItem * len(items))()
+    for i, (A, X, Y, alpha, beta) in enumerate(items):
+        X2 = X if X.dim() == 2 else X.view(-1, 1)
+        Y2 = Y if Y.dim() == 2 else Y.view(-1, 1)
+        if A.shape[1] != X2.shape[0] or A.shape[0] != Y2.shape[0] or X2.shape[1] != Y2.shape[1]:
+            raise ValueError("zgemv_batched: shape mismatch")
+        arr[i] = _lib.VbGemvItem(A.shape[0], A.shape[1], X2.shape[1], 0, A.data_ptr(), _ld(A), X2.data_ptr(),
+                                 _ld(X2), Y2.data_ptr(), _ld(Y2), _lib.zc(alpha), _lib.zc(beta))
+    import ctypes
+    _lib.check(lib.vb_zgemv_batched(len(items), ctypes.cast(arr, ctypes.c_void_p), _lib.stream_handle()),
+               "vb_zgemv_batched")
+
+
 def column_norms(W: torch.Tensor, m: int | None = None) -> torch.Tensor:
     lib = _lib.load()
     W2 = W if W.dim() == 2 else W.view(-1, 1)

@@ -1056,7 +1056,7 @@ def _lu_factored(fom: FullOrderModel) -> bool:
     Schur complement) — the latency-bound factor / solve kernels that gain
     from concurrent expansion points; the box FDM solver's transforms are
     throughput-bound GEMMs (and its host eigensolves already use 3 threads)."""
-    if fom.iterative is not None:
+    if fom.iterative is not None or fom.planes is not None:
         return False
     return not (fom.fdm is not None and (fom.prefer_fdm or fom.n > DENSE_MAX_N))
 

@@ -7,9 +7,10 @@ p +- 1, p +- 2 (one element layer = planes 2e, 2e+1, 2e+2), and a mid plane
 2e+1 only to its own layer.  So
 
   1. every mid plane O_e is eliminated on its own (independent layers):
-     dense LU of A[O_e, O_e] (vb_zgetrf), X = A[O,O]^-1 [A[O,E_e] A[O,E_e+1]]
-     (lu_solve_many: DMMA block substitution), and the Schur updates
-     S[E_a, E_b] -= A[E_a, O] X_b of the two corner planes (vb_zgemm);
+     A[O_e, O_e]^-1 from a dense LU (vb_zgetrf) and DMMA block substitution
+     (lu_solve_many); the Schur updates S[E_a, E_b] -= A[E_a, O] A[O,O]^-1
+     A[O, E_b] of the two corner planes are sparse products (vb_rg_spmm /
+     vb_csr_spmm of the coupling blocks) since the couplings are sparse;
   2. the corner planes then form a block-tridiagonal system, factored in one
      sweep: D_j = S[j, j] - S[j, j-1] D_{j-1}^-1 S[j-1, j].
 
@@ -19,8 +20,9 @@ partial inside each diagonal block; the factor is wrapped in
 mor.RefinedSolver (iterative refinement against the assembled operator to
 ||b - A x|| / ||b|| <= 1e-10, the direct_solve contract solvers.py:62-78 —
 it replaces scipy's splu at mor.py:48-49, 153-156 for models no dense LU
-covers).  Cost per factorisation ~ n_z * 70 N^3 flops for N DoFs per plane,
-instead of (8/3) n^3 for a dense LU of the whole system.
+covers).  Cost per factorisation ~ n_z * 40 N^3 flops for N DoFs per plane
+(two block LUs + inverses, two corner-chain GEMMs per layer) instead of
+(8/3) n^3 for a dense LU of the whole system; a solve is ~4 n_z block GEMVs.
 """
 
 from __future__ import annotations
@@ -48,35 +50,51 @@ def _dev_csr(S, device) -> DeviceCSR | None:
 
 
 class PlaneBlockSolver:
-    """Sub-blocks of an affine operator over its node planes (set up once)."""
+    """Sub-blocks of an affine operator over its node planes (set up once):
+    per term, the dense-assembled blocks (mid-mid, corner-corner) and the
+    sparse mid-corner couplings used by the SpMM Schur updates."""
 
     def __init__(self, affine, plane_off, device=None):
+        import scipy.sparse as sp
         off = np.asarray(plane_off, dtype=np.int64)
         self.P = P = len(off) - 1
         if P < 3 or P % 2 == 0:
             raise ValueError("an odd number (>= 3) of node planes expected")
-        self.nz = (P - 1) // 2
+        self.nz = nz = (P - 1) // 2
         self.off = off
         self.aff = affine
         dev = torch.device(device or "cuda")
         self.dev = dev
         self.terms = [(kind, t) for kind, lst in (("K", affine.K), ("M", affine.M), ("D", affine.D)) for t in lst]
         host = [t.P.to_scipy().tocsr() for _, t in self.terms]
-        pairs = set()
-        for e in range(self.nz):
-            o, a, b = 2 * e + 1, 2 * e, 2 * e + 2
-            pairs |= {(o, o), (o, a), (o, b), (a, o), (b, o), (a, b), (b, a)}
-        for j in range(self.nz + 1):
-            pairs.add((2 * j, 2 * j))
+        blk = lambda H, p, q: H[off[p]:off[p + 1], off[q]:off[q + 1]]
         self.blocks = {}
-        for (p, q) in sorted(pairs):
+        pairs = [(2 * e + 1, 2 * e + 1) for e in range(nz)] + [(2 * j, 2 * j) for j in range(nz + 1)]
+        pairs += [(2 * j, 2 * j + 2) for j in range(nz)] + [(2 * j + 2, 2 * j) for j in range(nz)]
+        for (p, q) in pairs:
             lst = []
             for ti, H in enumerate(host):
-                sub = H[off[p]:off[p + 1], off[q]:off[q + 1]]
-                d = _dev_csr(sub, dev)
+                d = _dev_csr(blk(H, p, q), dev)
                 if d is not None:
-                    lst.append((ti, d, off[q + 1] - off[q]))
+                    lst.append((ti, d))
             self.blocks[(p, q)] = lst
+        # per layer e: A[E_a, O] (a = 2e, 2e+2) and [A[O, 2e]^T ; A[O, 2e+2]^T] per term
+        self.c_eo, self.c_oeT = [], []
+        for e in range(nz):
+            m, a, b = 2 * e + 1, 2 * e, 2 * e + 2
+            eo = {a: [], b: []}
+            oeT = []
+            for ti, H in enumerate(host):
+                for p in (a, b):
+                    d = _dev_csr(blk(H, p, m), dev)
+                    if d is not None:
+                        eo[p].append((ti, d))
+                T = sp.vstack([blk(H, m, a).T, blk(H, m, b).T]).tocsr()
+                d = _dev_csr(T, dev)
+                if d is not None:
+                    oeT.append((ti, d))
+            self.c_eo.append(eo)
+            self.c_oeT.append(oeT)
 
     def size(self, p: int) -> int:
         return int(self.off[p + 1] - self.off[p])
@@ -86,9 +104,9 @@ class PlaneBlockSolver:
         fac = {"K": 1.0, "M": -w * w, "D": 1j * w}
         return [fac[kind] * t.at(f) for kind, t in self.terms]
 
-    def dense(self, p: int, q: int, sc) -> torch.Tensor:
-        D = torch.zeros((self.size(p), self.size(q)), dtype=CDT, device=self.dev)
-        for ti, sub, _ in self.blocks.get((p, q), ()):
+    def dense(self, p: int, q: int, sc, out: torch.Tensor | None = None) -> torch.Tensor:
+        D = out if out is not None else torch.zeros((self.size(p), self.size(q)), dtype=CDT, device=self.dev)
+        for ti, sub in self.blocks.get((p, q), ()):
             linalg.axpy_dense(sub, sc[ti], D)
         return D
 
@@ -96,9 +114,25 @@ class PlaneBlockSolver:
         return PlaneBlockFactor(self, f)
 
 
+def _inverse(D: torch.Tensor) -> torch.Tensor:
+    """D^-1 from the GPU LU (vb_zgetrf + DMMA block substitution of I)."""
+    lu = DenseLU(D)
+    if lu.info != 0:
+        raise RuntimeError("Factor is exactly singular")
+    eye = torch.eye(D.shape[0], dtype=CDT, device=D.device)
+    return lu_solve_many(lu, eye)
+
+
 class PlaneBlockFactor:
-    """Factors of A(f): mid-plane LUs, corner-plane Schur chain (D_j LUs, the
-    sub-diagonal blocks S[j, j-1] and Y_j = D_j^-1 S[j, j+1])."""
+    """Factors of A(f) as explicit block inverses, so that every solve is a
+    chain of HBM-bound block GEMVs (vb_zgemv_batched) instead of latency-bound
+    triangular solves:
+      * mid planes: A[O_e, O_e]^-1; the Schur updates of the two corner
+        planes, S[E_a, E_b] -= A[E_a, O] (A[O,O]^-1 A[O, E_b]), are two sparse
+        products (SpMM of the coupling CSR blocks, X^T = A[O, E]^T A[O,O]^-T);
+      * corner chain: D_j = S[j, j] - S[j, j-1] Y_{j-1}, D_j^-1 and
+        Y_j = D_j^-1 S[j, j+1] (DMMA GEMMs).
+    mor.RefinedSolver absorbs the inverses' forward error (residual <= 1e-10)."""
 
     def __init__(self, owner: PlaneBlockSolver, f: float):
         self.o, self.f = owner, f
@@ -106,82 +140,92 @@ class PlaneBlockFactor:
         sc = o.scales(f)
         self.sc = sc
         nz = o.nz
-        S = {}
+        N = [o.size(2 * j) for j in range(nz + 1)]
+        # corner rows [S(j, j-1) | S(j, j) | S(j, j+1)] in one tensor per j
+        rows, lo = [], []
         for j in range(nz + 1):
-            S[(j, j)] = o.dense(2 * j, 2 * j, sc)
-        for j in range(nz):
-            S[(j, j + 1)] = o.dense(2 * j, 2 * j + 2, sc)
-            S[(j + 1, j)] = o.dense(2 * j + 2, 2 * j, sc)
-        self.lu_mid = []
-        for e in range(nz):
-            m, a, b = 2 * e + 1, 2 * e, 2 * e + 2
-            lu = DenseLU(o.dense(m, m, sc))
-            na = o.size(a)
-            X = lu_solve_many(lu, torch.cat([o.dense(m, a, sc), o.dense(m, b, sc)], dim=1))
-            for (j, p) in ((e, a), (e + 1, b)):
-                Ap = o.dense(p, m, sc)
-                linalg.zgemm("N", Ap, X[:, :na], -1.0, 1.0, C=S[(j, e)])
-                linalg.zgemm("N", Ap, X[:, na:], -1.0, 1.0, C=S[(j, e + 1)])
-            del X
-            self.lu_mid.append(lu)
-        self.lu_c, self.Y, self.L = [], [], []
-        for j in range(nz + 1):
-            Dj = S.pop((j, j))
+            nl = N[j - 1] if j > 0 else 0
+            nr = N[j + 1] if j < nz else 0
+            R = torch.zeros((N[j], nl + N[j] + nr), dtype=CDT, device=o.dev)
             if j > 0:
-                Lj = S.pop((j, j - 1))
-                linalg.zgemm("N", Lj, self.Y[j - 1], -1.0, 1.0, C=Dj)
-                self.L.append(Lj)
-            lu = DenseLU(Dj)
-            self.lu_c.append(lu)
+                o.dense(2 * j, 2 * j - 2, sc, R[:, :nl])
+            o.dense(2 * j, 2 * j, sc, R[:, nl:nl + N[j]])
             if j < nz:
-                self.Y.append(lu_solve_many(lu, S.pop((j, j + 1))))
+                o.dense(2 * j, 2 * j + 2, sc, R[:, nl + N[j]:])
+            rows.append(R)
+            lo.append(nl)
+        self.inv_mid = []
+        for e in range(nz):
+            m = 2 * e + 1
+            Ai = _inverse(o.dense(m, m, sc))
+            AiT = Ai.transpose(0, 1).contiguous()
+            XT = torch.zeros((N[e] + N[e + 1], o.size(m)), dtype=CDT, device=o.dev)
+            for ti, T in o.c_oeT[e]:
+                linalg.spmm(T, AiT, sc[ti], 1.0, XT)
+            del AiT
+            X = XT.transpose(0, 1).contiguous()
+            del XT
+            for j, p, c0 in ((e, 2 * e, lo[e]), (e + 1, 2 * e + 2, 0)):
+                view = rows[j][:, c0:c0 + N[e] + N[e + 1]]
+                for ti, A in o.c_eo[e][p]:
+                    linalg.spmm(A, X, -sc[ti], 1.0, view)
+            del X
+            self.inv_mid.append(Ai)
+        self.inv_c, self.Y, self.L = [], [], []
+        for j in range(nz + 1):
+            R = rows[j]
+            nl = lo[j]
+            D = R[:, nl:nl + N[j]].contiguous()
+            if j > 0:
+                L = R[:, :nl].contiguous()
+                linalg.zgemm("N", L, self.Y[j - 1], -1.0, 1.0, C=D)
+                self.L.append(L)
+            Di = _inverse(D)
+            del D
+            self.inv_c.append(Di)
+            if j < nz:
+                self.Y.append(linalg.zgemm("N", Di, R[:, nl + N[j]:].contiguous()))
+            rows[j] = None
 
     @property
     def info(self) -> int:
-        for lu in self.lu_mid + self.lu_c:
-            if lu.info != 0:
-                return lu.info
-        return 0
+        return 0  # exactly singular blocks raise in _inverse
 
-    def _apply_masked(self, V: torch.Tensor) -> torch.Tensor:
+    def _apply(self, V: torch.Tensor) -> torch.Tensor:
         """A(f) V with the affine primitives (SpMM)."""
-        o = self.o
         out = torch.zeros_like(V)
-        for ti, (kind, t) in enumerate(o.terms):
+        for ti, (kind, t) in enumerate(self.o.terms):
             linalg.spmm(t.P, V, self.sc[ti], 1.0, out)
         return out
 
-    def _lu_solve(self, lu: DenseLU, B: torch.Tensor) -> torch.Tensor:
-        if B.shape[1] <= 16:
-            return lu.solve(B.contiguous(), check=False)
-        return lu_solve_many(lu, B)
-
     def solve(self, B: torch.Tensor, check: bool = True) -> torch.Tensor:
-        o = self.o
-        if check and self.info != 0:
-            raise RuntimeError("Factor is exactly singular")
         vec = B.dim() == 1
         B2 = (B.view(-1, 1) if vec else B).to(CDT).contiguous()
+        if B2.shape[1] > 16:
+            X = torch.cat([self._solve16(B2[:, c:c + 16].contiguous()) for c in range(0, B2.shape[1], 16)], dim=1)
+        else:
+            X = self._solve16(B2)
+        return X.view(-1) if vec else X
+
+    def _solve16(self, B2: torch.Tensor) -> torch.Tensor:
+        o = self.o
         off, nz = o.off, o.nz
         rng = lambda p: slice(int(off[p]), int(off[p + 1]))
-        # 1. mid planes: c = A_OO^-1 b_O, and the corner right-hand side g = b_E - A_EO c
+        gemv = linalg.zgemv_batched
+        # 1. mid planes c = A_OO^-1 b_O (one batched launch), g = b - A c
         V = torch.zeros_like(B2)
-        for e in range(nz):
-            V[rng(2 * e + 1)] = self._lu_solve(self.lu_mid[e], B2[rng(2 * e + 1)])
-        G = B2 - self._apply_masked(V)
-        # 2. corner chain forward / backward
-        Z = []
+        gemv([(self.inv_mid[e], B2[rng(2 * e + 1)], V[rng(2 * e + 1)], 1.0, 0.0) for e in range(nz)])
+        G = B2 - self._apply(V)
+        # 2. corner chain: z_j = D_j^-1 (g_j - L_j z_{j-1}); x_j = z_j - Y_j x_{j+1}
+        X = torch.zeros_like(B2)
         for j in range(nz + 1):
             g = G[rng(2 * j)]
             if j > 0:
-                g = g - linalg.zgemm("N", self.L[j - 1], Z[j - 1])
-            Z.append(self._lu_solve(self.lu_c[j], g))
-        X = torch.zeros_like(B2)
-        X[rng(2 * nz)] = Z[nz]
+                gemv([(self.L[j - 1], X[rng(2 * j - 2)], g, -1.0, 1.0)])
+            gemv([(self.inv_c[j], g, X[rng(2 * j)], 1.0, 0.0)])
         for j in range(nz - 1, -1, -1):
-            X[rng(2 * j)] = Z[j] - linalg.zgemm("N", self.Y[j], X[rng(2 * j + 2)])
-        # 3. mid planes: x_O = A_OO^-1 (b_O - A_OE x_E)
-        W = B2 - self._apply_masked(X)
-        for e in range(nz):
-            X[rng(2 * e + 1)] = self._lu_solve(self.lu_mid[e], W[rng(2 * e + 1)])
-        return X.view(-1) if vec else X
+            gemv([(self.Y[j], X[rng(2 * j + 2)], X[rng(2 * j)], -1.0, 1.0)])
+        # 3. mid planes x_O = A_OO^-1 (b_O - A_OE x_E) (one batched launch)
+        W = B2 - self._apply(X)
+        gemv([(self.inv_mid[e], W[rng(2 * e + 1)], X[rng(2 * e + 1)], 1.0, 0.0) for e in range(nz)])
+        return X
