@@ -64,6 +64,8 @@ class PlaneBlockSolver:
         self.off = off
         self.aff = affine
         dev = torch.device(device or "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
         self.terms = [(kind, t) for kind, lst in (("K", affine.K), ("M", affine.M), ("D", affine.D)) for t in lst]
         host = [t.P.to_scipy().tocsr() for _, t in self.terms]
