@@ -366,7 +366,7 @@ __global__ void colnorm_final_kernel(int m, int nb, const double* __restrict__ p
 // Y_b = alpha_b A_b X_b + beta_b Y_b for a batch of row-major complex matrices
 // with few right-hand sides (s <= 16): the solve phase of the plane-block
 // full-order solver (planes.py), a chain of HBM-bound block products.  One warp
-// per row of A: 16-B coalesced loads of the row (4 in flight per lane), X from
+// per row of A: 16-B coalesced loads of the row (8 in flight per lane), X from
 // L1/L2, s accumulators per lane, shuffle reduction; grid.y = batch item.
 constexpr int GEMV_NT = 256;
 
@@ -383,12 +383,12 @@ __device__ __forceinline__ void gemv_row(const vb_gemv_item& g, int row, int lan
 #pragma unroll
   for (int q = 0; q < (S > 0 ? S : 16); ++q) acc[q] = zmake(0.0, 0.0);
   int c = lane;
-  for (; c + 96 < g.n; c += 128) {
-    z_t av[4];
+  for (; c + 224 < g.n; c += 256) {
+    z_t av[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) av[u] = __ldcs(a + c + 32 * u);
+    for (int u = 0; u < 8; ++u) av[u] = __ldcs(a + c + 32 * u);
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int q = 0; q < (S > 0 ? S : 16); ++q)
         if (q < s) acc[q] = zfma(acc[q], av[u], __ldg(X + (int64_t)(c + 32 * u) * g.ldx + q));
