@@ -170,10 +170,11 @@ int vb_hex27_helmholtz_elements_chain(int n_elem, const double* xyz, const int32
  * reference's plane-stress element (vibrofem/assembly.py:31-67), Reissner-
  * Mindlin bending + 2x2 shear, Hughes-Brezzi drilling term (drill * G t),
  * rotated from the facet frame.  mat [n_elem] indexes props [n_mat][4] =
- * (E, nu, rho, t) (device); Ke, Me [n_elem][54][54] out. */
+ * (E, nu, rho, t) (device); Ke, Me [n_elem][54][54] out.  *bad_elem_host =
+ * first element with detJ <= 0 or a material index outside [0, n_mat), or -1. */
 int vb_facet_shell_elements(int n_elem, const double* xyz, const int32_t* conn, const int32_t* mat,
-                            const double* props, double drill, double* Ke, double* Me, int32_t* bad_elem_host,
-                            void* stream);
+                            const double* props, int n_mat, double drill, double* Ke, double* Me,
+                            int32_t* bad_elem_host, void* stream);
 
 /* ------------------------------------------------------------------------
  * Offline-phase linear algebra

@@ -70,8 +70,8 @@ _SIGS = {
     "vb_zgemv_batched": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
     "vb_hex27_helmholtz_elements_chain": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                     C.POINTER(C.c_int32), C.c_void_p]),
-    "vb_facet_shell_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
-                                          C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p]),
+    "vb_facet_shell_elements": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                          C.c_double, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p]),
     "vb_csr_spmm": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _z, C.c_int64, _z,
                               C.c_int64, VbComplex, VbComplex, C.c_void_p]),
     "vb_csr_row_groups": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -490,16 +490,20 @@ __device__ __forceinline__ void quad9_geom_chain(const double (*X)[2], const dou
 __global__ void __launch_bounds__(FS_NT) facet_shell_kernel(int n_elem, const double* __restrict__ xyz,
                                                             const int32_t* __restrict__ conn,
                                                             const int32_t* __restrict__ mat,
-                                                            const double* __restrict__ props, double drill,
-                                                            double* __restrict__ Ke, double* __restrict__ Me,
-                                                            int* __restrict__ bad) {
+                                                            const double* __restrict__ props, int n_mat,
+                                                            double drill, double* __restrict__ Ke,
+                                                            double* __restrict__ Me, int* __restrict__ bad) {
   __shared__ double X3[9][3], X[9][2], R[3][3], T[6][6];
   __shared__ double dF[9][18], wF[9], NF[9][9];
   __shared__ double dR[4][18], wR[4], NR[4][9];
   __shared__ double Ls[54 * 54];
   const int tid = threadIdx.x;
   for (int e = blockIdx.x; e < n_elem; e += gridDim.x) {
-    const int m = mat[e];
+    int m = mat[e];
+    if (m < 0 || m >= n_mat) {  // reported like a degenerate element (no out-of-range read)
+      if (tid == 0) atomicMin(bad, e);
+      m = 0;
+    }
     const double E = props[m * 4 + 0], nu = props[m * 4 + 1], rho = props[m * 4 + 2], t = props[m * 4 + 3];
     const double cm = E * t / (1.0 - nu * nu), cb = E * t * t * t / (12.0 * (1.0 - nu * nu));
     const double G = E / (2.0 * (1.0 + nu));
@@ -610,13 +614,14 @@ __global__ void __launch_bounds__(FS_NT) facet_shell_kernel(int n_elem, const do
 }
 
 int facet_shell_elements(int n_elem, const double* xyz, const int32_t* conn, const int32_t* mat,
-                         const double* props, double drill, double* Ke, double* Me, int32_t* bad_elem_host,
-                         cudaStream_t stream) {
+                         const double* props, int n_mat, double drill, double* Ke, double* Me,
+                         int32_t* bad_elem_host, cudaStream_t stream) {
   if (int rc = init_tables()) return rc;
   if (int rc = bad_flag_reset(stream)) return rc;
   if (n_elem > 0) {
     const int grid = n_elem < 148 * 16 ? n_elem : 148 * 16;
-    facet_shell_kernel<<<grid, FS_NT, 0, stream>>>(n_elem, xyz, conn, mat, props, drill, Ke, Me, bad_flag_dev());
+    facet_shell_kernel<<<grid, FS_NT, 0, stream>>>(n_elem, xyz, conn, mat, props, n_mat, drill, Ke, Me,
+                                                    bad_flag_dev());
     VB_LAUNCHED("facet_shell_kernel");
   }
   if (int rc = bad_flag_read(stream, bad_elem_host)) return rc;

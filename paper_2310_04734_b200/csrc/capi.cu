@@ -137,11 +137,12 @@ int vb_hex27_helmholtz_elements_chain(int n_elem, const double* xyz, const int32
 }
 
 int vb_facet_shell_elements(int n_elem, const double* xyz, const int32_t* conn, const int32_t* mat,
-                            const double* props, double drill, double* Ke, double* Me, int32_t* bad_elem_host,
-                            void* stream) {
-  VB_CHECK_ARG(n_elem >= 0 && xyz && conn && mat && props && Ke && Me && bad_elem_host && drill >= 0.0,
+                            const double* props, int n_mat, double drill, double* Ke, double* Me,
+                            int32_t* bad_elem_host, void* stream) {
+  VB_CHECK_ARG(n_elem >= 0 && n_mat > 0 && xyz && conn && mat && props && Ke && Me && bad_elem_host &&
+                   drill >= 0.0,
                "vb_facet_shell_elements: bad arguments");
-  return vb::facet_shell_elements(n_elem, xyz, conn, mat, props, drill, Ke, Me, bad_elem_host,
+  return vb::facet_shell_elements(n_elem, xyz, conn, mat, props, n_mat, drill, Ke, Me, bad_elem_host,
                                   (cudaStream_t)stream);
 }
 

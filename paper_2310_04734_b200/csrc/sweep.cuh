@@ -57,8 +57,8 @@ int csr_gather(int64_t nnz, const int64_t* gptr, const int32_t* gidx, const doub
 int hex27_helmholtz(int n_elem, const double* xyz, const int32_t* conn, double* Ke, double* Me,
                     int32_t* bad_elem_host, cudaStream_t stream, int chain = 0);
 int facet_shell_elements(int n_elem, const double* xyz, const int32_t* conn, const int32_t* mat,
-                         const double* props, double drill, double* Ke, double* Me, int32_t* bad_elem_host,
-                         cudaStream_t stream);
+                         const double* props, int n_mat, double drill, double* Ke, double* Me,
+                         int32_t* bad_elem_host, cudaStream_t stream);
 int quad9_face_mass(int n_faces, const double* xyz, const int32_t* fconn, double* Fe,
                     cudaStream_t stream);
 

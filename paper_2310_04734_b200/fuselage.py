@@ -519,10 +519,11 @@ def shell_elements(s_xyz_d: torch.Tensor, conn_d: torch.Tensor, mat_d: torch.Ten
     Me = torch.empty_like(Ke)
     bad = C.c_int32(-1)
     _lib.check(lib.vb_facet_shell_elements(ne, _lib.ptr(s_xyz_d), _lib.ptr(conn_d), _lib.ptr(mat_d),
-                                           _lib.ptr(props_d), float(drill), _lib.ptr(Ke), _lib.ptr(Me),
+                                           _lib.ptr(props_d), int(props_d.shape[0]), float(drill), _lib.ptr(Ke),
+                                           _lib.ptr(Me),
                                            C.byref(bad), _lib.stream_handle()), "vb_facet_shell_elements")
     if bad.value >= 0:
-        raise ValueError(f"non-positive Jacobian in shell element {bad.value}")
+        raise ValueError(f"non-positive Jacobian or bad material index in shell element {bad.value}")
     return Ke, Me
 
 

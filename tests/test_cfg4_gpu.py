@@ -171,3 +171,23 @@ def test_cfg4_reduced_resolution_rom_certified(cuda):
         _, e, _, _ = mor.relative_error(yf.ravel(), y[i].ravel())
         worst = max(worst, e)
     assert worst <= 1e-2, worst
+
+
+def test_facet_shell_rejects_bad_input(tiny, cuda):
+    """Material index outside [0, n_mat) and a degenerate facet raise
+    ValueError (the reference raises on detJ <= 0, assembly.py:85-86)."""
+    import torch
+    from paper_2310_04734_b200 import fuselage as fz
+    spec, fom, info = tiny
+    T = info["tables"]
+    props = torch.as_tensor(np.array(_props(spec)), device=cuda)
+    conn = torch.as_tensor(T.sh_conn[:5].astype(np.int32), device=cuda)
+    sx = torch.as_tensor(T.s_xyz, device=cuda)
+    mat = torch.as_tensor(np.array([0, 1, 7, 0, 0], np.int32), device=cuda)
+    with pytest.raises(ValueError, match="shell element 2"):
+        fz.shell_elements(sx, conn, mat, props, spec.drill)
+    bad = T.sh_conn[:1].copy()
+    bad[0, 6:] = bad[0, :3]           # collapsed facet
+    with pytest.raises(ValueError):
+        fz.shell_elements(sx, torch.as_tensor(bad.astype(np.int32), device=cuda),
+                          torch.zeros(1, dtype=torch.int32, device=cuda), props, spec.drill)

@@ -70,3 +70,17 @@ def test_offline_stages_repeat_bit_identical(cuda):
         assert _same(linalg.spmm(Kg, X, path=path), linalg.spmm(Kg, X, path=path))
     W = torch.randn(Kg.n, 40, dtype=torch.complex128, device=cuda)
     assert _same(linalg.zgemm("C", X, W), linalg.zgemm("C", X, W))
+
+
+def test_cfg4_assembly_and_plane_solver_repeat_bit_identical(cuda):
+    """cfg4: facet-shell / chain-rule element kernels + CSR gather, and the
+    plane-block factor + solve (LUs, block inverses, SpMM Schur updates,
+    batched GEMVs), twice each."""
+    from paper_2310_04734_b200 import fuselage as fz
+    spec = fz.FuselageSpec(n_th=16, n_stringers=8, n_z=6, floor_k=1, n_side=2)
+    fa, ia = fz.fuselage_model(spec, cuda)
+    fb, ib = fz.fuselage_model(spec, cuda)
+    for name in ("Ks", "Ms", "Kc", "Mi", "Cs", "CTi"):
+        assert _same(ia[name].data, ib[name].data) and _same(ia[name].indices, ib[name].indices), name
+    x = [fa.factor(173.0).solve(fa.load_dev(173.0)) for _ in range(2)]
+    assert _same(x[0], x[1])
