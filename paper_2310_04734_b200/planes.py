@@ -49,6 +49,22 @@ def _dev_csr(S, device) -> DeviceCSR | None:
                      torch.as_tensor(S.data.astype(np.float64), device=device))
 
 
+def _check_plane_structure(mats, off):
+    """Every coupling must stay inside one element layer: |p - q| <= 1, or
+    |p - q| = 2 between the two corner planes of a layer (even p, q).  Anything
+    else would be silently dropped by the block elimination."""
+    for H in mats:
+        H = H.tocoo()
+        p = np.searchsorted(off, H.row, side="right") - 1
+        q = np.searchsorted(off, H.col, side="right") - 1
+        d = np.abs(p - q)
+        bad = (d > 2) | ((d == 2) & ((p % 2 == 1) | (q % 2 == 1)))
+        if np.any(bad):
+            i = int(np.argmax(bad))
+            raise ValueError(f"operator couples node planes {int(p[i])} and {int(q[i])}: not a plane-major "
+                             "z-extruded quadratic model")
+
+
 class PlaneBlockSolver:
     """Sub-blocks of an affine operator over its node planes (set up once):
     per term, the dense-assembled blocks (mid-mid, corner-corner) and the
@@ -69,6 +85,7 @@ class PlaneBlockSolver:
         self.dev = dev
         self.terms = [(kind, t) for kind, lst in (("K", affine.K), ("M", affine.M), ("D", affine.D)) for t in lst]
         host = [t.P.to_scipy().tocsr() for _, t in self.terms]
+        _check_plane_structure(host, off)
         blk = lambda H, p, q: H[off[p]:off[p + 1], off[q]:off[q + 1]]
         self.blocks = {}
         pairs = [(2 * e + 1, 2 * e + 1) for e in range(nz)] + [(2 * j, 2 * j) for j in range(nz + 1)]

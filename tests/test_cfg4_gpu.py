@@ -191,3 +191,22 @@ def test_facet_shell_rejects_bad_input(tiny, cuda):
     with pytest.raises(ValueError):
         fz.shell_elements(sx, torch.as_tensor(bad.astype(np.int32), device=cuda),
                           torch.zeros(1, dtype=torch.int32, device=cuda), props, spec.drill)
+
+
+def test_plane_solver_rejects_foreign_structure(tiny, cuda):
+    """A primitive coupling node planes outside one element layer is refused
+    at setup (the block elimination would silently drop it)."""
+    import scipy.sparse as sp
+    import torch
+    from paper_2310_04734_b200.assembly import DeviceCSR
+    from paper_2310_04734_b200.mor import AffineOperator, AffineTerm
+    from paper_2310_04734_b200.planes import PlaneBlockSolver
+    spec, fom, info = tiny
+    off = info["mesh"].plane_off
+    n = fom.n
+    E = sp.csr_matrix(([1.0], ([int(off[1])], [int(off[3])])), shape=(n, n))   # mid plane 1 <-> mid plane 3
+    d = DeviceCSR(n, torch.as_tensor(E.indptr.astype(np.int32), device=cuda),
+                  torch.as_tensor(E.indices.astype(np.int32), device=cuda), torch.as_tensor(E.data, device=cuda))
+    aff = AffineOperator(K=list(fom.affine.K) + [AffineTerm(d, 1.0)], M=fom.affine.M, D=[], load=fom.affine.load)
+    with pytest.raises(ValueError, match="node planes 1 and 3"):
+        PlaneBlockSolver(aff, off, cuda)
