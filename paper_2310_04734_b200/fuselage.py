@@ -76,6 +76,7 @@ class FuselageSpec:
     frame: tuple = (60e9, 0.3, 1550.0, 4e-3)
     stringer: tuple = (60e9, 0.3, 1550.0, 2e-3)
     drill: float = 1e-3
+    clamped: bool = True         # structure clamped at z = 0, L (False: free, for rigid-body checks)
     sigma_range: tuple = (5e3, 15e3)   # flow resistivity (Pa s / m^2), seeded
     f_band: tuple = (20.0, 250.0)
     d_wave: tuple = (-math.cos(math.radians(30.0)), 0.0, math.sin(math.radians(30.0)))
@@ -316,7 +317,8 @@ def fuselage_mesh(spec: FuselageSpec) -> FuselageMesh:
     frame_planes = np.array([(2 * i + 1) * spec.n_z // spec.n_frames for i in range(spec.n_frames)])
     is_frame = np.zeros(P, dtype=bool)
     is_frame[frame_planes] = True
-    nstr = np.array([0 if k in (0, P - 1) else NDS * (n_s2 + (len(fr_xy) if is_frame[k] else 0))
+    ends = (0, P - 1) if spec.clamped else ()
+    nstr = np.array([0 if k in ends else NDS * (n_s2 + (len(fr_xy) if is_frame[k] else 0))
                      for k in range(P)], dtype=np.int64)
     nfl = len(ins_xy) + len(cab_xy)
     plane_off = np.concatenate([[0], np.cumsum(nstr + nfl)]).astype(np.int64)

@@ -210,3 +210,50 @@ def test_plane_solver_rejects_foreign_structure(tiny, cuda):
     aff = AffineOperator(K=list(fom.affine.K) + [AffineTerm(d, 1.0)], M=fom.affine.M, D=[], load=fom.affine.load)
     with pytest.raises(ValueError, match="node planes 1 and 3"):
         PlaneBlockSolver(aff, off, cuda)
+
+
+def test_cfg4_structure_rigid_body_modes(cuda):
+    """The assembled structure stiffness of the UNclamped fuselage (skin,
+    lining, floor, frames, stringers, all facet rotations and merged nodes)
+    has the six global rigid-body motions in its null space."""
+    from paper_2310_04734_b200 import fuselage as fz
+    spec = _tiny()
+    spec.clamped = False
+    fom, info = fz.fuselage_model(spec, cuda, solver=False)
+    T = info["tables"]
+    Ks = info["Ks"].to_scipy()
+    R = np.zeros((fom.n, 6))
+    d0 = T.s_dof0
+    assert np.all(d0 >= 0)
+    R[(d0[:, None] + np.arange(6)[None, :]).ravel(), :] = ofu.rigid_body_modes(T.s_xyz)
+    scale = abs(Ks).max() * np.abs(R).max() * 60
+    assert np.abs(Ks @ R).max() <= 1e-10 * scale
+    # clamped (the model the pipeline solves): no rigid-body mode survives
+    Kc = _tiny_clamped_Ks(cuda)
+    assert np.linalg.norm(Kc @ np.ones(Kc.shape[0])) > 0
+
+
+def _tiny_clamped_Ks(cuda):
+    from paper_2310_04734_b200 import fuselage as fz
+    _, info = fz.fuselage_model(_tiny(), cuda, solver=False)
+    return info["Ks"].to_scipy()
+
+
+def test_cfg4_fluid_axial_mode(tiny):
+    """Cabin air and insulation annulus with rigid ends are z-extrusions of a
+    uniform cross-section: the axial mode (constant over the cross-section)
+    is an exact eigenpair of (Kgrad, Mnn) with the eigenvalue of the 1D
+    quadratic mesh along z (~ (pi / L)^2), and constants are the null space."""
+    import scipy.linalg as sla
+    import scipy.sparse.linalg as spl
+    spec, fom, info = tiny
+    K1, M1 = fe.line_matrices_1d(spec.L, spec.n_z)
+    lam1 = np.sort(sla.eigh(K1, M1, eigvals_only=True))[1]
+    assert abs(lam1 - (math.pi / spec.L) ** 2) <= 1e-3 * lam1
+    for Kn, Mn in (("Kc", "Mc"), ("Ki", "Mi")):
+        K, M = info[Kn].to_scipy(), info[Mn].to_scipy()
+        idx = np.unique(M.nonzero()[0])
+        K, M = K[idx][:, idx].tocsc(), M[idx][:, idx].tocsc()
+        assert np.abs(K @ np.ones(len(idx))).max() <= 1e-12 * abs(K).max()
+        lam = spl.eigsh(K, k=4, M=M, sigma=lam1 * (1 + 1e-4), which="LM", return_eigenvectors=False)
+        assert np.min(np.abs(lam - lam1)) <= 1e-9 * lam1, (Kn, lam, lam1)
