@@ -59,6 +59,28 @@ def _krylov_worker(rank, ws, port, q):
     dist.destroy_process_group()
 
 
+CFG4_PTS = (45.0, 110.0, 170.0, 230.0)
+
+
+def _cfg4_tiny(dev):
+    from paper_2310_04734_b200 import fuselage as fz
+    spec = fz.FuselageSpec(n_th=16, n_stringers=8, n_z=6, floor_k=1, n_side=2)
+    return fz.fuselage_model(spec, dev)[0]
+
+
+def _krylov_cfg4_worker(rank, ws, port, q):
+    _env(rank, ws, port)
+    import torch
+    import torch.distributed as dist
+    from paper_2310_04734_b200 import dist as vdist
+    vdist.init(backend="gloo")
+    torch.cuda.set_device(0)
+    fom = _cfg4_tiny(torch.device("cuda:0"))
+    V = vdist.krylov_basis_sharded(fom, CFG4_PTS, 8)
+    q.put((rank, V.cpu().numpy()))
+    dist.destroy_process_group()
+
+
 def _singular_worker(rank, ws, port, q):
     _env(rank, ws, port)
     import torch
@@ -148,3 +170,15 @@ def test_sharded_sweep_singular_raises_on_every_rank(cuda):
     out = _run(_singular_worker, timeout=300)
     for rank in (0, 1):
         assert out[rank][0].startswith("LinAlgError"), out[rank]
+
+
+def test_sharded_krylov_cfg4_world2_equals_serial(cuda):
+    """cfg4 (plane-block full-order solver): expansion points split over two
+    ranks give the serial basis bit for bit."""
+    from paper_2310_04734_b200 import mor
+    out = _run(_krylov_cfg4_worker)
+    V2, _ = mor.krylov_basis(_cfg4_tiny(cuda), CFG4_PTS, 8, mimo=True)
+    V2 = V2.cpu().numpy()
+    for rank in (0, 1):
+        assert out[rank][0].shape == V2.shape
+        assert np.array_equal(out[rank][0], V2)
