@@ -673,6 +673,36 @@ def _basis_append_view(Vd, n: int, k: int, dev) -> torch.Tensor:
     return buf[:, :r + k]
 
 
+FAST_TRUST = 1e-5  # Cholesky-QR diagonal resolved by the Gram matrix (~sqrt(eps k) of the block norm)
+FAST_KEEP = 1e-8   # ... and far above the reference's drop threshold (ORTH_DROP_TOL = 1e-10)
+
+
+def _cholqr_keep_all(W: torch.Tensor, refs_dev: torch.Tensor):
+    """In-block orthonormalisation by one Cholesky QR (W = Q R, R^H R = W^H W)
+    when it provably takes the reference's decisions: R_jj is the norm of
+    column j after projection on the earlier columns — the quantity the
+    reference's MGS2 + drop rule tests (mor.py:129-134) — and the Gram
+    matrix resolves it to ~1e-2 wherever R_jj > FAST_TRUST * max ||w||, so
+    R_jj > FAST_KEEP * ||w_raw|| means "kept" with certainty.  Returns Q
+    (every column kept) or None (a column near dependence: the caller runs
+    the exact column-by-column Gram-Schmidt).  Two GEMMs over the block and a
+    host Cholesky of a k x k matrix instead of k rounds of grid reductions."""
+    kb = W.shape[1]
+    G = linalg.zgemm("C", W, W).cpu().numpy()
+    G = 0.5 * (G + G.conj().T)
+    refs = refs_dev.cpu().numpy()
+    try:
+        L = np.linalg.cholesky(G)
+    except np.linalg.LinAlgError:
+        return None
+    d = np.real(np.diag(L))
+    nmax = float(np.sqrt(np.max(np.real(np.diag(G))))) if kb else 0.0
+    if not (np.all(d > FAST_TRUST * nmax) and np.all(d > FAST_KEEP * refs)):
+        return None
+    Ri = torch.as_tensor(np.linalg.solve(L.conj().T, np.eye(kb)), device=W.device)   # R^-1
+    return linalg.zgemm("N", W, Ri)
+
+
 @_nvtx("vb.orthonormalise")
 def _orthonormalise(V, block):
     """Append the columns of `block` to V, twice-orthogonalised; columns that
@@ -705,7 +735,10 @@ def _orthonormalise(V, block):
         against_V(W)
     Qb = torch.empty((n, max(kb, 1)), dtype=CDT, device=dev)
     nk = 0
-    if fused:  # one cooperative kernel for the column loop below (vb_block_gs)
+    Qf = _cholqr_keep_all(W, refs_dev) if kb else None
+    if Qf is not None:  # every column provably kept: one Cholesky QR for the block
+        Qb, nk = Qf, kb
+    elif fused:  # one cooperative kernel for the column loop below (vb_block_gs)
         nk, _ = linalg.block_gs(W, Qb, refs_dev, ORTH_DROP_TOL, REORTH_RATIO)
     else:
         for j in range(kb):
@@ -729,19 +762,14 @@ def _orthonormalise(V, block):
         # block cost.  In place in the basis buffer; norms stay on the device.
         if Vd is not None:
             against_V(Q1)
-            if nk <= linalg.BLOCK_GS_MAX:
-                linalg.block_gs(Q1, Q1, no_drop=True)
-            else:
-                for j in range(nk):
-                    w = Q1[:, j:j + 1]
-                    if j:
-                        _cgs2_against(Q1[:, :j], w)
-                    w.div_(linalg.column_norms(w))
+        # the kept columns are orthonormal up to the rounding amplified by the
+        # in-block cancellation (or by the Gram matrix of the Cholesky-QR fast
+        # path): one more Cholesky QR re-orthonormalises them (CholQR2)
+        _cholqr_inplace(Q1)
     _BASIS_BUFS[newV.data_ptr()] = (r + nk, newV.stride(0), n)
     return newV.cpu().numpy() if is_np else newV
 
 
-@_nvtx("vb.orthonormalise_blocks")
 def _cholqr_inplace(Q: torch.Tensor):
     """Re-orthonormalise nearly orthonormal columns in place: Q <- Q R^-1 with
     R^H R = Q^H Q (Cholesky QR).  The columns come out of Gram-Schmidt
@@ -749,7 +777,7 @@ def _cholqr_inplace(Q: torch.Tensor):
     cond(Q) ~ 1 and one Cholesky QR is as accurate as another Gram-Schmidt
     pass (it is the same QR factor: R upper triangular with a positive
     diagonal is unique) at the cost of one Gram GEMM, a host Cholesky of a
-    <= 16 x 16 matrix and one GEMM, instead of 3 grid reductions per column."""
+    k x k matrix and one GEMM, instead of 3 grid reductions per column."""
     G = linalg.zgemm("C", Q, Q).cpu().numpy()
     G = 0.5 * (G + G.conj().T)
     R = np.linalg.cholesky(G).conj().T                      # G = R^H R
@@ -758,6 +786,7 @@ def _cholqr_inplace(Q: torch.Tensor):
     Q.copy_(T)
 
 
+@_nvtx("vb.orthonormalise_blocks")
 def orthonormalise_blocks(V, blocks):
     """Append several blocks to V at once — the same kept columns (in exact
     arithmetic) as `_orthonormalise` applied block by block (mor.py:122-135
@@ -816,8 +845,13 @@ def orthonormalise_blocks(V, blocks):
         Wc = W[:, c0:c0 + kb]
         if c0:
             against(Qk[:, :c0], Wc)                     # the group's earlier kept columns
-        nkc, _ = linalg.block_gs(Wc, Qk[:, c0:c0 + kb], refs[c0:c0 + kb], ORTH_DROP_TOL, REORTH_RATIO,
-                                 sync=False)
+        Qf = _cholqr_keep_all(Wc, refs[c0:c0 + kb])
+        if Qf is not None:
+            Qk[:, c0:c0 + kb].copy_(Qf)
+            nkc = torch.full((1,), kb, dtype=torch.int32, device=dev)
+        else:
+            nkc, _ = linalg.block_gs(Wc, Qk[:, c0:c0 + kb], refs[c0:c0 + kb], ORTH_DROP_TOL, REORTH_RATIO,
+                                     sync=False)
         counts.append(nkc)
         c0 += kb
     kept_sizes = [int(v) for v in torch.cat(counts).cpu().tolist()]   # one host read per group
@@ -834,14 +868,14 @@ def orthonormalise_blocks(V, blocks):
             c0 += b.shape[1]
         if Vd is not None:                              # pass 2
             against(Vd, Q1, passes=1)
-            q0 = 0
-            for kc in kept_sizes:
-                if kc:
-                    Qc = Q1[:, q0:q0 + kc]
-                    if q0:
-                        against(Q1[:, :q0], Qc)
-                    _cholqr_inplace(Qc)
-                q0 += kc
+        q0 = 0
+        for kc in kept_sizes:
+            if kc:
+                Qc = Q1[:, q0:q0 + kc]
+                if q0:
+                    against(Q1[:, :q0], Qc)
+                _cholqr_inplace(Qc)
+            q0 += kc
     _BASIS_BUFS[newV.data_ptr()] = (r + nk, newV.stride(0), n)
     return newV
 
