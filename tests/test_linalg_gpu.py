@@ -164,3 +164,38 @@ def test_orthonormalise_blocks_equals_sequential_appends(cuda):
     assert float((Vg[:, :30] - V0).abs().max()) == 0.0
     R = Vs - Vg @ (Vg.conj().T @ Vs)
     assert float(R.abs().max()) <= 1e-10
+
+
+def test_orthonormalise_cholqr_fast_path_decisions(cuda):
+    """_orthonormalise takes the Cholesky-QR fast path only when every column
+    is provably kept, and then matches the reference MGS2 basis (same span,
+    orthonormal to 1e-12); a block with a column near the drop threshold —
+    or a weakly dependent one the Gram matrix cannot resolve — goes through
+    the exact Gram-Schmidt with the reference's decisions (mor.py:122-135)."""
+    import torch
+    from oracle import mor as omor
+    from paper_2310_04734_b200 import linalg, mor
+    rng = np.random.default_rng(7)
+    n = 20000
+    V0 = np.linalg.qr(_c(rng, n, 12))[0]
+    cases = {"fast": _c(rng, n, 24),
+             "dropped": _c(rng, n, 6),
+             "weak": _c(rng, n, 6)}
+    cases["dropped"][:, 3] = cases["dropped"][:, 1] + 1e-12 * _c(rng, n)     # residual 1e-12: dropped
+    cases["weak"][:, 4] = cases["weak"][:, 0] + 1e-7 * _c(rng, n)            # 1e-7: kept, but unresolved by the Gram
+    calls = []
+    orig = mor._cholqr_keep_all
+    mor._cholqr_keep_all = lambda W, r: calls.append(orig(W, r) is not None) or orig(W, r)
+    try:
+        for name, B in cases.items():
+            calls.clear()
+            V = mor._orthonormalise(torch.as_tensor(V0, device=cuda), torch.as_tensor(B, device=cuda))
+            Vo = omor.orthonormalise(V0, B)
+            assert calls == [name == "fast"], (name, calls)
+            Vn = V.cpu().numpy()
+            assert Vn.shape == Vo.shape, name
+            assert np.abs(Vn.conj().T @ Vn - np.eye(Vn.shape[1])).max() <= 1e-12
+            assert np.abs(Vo - Vn @ (Vn.conj().T @ Vo)).max() <= 1e-8
+    finally:
+        mor._cholqr_keep_all = orig
+    assert linalg.BLOCK_GS_MAX == 16
