@@ -601,9 +601,14 @@ def run_ours(args):
     import torch
     from paper_2310_04734_b200 import _lib, dist as vdist, sweep, workloads
 
+    share = os.environ.get("VB_BENCH_SHARE_GPU") == "1"  # test hook: ranks share the visible GPUs (gloo)
+    if share:
+        os.environ.setdefault("VB_DIST_BACKEND", "gloo")
     rank, ws, local = vdist.init()
     _lib.require_cuda()
-    if torch.cuda.device_count() < ws:
+    if share:
+        local = local % torch.cuda.device_count()
+    elif torch.cuda.device_count() < ws:
         raise SystemExit(f"bench.py: {ws} ranks but only {torch.cuda.device_count()} visible GPUs")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -23,8 +23,8 @@ def world() -> tuple[int, int, int]:
 def init(backend: str | None = None):
     rank, ws, local = world()
     if ws > 1 and not dist.is_initialized():
-        if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend is None:  # VB_DIST_BACKEND: e.g. gloo for ranks sharing one GPU in tests
+            backend = os.environ.get("VB_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend, rank=rank, world_size=ws)
