@@ -134,3 +134,35 @@ def test_cfg4_full_size_dofs():
     from paper_2310_04734_b200 import fuselage as fz
     m = fz.fuselage_mesh(fz.cfg4_spec_full())
     assert m.n == 2_408_303      # BASELINE cfg4: ~2.4M DoFs
+
+
+@pytest.mark.parametrize("kw", [dict(n_th=16, n_stringers=8, n_z=6, floor_k=1, n_side=2),
+                                dict(n_th=80, n_z=6, n_r_ins=2, floor_k=3, n_side=4),
+                                dict(n_th=40, n_z=12, n_r_ins=2, stringer_h=0.04, n_side=5)])
+def test_cfg4_mesh_variants(kw):
+    """Other valid resolutions: positive Jacobians, flat facets, every DoF
+    used by some element, wet faces conforming; a stringer height that does
+    not meet the frame's mid radius gives frame-only nodes instead of merges."""
+    from paper_2310_04734_b200 import fuselage as fz
+    spec = fz.FuselageSpec(**kw)
+    m = fz.fuselage_mesh(spec)
+    T = fz.fuselage_tables(m)
+    for el, xy in ((m.cab_el, m.cab_xy), (m.ins_el, m.ins_xy)):
+        J = np.array([[np.linalg.det(fe.dshape_nd(fe.QUAD9_LEX_IDX, xi).T @ xy[e]) for xi in fe.gauss_nd(2)[0]]
+                      for e in el])
+        assert J.min() > 0
+    X = T.s_xyz[T.sh_conn]
+    nrm = np.cross(X[:, 2] - X[:, 0], X[:, 6] - X[:, 0])
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    assert np.abs(np.einsum("eic,ec->ei", X - X[:, :1], nrm)).max() <= 1e-12
+    used = np.zeros(m.n, dtype=bool)
+    sd = T.shell_dofs()
+    used[sd[sd >= 0]] = True
+    used[T.f_dof[T.cab_conn].ravel()] = True
+    used[T.f_dof[T.ins_conn].ravel()] = True
+    assert used.all()
+    sag = spec.R * (1 - math.cos(math.pi / spec.n_th)) + 1e-12
+    assert np.linalg.norm(T.s_xyz[T.cp_s] - T.f_xyz[T.cp_f], axis=2).max() <= sag
+    merged = abs(0.5 * (spec.R + spec.R - spec.ins) - (spec.R - spec.stringer_h)) < 1e-12
+    n_str_cols = 2 * spec.n_stringers
+    assert len(m.fr_xy) == (2 * spec.n_th - n_str_cols if merged else 2 * spec.n_th)
