@@ -257,3 +257,20 @@ def test_cfg4_fluid_axial_mode(tiny):
         assert np.abs(K @ np.ones(len(idx))).max() <= 1e-12 * abs(K).max()
         lam = spl.eigsh(K, k=4, M=M, sigma=lam1 * (1 + 1e-4), which="LM", return_eigenvectors=False)
         assert np.min(np.abs(lam - lam1)) <= 1e-9 * lam1, (Kn, lam, lam1)
+
+
+def test_cfg4_variant_frame_only_nodes_solves(cuda):
+    """A resolution with two insulation layers and stringers whose bottom
+    misses the frame's mid radius (frame-only nodes on the frame planes, so
+    the node planes have different sizes): plane-block solve = splu."""
+    import scipy.sparse.linalg as spl
+    from paper_2310_04734_b200 import fuselage as fz
+    spec = fz.FuselageSpec(n_th=16, n_stringers=8, n_z=6, floor_k=1, n_side=2, n_r_ins=2, stringer_h=0.04)
+    fom, info = fz.fuselage_model(spec, cuda)
+    assert len(info["mesh"].fr_xy) > 0 and len(set(np.diff(info["mesh"].plane_off))) > 2
+    f = 151.0
+    fac = fom.factor(f)
+    x = fac.solve(fom.load_dev(f)).cpu().numpy().ravel()
+    assert fac.last_residual <= 1e-10
+    xs = spl.splu(fom.operator(f).tocsc()).solve(fom.load(f))
+    assert np.linalg.norm(x - xs) <= 1e-7 * np.linalg.norm(xs)
