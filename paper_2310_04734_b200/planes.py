@@ -8,7 +8,7 @@ p +- 1, p +- 2 (one element layer = planes 2e, 2e+1, 2e+2), and a mid plane
 
   1. every mid plane O_e is eliminated on its own (independent layers):
      A[O_e, O_e]^-1 from a dense LU (vb_zgetrf) and DMMA block substitution
-     (lu_solve_many); the Schur updates S[E_a, E_b] -= A[E_a, O] A[O,O]^-1
+     (solvers.lu_inverse); the Schur updates S[E_a, E_b] -= A[E_a, O] A[O,O]^-1
      A[O, E_b] of the two corner planes are sparse products (vb_rg_spmm /
      vb_csr_spmm of the coupling blocks) since the couplings are sparse;
   2. the corner planes then form a block-tridiagonal system, factored in one
@@ -34,7 +34,7 @@ import torch
 
 from . import linalg
 from .assembly import DeviceCSR
-from .solvers import DenseLU, lu_solve_many
+from .solvers import DenseLU, lu_inverse
 
 CDT = torch.complex128
 
@@ -134,12 +134,8 @@ class PlaneBlockSolver:
 
 
 def _inverse(D: torch.Tensor) -> torch.Tensor:
-    """D^-1 from the GPU LU (vb_zgetrf + DMMA block substitution of I)."""
-    lu = DenseLU(D)
-    if lu.info != 0:
-        raise RuntimeError("Factor is exactly singular")
-    eye = torch.eye(D.shape[0], dtype=CDT, device=D.device)
-    return lu_solve_many(lu, eye)
+    """D^-1 from the GPU LU (vb_zgetrf + DMMA block substitution, solvers.lu_inverse)."""
+    return lu_inverse(DenseLU(D))
 
 
 class PlaneBlockFactor:

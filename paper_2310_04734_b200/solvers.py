@@ -148,3 +148,37 @@ def lu_solve_many(lu: DenseLU, B: torch.Tensor) -> torch.Tensor:
         if k0 > 0:
             linalg.zgemm("N", A[:k0, k0:k0 + w], T[:w], -1.0, 1.0, C=Y[:k0])
     return Y
+
+
+def lu_inverse(lu: DenseLU) -> torch.Tensor:
+    """A^-1 from vb_zgetrf factors (P A = L U): L^-1 is lower triangular, so
+    the forward substitution of the identity only touches the columns left of
+    the current block (1/3 of a full forward pass); then the backward pass
+    X = U^-1 L^-1 = (P A)^-1 and the column permutation A^-1[:, perm] = X."""
+    from . import linalg
+    if lu.info != 0:
+        raise RuntimeError("Factor is exactly singular")
+    n, nb = lu.n, LU_NB
+    Linv, Uinv, perm = _lu_aux_views(lu)
+    Y = torch.eye(n, dtype=CDT, device=lu.A.device)
+    T = torch.empty((nb, n), dtype=CDT, device=Y.device)
+    nblk = (n + nb - 1) // nb
+    A = lu.A
+    for kb in range(nblk):
+        k0 = kb * nb
+        w = min(nb, n - k0)
+        ke = k0 + w
+        linalg.zgemm("N", Linv[kb, :w, :w], Y[k0:ke, :ke], C=T[:w, :ke])
+        Y[k0:ke, :ke].copy_(T[:w, :ke])
+        if ke < n:
+            linalg.zgemm("N", A[ke:, k0:ke], T[:w, :ke], -1.0, 1.0, C=Y[ke:, :ke])
+    for kb in range(nblk - 1, -1, -1):
+        k0 = kb * nb
+        w = min(nb, n - k0)
+        linalg.zgemm("N", Uinv[kb, :w, :w], Y[k0:k0 + w], C=T[:w])
+        Y[k0:k0 + w].copy_(T[:w])
+        if k0 > 0:
+            linalg.zgemm("N", A[:k0, k0:k0 + w], T[:w], -1.0, 1.0, C=Y[:k0])
+    out = torch.empty_like(Y)
+    out[:, perm] = Y
+    return out
