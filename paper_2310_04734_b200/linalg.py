@@ -157,10 +157,11 @@ def zgemm(transa: str, A: torch.Tensor, B: torch.Tensor, alpha=1.0, beta=0.0,
         C = torch.empty((m, n), dtype=CDT, device=A.device)
         beta = 0.0
     C2 = C if C.dim() == 2 else C.view(-1, 1)
-    wb = lib.vb_zgemm_workspace_bytes(transa.encode(), m, n, k)
-    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=A.device)
-    _lib.check(lib.vb_zgemm(transa.encode(), m, n, k, _lib.zc(alpha), C_ptr(A2), _ld(A2), C_ptr(B2),
-                            _ld(B2), _lib.zc(beta), C_ptr(C2), _ld(C2), C_ptr(work), wb,
+    ta = transa.encode()
+    wb = lib.vb_zgemm_workspace_bytes(ta, m, n, k) if transa != "N" else 0  # 'N' takes no workspace
+    work = C_ptr(torch.empty(max(wb, 1), dtype=torch.uint8, device=A.device)) if wb else None
+    _lib.check(lib.vb_zgemm(ta, m, n, k, _lib.zc(alpha), C_ptr(A2), _ld(A2), C_ptr(B2),
+                            _ld(B2), _lib.zc(beta), C_ptr(C2), _ld(C2), work, wb,
                             _lib.stream_handle()), "vb_zgemm")
     return C
 
