@@ -159,10 +159,13 @@ def zgemm(transa: str, A: torch.Tensor, B: torch.Tensor, alpha=1.0, beta=0.0,
     C2 = C if C.dim() == 2 else C.view(-1, 1)
     ta = transa.encode()
     wb = lib.vb_zgemm_workspace_bytes(ta, m, n, k) if transa != "N" else 0  # 'N' takes no workspace
-    work = C_ptr(torch.empty(max(wb, 1), dtype=torch.uint8, device=A.device)) if wb else None
+    # the workspace tensor must outlive the launch (another host thread could
+    # otherwise be handed the freed block by the caching allocator)
+    work = torch.empty(wb, dtype=torch.uint8, device=A.device) if wb else None
     _lib.check(lib.vb_zgemm(ta, m, n, k, _lib.zc(alpha), C_ptr(A2), _ld(A2), C_ptr(B2),
-                            _ld(B2), _lib.zc(beta), C_ptr(C2), _ld(C2), work, wb,
+                            _ld(B2), _lib.zc(beta), C_ptr(C2), _ld(C2), C_ptr(work) if wb else None, wb,
                             _lib.stream_handle()), "vb_zgemm")
+    del work
     return C
 
 
