@@ -123,9 +123,9 @@ class Pattern:
     def gather(self, triplet_vals: torch.Tensor) -> DeviceCSR:
         lib = _lib.load()
         vals = torch.empty(self.nnz, dtype=torch.float64, device=self.indptr.device)
+        tv = triplet_vals.contiguous()  # alive through the launch (a temporary copy otherwise)
         _lib.check(lib.vb_csr_gather(self.nnz, _lib.ptr(self.gather_ptr), _lib.ptr(self.gather_idx),
-                                     _lib.ptr(triplet_vals.contiguous()), _lib.ptr(vals),
-                                     _lib.stream_handle()), "vb_csr_gather")
+                                     _lib.ptr(tv), _lib.ptr(vals), _lib.stream_handle()), "vb_csr_gather")
         return DeviceCSR(self.n, self.indptr, self.indices, vals)
 
     def gather2(self, tv0: torch.Tensor, tv1: torch.Tensor):
@@ -133,9 +133,10 @@ class Pattern:
         lib = _lib.load()
         v0 = torch.empty(self.nnz, dtype=torch.float64, device=self.indptr.device)
         v1 = torch.empty_like(v0)
+        t0, t1 = tv0.contiguous(), tv1.contiguous()  # alive through the launch
         _lib.check(lib.vb_csr_gather2(self.nnz, _lib.ptr(self.gather_ptr), _lib.ptr(self.gather_idx),
-                                      _lib.ptr(tv0.contiguous()), _lib.ptr(tv1.contiguous()), _lib.ptr(v0),
-                                      _lib.ptr(v1), _lib.stream_handle()), "vb_csr_gather2")
+                                      _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(v0), _lib.ptr(v1),
+                                      _lib.stream_handle()), "vb_csr_gather2")
         return (DeviceCSR(self.n, self.indptr, self.indices, v0), DeviceCSR(self.n, self.indptr, self.indices, v1))
 
 

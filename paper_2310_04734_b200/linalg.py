@@ -205,8 +205,8 @@ def scale_columns(W: torch.Tensor, scale: torch.Tensor, m: int | None = None):
     lib = _lib.load()
     W2 = W if W.dim() == 2 else W.view(-1, 1)
     m = W2.shape[1] if m is None else m
-    _lib.check(lib.vb_scale_columns(W2.shape[0], m, C_ptr(W2), _ld(W2),
-                                    C_ptr(scale.to(torch.float64).contiguous()), _lib.stream_handle()),
+    sc = scale.to(torch.float64).contiguous()  # alive through the launch
+    _lib.check(lib.vb_scale_columns(W2.shape[0], m, C_ptr(W2), _ld(W2), C_ptr(sc), _lib.stream_handle()),
                "vb_scale_columns")
     return W
 
@@ -226,7 +226,8 @@ def block_gs(W: torch.Tensor, Q: torch.Tensor, refs: torch.Tensor | None = None,
     nk = torch.zeros(1, dtype=torch.int32, device=W.device)
     wb = lib.vb_block_gs_workspace_bytes()
     work = torch.empty(max(wb, 1), dtype=torch.uint8, device=W.device)
-    rp = _lib.ptr(refs.contiguous()) if refs is not None else None
+    refs_c = refs.contiguous() if refs is not None else None  # alive through the launch
+    rp = _lib.ptr(refs_c) if refs_c is not None else None
     _lib.check(lib.vb_block_gs(n, kb, C_ptr(W), _ld(W), rp, tol, reorth, int(no_drop), C_ptr(Q), _ld(Q),
                                _lib.ptr(kept), _lib.ptr(nk), C_ptr(work), wb, _lib.stream_handle()),
                "vb_block_gs")
