@@ -1040,10 +1040,24 @@ def krylov_blocks_concurrent(fom: FullOrderModel, points, m: int, second_order: 
             st.synchronize()
         finally:
             lib.vb_set_lu_max_ctas(0)
+        _record_stream(out, caller)
         return out
 
     with ThreadPoolExecutor(nw, thread_name_prefix="vb_krylov") as ex:
         return list(ex.map(work, pts))
+
+
+def _record_stream(obj, stream):
+    """Mark the device tensors a worker produced on its own stream as used by
+    `stream` (the caller's), so the caching allocator never hands their
+    blocks to a later allocation on the worker stream while the caller's
+    kernels may still read them."""
+    if isinstance(obj, torch.Tensor):
+        if obj.is_cuda:
+            obj.record_stream(stream)
+    elif isinstance(obj, (list, tuple)):
+        for o in obj:
+            _record_stream(o, stream)
 
 
 def fom_outputs_concurrent(fom: FullOrderModel, freqs, workers: int | None = None) -> list:
