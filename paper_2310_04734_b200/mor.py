@@ -110,6 +110,7 @@ def _to_dense_dev(M, device) -> torch.Tensor:
 
 
 _PROVIDER_CACHE: dict = {}
+_PROVIDER_LOCK = __import__("threading").Lock()  # concurrent expansion points share the cache
 
 
 def _provider_on_device(M, device):
@@ -119,7 +120,8 @@ def _provider_on_device(M, device):
     Providers that return the same object every call (the reference tests'
     `lambda f: K`) hit the cache."""
     key = (id(M), str(device))
-    hit = _PROVIDER_CACHE.get(key)
+    with _PROVIDER_LOCK:
+        hit = _PROVIDER_CACHE.get(key)
     if hit is not None and hit[0] is M:
         return hit[1]
     if sp.issparse(M):
@@ -127,9 +129,10 @@ def _provider_on_device(M, device):
         val = ("csr", device_csr_terms(M, device))
     else:
         val = ("dense", _to_dense_dev(M, device))
-    if len(_PROVIDER_CACHE) > 32:
-        _PROVIDER_CACHE.pop(next(iter(_PROVIDER_CACHE)))
-    _PROVIDER_CACHE[key] = (M, val)
+    with _PROVIDER_LOCK:
+        while len(_PROVIDER_CACHE) > 32:
+            _PROVIDER_CACHE.pop(next(iter(_PROVIDER_CACHE)))
+        _PROVIDER_CACHE[key] = (M, val)
     return val
 
 
