@@ -1134,15 +1134,33 @@ def krylov_basis(fom: FullOrderModel, points, m: int, second_order: bool = False
         if _lu_factored(fom):  # dense LU factors are GBs: no look-ahead
             res = [run(fom, f, m, second_order) for f in pts]
         else:
+            # plane-block factors (cfg4) are GPU work: the factorisation of point
+            # p+1 runs on its own stream, overlapping point p's moment solves on
+            # the caller's stream (the factor is finished before it is used, and
+            # the caller's stream is drained before a factor is released, so the
+            # caching allocator never hands its blocks to the other stream early)
+            side = fom.planes is not None and SIDE_STREAM_FACTORS
+            main = torch.cuda.current_stream(dev)
+            if side:
+                main.synchronize()
             with ThreadPoolExecutor(1, thread_name_prefix="vb_factor") as ex:
                 def prep(f):
                     torch.cuda.set_device(dev)
-                    return fom.factor(f)
+                    if not side:
+                        return fom.factor(f)
+                    st = torch.cuda.Stream(device=dev)
+                    with torch.cuda.stream(st):
+                        lu = fom.factor(f)
+                    st.synchronize()
+                    return lu
                 res, nxt = [], ex.submit(prep, pts[0]) if pts else None
                 for i, f in enumerate(pts):
                     lu = nxt.result()
                     nxt = ex.submit(prep, pts[i + 1]) if i + 1 < len(pts) else None
                     res.append(run(fom, f, m, second_order, lu=lu))
+                    if side:
+                        main.synchronize()
+                    del lu
     V, flags, group = None, [], []
     for r in res:
         if mimo:  # per-source blocks appended together, >= GROUP_COLS columns per group
@@ -1160,6 +1178,7 @@ def krylov_basis(fom: FullOrderModel, points, m: int, second_order: bool = False
 
 
 GROUP_COLS = 64  # columns appended per orthonormalise_blocks call in krylov_basis (MIMO)
+SIDE_STREAM_FACTORS = True  # plane-block factor of the next point on its own stream (krylov_basis)
 
 
 # ------------------------------------------------------ certification ----
