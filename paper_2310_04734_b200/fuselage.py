@@ -379,9 +379,8 @@ def fuselage_tables(m: FuselageMesh) -> FuselageTables:
         s_xyz[s_base[k]:s_base[k + 1], 2] = m.z[k]
         s_dof0[s_base[k]:s_base[k + 1]] = (m.plane_off[k] + NDS * np.arange(cnt)) if m.plane_nstruct[k] else -1
 
-    def sn(local, k):
-        return s_base[k] + local
-
+    # structure node (plane-local id, plane k) -> s_base[k] + id; fluid node
+    # (insulation 2D id, plane k) -> k nfl + id, cabin 2D id -> k nfl + n_i2 + id
     n_i2, n_c2 = len(m.ins_xy), len(m.cab_xy)
     nfl = n_i2 + n_c2
     f_xy = np.vstack([m.ins_xy, m.cab_xy])
@@ -392,69 +391,83 @@ def fuselage_tables(m: FuselageMesh) -> FuselageTables:
         f_xyz[k * nfl:(k + 1) * nfl, 2] = m.z[k]
         f_dof[k * nfl:(k + 1) * nfl] = m.plane_off[k] + m.plane_nstruct[k] + np.arange(nfl)
 
-    def fi(local2d, k):  # insulation 2D node -> fluid node id
-        return k * nfl + local2d
-
-    def fc(local2d, k):  # cabin
-        return k * nfl + n_i2 + local2d
-
-    sh, mat, skin_el = [], [], []
-    cab, ins = [], []
-    cp_s, cp_f, cp_kind, cp_sign = [], [], [], []
-    fl_ids = m.floor_ids
+    # element tables, vectorised per z layer in the element order of the
+    # original per-element loops: per layer [skin e, lining e] for each e,
+    # floor elements, stringers (web 0, web 1, bottom), then the fluids; the
+    # frames (one plane each) after all layers.  Coupling faces per layer:
+    # [skin-ins e, lining-ins e, (lining-cabin e)] for each e, then floor.
+    i_out = 2 * sp_.n_r_ins
+    nri = i_out + 1
+    e_ = np.arange(nth)
+    js = (2 * e_[:, None] + np.arange(3)[None, :]) % nj                  # (nth, 3) angle nodes a
     arc = m.cab_arc
+    in_arc = np.array([all(int(j) in arc for j in row) for row in js])
+    arc_node = np.full(nj, -1, dtype=np.int64)
+    for j, q in arc.items():
+        arc_node[j] = q
+    nfloor = (len(m.floor_ids) - 1) // 2
+    fq = 2 * np.arange(nfloor)[:, None] + np.arange(3)[None, :]          # (nfloor, 3)
+    strg = np.array(m.stringer_nodes, dtype=np.int64).reshape(-1, 7)       # j0, j1, w0, w1, b0, bm, b1
+    sh_l, mat_l, skin_l, cp_s_l, cp_f_l, cp_k_l, cp_g_l, ins_l, cab_l = ([] for _ in range(9))
+    n_sh = 0
+    ab = lambda nodes_a, ks: (nodes_a[..., None, :] + s_base[np.asarray(ks)][None, :, None]).reshape(
+        nodes_a.shape[0], 9)                                               # [a + 3b] = node(a) in plane ks[b]
     for lay in range(sp_.n_z):
-        ks = [2 * lay, 2 * lay + 1, 2 * lay + 2]
+        ks = np.array([2 * lay, 2 * lay + 1, 2 * lay + 2])
+        skin = ab(m.skin_ids[js], ks)
+        lining = ab(m.lin_ids[js], ks)
+        per_e = np.stack([skin, lining], axis=1).reshape(-1, 9)           # skin e, lining e, ...
+        sh_l.append(per_e)
+        mat_l.append(np.tile([0, 1], nth))
+        skin_l.append(n_sh + 2 * e_)
+        n_sh += 2 * nth
+        fins_out = (i_out + nri * js)[:, None, :] + (ks * nfl)[None, :, None]   # (nth, 3 b, 3 a)
+        fins_in = (nri * js)[:, None, :] + (ks * nfl)[None, :, None]
+        fcab = (n_i2 + arc_node[js])[:, None, :] + (ks * nfl)[None, :, None]
         for e in range(nth):
-            js = [(2 * e + a) % nj for a in range(3)]
-            skin = [sn(m.skin_ids[js[a]], ks[b]) for b in range(3) for a in range(3)]
-            skin_el.append(len(sh))
-            sh.append(skin)
-            mat.append(0)
-            lining = [sn(m.lin_ids[js[a]], ks[b]) for b in range(3) for a in range(3)]
-            sh.append(lining)
-            mat.append(1)
-            # skin <-> outer insulation face, lining <-> inner face (normal sign: see below)
-            i_out = 2 * sp_.n_r_ins
-            nri = i_out + 1
-            cp_s.append(skin)
-            cp_f.append([fi(i_out + nri * js[a], ks[b]) for b in range(3) for a in range(3)])
-            cp_kind.append(0)
-            cp_sign.append(-1.0)
-            cp_s.append(lining)
-            cp_f.append([fi(0 + nri * js[a], ks[b]) for b in range(3) for a in range(3)])
-            cp_kind.append(0)
-            cp_sign.append(+1.0)
-            if all(j in arc for j in js):
-                cp_s.append(lining)
-                cp_f.append([fc(arc[js[a]], ks[b]) for b in range(3) for a in range(3)])
-                cp_kind.append(1)
-                cp_sign.append(-1.0)
-        for q in range((len(fl_ids) - 1) // 2):
-            fl = [sn(fl_ids[2 * q + a], ks[b]) for b in range(3) for a in range(3)]
-            sh.append(fl)
-            mat.append(2)
-            cp_s.append(fl)
-            cp_f.append([fc(m.cab_floor[2 * q + a], ks[b]) for b in range(3) for a in range(3)])
-            cp_kind.append(1)
-            cp_sign.append(-1.0)   # floor e3 = -y, the cabin is above: n = +y
-        for (j0, j1, w0, w1, b0, bm, b1) in m.stringer_nodes:
-            for jw, wm, bb in ((j0, w0, b0), (j1, w1, b1)):
-                sh.append([sn(n_, ks[b]) for b in range(3) for n_ in (m.skin_ids[jw], wm, bb)])
-                mat.append(4)
-            sh.append([sn(n_, ks[b]) for b in range(3) for n_ in (b0, bm, b1)])
-            mat.append(4)
-        for el in m.ins_el:
-            ins.append([fi(el[q % 9], ks[q // 9]) for q in range(27)])
-        for el in m.cab_el:
-            cab.append([fc(el[q % 9], ks[q // 9]) for q in range(27)])
+            cp_s_l += [skin[e], lining[e]]
+            cp_f_l += [fins_out[e].ravel(), fins_in[e].ravel()]
+            cp_k_l += [0, 0]
+            cp_g_l += [-1.0, 1.0]
+            if in_arc[e]:
+                cp_s_l.append(lining[e])
+                cp_f_l.append(fcab[e].ravel())
+                cp_k_l.append(1)
+                cp_g_l.append(-1.0)
+        fl = ab(m.floor_ids[fq], ks)
+        sh_l.append(fl)
+        mat_l.append(np.full(nfloor, 2))
+        n_sh += nfloor
+        for q in range(nfloor):
+            cp_s_l.append(fl[q])
+            cp_f_l.append(((n_i2 + m.cab_floor[fq[q]])[None, :] + (ks * nfl)[:, None]).ravel())
+            cp_k_l.append(1)
+            cp_g_l.append(-1.0)   # floor e3 = -y, the cabin is above: n = +y
+        if len(strg):
+            web0 = ab(np.stack([m.skin_ids[strg[:, 0]], strg[:, 2], strg[:, 4]], 1), ks)
+            web1 = ab(np.stack([m.skin_ids[strg[:, 1]], strg[:, 3], strg[:, 6]], 1), ks)
+            bot = ab(strg[:, 4:7], ks)
+            sh_l.append(np.stack([web0, web1, bot], 1).reshape(-1, 9))
+            mat_l.append(np.full(3 * len(strg), 4))
+            n_sh += 3 * len(strg)
+        q27 = np.arange(27)
+        ins_l.append(m.ins_el[:, q27 % 9] + (ks[q27 // 9] * nfl)[None, :])
+        cab_l.append(n_i2 + m.cab_el[:, q27 % 9] + (ks[q27 // 9] * nfl)[None, :])
     for k in m.frame_planes:
-        for e in range(nth):
-            js = [(2 * e + b) % nj for b in range(3)]
-            sh.append([sn(n_, k) for b in range(3) for n_ in (m.lin_ids[js[b]], m.mid_ids[js[b]], m.skin_ids[js[b]])])
-            mat.append(3)
-    sh = np.array(sh, dtype=np.int64)
-    cp_s = np.array(cp_s, dtype=np.int64)
+        jb = js                                                               # b along the angle
+        nodes = np.stack([m.lin_ids[jb], m.mid_ids[jb], m.skin_ids[jb]], 2)   # (nth, 3 b, 3 a)
+        sh_l.append((nodes + s_base[k]).reshape(nth, 9))
+        mat_l.append(np.full(nth, 3))
+        n_sh += nth
+    c = lambda a: np.ascontiguousarray(a, dtype=np.int64)  # row-major (fancy indexing may give F order)
+    sh = c(np.concatenate(sh_l))
+    mat = np.concatenate(mat_l)
+    skin_el = np.concatenate(skin_l)
+    cab = c(np.concatenate(cab_l))
+    ins = c(np.concatenate(ins_l))
+    cp_s = c(np.array(cp_s_l))
+    cp_f = c(np.array(cp_f_l))
+    cp_kind, cp_sign = cp_k_l, cp_g_l
     # normals from the flat structure facets: e3 = (x2 - x0) x (x6 - x0) / |.|, n = sign * e3
     X = s_xyz[cp_s]
     e3 = np.cross(X[:, 2] - X[:, 0], X[:, 6] - X[:, 0])
@@ -462,7 +475,7 @@ def fuselage_tables(m: FuselageMesh) -> FuselageTables:
     cp_n = e3 * np.array(cp_sign)[:, None]
     return FuselageTables(s_xyz=s_xyz, s_dof0=s_dof0, f_xyz=f_xyz, f_dof=f_dof, sh_conn=sh,
                           sh_mat=np.array(mat, dtype=np.int32), cab_conn=np.array(cab, dtype=np.int64),
-                          ins_conn=np.array(ins, dtype=np.int64), cp_s=cp_s, cp_f=np.array(cp_f, dtype=np.int64),
+                          ins_conn=np.array(ins, dtype=np.int64), cp_s=cp_s, cp_f=cp_f,
                           cp_n=cp_n, cp_kind=np.array(cp_kind, dtype=np.int32),
                           skin_el=np.array(skin_el, dtype=np.int64))
 
@@ -645,7 +658,8 @@ def fuselage_model(spec: FuselageSpec | None = None, device=None, solver: bool =
     n_i2 = len(m.ins_xy)
     nfl = n_i2 + len(m.cab_xy)
     inner2 = np.nonzero(~m.cab_boundary)[0]
-    cand = np.array([m.plane_off[k] + m.plane_nstruct[k] + n_i2 + q for k in range(1, m.P - 1) for q in inner2])
+    ks = np.arange(1, m.P - 1)
+    cand = ((m.plane_off[ks] + m.plane_nstruct[ks] + n_i2)[:, None] + inner2[None, :]).ravel()
     rec = np.sort(rng.choice(cand, spec.n_rec, replace=False)).astype(np.int64)
     Cmat = np.zeros((spec.n_rec, n))
     Cmat[np.arange(spec.n_rec), rec] = 1.0

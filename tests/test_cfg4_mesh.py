@@ -166,3 +166,14 @@ def test_cfg4_mesh_variants(kw):
     merged = abs(0.5 * (spec.R + spec.R - spec.ins) - (spec.R - spec.stringer_h)) < 1e-12
     n_str_cols = 2 * spec.n_stringers
     assert len(m.fr_xy) == (2 * spec.n_th - n_str_cols if merged else 2 * spec.n_th)
+
+
+def test_cfg4_tables_are_row_major():
+    """Element tables go to the C ABI: row-major int64 (the vectorised builder
+    uses fancy indexing, which can return Fortran-ordered arrays)."""
+    from paper_2310_04734_b200 import fuselage as fz
+    T = fz.fuselage_tables(fz.fuselage_mesh(fz.FuselageSpec(n_th=16, n_stringers=8, n_z=6, floor_k=1, n_side=2)))
+    for name in ("sh_conn", "cab_conn", "ins_conn", "cp_s", "cp_f"):
+        a = getattr(T, name)
+        assert a.flags["C_CONTIGUOUS"] and a.dtype == np.int64, name
+        assert a.astype(np.int32).flags["C_CONTIGUOUS"], name
